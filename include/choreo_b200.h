@@ -1,0 +1,138 @@
+/*
+ * choreo_b200.h — C-ABI of the B200-native choreographed-attention hot path.
+ *
+ * The reference (/root/reference/pkg, pure Python/NumPy) has no FFI layer; its
+ * hot path sits behind Python objects.  Each entry point below replaces one
+ * reference function on that path (file:line relative to
+ * /root/reference/pkg/src/choreo/) and is what a binding for the reference's
+ * Engine would call (see INTEGRATION.md for the ctypes binding).
+ *
+ * Conventions (every function):
+ *   - plain device pointers + sizes; no torch / C++ types; never allocates or
+ *     frees device memory (the caller owns every buffer);
+ *   - `stream` is a cudaStream_t passed as void*; all work is asynchronous on it;
+ *   - returns 0 on success, a negative CHOREO_E* code otherwise; never throws;
+ *   - dtype codes: CHOREO_F32 (0) and CHOREO_BF16 (1).
+ *
+ * KV pool layout (one pool for K, one for V):
+ *   pool[layer][kv_head][page][slot][head_dim], pages of `page_size` slots.
+ * Every page belongs to exactly one message; a message's tokens fill its page
+ * chain in within-message order.  Keys are stored post-rotation at the
+ * message's current logical position (reference cache.py:3-7).
+ */
+#ifndef CHOREO_B200_H
+#define CHOREO_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CHOREO_F32 0
+#define CHOREO_BF16 1
+
+#define CHOREO_OK 0
+#define CHOREO_EINVAL (-1)   /* bad argument (shape, dtype, null pointer) */
+#define CHOREO_ELAUNCH (-2)  /* CUDA launch / runtime failure */
+#define CHOREO_EUNSUPPORTED (-3)
+
+/* ABI version (major*100 + minor). */
+int choreo_abi_version(void);
+
+/* Last CUDA error string recorded by this library (thread-local, never NULL). */
+const char* choreo_last_error(void);
+
+/* x[r, :] = embed[ids[r], :] as f32.  Replaces model.py:162 (`weights.embed[ids]`). */
+int choreo_embed(const void* embed, int embed_dtype, int d, const int32_t* ids, int n_rows,
+                 float* x, void* stream);
+
+/* Pre-norm residual step: if delta != NULL, x += delta (f32 residual stream);
+ * out = x / sqrt(mean(x^2) + eps) * w, written in out_dtype.
+ * Replaces model.py:171,185-186,189 (residual adds + tensor.py:78-80 rms_norm).
+ * row_map (optional, may be NULL): out row i normalises x row row_map[i] and
+ * skips the residual add (used to pick logit rows). */
+int choreo_residual_rmsnorm(float* x, const void* delta, int delta_dtype, const void* w,
+                            int w_dtype, int n_rows, int d, float eps, void* out, int out_dtype,
+                            const int32_t* row_map, int n_out, void* stream);
+
+/* out[r, i] = silu(gu[r, i]) * gu[r, f + i]  (gate | up concatenated).
+ * Replaces model.py:187 and tensor.py:83-84. */
+int choreo_silu_mul(const void* gu, int gu_dtype, int n_rows, int f, void* out, int out_dtype,
+                    void* stream);
+
+/* K1 rope_append: for each new-token row r at logical position pos[r],
+ *   q_out[r, h, :]   = rotate(qkv[r, q_h], pos[r])           (f32)
+ *   K[layer][h][dst_page[r]][dst_slot[r]] = rotate(qkv[r, k_h], pos[r])
+ *   V[layer][h][dst_page[r]][dst_slot[r]] = qkv[r, v_h]
+ * with qkv rows laid out [q (n_heads*hd) | k (n_kv*hd) | v (n_kv*hd)].
+ * Rotation is the reference's interleaved-pair RoPE read from the f64-derived
+ * table cos/sin[(pos + W) * (hd/2) + i] (tensor.py:87-143).
+ * Replaces model.py:172-176 + cache.py:98-135 (append_tokens) fused. */
+int choreo_rope_append(const void* qkv, int qkv_dtype, int ld_qkv, int n_rows,
+                       const int32_t* pos, const int32_t* dst_page, const int32_t* dst_slot,
+                       float* q_out, void* k_pool, void* v_pool, int pool_dtype, int layer,
+                       int n_kv, int n_pages, int page_size, int n_heads, int head_dim,
+                       const float* cos_t, const float* sin_t, int max_delta, void* stream);
+
+/* K2 rerotate: in-place rotation of cached keys by a per-page delta, all layers:
+ *   for l, h, i < n_list, s < page_len[i]:  K[l][h][pages[i]][s] = rotate(., delta[i])
+ * |delta| <= max_delta.  V is never touched.  delta == 0 pages are skipped.
+ * Replaces cache.py:139-160 (reposition_message) + tensor.py:115-122. */
+int choreo_rerotate(void* k_pool, int pool_dtype, int n_layers, int n_kv, int n_pages,
+                    int page_size, int head_dim, const int32_t* pages, const int32_t* page_len,
+                    const int32_t* delta, int n_list, const float* cos_t, const float* sin_t,
+                    int max_delta, void* stream);
+
+/* K3 assemble: prompt assembly on device.  Inputs (device int32):
+ *   msg_len[m], msg_pt[m] (offset of message m's page chain in page_table), page_table[]
+ *   calls[5*c..]: {own msg, parent offset, parent count, row offset, row count}
+ *   call_parents[]: parent message ids, in the call's parent order
+ *   row_t[r]: the row's within-message token index (rows grouped by call, ascending t);
+ *             the row sees its own message's tokens 0..t
+ *   patch[2*i], patch[2*i+1]: page_table[patch[2i]] = patch[2i+1], applied first
+ * Outputs (device int32):
+ *   vis_page[], vis_len[], vis_own[]: each call's visible page list — parent pages in
+ *       parent order (vis_own = -1), then own pages up to the call's last row
+ *       (vis_own = own token index of slot 0); pages past a block's last row are skipped
+ *   items[6*i..]: {row_begin, n_rows, vis_begin, n_vis_pages, part_base, call}
+ *   row_part[3*r..]: {first partial of the row, partial stride, partial count}
+ *   counts[0..3] = {n_vis_pages, n_items, n_partials, status (0 ok, -1 over capacity)}
+ * Visibility is exactly reference masking.py:36-53 (parents' tokens + own tokens with
+ * j <= query j) at page granularity; tests expand it to token level against the oracle.
+ * Replaces engine.py:203-245 layout + masking.py:43-53 visible_cache_indices. */
+int choreo_assemble(const int32_t* msg_len, const int32_t* msg_pt, int32_t* page_table,
+                    const int32_t* calls, const int32_t* call_parents, int n_calls,
+                    const int32_t* row_t, int n_rows, const int32_t* patch, int n_patch,
+                    int page_size, int rows_per_block, int pages_per_item, int32_t* vis_page,
+                    int32_t* vis_len, int32_t* vis_own, int32_t* items, int32_t* row_part,
+                    int32_t* counts, int cap_pages, int cap_items, int cap_parts, void* stream);
+
+/* K5 split-KV attention over assembled work items (prefill and decode rows alike).
+ * q: f32 [n_rows][n_heads][hd] (already rotated, K1).  For each item and KV head writes
+ * per-(row, q-head) partials: part_o f32 [n_partials][n_heads][hd] (normalised) and
+ * part_lse f32 [n_partials][n_heads] (natural-log sum-exp; -inf if nothing visible).
+ * grid_ctas = number of persistent CTAs (0 = auto).  Replaces model.py:177-184 +
+ * tensor.py:65-75 (gather, concat, scores, masked softmax, PV). */
+int choreo_attn_split(const float* q, const void* k_pool, const void* v_pool, int pool_dtype,
+                      int layer, int n_kv, int n_pages, int page_size, int n_heads, int head_dim,
+                      const int32_t* row_t, const int32_t* vis_page, const int32_t* vis_len,
+                      const int32_t* vis_own, const int32_t* items, const int32_t* counts,
+                      int max_items, float* part_o, float* part_lse, int grid_ctas,
+                      void* stream);
+
+/* Combine partials into out[r][h][:] (out_dtype) with the LSE merge. */
+int choreo_attn_combine(const float* part_o, const float* part_lse, const int32_t* row_part,
+                        int n_rows, int n_heads, int head_dim, void* out, int out_dtype,
+                        void* stream);
+
+/* K6 select: greedy argmax over generatable ids {0..255, 257} with first-index
+ * tie-break, one row per logits row (engine.py:371, tokenizer.py:39-44). */
+int choreo_select_greedy(const float* logits, int n_rows, int ld, int vocab, int32_t* out_tok,
+                         void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CHOREO_B200_H */

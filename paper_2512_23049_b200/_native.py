@@ -1,0 +1,102 @@
+"""ctypes binding of the sm_100a C-ABI library (include/choreo_b200.h).
+
+There is no fallback: if the in-tree ``_choreo_b200.so`` is missing or fails to
+load, every engine entry point raises ``NativeError``.  Build it with
+``python -m paper_2512_23049_b200.build`` (or ``__graft_entry__.build()``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import NativeError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_choreo_b200.so")
+
+F32 = 0
+BF16 = 1
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_F = ctypes.c_float
+
+# name -> argtypes (all functions return int status)
+SIGNATURES: dict[str, list] = {
+    "choreo_embed": [_P, _I, _I, _P, _I, _P, _P],
+    "choreo_residual_rmsnorm": [_P, _P, _I, _P, _I, _I, _I, _F, _P, _I, _P, _I, _P],
+    "choreo_silu_mul": [_P, _I, _I, _I, _P, _I, _P],
+    "choreo_rope_append": [_P, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I,
+                           _P, _P, _I, _P],
+    "choreo_rerotate": [_P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _I, _P, _P, _I, _P],
+    "choreo_assemble": [_P, _P, _P, _P, _P, _I, _P, _I, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P,
+                        _P, _I, _I, _I, _P],
+    "choreo_attn_split": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _P,
+                          _P, _I, _P],
+    "choreo_attn_combine": [_P, _P, _P, _I, _I, _I, _P, _I, _P],
+    "choreo_select_greedy": [_P, _I, _I, _I, _P, _P],
+}
+EXTRA = ["choreo_abi_version", "choreo_last_error"]
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise NativeError(f"CUDA extension not built: {LIB_PATH} is missing "
+                          "(run `python -m paper_2512_23049_b200.build`); there is no CPU fallback")
+    try:
+        lib = ctypes.CDLL(LIB_PATH)
+    except OSError as exc:
+        raise NativeError(f"cannot load {LIB_PATH}: {exc}") from exc
+    for name, args in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_int
+    lib.choreo_abi_version.restype = ctypes.c_int
+    lib.choreo_last_error.restype = ctypes.c_char_p
+    _lib = lib
+    return lib
+
+
+class _Caller:
+    def __init__(self, name: str) -> None:
+        self.name = name
+        self.fn = None
+
+    def __call__(self, *args) -> None:
+        if self.fn is None:
+            self.fn = getattr(load(), self.name)
+        rc = self.fn(*args)
+        if rc != 0:
+            msg = load().choreo_last_error().decode(errors="replace")
+            raise NativeError(f"{self.name} failed with code {rc}: {msg}")
+
+
+embed = _Caller("choreo_embed")
+residual_rmsnorm = _Caller("choreo_residual_rmsnorm")
+silu_mul = _Caller("choreo_silu_mul")
+rope_append = _Caller("choreo_rope_append")
+rerotate = _Caller("choreo_rerotate")
+assemble = _Caller("choreo_assemble")
+attn_split = _Caller("choreo_attn_split")
+attn_combine = _Caller("choreo_attn_combine")
+select_greedy = _Caller("choreo_select_greedy")
+
+
+def ptr(t) -> int | None:
+    """Raw device pointer of a torch tensor (None for None)."""
+    return None if t is None else t.data_ptr()
+
+
+def dtype_code(dtype) -> int:
+    import torch
+
+    if dtype == torch.float32:
+        return F32
+    if dtype == torch.bfloat16:
+        return BF16
+    raise NativeError(f"unsupported dtype {dtype}")

@@ -1,0 +1,147 @@
+// Row-wise pieces of the forward step around the attention/GEMM hot ops:
+// embedding gather, fused residual add + RMSNorm, SiLU-gate, greedy select (K6).
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "common.cuh"
+
+namespace choreo {
+
+static thread_local char g_err[256] = "";
+
+void set_last_error(const char* where, cudaError_t err) {
+  snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(err));
+}
+
+__global__ void embed_kernel(const void* __restrict__ embed, int dt, int d,
+                             const int32_t* __restrict__ ids, float* __restrict__ x) {
+  const int r = blockIdx.x;
+  const int64_t src = (int64_t)ids[r] * d;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) x[(int64_t)r * d + i] = load_any(embed, dt, src + i);
+}
+
+// One CTA per output row.  x is the f32 residual stream.
+__global__ void residual_rmsnorm_kernel(float* __restrict__ x, const void* __restrict__ delta,
+                                        int delta_dt, const void* __restrict__ w, int w_dt, int d,
+                                        float eps, void* __restrict__ out, int out_dt,
+                                        const int32_t* __restrict__ row_map) {
+  const int r_out = blockIdx.x;
+  const int r = row_map ? row_map[r_out] : r_out;
+  float* xr = x + (int64_t)r * d;
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    float v = xr[i];
+    if (delta) {
+      v += load_any(delta, delta_dt, (int64_t)r * d + i);
+      xr[i] = v;
+    }
+    ss += v * v;
+  }
+  if (!out) return;
+  __shared__ float red[32];
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  const float inv = 1.0f / sqrtf(red[0] / (float)d + eps);
+  for (int i = threadIdx.x; i < d; i += blockDim.x)
+    store_any(out, out_dt, (int64_t)r_out * d + i, xr[i] * inv * load_any(w, w_dt, i));
+}
+
+__global__ void silu_mul_kernel(const void* __restrict__ gu, int dt, int64_t n, int f,
+                                void* __restrict__ out, int out_dt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / f, c = i % f;
+    const float g = load_any(gu, dt, r * 2 * f + c);
+    const float u = load_any(gu, dt, r * 2 * f + f + c);
+    store_any(out, out_dt, i, g / (1.0f + expf(-g)) * u);
+  }
+}
+
+// K6: one warp per row; generatable ids are 0..255 and 257 (EOS).  Ties keep the
+// lowest id, as np.argmax does (engine.py:371).
+__global__ void select_greedy_kernel(const float* __restrict__ logits, int n_rows, int64_t ld,
+                                     int32_t* __restrict__ out) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= n_rows) return;
+  const float* lr = logits + row * ld;
+  float best = -INFINITY;
+  int idx = 0x7fffffff;
+  for (int i = lane; i < 258; i += 32) {
+    if (i == 256) continue;
+    const float v = lr[i];
+    if (v > best || (v == best && i < idx)) { best = v; idx = i; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (ob > best || (ob == best && oi < idx)) { best = ob; idx = oi; }
+  }
+  if (lane == 0) out[row] = idx == 0x7fffffff ? 0 : idx;
+}
+
+}  // namespace choreo
+
+using namespace choreo;
+
+extern "C" {
+
+int choreo_abi_version(void) { return 100; }
+
+const char* choreo_last_error(void) { return g_err; }
+
+int choreo_embed(const void* embed, int embed_dtype, int d, const int32_t* ids, int n_rows,
+                 float* x, void* stream) {
+  if (!embed || !ids || !x || d <= 0 || n_rows < 0 || !dtype_ok(embed_dtype)) return CHOREO_EINVAL;
+  if (n_rows == 0) return CHOREO_OK;
+  embed_kernel<<<n_rows, 256, 0, as_stream(stream)>>>(embed, embed_dtype, d, ids, x);
+  return launch_status("choreo_embed");
+}
+
+int choreo_residual_rmsnorm(float* x, const void* delta, int delta_dtype, const void* w,
+                            int w_dtype, int n_rows, int d, float eps, void* out, int out_dtype,
+                            const int32_t* row_map, int n_out, void* stream) {
+  if (!x || d <= 0 || n_rows < 0) return CHOREO_EINVAL;
+  if (out && (!w || !dtype_ok(w_dtype) || !dtype_ok(out_dtype))) return CHOREO_EINVAL;
+  if (delta && !dtype_ok(delta_dtype)) return CHOREO_EINVAL;
+  if (row_map && (delta || !out)) return CHOREO_EINVAL;
+  const int rows = row_map ? n_out : n_rows;
+  if (rows == 0) return CHOREO_OK;
+  const int threads = d >= 2048 ? 512 : (d >= 256 ? 256 : 64);
+  residual_rmsnorm_kernel<<<rows, threads, 0, as_stream(stream)>>>(x, delta, delta_dtype, w, w_dtype,
+                                                                    d, eps, out, out_dtype, row_map);
+  return launch_status("choreo_residual_rmsnorm");
+}
+
+int choreo_silu_mul(const void* gu, int gu_dtype, int n_rows, int f, void* out, int out_dtype,
+                    void* stream) {
+  if (!gu || !out || f <= 0 || n_rows < 0 || !dtype_ok(gu_dtype) || !dtype_ok(out_dtype))
+    return CHOREO_EINVAL;
+  const int64_t n = (int64_t)n_rows * f;
+  if (n == 0) return CHOREO_OK;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  silu_mul_kernel<<<(int)blocks, 256, 0, as_stream(stream)>>>(gu, gu_dtype, n, f, out, out_dtype);
+  return launch_status("choreo_silu_mul");
+}
+
+int choreo_select_greedy(const float* logits, int n_rows, int ld, int vocab, int32_t* out_tok,
+                         void* stream) {
+  if (!logits || !out_tok || n_rows < 0 || vocab < 258 || ld < vocab) return CHOREO_EINVAL;
+  if (n_rows == 0) return CHOREO_OK;
+  const int warps = 4;
+  select_greedy_kernel<<<(n_rows + warps - 1) / warps, 32 * warps, 0, as_stream(stream)>>>(
+      logits, n_rows, ld, out_tok);
+  return launch_status("choreo_select_greedy");
+}
+
+}  // extern "C"

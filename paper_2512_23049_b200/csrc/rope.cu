@@ -1,0 +1,175 @@
+// K1 rope_append and K2 rerotate: the two position kernels of the global cache.
+//
+// Rotation is the reference's interleaved-pair RoPE (tensor.py:87-143): pair i of a
+// head vector is (x[2i], x[2i+1]) and rotates by delta * base^(-2i/hd).  The cos/sin
+// values come from the f64-derived table cos/sin[(delta + W) * (hd/2) + i] stored as
+// f32 (tensor.py:103-107), so index math is exact and values match the reference's
+// table cast to f32.
+#include "common.cuh"
+
+namespace choreo {
+
+// ---- K1 ------------------------------------------------------------------------
+// One thread per rotation pair of (row, head); q heads first, then k heads, then v
+// (v pairs are copied unrotated).  Writes q (f32) and the pool slot of each row.
+template <typename TI, typename TP>
+__global__ void rope_append_kernel(const TI* __restrict__ qkv, int ld, int n_rows,
+                                   const int32_t* __restrict__ pos,
+                                   const int32_t* __restrict__ dst_page,
+                                   const int32_t* __restrict__ dst_slot, float* __restrict__ q_out,
+                                   TP* __restrict__ kp, TP* __restrict__ vp, int layer, int n_kv,
+                                   int n_pages, int page_size, int n_heads, int hd,
+                                   const float* __restrict__ cos_t,
+                                   const float* __restrict__ sin_t, int max_delta) {
+  const int half = hd >> 1;
+  const int per_row = (n_heads + 2 * n_kv) * half;
+  const int64_t total = (int64_t)n_rows * per_row;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(u / per_row);
+    int rem = (int)(u % per_row);
+    const int head = rem / half;  // 0..n_heads+2*n_kv-1 in qkv column order
+    const int i = rem % half;
+    const TI* src = qkv + (int64_t)r * ld + head * hd + 2 * i;
+    const float e = to_f32(src[0]);
+    const float o = to_f32(src[1]);
+    if (head >= n_heads + n_kv) {  // v: copy
+      const int h = head - n_heads - n_kv;
+      TP* dst = vp + pool_off(layer, h, dst_page[r], dst_slot[r], n_kv, n_pages, page_size, hd) + 2 * i;
+      dst[0] = from_f32<TP>(e);
+      dst[1] = from_f32<TP>(o);
+      continue;
+    }
+    const int64_t t = (int64_t)(pos[r] + max_delta) * half + i;
+    const float c = cos_t[t], s = sin_t[t];
+    const float re = e * c - o * s;
+    const float ro = e * s + o * c;
+    if (head < n_heads) {
+      float* dst = q_out + ((int64_t)r * n_heads + head) * hd + 2 * i;
+      dst[0] = re;
+      dst[1] = ro;
+    } else {
+      const int h = head - n_heads;
+      TP* dst = kp + pool_off(layer, h, dst_page[r], dst_slot[r], n_kv, n_pages, page_size, hd) + 2 * i;
+      dst[0] = from_f32<TP>(re);
+      dst[1] = from_f32<TP>(ro);
+    }
+  }
+}
+
+// ---- K2 ------------------------------------------------------------------------
+// One 16-byte vector (8 bf16 / 4 f32 = 4 / 2 pairs) per thread-iteration, 128-bit
+// loads and stores, grid-stride over (layer, kv head, listed page, slot, vector).
+// Pages with delta == 0 are skipped (reference: zero delta is a bitwise no-op,
+// cache.py:152-153); slots past page_len are not touched.
+template <typename T>
+struct Vec16;
+template <>
+struct Vec16<__nv_bfloat16> {
+  static constexpr int N = 8;
+};
+template <>
+struct Vec16<float> {
+  static constexpr int N = 4;
+};
+
+template <typename T>
+__global__ void rerotate_kernel(T* __restrict__ kp, int n_layers, int n_kv, int n_pages,
+                                int page_size, int hd, const int32_t* __restrict__ pages,
+                                const int32_t* __restrict__ page_len,
+                                const int32_t* __restrict__ delta, int n_list,
+                                const float* __restrict__ cos_t, const float* __restrict__ sin_t,
+                                int max_delta) {
+  constexpr int N = Vec16<T>::N;
+  const int vpr = hd / N;  // vectors per token row
+  const int half = hd >> 1;
+  const int64_t per_page = (int64_t)page_size * vpr;
+  const int64_t total = (int64_t)n_layers * n_kv * n_list * per_page;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lhi = u / per_page;
+    const int in_page = (int)(u % per_page);
+    const int i = (int)(lhi % n_list);
+    const int lh = (int)(lhi / n_list);
+    const int slot = in_page / vpr;
+    const int vec = in_page % vpr;
+    const int dl = delta[i];
+    if (dl == 0 || slot >= page_len[i]) continue;
+    const int layer = lh / n_kv, h = lh % n_kv;
+    T* p = kp + pool_off(layer, h, pages[i], slot, n_kv, n_pages, page_size, hd) + vec * N;
+    uint4 raw = *reinterpret_cast<const uint4*>(p);
+    T* x = reinterpret_cast<T*>(&raw);
+    const int64_t trow = (int64_t)(dl + max_delta) * half + vec * (N / 2);
+#pragma unroll
+    for (int j = 0; j < N / 2; ++j) {
+      const float c = __ldg(cos_t + trow + j), s = __ldg(sin_t + trow + j);
+      const float e = to_f32(x[2 * j]), o = to_f32(x[2 * j + 1]);
+      x[2 * j] = from_f32<T>(e * c - o * s);
+      x[2 * j + 1] = from_f32<T>(e * s + o * c);
+    }
+    *reinterpret_cast<uint4*>(p) = raw;
+  }
+}
+
+static int grid_for(int64_t total, int threads) {
+  int64_t b = (total + threads - 1) / threads;
+  const int64_t cap = 148 * 16;
+  return (int)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+}  // namespace choreo
+
+using namespace choreo;
+
+extern "C" {
+
+int choreo_rope_append(const void* qkv, int qkv_dtype, int ld_qkv, int n_rows,
+                       const int32_t* pos, const int32_t* dst_page, const int32_t* dst_slot,
+                       float* q_out, void* k_pool, void* v_pool, int pool_dtype, int layer,
+                       int n_kv, int n_pages, int page_size, int n_heads, int head_dim,
+                       const float* cos_t, const float* sin_t, int max_delta, void* stream) {
+  if (!qkv || !pos || !dst_page || !dst_slot || !q_out || !k_pool || !v_pool || !cos_t || !sin_t)
+    return CHOREO_EINVAL;
+  if (!dtype_ok(qkv_dtype) || !dtype_ok(pool_dtype) || head_dim < 2 || (head_dim & 1) ||
+      n_kv <= 0 || n_heads % n_kv || ld_qkv < (n_heads + 2 * n_kv) * head_dim)
+    return CHOREO_EINVAL;
+  if (n_rows == 0) return CHOREO_OK;
+  const int64_t total = (int64_t)n_rows * (n_heads + 2 * n_kv) * (head_dim / 2);
+  const int blocks = grid_for(total, 256);
+  auto s = as_stream(stream);
+#define K1(TI, TP)                                                                               \
+  rope_append_kernel<TI, TP><<<blocks, 256, 0, s>>>(                                             \
+      (const TI*)qkv, ld_qkv, n_rows, pos, dst_page, dst_slot, q_out, (TP*)k_pool, (TP*)v_pool, \
+      layer, n_kv, n_pages, page_size, n_heads, head_dim, cos_t, sin_t, max_delta)
+  if (qkv_dtype == CHOREO_F32 && pool_dtype == CHOREO_F32) K1(float, float);
+  else if (qkv_dtype == CHOREO_F32 && pool_dtype == CHOREO_BF16) K1(float, __nv_bfloat16);
+  else if (qkv_dtype == CHOREO_BF16 && pool_dtype == CHOREO_BF16) K1(__nv_bfloat16, __nv_bfloat16);
+  else K1(__nv_bfloat16, float);
+#undef K1
+  return launch_status("choreo_rope_append");
+}
+
+int choreo_rerotate(void* k_pool, int pool_dtype, int n_layers, int n_kv, int n_pages,
+                    int page_size, int head_dim, const int32_t* pages, const int32_t* page_len,
+                    const int32_t* delta, int n_list, const float* cos_t, const float* sin_t,
+                    int max_delta, void* stream) {
+  if (!k_pool || !pages || !page_len || !delta || !cos_t || !sin_t || !dtype_ok(pool_dtype))
+    return CHOREO_EINVAL;
+  const int vec = pool_dtype == CHOREO_BF16 ? 8 : 4;
+  if (head_dim % vec) return CHOREO_EINVAL;
+  if (n_list == 0) return CHOREO_OK;
+  const int64_t total = (int64_t)n_layers * n_kv * n_list * page_size * (head_dim / vec);
+  const int blocks = grid_for(total, 256);
+  auto s = as_stream(stream);
+  if (pool_dtype == CHOREO_BF16)
+    rerotate_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(
+        (__nv_bfloat16*)k_pool, n_layers, n_kv, n_pages, page_size, head_dim, pages, page_len,
+        delta, n_list, cos_t, sin_t, max_delta);
+  else
+    rerotate_kernel<float><<<blocks, 256, 0, s>>>((float*)k_pool, n_layers, n_kv, n_pages,
+                                                  page_size, head_dim, pages, page_len, delta,
+                                                  n_list, cos_t, sin_t, max_delta);
+  return launch_status("choreo_rerotate");
+}
+
+}  // extern "C"

@@ -1,0 +1,426 @@
+"""Drop-in choreography Engine over the device cache (reference engine.py:133-468).
+
+Same public surface and semantics as the reference ``Engine``: ``prefill``,
+``prefill_parallel``, ``decode``, ``decode_parallel``, ``message_text``,
+``message_token_count``, ``generated_token_ids``, ``clone``, ``stats`` /
+``last_stats``, ``kind``, ``seed``, ``config``, ``record_logits`` and a ``cache``
+with the reference's inspection surface.  All validation runs on the host mirror
+before any device work (ids are never burned by a failed call).
+
+What differs is the schedule, never the result:
+* every step is ONE batched forward over all rows of all messages in it
+  (the reference loops over groups, model.py:138-142);
+* a parallel decode encodes all headers in the first step (the reference feeds
+  one header token per step, engine.py:452-455).  Each message's tokens only
+  depend on its own tokens and its parents, so outputs are identical; the
+  reference's physical interleaving is reproduced in the cache's views;
+* greedy selection runs on the device (K6) over the generatable ids.
+CallStats FLOPs follow the reference's analytic accounting per op exactly.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .cache import DeviceKvCache, RotationTableDevice
+from .config import EOS_MSG, ModelConfig
+from .errors import (CapacityError, EmptyHeaderError, InvalidCallError, OffsetConflictError,
+                     UnknownMessageError, WindowOverflowError)
+from .model import CallRows, Runner, StepPlan
+from .tokenizer import decode_tokens, encode_text, frame_header, frame_message, generatable_mask
+from .weights import DeviceWeights, WeightSet
+
+
+@dataclass(frozen=True)
+class SamplingParams:
+    """engine.py:45-69."""
+
+    mode: str = "greedy"
+    temperature: float = 0.7
+    top_p: float = 0.95
+    seed: int = 0
+    max_tokens: int = 64
+
+    def __post_init__(self) -> None:
+        if self.mode not in ("greedy", "temperature"):
+            raise InvalidCallError(f"unknown sampling mode {self.mode!r}")
+        if self.mode == "temperature" and self.temperature <= 0:
+            raise InvalidCallError("temperature must be > 0")
+        if not 0 < self.top_p <= 1:
+            raise InvalidCallError("top_p must be in (0, 1]")
+        if self.max_tokens < 0:
+            raise InvalidCallError("max_tokens must be >= 0")
+
+
+@dataclass(frozen=True)
+class PrefillCall:
+    message: str
+    parents: Sequence[int] = ()
+    offsets: Sequence[int | None] | None = None
+    new_offset: int | None = None
+
+
+@dataclass(frozen=True)
+class DecodeCall:
+    header: str
+    parents: Sequence[int] = ()
+    offsets: Sequence[int | None] | None = None
+    new_offset: int | None = None
+    sampling: SamplingParams = field(default_factory=SamplingParams)
+
+
+@dataclass
+class CallStats:
+    """engine.py:93-106."""
+
+    op: str
+    ids: list
+    prefill_flops: int = 0
+    decode_flops: int = 0
+    tokens_encoded: int = 0
+    cache_hit_tokens: int = 0
+    repositioned_tokens: int = 0
+    ttft: dict = field(default_factory=dict)
+    wall: float = 0.0
+    logits: dict | None = None
+
+
+def encode_flops(config: ModelConfig, t_new: int, ctx: int, rows: str) -> int:
+    """Analytic FLOPs of one group (model.py:218-235), GQA-aware projections."""
+    if t_new == 0:
+        return 0
+    d, L = config.model_dim, config.n_layers
+    nrow = {"all": t_new, "last": 1, "none": 0}[rows]
+    return (L * 2 * t_new * (2 * d * d + 2 * d * config.kv_dim) + L * 4 * t_new * d * (ctx + t_new)
+            + L * 6 * t_new * d * config.ffn_dim + 2 * nrow * d * config.vocab_size)
+
+
+class _Dec:
+    """Per-message decode progress (engine.py:109-130)."""
+
+    __slots__ = ("mid", "call", "hdr", "new_off", "parents", "n_par", "forced", "generated",
+                 "appended", "sel", "done", "finishing", "last_row")
+
+    def __init__(self, mid, call, hdr, new_off, parents, n_par, forced):
+        self.mid, self.call, self.hdr, self.new_off = mid, call, hdr, new_off
+        self.parents, self.n_par, self.forced = parents, n_par, forced
+        self.generated: list[int] = []
+        self.appended = 0
+        self.sel = 0
+        self.done = False
+        self.finishing = False
+        self.last_row = None
+
+
+class Engine:
+    """Cache-choreography engine on one B200: paged global KV cache + sm_100a kernels."""
+
+    kind = "choreo"
+
+    def __init__(self, weights, *, capacity: int = 65536, seed: int = 0,
+                 record_logits: bool = False, dtype=None, device=None, page_size: int = 64) -> None:
+        nat.load()  # fail loudly without the CUDA extension
+        device = torch.device(device or "cuda")
+        if isinstance(weights, WeightSet):
+            dtype = dtype or torch.bfloat16
+            weights = DeviceWeights.from_host(weights, dtype=dtype, device=device)
+        self.weights: DeviceWeights = weights
+        self.config: ModelConfig = weights.config
+        self.seed = int(seed)
+        self.record_logits = record_logits
+        self.device = device
+        self.cache = DeviceKvCache(self.config, capacity=capacity, dtype=weights.torch_dtype,
+                                   device=device, page_size=page_size)
+        self.rotation = RotationTableDevice(self.config, device)
+        self._runner = Runner(self.weights, self.cache, self.rotation)
+        self._generatable = generatable_mask(self.config.vocab_size)
+        self._next_id = 0
+        self.stats: list[CallStats] = []
+
+    # -- public API (engine.py:153-199) ------------------------------------------------
+
+    def prefill(self, call: PrefillCall) -> int:
+        return self._prefill_batch([call], op="prefill")[0]
+
+    def prefill_parallel(self, calls: Sequence[PrefillCall]) -> list[int]:
+        return self._prefill_batch(list(calls), op="prefill_parallel")
+
+    def decode(self, call: DecodeCall, force_tokens=None) -> int:
+        return self._decode_batch([call], [force_tokens], op="decode")[0]
+
+    def decode_parallel(self, calls: Sequence[DecodeCall], force_tokens=None) -> list[int]:
+        forces = list(force_tokens) if force_tokens is not None else [None] * len(calls)
+        if len(forces) != len(calls):
+            raise InvalidCallError("force_tokens length must match calls")
+        return self._decode_batch(list(calls), forces, op="decode_parallel")
+
+    def message_text(self, message_id: int) -> str:
+        return self.cache.message_span(message_id).text
+
+    def message_token_count(self, message_id: int) -> int:
+        return self.cache.message_length(message_id)
+
+    def generated_token_ids(self, message_id: int) -> list[int]:
+        span = self.cache.message_span(message_id)
+        if span.kind != "decoded":
+            raise InvalidCallError(f"message {message_id} was not decoded")
+        return [int(t) for t in span.token_ids[len(frame_header(span.header)):]]
+
+    def clone(self) -> "Engine":
+        other = Engine.__new__(Engine)
+        other.weights, other.config, other.seed = self.weights, self.config, self.seed
+        other.record_logits, other.device = self.record_logits, self.device
+        other.cache = self.cache.clone()
+        other.rotation = self.rotation
+        other._runner = Runner(self.weights, other.cache, self.rotation)
+        other._generatable = self._generatable
+        other._next_id = self._next_id
+        other.stats = []
+        return other
+
+    @property
+    def last_stats(self) -> CallStats:
+        return self.stats[-1]
+
+    @property
+    def kernel_launches(self) -> int:
+        return self._runner.launches
+
+    # -- validation and layout (engine.py:203-258) ---------------------------------------
+
+    def _resolve_calls(self, calls, new_lens):
+        window = self.config.context_window
+        agreed: dict[int, int] = {}
+        layouts = []
+        for call, new_len in zip(calls, new_lens):
+            parents = [int(p) for p in call.parents]
+            if len(set(parents)) != len(parents):
+                raise InvalidCallError(f"duplicate parents {parents}")
+            for p in parents:
+                if p not in self.cache:
+                    raise UnknownMessageError(f"unknown parent id {p}")
+            offsets = list(call.offsets) if call.offsets is not None else [None] * len(parents)
+            if len(offsets) != len(parents):
+                raise InvalidCallError(
+                    f"offsets length {len(offsets)} != parents length {len(parents)}")
+            prev_end = 0
+            for p, off in zip(parents, offsets):
+                o = prev_end if off is None else int(off)
+                if o < 0:
+                    raise InvalidCallError(f"negative offset {o} for parent {p}")
+                plen = self.cache.message_length(p)
+                if o + plen > window:
+                    raise WindowOverflowError(f"parent {p} (len {plen}) does not fit at offset {o}")
+                if p in agreed and agreed[p] != o:
+                    raise OffsetConflictError(
+                        f"parent {p} placed at both {agreed[p]} and {o} in one batch")
+                agreed[p] = o
+                prev_end = o + plen
+            new_off = int(call.new_offset) if call.new_offset is not None else prev_end
+            if new_off < 0:
+                raise InvalidCallError(f"negative new_offset {new_off}")
+            if new_off + new_len > window:
+                raise WindowOverflowError(
+                    f"new message (len {new_len}) does not fit at offset {new_off}")
+            layouts.append((parents, new_off))
+        return agreed, layouts
+
+    def _check_capacity(self, n_tokens: int) -> None:
+        if self.cache.token_count + n_tokens > self.cache.capacity:
+            raise CapacityError(f"{n_tokens} new tokens exceed capacity {self.cache.capacity} "
+                                f"(token_count {self.cache.token_count})")
+
+    def _alloc_id(self) -> int:
+        self._next_id += 1
+        return self._next_id - 1
+
+    def _parent_tokens(self, parents) -> int:
+        return sum(self.cache.message_length(p) for p in parents)
+
+    # -- prefill (engine.py:262-294) --------------------------------------------------------
+
+    def _prefill_batch(self, calls: list, op: str) -> list[int]:
+        t0 = time.perf_counter()
+        if not calls:
+            return []
+        framed = [frame_message(c.message) for c in calls]
+        agreed, layouts = self._resolve_calls(calls, [len(f) for f in framed])
+        self._check_capacity(sum(len(f) for f in framed))
+        stats = CallStats(op=op, ids=[])
+        stats.repositioned_tokens = self.cache.reposition_many(agreed, self.rotation)
+        ids = [self._alloc_id() for _ in calls]
+        stats.ids = ids
+        rows = []
+        for mid, call, toks, (parents, new_off) in zip(ids, calls, framed, layouts):
+            self.cache.register_message(mid, "prefilled", new_off, text=call.message,
+                                        max_tokens=len(toks))
+            n_vis = self._parent_tokens(parents)
+            pages, slots = self.cache.reserve_slots(mid, toks)
+            rows.append(CallRows(mid, parents, 0, toks, pages, slots, new_off))
+            stats.prefill_flops += encode_flops(self.config, len(toks), n_vis, "none")
+            stats.cache_hit_tokens += n_vis
+            stats.tokens_encoded += len(toks)
+        self._runner.forward(StepPlan(rows, np.zeros(0, np.int32)))
+        for mid, toks in zip(ids, framed):
+            self.cache.log_append(mid, 0, len(toks))
+        torch.cuda.current_stream(self.device).synchronize()
+        stats.wall = time.perf_counter() - t0
+        self.stats.append(stats)
+        return ids
+
+    # -- decode (engine.py:298-463) ---------------------------------------------------------
+
+    def _decode_batch(self, calls: list, forces: list, op: str) -> list[int]:
+        t0 = time.perf_counter()
+        if not calls:
+            return []
+        for call in calls:
+            if not call.header:
+                raise EmptyHeaderError("decode header must be non-empty")
+        headers = [frame_header(c.header) for c in calls]
+        agreed, layouts = self._resolve_calls(calls, [len(h) for h in headers])
+        self._check_capacity(sum(len(h) for h in headers))
+        stats = CallStats(op=op, ids=[], logits={} if self.record_logits else None)
+        stats.repositioned_tokens = self.cache.reposition_many(agreed, self.rotation)
+        ids = [self._alloc_id() for _ in calls]
+        stats.ids = ids
+        states = []
+        W = self.config.context_window
+        for mid, call, hdr, force, (parents, new_off) in zip(ids, calls, headers, forces, layouts):
+            cap = min(W - new_off, len(hdr) + call.sampling.max_tokens)
+            self.cache.register_message(mid, "decoded", new_off, header=call.header,
+                                        max_tokens=max(cap, len(hdr)))
+            n_par = self._parent_tokens(parents)
+            forced = list(encode_text(force)) if isinstance(force, str) else (
+                None if force is None else [int(t) for t in force])
+            states.append(_Dec(mid, call, hdr, new_off, parents, n_par, forced))
+            stats.cache_hit_tokens += n_par
+            if self.record_logits:
+                stats.logits[mid] = []
+        lone = len(states) == 1
+        firsts = [self.cache.message_length(s.mid) for s in states]
+        try:
+            self._decode_loop(states, stats, t0, lone)
+        finally:
+            counts = [self.cache.message_length(s.mid) - f for s, f in zip(states, firsts)]
+            if lone:
+                self.cache.log_append(states[0].mid, firsts[0], counts[0])
+            else:
+                self.cache.log_interleaved([s.mid for s in states], firsts, counts)
+            for s in states:
+                self.cache.set_text(s.mid, s.call.header + decode_tokens(s.generated))
+        stats.wall = time.perf_counter() - t0
+        self.stats.append(stats)
+        return ids
+
+    def _decode_loop(self, states: list, stats: CallStats, t0: float, lone: bool) -> None:
+        """Encode pending tokens for all active messages per step, then select.
+
+        Event order per message is the reference's: encode header, select,
+        [encode token, select]*, with the stop rules of engine.py:394-413/448-463.
+        """
+        pending = {s.mid: list(s.hdr) for s in states}
+        while True:
+            active = [s for s in states if not s.done and pending[s.mid]]
+            if not active:
+                return
+            calls, logit_rows, owners, r = [], [], [], 0
+            for s in active:
+                toks = pending[s.mid]
+                self._check_capacity(len(toks))
+                first = s.appended
+                pages, slots = self.cache.reserve_slots(s.mid, toks)
+                calls.append(CallRows(s.mid, s.parents, first, toks, pages, slots, s.new_off))
+                r += len(toks)
+                # FLOP accounting as the reference would have executed it
+                if lone or len(states) == 1:
+                    if first == 0:
+                        stats.decode_flops += encode_flops(self.config, len(toks), s.n_par, "last")
+                    else:
+                        stats.decode_flops += encode_flops(self.config, 1, s.n_par + first, "all")
+                else:
+                    for j in range(len(toks)):
+                        stats.decode_flops += encode_flops(self.config, 1, s.n_par + first + j, "all")
+                stats.tokens_encoded += len(toks)
+                s.appended += len(toks)
+                if not s.finishing:
+                    logit_rows.append(r - 1)
+                    owners.append(s)
+            logits = self._runner.forward(StepPlan(calls, np.asarray(logit_rows, np.int32)))
+            for s in active:
+                pending[s.mid] = []
+                if s.finishing:
+                    s.done = True
+            if not owners:
+                continue
+            greedy_tok = None
+            if any(s.forced is None and s.call.sampling.mode == "greedy" for s in owners):
+                out = torch.empty(len(owners), dtype=torch.int32, device=self.device)
+                nat.select_greedy(logits.data_ptr(), len(owners), logits.shape[1],
+                                  logits.shape[1], out.data_ptr(),
+                                  torch.cuda.current_stream(self.device).cuda_stream)
+                self._runner.launches += 1
+                greedy_tok = out.cpu().numpy()
+            host_logits = None
+            if self.record_logits or any(s.forced is None and s.call.sampling.mode != "greedy"
+                                         for s in owners):
+                host_logits = logits.double().cpu().numpy()
+            else:
+                torch.cuda.current_stream(self.device).synchronize()
+            for i, s in enumerate(owners):
+                if stats.logits is not None:
+                    stats.logits[s.mid].append(host_logits[i].copy())
+                if s.sel == 0:
+                    stats.ttft[s.mid] = time.perf_counter() - t0
+                k = s.sel
+                s.sel += 1
+                if s.forced is not None:
+                    tok = s.forced[k] if k < len(s.forced) else None
+                elif s.call.sampling.mode == "greedy":
+                    tok = int(greedy_tok[i])
+                else:
+                    tok = _sample_nucleus(host_logits[i], self._generatable, s.call.sampling,
+                                          self.seed, s.mid, k)
+                if tok is None or tok == EOS_MSG or not self._may_accept(s):
+                    s.done = True
+                    continue
+                s.generated.append(tok)
+                pending[s.mid] = [tok]
+                if len(s.generated) >= s.call.sampling.max_tokens:
+                    s.finishing = True
+
+    def _may_accept(self, s: _Dec) -> bool:
+        """engine.py:394-399."""
+        if len(s.generated) >= s.call.sampling.max_tokens:
+            return False
+        return s.new_off + s.appended < self.config.context_window
+
+
+def _stream_uniform(engine_seed: int, sampling_seed: int, msg_id: int, sel_index: int) -> float:
+    """Counter-based Philox draw keyed (engine seed, sampling seed) (engine.py:388-392)."""
+    key = np.array([engine_seed & 0xFFFFFFFFFFFFFFFF, sampling_seed & 0xFFFFFFFFFFFFFFFF],
+                   dtype=np.uint64)
+    counter = np.array([sel_index, msg_id, 0, 0], dtype=np.uint64)
+    return np.random.Generator(np.random.Philox(counter=counter, key=key)).random()
+
+
+def _sample_nucleus(logits: np.ndarray, generatable: np.ndarray, params: SamplingParams,
+                    engine_seed: int, msg_id: int, sel_index: int) -> int:
+    """Temperature + top-p over generatable ids, prob-desc / id-asc (engine.py:374-386)."""
+    z = np.where(generatable, logits / params.temperature, -np.inf)
+    z = z - z.max()
+    probs = np.exp(z)
+    probs /= probs.sum()
+    order = np.lexsort((np.arange(len(probs)), -probs))
+    csum = np.cumsum(probs[order])
+    cut = min(int(np.searchsorted(csum, params.top_p, side="left")), len(order) - 1)
+    kept = order[:cut + 1]
+    kcs = np.cumsum(probs[kept] / probs[kept].sum())
+    u = _stream_uniform(engine_seed, params.seed, msg_id, sel_index)
+    return int(kept[min(int(np.searchsorted(kcs, u, side="right")), len(kept) - 1)])

@@ -1,0 +1,198 @@
+"""One forward step over a batch of new-token rows, on the device.
+
+Reference: model.py:126-193 (``forward_step`` / ``_forward_group``).  The
+reference runs one group (message) at a time and never batches across messages;
+here every row of every message in the step goes through one pass:
+
+    embed -> per layer [ residual+RMSNorm -> QKV GEMM -> K1 rope_append (q rotated,
+    K/V written into the message's pages) -> K5 split-KV attention over the
+    K3-assembled page lists -> combine -> O GEMM -> residual+RMSNorm -> gate|up
+    GEMM -> SiLU*up -> down GEMM ] -> final norm on the logit rows -> head GEMM.
+
+New K/V are appended inside the step (before attention), so rows of the same
+message see each other causally through the pool while batch peers — which are
+never in each other's page lists — stay invisible, exactly as the reference's
+mask [ones(T, n_ctx) | tril(T, T)] (model.py:166-168).  Dense projections are
+cuBLAS GEMMs via torch (bf16 in, f32 accumulate); the residual stream is f32.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .cache import DeviceKvCache, RotationTableDevice, cdiv
+from .weights import DeviceWeights
+
+RMS_EPS = 1e-6  # model.py:28
+
+
+@dataclass
+class CallRows:
+    """Rows one message contributes to a step (tokens at consecutive positions)."""
+
+    msg: int
+    parents: list
+    first_t: int  # within-message index of the first new token
+    tokens: list
+    pages: np.ndarray
+    slots: np.ndarray
+    offset: int  # message offset (position of token 0)
+
+
+@dataclass
+class StepPlan:
+    calls: list
+    logit_rows: np.ndarray  # row indices needing logits
+
+    @property
+    def n_rows(self) -> int:
+        return sum(len(c.tokens) for c in self.calls)
+
+
+def plan_counts(calls: list, msg_len: np.ndarray, P: int, rpb: int, ppi: int):
+    """Host replica of K3's sizing (assemble.cu plan_call): (vis pages, items, partials)."""
+    v = it = pa = 0
+    for c in calls:
+        pp = sum(cdiv(int(msg_len[p]), P) for p in c.parents)
+        n = len(c.tokens)
+        if n == 0:
+            continue
+        t = c.first_t + np.arange(n)
+        v += pp + int(t[-1]) // P + 1
+        for b in range(0, n, rpb):
+            nr = min(rpb, n - b)
+            ch = cdiv(pp + int(t[b + nr - 1]) // P + 1, ppi)
+            it += ch
+            pa += ch * nr
+    return v, it, pa
+
+
+class Runner:
+    """Executes StepPlans for one (weights, cache) pair on the current stream."""
+
+    def __init__(self, weights: DeviceWeights, cache: DeviceKvCache,
+                 rotation: RotationTableDevice) -> None:
+        self.w = weights
+        self.cache = cache
+        self.rot = rotation
+        self.cfg = weights.config
+        self.dt = weights.torch_dtype
+        self.dtc = nat.dtype_code(self.dt)
+        self.pool_dtc = nat.dtype_code(cache.dtype)
+        self.dev = cache.device
+        G = self.cfg.n_heads // self.cfg.kv_heads
+        self.rows_per_block = max(1, min(16, 64 // G))
+        self.launches = 0  # our kernels launched (for bench accounting)
+
+    def _mm(self, a, w, out_f32: bool):
+        if out_f32 and a.dtype != torch.float32:
+            return torch.mm(a, w.t(), out_dtype=torch.float32)
+        return torch.mm(a, w.t())
+
+    def forward(self, plan: StepPlan) -> torch.Tensor | None:
+        cfg, cache = self.cfg, self.cache
+        stream = torch.cuda.current_stream(self.dev).cuda_stream
+        R = plan.n_rows
+        H, Hk, hd, d = cfg.n_heads, cfg.kv_heads, cfg.head_dim, cfg.model_dim
+        P = cache.page_size
+        cache.sync_tables()
+
+        # ---- host-side packing of the step description (ints only) ----
+        ids = np.concatenate([np.asarray(c.tokens, np.int32) for c in plan.calls])
+        row_t = np.concatenate([c.first_t + np.arange(len(c.tokens), dtype=np.int32)
+                                for c in plan.calls])
+        pos = np.concatenate([c.offset + c.first_t + np.arange(len(c.tokens), dtype=np.int32)
+                              for c in plan.calls])
+        pages = np.concatenate([np.asarray(c.pages, np.int32) for c in plan.calls])
+        slots = np.concatenate([np.asarray(c.slots, np.int32) for c in plan.calls])
+        call_tab, parents, row_off = [], [], 0
+        for c in plan.calls:
+            call_tab += [c.msg, len(parents), len(c.parents), row_off, len(c.tokens)]
+            parents += list(c.parents)
+            row_off += len(c.tokens)
+        n_calls = len(plan.calls)
+        msg_len = cache.msg_len.host
+        total_pages = sum(
+            (sum(cdiv(int(msg_len[p]), P) for p in c.parents) + (c.first_t + len(c.tokens) - 1) // P + 1)
+            * cdiv(len(c.tokens), self.rows_per_block) for c in plan.calls)
+        target_items = max(1, (4 * 148) // Hk)
+        ppi = max(1, cdiv(total_pages, target_items))
+        n_vis, n_items, n_parts = plan_counts(plan.calls, msg_len, P, self.rows_per_block, ppi)
+        n_log = len(plan.logit_rows)
+
+        ints = np.concatenate([ids, row_t, pos, pages, slots, np.asarray(call_tab, np.int32),
+                               np.asarray(parents + [0], np.int32),
+                               np.asarray(plan.logit_rows, np.int32)])
+        dints = torch.from_numpy(ints).to(self.dev, non_blocking=False)
+        o = 0
+
+        def take(n):
+            nonlocal o
+            t = dints[o:o + n]
+            o += n
+            return t
+
+        ids_d, rowt_d, pos_d, page_d, slot_d = (take(R) for _ in range(5))
+        calls_d = take(5 * n_calls)
+        parents_d = take(len(parents) + 1)
+        logit_d = take(n_log)
+
+        vis = torch.empty(3, max(n_vis, 1), dtype=torch.int32, device=self.dev)
+        items = torch.empty(max(n_items, 1), 6, dtype=torch.int32, device=self.dev)
+        row_part = torch.empty(R, 3, dtype=torch.int32, device=self.dev)
+        counts = torch.empty(4, dtype=torch.int32, device=self.dev)
+        nat.assemble(cache.msg_len.dev.data_ptr(), cache.msg_pt.dev.data_ptr(),
+                     cache.page_table.dev.data_ptr(), calls_d.data_ptr(), parents_d.data_ptr(),
+                     n_calls, rowt_d.data_ptr(), R, None, 0, P, self.rows_per_block, ppi,
+                     vis[0].data_ptr(), vis[1].data_ptr(), vis[2].data_ptr(), items.data_ptr(),
+                     row_part.data_ptr(), counts.data_ptr(), n_vis, n_items, n_parts, stream)
+        self.launches += 1
+
+        x = torch.empty(R, d, dtype=torch.float32, device=self.dev)
+        nat.embed(self.w.embed.data_ptr(), self.dtc, d, ids_d.data_ptr(), R, x.data_ptr(), stream)
+        q = torch.empty(R, H, hd, dtype=torch.float32, device=self.dev)
+        part_o = torch.empty(max(n_parts, 1), H, hd, dtype=torch.float32, device=self.dev)
+        part_lse = torch.empty(max(n_parts, 1), H, dtype=torch.float32, device=self.dev)
+        attn = torch.empty(R, H * hd, dtype=self.dt, device=self.dev)
+        h = torch.empty(R, d, dtype=self.dt, device=self.dev)
+        act = torch.empty(R, cfg.ffn_dim, dtype=self.dt, device=self.dev)
+        delta = None
+        launches = 2
+        for layer, lw in enumerate(self.w.layers):
+            nat.residual_rmsnorm(x.data_ptr(), nat.ptr(delta), nat.F32, lw["attn_norm"].data_ptr(),
+                                 self.dtc, R, d, RMS_EPS, h.data_ptr(), self.dtc, None, 0, stream)
+            qkv = self._mm(h, lw["w_qkv"], out_f32=True)
+            nat.rope_append(qkv.data_ptr(), nat.dtype_code(qkv.dtype), qkv.shape[1], R,
+                            pos_d.data_ptr(), page_d.data_ptr(), slot_d.data_ptr(), q.data_ptr(),
+                            cache.k_pool.data_ptr(), cache.v_pool.data_ptr(), self.pool_dtc, layer,
+                            Hk, cache.n_pages, P, H, hd, self.rot.cos.data_ptr(),
+                            self.rot.sin.data_ptr(), self.rot.max_delta, stream)
+            nat.attn_split(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(),
+                           self.pool_dtc, layer, Hk, cache.n_pages, P, H, hd, rowt_d.data_ptr(),
+                           vis[0].data_ptr(), vis[1].data_ptr(), vis[2].data_ptr(),
+                           items.data_ptr(), counts.data_ptr(), n_items, part_o.data_ptr(),
+                           part_lse.data_ptr(), 0, stream)
+            nat.attn_combine(part_o.data_ptr(), part_lse.data_ptr(), row_part.data_ptr(), R, H,
+                             hd, attn.data_ptr(), self.dtc, stream)
+            ao = self._mm(attn, lw["wo"], out_f32=True)
+            nat.residual_rmsnorm(x.data_ptr(), ao.data_ptr(), nat.F32, lw["ffn_norm"].data_ptr(),
+                                 self.dtc, R, d, RMS_EPS, h.data_ptr(), self.dtc, None, 0, stream)
+            gu = self._mm(h, lw["w_gu"], out_f32=False)
+            nat.silu_mul(gu.data_ptr(), self.dtc, R, cfg.ffn_dim, act.data_ptr(), self.dtc, stream)
+            delta = self._mm(act, lw["w_down"], out_f32=True)
+            launches += 6
+        nat.residual_rmsnorm(x.data_ptr(), delta.data_ptr(), nat.F32, None, 0, R, d, RMS_EPS,
+                             None, 0, None, 0, stream)
+        launches += 1
+        self.launches += launches
+        if n_log == 0:
+            return None
+        xn = torch.empty(n_log, d, dtype=self.dt, device=self.dev)
+        nat.residual_rmsnorm(x.data_ptr(), None, 0, self.w.out_norm.data_ptr(), self.dtc, R, d,
+                             RMS_EPS, xn.data_ptr(), self.dtc, logit_d.data_ptr(), n_log, stream)
+        self.launches += 1
+        return self._mm(xn, self.w.out_head, out_f32=True)

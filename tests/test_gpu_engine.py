@@ -1,0 +1,263 @@
+"""Engine-level parity on the B200: the drop-in Engine against the reference (golden
+vectors recorded from it) and against the CPU oracle run live.
+
+Tolerances (BASELINE.json north_star): f32 variant logits within 1e-4 of the
+reference (f64); bf16 variant logits within 2e-2 with both sides on the same
+bf16-rounded weights; greedy tokens identical on the fixture workflows; page
+tables / positions / physical layout bit-exact.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import choreo_oracle as O  # noqa: E402
+
+import paper_2512_23049_b200 as P  # noqa: E402
+from paper_2512_23049_b200.script import run_script  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+SCRIPTS = sorted(n[:-5] for n in os.listdir(os.path.join(GOLD, "scripts")))
+TOL = {"f32": 1e-4, "bf16": 2e-2}
+
+
+def _load(name):
+    with open(os.path.join(GOLD, name)) as fh:
+        return json.load(fh)
+
+
+PINS = _load("ref_pins.json")
+RUNS = {v: _load(f"ref_runs_{v}.json") for v in ("f64", "bf16")}
+LOGITS = {v: np.load(os.path.join(GOLD, f"ref_logits_{v}.npz")) for v in ("f64", "bf16")}
+
+
+def _host_weights(variant):
+    w = P.init_weights(P.DEFAULT_CONFIG)
+    return w if variant == "f64" else w.rounded("bf16")
+
+
+_DEV_W = {}
+
+
+def _engine(mode, **kw):
+    """mode f32: reference f64 weights held in f32; mode bf16: bf16-rounded weights."""
+    if mode not in _DEV_W:
+        variant = "f64" if mode == "f32" else "bf16"
+        dt = torch.float32 if mode == "f32" else torch.bfloat16
+        _DEV_W[mode] = P.DeviceWeights.from_host(_host_weights(variant), dtype=dt)
+    return P.Engine(_DEV_W[mode], **kw)
+
+
+def _variant(mode):
+    return "f64" if mode == "f32" else "bf16"
+
+
+@pytest.mark.parametrize("mode", ["f32", "bf16"])
+@pytest.mark.parametrize("script", SCRIPTS)
+def test_fixture_script_teacher_forced_logits(mode, script):
+    """Replay each fixture script forced to the reference's tokens; compare every
+    selection's logits and all trace accounting."""
+    want = RUNS[_variant(mode)][script]
+    forcing = {m["name"]: m["generated"] for s in want["steps"] for m in s["messages"]
+               if m["generated"] is not None}
+    eng = _engine(mode, record_logits=True)
+    trace = run_script(eng, _load(f"scripts/{script}.json"), force=forcing)
+    worst = 0.0
+    for got, ws in zip(trace.steps, want["steps"], strict=True):
+        for key in ("prefill_flops", "decode_flops", "tokens_encoded", "cache_hit_tokens",
+                    "repositioned_tokens"):
+            assert getattr(got, key) == ws[key], (got.name, key)
+        for gm, wm in zip(got.messages, ws["messages"], strict=True):
+            assert (gm.message_id, gm.generated, gm.text, gm.token_count) == \
+                (wm["id"], wm["generated"], wm["text"], wm["tokens"])
+        for name, rows in (got.logits or {}).items():
+            ref = LOGITS[_variant(mode)][f"{script}/{name}"]
+            assert len(rows) == len(ref)
+            worst = max(worst, float(np.abs(np.stack(rows) - ref).max()))
+    assert worst <= TOL[mode], f"max |dlogit| {worst:.3e}"
+    n = eng.cache.token_count
+    assert eng.cache.msg_ids[:n].tolist() == want["msg_ids"]
+    assert eng.cache.positions[:n].tolist() == want["positions"]
+    assert eng.cache.token_ids[:n].tolist() == want["token_ids"]
+
+
+@pytest.mark.parametrize("mode", ["f32", "bf16"])
+@pytest.mark.parametrize("script", SCRIPTS)
+def test_fixture_script_free_run_greedy_tokens(mode, script):
+    want = RUNS[_variant(mode)][script]
+    trace = run_script(_engine(mode), _load(f"scripts/{script}.json"))
+    got = [m.generated for s in trace.steps for m in s.messages]
+    ref = [m["generated"] for s in want["steps"] for m in s["messages"]]
+    assert got == ref
+
+
+@pytest.mark.parametrize("mode", ["f32", "bf16"])
+def test_c1_choreography(mode):
+    """Config C1: reordered subset [C, A] with a gap of 5 and A moved by +37."""
+    want = RUNS[_variant(mode)]["C1"]
+    ref_logits = LOGITS[_variant(mode)]["C1/answer"]
+    eng = _engine(mode, record_logits=True)
+    t = PINS["c1_texts"]
+    a = eng.prefill(P.PrefillCall(t["A"]))
+    b = eng.prefill(P.PrefillCall(t["B"]))
+    c = eng.prefill(P.PrefillCall(t["C"]))
+    m = eng.decode(P.DecodeCall("Answer:", parents=[c, a], offsets=[0, 37],
+                                sampling=P.SamplingParams(max_tokens=16)))
+    assert [a, b, c, m] == want["ids"]
+    assert eng.generated_token_ids(m) == want["generated"]
+    assert eng.last_stats.repositioned_tokens == want["repositioned"]
+    n = eng.cache.token_count
+    assert eng.cache.positions[:n].tolist() == want["positions"]
+    assert eng.cache.msg_ids[:n].tolist() == want["msg_ids"]
+    got = np.stack(eng.last_stats.logits[m])
+    assert float(np.abs(got - ref_logits).max()) <= TOL[mode]
+
+
+def _small(mode, **kw):
+    cfg = P.ModelConfig(n_layers=2, n_heads=2, head_dim=8, ffn_dim=64, vocab_size=512,
+                        context_window=256)
+    ws = P.init_weights(cfg)
+    dt = torch.float32 if mode == "f32" else torch.bfloat16
+    return P.Engine(P.DeviceWeights.from_host(ws, dtype=dt), capacity=4096, **kw)
+
+
+def _phys(e):
+    return [int(e.cache.msg_ids[i]) for i in range(e.cache.token_count)]
+
+
+def test_interleaving_with_early_dropout():
+    e = _small("f32")
+    m0, m1 = e.decode_parallel([P.DecodeCall("A"), P.DecodeCall("B")],
+                               force_tokens=[[10, 11], [20, 21, 22, 23, 24]])
+    assert _phys(e) == [m0, m1, m0, m1, m0, m1, m0, m1, m1, m1, m1]
+    assert e.generated_token_ids(m0) == [10, 11]
+    assert e.generated_token_ids(m1) == [20, 21, 22, 23, 24]
+
+
+def test_offsets_and_reposition_positions():
+    e = _small("f32")
+    a = e.prefill(P.PrefillCall("ab"))
+    b = e.prefill(P.PrefillCall("x", parents=[a], offsets=[5]))
+    pos = lambda m: [int(e.cache.positions[i]) for i in range(e.cache.token_count)  # noqa: E731
+                     if e.cache.msg_ids[i] == m]
+    assert pos(a) == [5, 6, 7, 8] and pos(b) == [9, 10, 11]
+    assert e.last_stats.repositioned_tokens == 4
+    c = e.decode(P.DecodeCall("Q", parents=[a, b], sampling=P.SamplingParams(max_tokens=0)))
+    assert pos(a) == [0, 1, 2, 3] and pos(b) == [4, 5, 6] and pos(c) == [7, 8]
+
+
+@pytest.mark.parametrize("exc,mk", [
+    (P.EmptyHeaderError, lambda a: P.DecodeCall("", parents=[a])),
+    (P.UnknownMessageError, lambda a: P.DecodeCall("Q", parents=[a, 99])),
+    (P.InvalidCallError, lambda a: P.DecodeCall("Q", parents=[a, a])),
+    (P.InvalidCallError, lambda a: P.DecodeCall("Q", parents=[a], offsets=[0, 1])),
+    (P.InvalidCallError, lambda a: P.DecodeCall("Q", parents=[a], offsets=[-2])),
+    (P.InvalidCallError, lambda a: P.DecodeCall("Q", parents=[a], new_offset=-1)),
+    (P.WindowOverflowError, lambda a: P.DecodeCall("Q", parents=[a], offsets=[250])),
+])
+def test_error_contract_leaves_cache_unchanged(exc, mk):
+    e = _small("f32")
+    a = e.prefill(P.PrefillCall("seed text"))
+    before = (e.cache.token_count, e._next_id, len(e.stats), e.cache.positions.tolist())
+    k_before = e.cache.keys.copy()
+    with pytest.raises(exc):
+        e.decode(mk(a))
+    assert (e.cache.token_count, e._next_id, len(e.stats), e.cache.positions.tolist()) == before
+    np.testing.assert_array_equal(e.cache.keys, k_before)
+    assert e.prefill(P.PrefillCall("next")) == a + 1
+
+
+def test_offset_conflict_and_capacity():
+    e = _small("f32")
+    a = e.prefill(P.PrefillCall("sys"))
+    with pytest.raises(P.OffsetConflictError):
+        e.decode_parallel([P.DecodeCall("A", parents=[a], offsets=[0]),
+                           P.DecodeCall("B", parents=[a], offsets=[3])])
+    cfg = e.config
+    small = P.Engine(P.DeviceWeights.from_host(P.init_weights(cfg), dtype=torch.float32), capacity=8)
+    small.prefill(P.PrefillCall("abcd"))
+    with pytest.raises(P.CapacityError):
+        small.prefill(P.PrefillCall("efg"))
+    assert small.cache.token_count == 6
+
+
+def test_forced_eos_and_window_edge():
+    e = _small("f32")
+    m = e.decode(P.DecodeCall("H"), force_tokens=[65, P.EOS_MSG, 66])
+    assert e.generated_token_ids(m) == [65]
+    W = e.config.context_window
+    m2 = e.decode(P.DecodeCall("A", new_offset=W - 2))
+    assert e.generated_token_ids(m2) == [] and e.message_token_count(m2) == 2
+    m3 = e.decode(P.DecodeCall("Hdr", sampling=P.SamplingParams(max_tokens=0)))
+    assert e.generated_token_ids(m3) == []
+
+
+@pytest.mark.parametrize("mode", ["f32", "bf16"])
+@pytest.mark.parametrize("sampling", [
+    P.SamplingParams(mode="greedy", max_tokens=8),
+    P.SamplingParams(mode="temperature", temperature=0.9, top_p=0.9, seed=7, max_tokens=8)])
+def test_parallel_matches_lone(mode, sampling):
+    e = _small(mode, record_logits=True)
+    a = e.prefill(P.PrefillCall("first parent text"))
+    b = e.prefill(P.PrefillCall("second parent text"))
+    calls = [P.DecodeCall("Ans A:", parents=[a], sampling=sampling),
+             P.DecodeCall("Ans B:", parents=[b, a], offsets=[0, 40], sampling=sampling)]
+    par, seq = e.clone(), e.clone()
+    ids_par = par.decode_parallel(calls)
+    lp = par.last_stats.logits
+    ids_seq = [seq.decode(c) for c in calls]
+    assert ids_par == ids_seq
+    for i, mid in enumerate(ids_par):
+        assert par.generated_token_ids(mid) == seq.generated_token_ids(mid)
+        ls = seq.stats[i].logits[mid]
+        assert len(ls) == len(lp[mid])
+        err = max(float(np.abs(x - y).max()) for x, y in zip(lp[mid], ls))
+        assert err <= (1e-4 if mode == "f32" else 2e-2)
+
+
+def test_gqa_engine_matches_oracle_live():
+    """GQA (n_kv_heads < n_heads) has no reference; the oracle's GQA restatement
+    (which reduces exactly to the reference at Hkv == H) is the checker."""
+    shape = O.Shape(n_layers=2, n_heads=8, n_kv_heads=2, head_dim=16, ffn_dim=96, vocab_size=300,
+                    context_window=512, rope_base=500000.0)
+    cfg = P.ModelConfig(**{k: getattr(shape, k) for k in shape.__dataclass_fields__})
+    ow = O.init_weights(shape)
+    ws = P.init_weights(cfg)
+    np.testing.assert_array_equal(ws.layers[1].wk, ow["layers"][1]["wk"])
+    ref = O.Oracle(O.round_weights(ow, "f32"), shape, record_logits=True)
+    eng = P.Engine(P.DeviceWeights.from_host(ws, dtype=torch.float32), record_logits=True)
+    for e, mk_p, mk_d in ((ref, lambda **k: k, lambda **k: k),
+                          (eng, lambda **k: P.PrefillCall(**k), lambda **k: P.DecodeCall(**k))):
+        x = e.prefill(mk_p(message="a long enough parent message " * 3))
+        y = e.prefill(mk_p(message="second message", parents=[x]))
+        sp = O.Sampling(max_tokens=12) if e is ref else P.SamplingParams(max_tokens=12)
+        calls = [mk_d(header="Q1:", parents=[y, x], offsets=[0, 30], sampling=sp),
+                 mk_d(header="Q2 longer:", parents=[x], offsets=[30], new_offset=200, sampling=sp)]
+        (e.decode_batch if e is ref else e.decode_parallel)(calls)
+    for m in (2, 3):
+        assert ref.generated(m) == eng.generated_token_ids(m)
+        got = np.stack(eng.stats[-1].logits[m])
+        want = np.stack(ref.stats[-1].logits[m])
+        assert float(np.abs(got - want).max()) <= 1e-4
+
+
+def test_keys_views_match_oracle_after_moves():
+    """Compat K/V views (physical order) equal the oracle's cache after repositions."""
+    shape = O.SMALL
+    ref = O.Oracle(O.round_weights(O.init_weights(shape), "f32"), shape)
+    eng = _small("f32")
+    for e in (ref, eng):
+        call = (lambda **k: k) if e is ref else (lambda **k: P.PrefillCall(**k))
+        a = e.prefill(call(message="alpha beta"))
+        e.prefill(call(message="gamma", parents=[a], offsets=[17]))
+        e.prefill(call(message="delta", parents=[a], offsets=[3], new_offset=40))
+    n = eng.cache.token_count
+    np.testing.assert_allclose(eng.cache.keys, ref.store.K[:, :n], rtol=1e-5, atol=1e-5)
+    np.testing.assert_allclose(eng.cache.values, ref.store.V[:, :n], rtol=1e-5, atol=1e-5)
+    assert eng.cache.positions.tolist() == ref.store.pos[:n].tolist()

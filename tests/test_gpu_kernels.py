@@ -1,0 +1,262 @@
+"""Kernel-level parity of the sm_100a C-ABI library against the CPU oracle (GPU).
+
+Index math (pages, slots, positions, visible sets) is checked bit-exact; values
+within dtype tolerance (f32: 1e-5 relative; bf16: one bf16 rounding).
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import choreo_oracle as O  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+from paper_2512_23049_b200 import _native as nat  # noqa: E402
+from paper_2512_23049_b200.cache import DeviceKvCache, RotationTableDevice  # noqa: E402
+from paper_2512_23049_b200.config import ModelConfig  # noqa: E402
+
+DT = {"f32": torch.float32, "bf16": torch.bfloat16}
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _bf16_round(a: np.ndarray) -> np.ndarray:
+    return torch.from_numpy(np.asarray(a, np.float32)).to(torch.bfloat16).float().numpy()
+
+
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+@pytest.mark.parametrize("hd,H,Hk", [(16, 4, 4), (128, 32, 8), (64, 8, 2)])
+def test_rope_append(dt, hd, H, Hk):
+    cfg = ModelConfig(n_layers=2, n_heads=H, n_kv_heads=Hk, head_dim=hd, ffn_dim=32,
+                      vocab_size=300, context_window=4096, rope_base=500000.0)
+    rot = RotationTableDevice(cfg, "cuda")
+    orot = O.Rotor(O.Shape(head_dim=hd, context_window=4096, rope_base=500000.0))
+    rng = np.random.default_rng(0)
+    R, n_pages, P = 37, 5, 64
+    qkv = rng.standard_normal((R, (H + 2 * Hk) * hd)).astype(np.float32)
+    pos = rng.integers(0, 4096, R).astype(np.int32)
+    flat = rng.permutation(n_pages * P)[:R]
+    page, slot = (flat // P).astype(np.int32), (flat % P).astype(np.int32)
+    kp = torch.zeros(2, Hk, n_pages, P, hd, dtype=DT[dt], device="cuda")
+    vp = torch.zeros_like(kp)
+    q = torch.empty(R, H, hd, device="cuda")
+    d = {k: torch.from_numpy(v).cuda() for k, v in dict(qkv=qkv, pos=pos, page=page, slot=slot).items()}
+    nat.rope_append(d["qkv"].data_ptr(), nat.F32, qkv.shape[1], R, d["pos"].data_ptr(),
+                    d["page"].data_ptr(), d["slot"].data_ptr(), q.data_ptr(), kp.data_ptr(),
+                    vp.data_ptr(), nat.dtype_code(DT[dt]), 1, Hk, n_pages, P, H, hd,
+                    rot.cos.data_ptr(), rot.sin.data_ptr(), rot.max_delta, _stream())
+    torch.cuda.synchronize()
+    x = qkv.astype(np.float64)
+    q_ref = orot.by_position(x[:, :H * hd].reshape(R, H, hd), pos)
+    k_ref = orot.by_position(x[:, H * hd:(H + Hk) * hd].reshape(R, Hk, hd), pos)
+    v_ref = x[:, (H + Hk) * hd:].reshape(R, Hk, hd)
+    np.testing.assert_allclose(q.cpu().numpy(), q_ref, rtol=1e-5, atol=1e-5)
+    k_got = kp[1].permute(1, 2, 0, 3).float().cpu().numpy()[page, slot]  # (R, Hk, hd)
+    v_got = vp[1].permute(1, 2, 0, 3).float().cpu().numpy()[page, slot]
+    tol = dict(rtol=1e-5, atol=1e-5) if dt == "f32" else dict(rtol=2 ** -8, atol=1e-6)
+    np.testing.assert_allclose(k_got, k_ref, **tol)
+    np.testing.assert_allclose(v_got, v_ref, **tol)
+    assert kp[0].abs().sum().item() == 0  # other layers untouched
+
+
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+@pytest.mark.parametrize("hd", [8, 16, 128])
+def test_rerotate(dt, hd):
+    W = 2048
+    cfg = ModelConfig(n_layers=3, n_heads=2, head_dim=hd, context_window=W)
+    rot = RotationTableDevice(cfg, "cuda")
+    orot = O.Rotor(O.Shape(head_dim=hd, context_window=W))
+    rng = np.random.default_rng(1)
+    L, Hk, n_pages, P = 3, 2, 9, 64
+    pool = rng.standard_normal((L, Hk, n_pages, P, hd)).astype(np.float32)
+    if dt == "bf16":
+        pool = _bf16_round(pool)
+    kp = torch.from_numpy(pool).to(DT[dt]).cuda()
+    pages = np.array([7, 2, 4, 0], np.int32)
+    lens = np.array([64, 13, 1, 64], np.int32)
+    deltas = np.array([37, -W, 0, W], np.int32)
+    arr = torch.from_numpy(np.stack([pages, lens, deltas])).cuda()
+    nat.rerotate(kp.data_ptr(), nat.dtype_code(DT[dt]), L, Hk, n_pages, P, hd, arr[0].data_ptr(),
+                 arr[1].data_ptr(), arr[2].data_ptr(), 4, rot.cos.data_ptr(), rot.sin.data_ptr(),
+                 W, _stream())
+    got = kp.float().cpu().numpy()
+    want = pool.astype(np.float64).copy()
+    for pg, ln, dl in zip(pages, lens, deltas):
+        want[:, :, pg, :ln] = orot.by_delta(want[:, :, pg, :ln], int(dl))
+    tol = dict(rtol=1e-5, atol=1e-5) if dt == "f32" else dict(rtol=2 ** -8, atol=1e-6)
+    np.testing.assert_allclose(got, want, **tol)
+    # untouched: slots past page_len, unlisted pages, delta == 0 page (bitwise)
+    np.testing.assert_array_equal(got[:, :, 2, 13:], pool[:, :, 2, 13:])
+    np.testing.assert_array_equal(got[:, :, [1, 3, 5, 6, 8]], pool[:, :, [1, 3, 5, 6, 8]])
+    np.testing.assert_array_equal(got[:, :, 4], pool[:, :, 4])
+
+
+def test_select_greedy_ties_and_mask():
+    rng = np.random.default_rng(2)
+    V = 512
+    logits = rng.standard_normal((9, V)).astype(np.float32)
+    logits[0, 256] = 100.0       # BOS is not generatable
+    logits[1, 300] = 100.0       # nor reserved/vocab tail
+    logits[2, [5, 9, 200]] = 7.0  # tie -> lowest id
+    logits[3, 257] = 50.0        # EOS is generatable
+    d = torch.from_numpy(logits).cuda()
+    out = torch.empty(9, dtype=torch.int32, device="cuda")
+    nat.select_greedy(d.data_ptr(), 9, V, V, out.data_ptr(), _stream())
+    mask = O.sampler_mask(V)
+    want = [int(np.argmax(np.where(mask, r.astype(np.float64), -np.inf))) for r in logits]
+    assert out.cpu().tolist() == want
+    assert want[2] == 5 and want[3] == 257
+
+
+def _random_cache(cfg, rng, n_msgs, P=64, dtype=torch.float32):
+    cache = DeviceKvCache(cfg, capacity=1 << 16, dtype=dtype, device="cuda", page_size=P)
+    lens = rng.integers(1, 3 * P, n_msgs)
+    for m, n in enumerate(lens):
+        cache.register_message(m, "prefilled", 0, max_tokens=int(n))
+        cache.reserve_slots(m, [1] * int(n))
+        cache.log_append(m, 0, int(n))
+    cache.k_pool.copy_(torch.randn_like(cache.k_pool))
+    cache.v_pool.copy_(torch.randn_like(cache.v_pool))
+    return cache, lens
+
+
+def _assemble(cache, calls, rpb, ppi):
+    """calls: list of (own msg, parents, row_t list).  Returns host copies of K3 outputs."""
+    from paper_2512_23049_b200.model import plan_counts, CallRows
+    tab, par, row_t, off = [], [], [], 0
+    for own, parents, ts in calls:
+        tab += [own, len(par), len(parents), off, len(ts)]
+        par += parents
+        row_t += ts
+        off += len(ts)
+    cr = [CallRows(own, parents, ts[0], [0] * len(ts), None, None, 0) for own, parents, ts in calls]
+    n_vis, n_items, n_parts = plan_counts(cr, cache.msg_len.host, cache.page_size, rpb, ppi)
+    cache.sync_tables()
+    dev = lambda a: torch.tensor(a, dtype=torch.int32, device="cuda")  # noqa: E731
+    tab_d, par_d, rt_d = dev(tab), dev(par + [0]), dev(row_t)
+    vis = torch.full((3, max(n_vis, 1)), -7, dtype=torch.int32, device="cuda")
+    items = torch.full((max(n_items, 1), 6), -7, dtype=torch.int32, device="cuda")
+    row_part = torch.empty(len(row_t), 3, dtype=torch.int32, device="cuda")
+    counts = torch.empty(4, dtype=torch.int32, device="cuda")
+    nat.assemble(cache.msg_len.dev.data_ptr(), cache.msg_pt.dev.data_ptr(),
+                 cache.page_table.dev.data_ptr(), tab_d.data_ptr(), par_d.data_ptr(), len(calls),
+                 rt_d.data_ptr(), len(row_t), None, 0, cache.page_size, rpb, ppi,
+                 vis[0].data_ptr(), vis[1].data_ptr(), vis[2].data_ptr(), items.data_ptr(),
+                 row_part.data_ptr(), counts.data_ptr(), n_vis, n_items, n_parts, _stream())
+    out = dict(vis=vis.cpu().numpy(), items=items.cpu().numpy(), row_part=row_part.cpu().numpy(),
+               counts=counts.cpu().numpy(), row_t=np.asarray(row_t), plan=(n_vis, n_items, n_parts))
+    return out, (rt_d, vis, items, row_part, counts)
+
+
+def _expand_rows(cache, out, n_rows):
+    """Token-level (msg, idx) visible sets per row, from K3 items; checks no duplicates."""
+    page_owner = {}
+    for m, e in cache._messages.items():
+        for i, pg in enumerate(e.pages):
+            page_owner[pg] = (m, i)
+    P = cache.page_size
+    sets = [[] for _ in range(n_rows)]
+    for it in out["items"][:out["counts"][1]]:
+        r0, nr, vb, nv = it[:4]
+        for r in range(r0, r0 + nr):
+            t = out["row_t"][r]
+            for k in range(vb, vb + nv):
+                pg, ln, own = out["vis"][:, k]
+                m, pi = page_owner[int(pg)]
+                for s in range(ln):
+                    if own < 0 or own + s <= t:
+                        sets[r].append((m, pi * P + s))
+    for s in sets:
+        assert len(s) == len(set(s)), "a token is covered twice"
+    return [sorted(s) for s in sets]
+
+
+@pytest.mark.parametrize("rpb,ppi", [(1, 1), (4, 3), (16, 1000)])
+def test_assemble_visible_sets_match_oracle(rpb, ppi):
+    rng = np.random.default_rng(3)
+    cfg = ModelConfig(n_layers=1, n_heads=2, head_dim=8)
+    cache, lens = _random_cache(cfg, rng, 12)
+    calls = []
+    nxt = 12
+    for c in range(5):
+        parents = [int(p) for p in rng.permutation(12)[:rng.integers(0, 6)]]
+        own = nxt
+        nxt += 1
+        n_new = int(rng.integers(1, 150))
+        pre = int(rng.integers(0, 70)) if c % 2 else 0  # tokens already cached for own msg
+        cache.register_message(own, "decoded", 0)
+        cache.reserve_slots(own, [1] * (pre + n_new))
+        cache.log_append(own, 0, pre + n_new)
+        calls.append((own, parents, list(range(pre, pre + n_new))))
+    out, _ = _assemble(cache, calls, rpb, ppi)
+    assert out["counts"][3] == 0
+    assert tuple(out["counts"][:3]) == out["plan"]
+    sets = _expand_rows(cache, out, len(out["row_t"]))
+    # oracle: reference visibility over the physical store
+    st = O.Store(O.Shape(n_layers=1, n_heads=2, head_dim=8), 1 << 16)
+    for m, e in sorted(cache._messages.items()):
+        st.msgs[m] = O.Msg(e.kind, 0, "", None)
+        z = np.zeros((1, len(e.tokens), 2, 8))
+        st.append(m, e.tokens, np.arange(len(e.tokens)), z, z)
+    r = 0
+    for own, parents, ts in calls:
+        for t in ts:
+            vis = st.visible(own, parents)
+            want = sorted((int(st.mid[i]), int(st.pos[i])) for i in vis
+                          if st.mid[i] != own or st.pos[i] <= t)
+            assert sets[r] == want, f"row {r}"
+            r += 1
+
+
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+@pytest.mark.parametrize("hd,H,Hk", [(16, 4, 4), (128, 32, 8), (64, 8, 1)])
+def test_attention_matches_dense_reference(dt, hd, H, Hk):
+    rng = np.random.default_rng(4)
+    cfg = ModelConfig(n_layers=2, n_heads=H, n_kv_heads=Hk, head_dim=hd)
+    cache, lens = _random_cache(cfg, rng, 8, dtype=DT[dt])
+    own = 8
+    cache.register_message(own, "decoded", 0)
+    cache.reserve_slots(own, [1] * 90)
+    cache.log_append(own, 0, 90)
+    cache.k_pool.copy_(torch.randn_like(cache.k_pool))
+    cache.v_pool.copy_(torch.randn_like(cache.v_pool))
+    calls = [(own, [3, 1, 6], list(range(60, 90))), (7, [], [int(lens[7]) - 1])]
+    G = H // Hk
+    rpb = max(1, min(16, 64 // G))
+    out, (rt_d, vis, items, row_part, counts) = _assemble(cache, calls, rpb, 2)
+    R = len(out["row_t"])
+    q = torch.randn(R, H, hd, device="cuda")
+    n_parts = out["plan"][2]
+    part_o = torch.empty(n_parts, H, hd, device="cuda")
+    part_lse = torch.empty(n_parts, H, device="cuda")
+    o = torch.empty(R, H * hd, dtype=torch.float32, device="cuda")
+    L = 1
+    nat.attn_split(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(),
+                   nat.dtype_code(DT[dt]), L, Hk, cache.n_pages, cache.page_size, H, hd,
+                   rt_d.data_ptr(), vis[0].data_ptr(), vis[1].data_ptr(), vis[2].data_ptr(),
+                   items.data_ptr(), counts.data_ptr(), out["plan"][1], part_o.data_ptr(),
+                   part_lse.data_ptr(), 0, _stream())
+    nat.attn_combine(part_o.data_ptr(), part_lse.data_ptr(), row_part.data_ptr(), R, H, hd,
+                     o.data_ptr(), nat.F32, _stream())
+    torch.cuda.synchronize()
+    sets = _expand_rows(cache, out, R)
+    K = cache.k_pool[L].float().cpu().numpy().astype(np.float64)  # (Hk, pages, P, hd)
+    V = cache.v_pool[L].float().cpu().numpy().astype(np.float64)
+    qn = q.cpu().numpy().astype(np.float64)
+    P = cache.page_size
+    got = o.cpu().numpy().reshape(R, H, hd)
+    for r in range(R):
+        toks = sets[r]
+        pg = np.array([cache._messages[m].pages[i // P] for m, i in toks])
+        sl = np.array([i % P for m, i in toks])
+        for h in range(H):
+            kh = h // G
+            kk, vv = K[kh, pg, sl], V[kh, pg, sl]
+            s = kk @ qn[r, h] / np.sqrt(hd)
+            p = np.exp(s - s.max())
+            p /= p.sum()
+            np.testing.assert_allclose(got[r, h], p @ vv, rtol=1e-4, atol=1e-4)
