@@ -47,19 +47,28 @@ const char* choreo_last_error(void);
 int choreo_embed(const void* embed, int embed_dtype, int d, const int32_t* ids, int n_rows,
                  float* x, void* stream);
 
-/* Pre-norm residual step: if delta != NULL, x += delta (f32 residual stream);
- * out = x / sqrt(mean(x^2) + eps) * w, written in out_dtype.
- * Replaces model.py:171,185-186,189 (residual adds + tensor.py:78-80 rms_norm).
- * row_map (optional, may be NULL): out row i normalises x row row_map[i] and
- * skips the residual add (used to pick logit rows). */
-int choreo_residual_rmsnorm(float* x, const void* delta, int delta_dtype, const void* w,
-                            int w_dtype, int n_rows, int d, float eps, void* out, int out_dtype,
-                            const int32_t* row_map, int n_out, void* stream);
+/* Split activations ("*_split" flags): a bf16 activation row y is emitted as the pair
+ * hi = bf16(y) at row r and lo = bf16(y - hi) at row n + r of a stacked [2n][.] buffer;
+ * a bf16 GEMM over the 2n rows then a sum of the two output halves sees y with ~16
+ * mantissa bits.  Consumers of such a stacked f32 GEMM output take *_split = 1 and
+ * add rows r and n + r.  Decode GEMMs are weight-bandwidth bound, so the extra rows
+ * are free there. */
+
+/* Pre-norm residual step: if delta != NULL, x += delta (f32 residual stream; with
+ * delta_split, delta rows r and n_rows + r are both added);
+ * out = x / sqrt(mean(x^2) + eps) * w, written in out_dtype (hi/lo pair if out_split).
+ * out == NULL: residual add only.  row_map (optional): out row i normalises x row
+ * row_map[i], no residual add (used to pick logit rows).
+ * Replaces model.py:171,185-186,189 (residual adds + tensor.py:78-80 rms_norm). */
+int choreo_residual_rmsnorm(float* x, const void* delta, int delta_dtype, int delta_split,
+                            const void* w, int w_dtype, int n_rows, int d, float eps, void* out,
+                            int out_dtype, int out_split, const int32_t* row_map, int n_out,
+                            void* stream);
 
 /* out[r, i] = silu(gu[r, i]) * gu[r, f + i]  (gate | up concatenated).
  * Replaces model.py:187 and tensor.py:83-84. */
-int choreo_silu_mul(const void* gu, int gu_dtype, int n_rows, int f, void* out, int out_dtype,
-                    void* stream);
+int choreo_silu_mul(const void* gu, int gu_dtype, int in_split, int n_rows, int f, void* out,
+                    int out_dtype, int out_split, void* stream);
 
 /* K1 rope_append: for each new-token row r at logical position pos[r],
  *   q_out[r, h, :]   = rotate(qkv[r, q_h], pos[r])           (f32)
@@ -69,7 +78,7 @@ int choreo_silu_mul(const void* gu, int gu_dtype, int n_rows, int f, void* out, 
  * Rotation is the reference's interleaved-pair RoPE read from the f64-derived
  * table cos/sin[(pos + W) * (hd/2) + i] (tensor.py:87-143).
  * Replaces model.py:172-176 + cache.py:98-135 (append_tokens) fused. */
-int choreo_rope_append(const void* qkv, int qkv_dtype, int ld_qkv, int n_rows,
+int choreo_rope_append(const void* qkv, int qkv_dtype, int ld_qkv, int n_rows, int qkv_split,
                        const int32_t* pos, const int32_t* dst_page, const int32_t* dst_slot,
                        float* q_out, void* k_pool, void* v_pool, int pool_dtype, int layer,
                        int n_kv, int n_pages, int page_size, int n_heads, int head_dim,
@@ -121,15 +130,16 @@ int choreo_attn_split(const float* q, const void* k_pool, const void* v_pool, in
                       int max_items, float* part_o, float* part_lse, int grid_ctas,
                       void* stream);
 
-/* Combine partials into out[r][h][:] (out_dtype) with the LSE merge. */
+/* Combine partials into out[r][h][:] (out_dtype; hi/lo pair if out_split) with the
+ * LSE merge. */
 int choreo_attn_combine(const float* part_o, const float* part_lse, const int32_t* row_part,
                         int n_rows, int n_heads, int head_dim, void* out, int out_dtype,
-                        void* stream);
+                        int out_split, void* stream);
 
 /* K6 select: greedy argmax over generatable ids {0..255, 257} with first-index
  * tie-break, one row per logits row (engine.py:371, tokenizer.py:39-44). */
-int choreo_select_greedy(const float* logits, int n_rows, int ld, int vocab, int32_t* out_tok,
-                         void* stream);
+int choreo_select_greedy(const float* logits, int n_rows, int ld, int vocab, int split,
+                         int32_t* out_tok, void* stream);
 
 #ifdef __cplusplus
 }

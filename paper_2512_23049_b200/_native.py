@@ -24,17 +24,17 @@ _F = ctypes.c_float
 # name -> argtypes (all functions return int status)
 SIGNATURES: dict[str, list] = {
     "choreo_embed": [_P, _I, _I, _P, _I, _P, _P],
-    "choreo_residual_rmsnorm": [_P, _P, _I, _P, _I, _I, _I, _F, _P, _I, _P, _I, _P],
-    "choreo_silu_mul": [_P, _I, _I, _I, _P, _I, _P],
-    "choreo_rope_append": [_P, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I,
-                           _P, _P, _I, _P],
+    "choreo_residual_rmsnorm": [_P, _P, _I, _I, _P, _I, _I, _I, _F, _P, _I, _I, _P, _I, _P],
+    "choreo_silu_mul": [_P, _I, _I, _I, _I, _P, _I, _I, _P],
+    "choreo_rope_append": [_P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I,
+                           _I, _P, _P, _I, _P],
     "choreo_rerotate": [_P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _I, _P, _P, _I, _P],
     "choreo_assemble": [_P, _P, _P, _P, _P, _I, _P, _I, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P,
                         _P, _I, _I, _I, _P],
     "choreo_attn_split": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _P,
                           _P, _I, _P],
-    "choreo_attn_combine": [_P, _P, _P, _I, _I, _I, _P, _I, _P],
-    "choreo_select_greedy": [_P, _I, _I, _I, _P, _P],
+    "choreo_attn_combine": [_P, _P, _P, _I, _I, _I, _P, _I, _I, _P],
+    "choreo_select_greedy": [_P, _I, _I, _I, _I, _P, _P],
 }
 EXTRA = ["choreo_abi_version", "choreo_last_error"]
 

@@ -160,7 +160,7 @@ template <typename TO>
 __global__ void attn_combine_kernel(const float* __restrict__ part_o,
                                     const float* __restrict__ part_lse,
                                     const int32_t* __restrict__ row_part, int n_heads, int hd,
-                                    TO* __restrict__ out) {
+                                    int split, TO* __restrict__ out) {
   const int r = blockIdx.x;
   const int pb = row_part[3 * r], stride = row_part[3 * r + 1], n = row_part[3 * r + 2];
   for (int i = threadIdx.x; i < n_heads * hd; i += blockDim.x) {
@@ -178,7 +178,11 @@ __global__ void attn_combine_kernel(const float* __restrict__ part_o,
         den += wgt;
       }
     }
-    out[((int64_t)r * n_heads + h) * hd + d] = from_f32<TO>(den > 0.f ? num / den : 0.f);
+    const float y = den > 0.f ? num / den : 0.f;
+    const int64_t oi = ((int64_t)r * n_heads + h) * hd + d;
+    const TO hi = from_f32<TO>(y);
+    out[oi] = hi;
+    if (split) out[(int64_t)gridDim.x * n_heads * hd + oi] = from_f32<TO>(y - to_f32(hi));
   }
 }
 
@@ -237,16 +241,17 @@ int choreo_attn_split(const float* q, const void* k_pool, const void* v_pool, in
 
 int choreo_attn_combine(const float* part_o, const float* part_lse, const int32_t* row_part,
                         int n_rows, int n_heads, int head_dim, void* out, int out_dtype,
-                        void* stream) {
+                        int out_split, void* stream) {
   if (!part_o || !part_lse || !row_part || !out || !dtype_ok(out_dtype)) return CHOREO_EINVAL;
+  if (out_split && out_dtype != CHOREO_BF16) return CHOREO_EINVAL;
   if (n_rows == 0) return CHOREO_OK;
   auto s = as_stream(stream);
   if (out_dtype == CHOREO_BF16)
     attn_combine_kernel<__nv_bfloat16><<<n_rows, 256, 0, s>>>(part_o, part_lse, row_part, n_heads,
-                                                              head_dim, (__nv_bfloat16*)out);
+                                                              head_dim, out_split, (__nv_bfloat16*)out);
   else
     attn_combine_kernel<float><<<n_rows, 256, 0, s>>>(part_o, part_lse, row_part, n_heads,
-                                                      head_dim, (float*)out);
+                                                      head_dim, 0, (float*)out);
   return launch_status("choreo_attn_combine");
 }
 

@@ -22,10 +22,27 @@ __global__ void embed_kernel(const void* __restrict__ embed, int dt, int d,
 }
 
 // One CTA per output row.  x is the f32 residual stream.
+// Split activations: when out_split, row r of the output is written as a bf16
+// pair hi = bf16(y), lo = bf16(y - hi) at rows r and n_out + r, so a bf16 GEMM over
+// the stacked 2n rows followed by a sum of the halves sees y with ~16 mantissa bits
+// (memory-bound decode GEMMs read the weights once either way).  delta_split sums
+// such a stacked f32 GEMM output (rows r and n_rows + r) into the residual.
+__device__ __forceinline__ void store_split(void* out, int dt, int64_t i_hi, int64_t i_lo,
+                                            float y, int split) {
+  if (split) {
+    const __nv_bfloat16 hi = __float2bfloat16_rn(y);
+    reinterpret_cast<__nv_bfloat16*>(out)[i_hi] = hi;
+    reinterpret_cast<__nv_bfloat16*>(out)[i_lo] = __float2bfloat16_rn(y - __bfloat162float(hi));
+  } else {
+    store_any(out, dt, i_hi, y);
+  }
+}
+
 __global__ void residual_rmsnorm_kernel(float* __restrict__ x, const void* __restrict__ delta,
-                                        int delta_dt, const void* __restrict__ w, int w_dt, int d,
+                                        int delta_dt, int delta_split, int n_rows,
+                                        const void* __restrict__ w, int w_dt, int d,
                                         float eps, void* __restrict__ out, int out_dt,
-                                        const int32_t* __restrict__ row_map) {
+                                        int out_split, const int32_t* __restrict__ row_map) {
   const int r_out = blockIdx.x;
   const int r = row_map ? row_map[r_out] : r_out;
   float* xr = x + (int64_t)r * d;
@@ -34,6 +51,7 @@ __global__ void residual_rmsnorm_kernel(float* __restrict__ x, const void* __res
     float v = xr[i];
     if (delta) {
       v += load_any(delta, delta_dt, (int64_t)r * d + i);
+      if (delta_split) v += load_any(delta, delta_dt, (int64_t)(n_rows + r) * d + i);
       xr[i] = v;
     }
     ss += v * v;
@@ -51,24 +69,30 @@ __global__ void residual_rmsnorm_kernel(float* __restrict__ x, const void* __res
   __syncthreads();
   const float inv = 1.0f / sqrtf(red[0] / (float)d + eps);
   for (int i = threadIdx.x; i < d; i += blockDim.x)
-    store_any(out, out_dt, (int64_t)r_out * d + i, xr[i] * inv * load_any(w, w_dt, i));
+    store_split(out, out_dt, (int64_t)r_out * d + i, (int64_t)(gridDim.x + r_out) * d + i,
+                xr[i] * inv * load_any(w, w_dt, i), out_split);
 }
 
-__global__ void silu_mul_kernel(const void* __restrict__ gu, int dt, int64_t n, int f,
-                                void* __restrict__ out, int out_dt) {
+__global__ void silu_mul_kernel(const void* __restrict__ gu, int dt, int in_split, int n_rows,
+                                int f, void* __restrict__ out, int out_dt, int out_split) {
+  const int64_t n = (int64_t)n_rows * f, lo_in = (int64_t)n_rows * 2 * f;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / f, c = i % f;
-    const float g = load_any(gu, dt, r * 2 * f + c);
-    const float u = load_any(gu, dt, r * 2 * f + f + c);
-    store_any(out, out_dt, i, g / (1.0f + expf(-g)) * u);
+    float g = load_any(gu, dt, r * 2 * f + c);
+    float u = load_any(gu, dt, r * 2 * f + f + c);
+    if (in_split) {
+      g += load_any(gu, dt, lo_in + r * 2 * f + c);
+      u += load_any(gu, dt, lo_in + r * 2 * f + f + c);
+    }
+    store_split(out, out_dt, i, n + i, g / (1.0f + expf(-g)) * u, out_split);
   }
 }
 
 // K6: one warp per row; generatable ids are 0..255 and 257 (EOS).  Ties keep the
 // lowest id, as np.argmax does (engine.py:371).
 __global__ void select_greedy_kernel(const float* __restrict__ logits, int n_rows, int64_t ld,
-                                     int32_t* __restrict__ out) {
+                                     int split, int32_t* __restrict__ out) {
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= n_rows) return;
@@ -77,7 +101,7 @@ __global__ void select_greedy_kernel(const float* __restrict__ logits, int n_row
   int idx = 0x7fffffff;
   for (int i = lane; i < 258; i += 32) {
     if (i == 256) continue;
-    const float v = lr[i];
+    const float v = split ? lr[i] + lr[(int64_t)n_rows * ld + i] : lr[i];
     if (v > best || (v == best && i < idx)) { best = v; idx = i; }
   }
 #pragma unroll
@@ -107,40 +131,45 @@ int choreo_embed(const void* embed, int embed_dtype, int d, const int32_t* ids, 
   return launch_status("choreo_embed");
 }
 
-int choreo_residual_rmsnorm(float* x, const void* delta, int delta_dtype, const void* w,
-                            int w_dtype, int n_rows, int d, float eps, void* out, int out_dtype,
-                            const int32_t* row_map, int n_out, void* stream) {
+int choreo_residual_rmsnorm(float* x, const void* delta, int delta_dtype, int delta_split,
+                            const void* w, int w_dtype, int n_rows, int d, float eps, void* out,
+                            int out_dtype, int out_split, const int32_t* row_map, int n_out,
+                            void* stream) {
   if (!x || d <= 0 || n_rows < 0) return CHOREO_EINVAL;
   if (out && (!w || !dtype_ok(w_dtype) || !dtype_ok(out_dtype))) return CHOREO_EINVAL;
   if (delta && !dtype_ok(delta_dtype)) return CHOREO_EINVAL;
   if (row_map && (delta || !out)) return CHOREO_EINVAL;
+  if (out_split && out_dtype != CHOREO_BF16) return CHOREO_EINVAL;
   const int rows = row_map ? n_out : n_rows;
   if (rows == 0) return CHOREO_OK;
   const int threads = d >= 2048 ? 512 : (d >= 256 ? 256 : 64);
-  residual_rmsnorm_kernel<<<rows, threads, 0, as_stream(stream)>>>(x, delta, delta_dtype, w, w_dtype,
-                                                                    d, eps, out, out_dtype, row_map);
+  residual_rmsnorm_kernel<<<rows, threads, 0, as_stream(stream)>>>(
+      x, delta, delta_dtype, delta_split, n_rows, w, w_dtype, d, eps, out, out_dtype, out_split,
+      row_map);
   return launch_status("choreo_residual_rmsnorm");
 }
 
-int choreo_silu_mul(const void* gu, int gu_dtype, int n_rows, int f, void* out, int out_dtype,
-                    void* stream) {
+int choreo_silu_mul(const void* gu, int gu_dtype, int in_split, int n_rows, int f, void* out,
+                    int out_dtype, int out_split, void* stream) {
   if (!gu || !out || f <= 0 || n_rows < 0 || !dtype_ok(gu_dtype) || !dtype_ok(out_dtype))
     return CHOREO_EINVAL;
+  if (out_split && out_dtype != CHOREO_BF16) return CHOREO_EINVAL;
   const int64_t n = (int64_t)n_rows * f;
   if (n == 0) return CHOREO_OK;
   int64_t blocks = (n + 255) / 256;
   if (blocks > 148 * 64) blocks = 148 * 64;
-  silu_mul_kernel<<<(int)blocks, 256, 0, as_stream(stream)>>>(gu, gu_dtype, n, f, out, out_dtype);
+  silu_mul_kernel<<<(int)blocks, 256, 0, as_stream(stream)>>>(gu, gu_dtype, in_split, n_rows, f,
+                                                               out, out_dtype, out_split);
   return launch_status("choreo_silu_mul");
 }
 
-int choreo_select_greedy(const float* logits, int n_rows, int ld, int vocab, int32_t* out_tok,
-                         void* stream) {
+int choreo_select_greedy(const float* logits, int n_rows, int ld, int vocab, int split,
+                         int32_t* out_tok, void* stream) {
   if (!logits || !out_tok || n_rows < 0 || vocab < 258 || ld < vocab) return CHOREO_EINVAL;
   if (n_rows == 0) return CHOREO_OK;
   const int warps = 4;
   select_greedy_kernel<<<(n_rows + warps - 1) / warps, 32 * warps, 0, as_stream(stream)>>>(
-      logits, n_rows, ld, out_tok);
+      logits, n_rows, ld, split, out_tok);
   return launch_status("choreo_select_greedy");
 }
 

@@ -13,7 +13,7 @@ namespace choreo {
 // One thread per rotation pair of (row, head); q heads first, then k heads, then v
 // (v pairs are copied unrotated).  Writes q (f32) and the pool slot of each row.
 template <typename TI, typename TP>
-__global__ void rope_append_kernel(const TI* __restrict__ qkv, int ld, int n_rows,
+__global__ void rope_append_kernel(const TI* __restrict__ qkv, int ld, int n_rows, int split,
                                    const int32_t* __restrict__ pos,
                                    const int32_t* __restrict__ dst_page,
                                    const int32_t* __restrict__ dst_slot, float* __restrict__ q_out,
@@ -31,8 +31,12 @@ __global__ void rope_append_kernel(const TI* __restrict__ qkv, int ld, int n_row
     const int head = rem / half;  // 0..n_heads+2*n_kv-1 in qkv column order
     const int i = rem % half;
     const TI* src = qkv + (int64_t)r * ld + head * hd + 2 * i;
-    const float e = to_f32(src[0]);
-    const float o = to_f32(src[1]);
+    float e = to_f32(src[0]);
+    float o = to_f32(src[1]);
+    if (split) {  // stacked hi/lo GEMM halves (rows r and n_rows + r)
+      e += to_f32(src[(int64_t)n_rows * ld]);
+      o += to_f32(src[(int64_t)n_rows * ld + 1]);
+    }
     if (head >= n_heads + n_kv) {  // v: copy
       const int h = head - n_heads - n_kv;
       TP* dst = vp + pool_off(layer, h, dst_page[r], dst_slot[r], n_kv, n_pages, page_size, hd) + 2 * i;
@@ -123,7 +127,7 @@ using namespace choreo;
 
 extern "C" {
 
-int choreo_rope_append(const void* qkv, int qkv_dtype, int ld_qkv, int n_rows,
+int choreo_rope_append(const void* qkv, int qkv_dtype, int ld_qkv, int n_rows, int qkv_split,
                        const int32_t* pos, const int32_t* dst_page, const int32_t* dst_slot,
                        float* q_out, void* k_pool, void* v_pool, int pool_dtype, int layer,
                        int n_kv, int n_pages, int page_size, int n_heads, int head_dim,
@@ -139,7 +143,7 @@ int choreo_rope_append(const void* qkv, int qkv_dtype, int ld_qkv, int n_rows,
   auto s = as_stream(stream);
 #define K1(TI, TP)                                                                               \
   rope_append_kernel<TI, TP><<<blocks, 256, 0, s>>>(                                             \
-      (const TI*)qkv, ld_qkv, n_rows, pos, dst_page, dst_slot, q_out, (TP*)k_pool, (TP*)v_pool, \
+      (const TI*)qkv, ld_qkv, n_rows, qkv_split, pos, dst_page, dst_slot, q_out, (TP*)k_pool, (TP*)v_pool, \
       layer, n_kv, n_pages, page_size, n_heads, head_dim, cos_t, sin_t, max_delta)
   if (qkv_dtype == CHOREO_F32 && pool_dtype == CHOREO_F32) K1(float, float);
   else if (qkv_dtype == CHOREO_F32 && pool_dtype == CHOREO_BF16) K1(float, __nv_bfloat16);

@@ -124,7 +124,8 @@ class Engine:
     kind = "choreo"
 
     def __init__(self, weights, *, capacity: int = 65536, seed: int = 0,
-                 record_logits: bool = False, dtype=None, device=None, page_size: int = 64) -> None:
+                 record_logits: bool = False, dtype=None, device=None, page_size: int = 64,
+                 split_activations: bool = True) -> None:
         nat.load()  # fail loudly without the CUDA extension
         device = torch.device(device or "cuda")
         if isinstance(weights, WeightSet):
@@ -138,7 +139,7 @@ class Engine:
         self.cache = DeviceKvCache(self.config, capacity=capacity, dtype=weights.torch_dtype,
                                    device=device, page_size=page_size)
         self.rotation = RotationTableDevice(self.config, device)
-        self._runner = Runner(self.weights, self.cache, self.rotation)
+        self._runner = Runner(self.weights, self.cache, self.rotation, split_activations)
         self._generatable = generatable_mask(self.config.vocab_size)
         self._next_id = 0
         self.stats: list[CallStats] = []
@@ -178,7 +179,7 @@ class Engine:
         other.record_logits, other.device = self.record_logits, self.device
         other.cache = self.cache.clone()
         other.rotation = self.rotation
-        other._runner = Runner(self.weights, other.cache, self.rotation)
+        other._runner = Runner(self.weights, other.cache, self.rotation, self._runner.split)
         other._generatable = self._generatable
         other._next_id = self._next_id
         other.stats = []
@@ -360,17 +361,20 @@ class Engine:
             if not owners:
                 continue
             greedy_tok = None
+            n_own = len(owners)
+            split = int(self._runner.split)
             if any(s.forced is None and s.call.sampling.mode == "greedy" for s in owners):
-                out = torch.empty(len(owners), dtype=torch.int32, device=self.device)
-                nat.select_greedy(logits.data_ptr(), len(owners), logits.shape[1],
-                                  logits.shape[1], out.data_ptr(),
+                out = torch.empty(n_own, dtype=torch.int32, device=self.device)
+                nat.select_greedy(logits.data_ptr(), n_own, logits.shape[1], logits.shape[1],
+                                  split, out.data_ptr(),
                                   torch.cuda.current_stream(self.device).cuda_stream)
                 self._runner.launches += 1
                 greedy_tok = out.cpu().numpy()
             host_logits = None
             if self.record_logits or any(s.forced is None and s.call.sampling.mode != "greedy"
                                          for s in owners):
-                host_logits = logits.double().cpu().numpy()
+                hl = logits.double().cpu().numpy()
+                host_logits = hl[:n_own] + hl[n_own:] if split else hl
             else:
                 torch.cuda.current_stream(self.device).synchronize()
             for i, s in enumerate(owners):

@@ -75,7 +75,7 @@ class Runner:
     """Executes StepPlans for one (weights, cache) pair on the current stream."""
 
     def __init__(self, weights: DeviceWeights, cache: DeviceKvCache,
-                 rotation: RotationTableDevice) -> None:
+                 rotation: RotationTableDevice, split_activations: bool = True) -> None:
         self.w = weights
         self.cache = cache
         self.rot = rotation
@@ -87,6 +87,8 @@ class Runner:
         G = self.cfg.n_heads // self.cfg.kv_heads
         self.rows_per_block = max(1, min(16, 64 // G))
         self.launches = 0  # our kernels launched (for bench accounting)
+        # bf16 engines carry GEMM activations as hi/lo bf16 pairs (see choreo_b200.h)
+        self.split = self.dt == torch.bfloat16 and split_activations
 
     def _mm(self, a, w, out_f32: bool):
         if out_f32 and a.dtype != torch.float32:
@@ -94,6 +96,8 @@ class Runner:
         return torch.mm(a, w.t())
 
     def forward(self, plan: StepPlan) -> torch.Tensor | None:
+        """Run one step; returns f32 logits [S * n_logit_rows, V] (S = 2 when split:
+        rows i and n + i are the hi/lo halves to be summed) or None."""
         cfg, cache = self.cfg, self.cache
         stream = torch.cuda.current_stream(self.dev).cuda_stream
         R = plan.n_rows
@@ -152,22 +156,25 @@ class Runner:
                      row_part.data_ptr(), counts.data_ptr(), n_vis, n_items, n_parts, stream)
         self.launches += 1
 
+        S = 2 if self.split else 1  # stacked hi/lo activation rows
+        sp = int(self.split)
         x = torch.empty(R, d, dtype=torch.float32, device=self.dev)
         nat.embed(self.w.embed.data_ptr(), self.dtc, d, ids_d.data_ptr(), R, x.data_ptr(), stream)
         q = torch.empty(R, H, hd, dtype=torch.float32, device=self.dev)
         part_o = torch.empty(max(n_parts, 1), H, hd, dtype=torch.float32, device=self.dev)
         part_lse = torch.empty(max(n_parts, 1), H, dtype=torch.float32, device=self.dev)
-        attn = torch.empty(R, H * hd, dtype=self.dt, device=self.dev)
-        h = torch.empty(R, d, dtype=self.dt, device=self.dev)
-        act = torch.empty(R, cfg.ffn_dim, dtype=self.dt, device=self.dev)
+        attn = torch.empty(S * R, H * hd, dtype=self.dt, device=self.dev)
+        h = torch.empty(S * R, d, dtype=self.dt, device=self.dev)
+        act = torch.empty(S * R, cfg.ffn_dim, dtype=self.dt, device=self.dev)
         delta = None
         launches = 2
         for layer, lw in enumerate(self.w.layers):
-            nat.residual_rmsnorm(x.data_ptr(), nat.ptr(delta), nat.F32, lw["attn_norm"].data_ptr(),
-                                 self.dtc, R, d, RMS_EPS, h.data_ptr(), self.dtc, None, 0, stream)
+            nat.residual_rmsnorm(x.data_ptr(), nat.ptr(delta), nat.F32, sp,
+                                 lw["attn_norm"].data_ptr(), self.dtc, R, d, RMS_EPS, h.data_ptr(),
+                                 self.dtc, sp, None, 0, stream)
             qkv = self._mm(h, lw["w_qkv"], out_f32=True)
-            nat.rope_append(qkv.data_ptr(), nat.dtype_code(qkv.dtype), qkv.shape[1], R,
-                            pos_d.data_ptr(), page_d.data_ptr(), slot_d.data_ptr(), q.data_ptr(),
+            nat.rope_append(qkv.data_ptr(), nat.F32, qkv.shape[1], R, sp, pos_d.data_ptr(),
+                            page_d.data_ptr(), slot_d.data_ptr(), q.data_ptr(),
                             cache.k_pool.data_ptr(), cache.v_pool.data_ptr(), self.pool_dtc, layer,
                             Hk, cache.n_pages, P, H, hd, self.rot.cos.data_ptr(),
                             self.rot.sin.data_ptr(), self.rot.max_delta, stream)
@@ -177,22 +184,25 @@ class Runner:
                            items.data_ptr(), counts.data_ptr(), n_items, part_o.data_ptr(),
                            part_lse.data_ptr(), 0, stream)
             nat.attn_combine(part_o.data_ptr(), part_lse.data_ptr(), row_part.data_ptr(), R, H,
-                             hd, attn.data_ptr(), self.dtc, stream)
+                             hd, attn.data_ptr(), self.dtc, sp, stream)
             ao = self._mm(attn, lw["wo"], out_f32=True)
-            nat.residual_rmsnorm(x.data_ptr(), ao.data_ptr(), nat.F32, lw["ffn_norm"].data_ptr(),
-                                 self.dtc, R, d, RMS_EPS, h.data_ptr(), self.dtc, None, 0, stream)
-            gu = self._mm(h, lw["w_gu"], out_f32=False)
-            nat.silu_mul(gu.data_ptr(), self.dtc, R, cfg.ffn_dim, act.data_ptr(), self.dtc, stream)
+            nat.residual_rmsnorm(x.data_ptr(), ao.data_ptr(), nat.F32, sp,
+                                 lw["ffn_norm"].data_ptr(), self.dtc, R, d, RMS_EPS, h.data_ptr(),
+                                 self.dtc, sp, None, 0, stream)
+            gu = self._mm(h, lw["w_gu"], out_f32=True)  # f32 pre-activations (parity)
+            nat.silu_mul(gu.data_ptr(), nat.F32, sp, R, cfg.ffn_dim, act.data_ptr(), self.dtc, sp,
+                         stream)
             delta = self._mm(act, lw["w_down"], out_f32=True)
             launches += 6
-        nat.residual_rmsnorm(x.data_ptr(), delta.data_ptr(), nat.F32, None, 0, R, d, RMS_EPS,
-                             None, 0, None, 0, stream)
+        nat.residual_rmsnorm(x.data_ptr(), delta.data_ptr(), nat.F32, sp, None, 0, R, d, RMS_EPS,
+                             None, 0, 0, None, 0, stream)
         launches += 1
         self.launches += launches
         if n_log == 0:
             return None
-        xn = torch.empty(n_log, d, dtype=self.dt, device=self.dev)
-        nat.residual_rmsnorm(x.data_ptr(), None, 0, self.w.out_norm.data_ptr(), self.dtc, R, d,
-                             RMS_EPS, xn.data_ptr(), self.dtc, logit_d.data_ptr(), n_log, stream)
+        xn = torch.empty(S * n_log, d, dtype=self.dt, device=self.dev)
+        nat.residual_rmsnorm(x.data_ptr(), None, 0, 0, self.w.out_norm.data_ptr(), self.dtc, R, d,
+                             RMS_EPS, xn.data_ptr(), self.dtc, sp, logit_d.data_ptr(), n_log,
+                             stream)
         self.launches += 1
         return self._mm(xn, self.w.out_head, out_f32=True)

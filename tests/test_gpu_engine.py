@@ -206,7 +206,7 @@ def test_parallel_matches_lone(mode, sampling):
     e = _small(mode, record_logits=True)
     a = e.prefill(P.PrefillCall("first parent text"))
     b = e.prefill(P.PrefillCall("second parent text"))
-    calls = [P.DecodeCall("Ans A:", parents=[a], sampling=sampling),
+    calls = [P.DecodeCall("Ans A:", parents=[a], offsets=[40], sampling=sampling),
              P.DecodeCall("Ans B:", parents=[b, a], offsets=[0, 40], sampling=sampling)]
     par, seq = e.clone(), e.clone()
     ids_par = par.decode_parallel(calls)

@@ -45,7 +45,7 @@ def test_rope_append(dt, hd, H, Hk):
     vp = torch.zeros_like(kp)
     q = torch.empty(R, H, hd, device="cuda")
     d = {k: torch.from_numpy(v).cuda() for k, v in dict(qkv=qkv, pos=pos, page=page, slot=slot).items()}
-    nat.rope_append(d["qkv"].data_ptr(), nat.F32, qkv.shape[1], R, d["pos"].data_ptr(),
+    nat.rope_append(d["qkv"].data_ptr(), nat.F32, qkv.shape[1], R, 0, d["pos"].data_ptr(),
                     d["page"].data_ptr(), d["slot"].data_ptr(), q.data_ptr(), kp.data_ptr(),
                     vp.data_ptr(), nat.dtype_code(DT[dt]), 1, Hk, n_pages, P, H, hd,
                     rot.cos.data_ptr(), rot.sin.data_ptr(), rot.max_delta, _stream())
@@ -105,7 +105,7 @@ def test_select_greedy_ties_and_mask():
     logits[3, 257] = 50.0        # EOS is generatable
     d = torch.from_numpy(logits).cuda()
     out = torch.empty(9, dtype=torch.int32, device="cuda")
-    nat.select_greedy(d.data_ptr(), 9, V, V, out.data_ptr(), _stream())
+    nat.select_greedy(d.data_ptr(), 9, V, V, 0, out.data_ptr(), _stream())
     mask = O.sampler_mask(V)
     want = [int(np.argmax(np.where(mask, r.astype(np.float64), -np.inf))) for r in logits]
     assert out.cpu().tolist() == want
@@ -241,7 +241,7 @@ def test_attention_matches_dense_reference(dt, hd, H, Hk):
                    items.data_ptr(), counts.data_ptr(), out["plan"][1], part_o.data_ptr(),
                    part_lse.data_ptr(), 0, _stream())
     nat.attn_combine(part_o.data_ptr(), part_lse.data_ptr(), row_part.data_ptr(), R, H, hd,
-                     o.data_ptr(), nat.F32, _stream())
+                     o.data_ptr(), nat.F32, 0, _stream())
     torch.cuda.synchronize()
     sets = _expand_rows(cache, out, R)
     K = cache.k_pool[L].float().cpu().numpy().astype(np.float64)  # (Hk, pages, P, hd)
