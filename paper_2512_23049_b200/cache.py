@@ -204,6 +204,10 @@ class DeviceKvCache:
     def message_length(self, message_id: int) -> int:
         return self._entry(message_id).length
 
+    def message_length_or_none(self, message_id: int) -> int | None:
+        e = self._messages.get(message_id)
+        return None if e is None else e.length
+
     def message_offset(self, message_id: int) -> int:
         return self._entry(message_id).offset
 

@@ -101,6 +101,50 @@ def encode_flops(config: ModelConfig, t_new: int, ctx: int, rows: str) -> int:
             + L * 6 * t_new * d * config.ffn_dim + 2 * nrow * d * config.vocab_size)
 
 
+def resolve_calls(calls, new_lens, length_of, window: int):
+    """Validate a batch's parents/offsets and lay it out (engine.py:203-245).
+
+    ``length_of(msg)`` returns a message's token count, or None if unknown.
+    Omitted offsets default to right after the preceding parent (first to 0),
+    new_offset to right after the last parent; a parent shared within the batch
+    must get one offset.  Returns (agreed {parent: offset}, [(parents, new_offset)]).
+    Raises before any mutation.
+    """
+    agreed: dict[int, int] = {}
+    layouts = []
+    for call, new_len in zip(calls, new_lens):
+        parents = [int(p) for p in call.parents]
+        if len(set(parents)) != len(parents):
+            raise InvalidCallError(f"duplicate parents {parents}")
+        lens = [length_of(p) for p in parents]
+        for p, n in zip(parents, lens):
+            if n is None:
+                raise UnknownMessageError(f"unknown parent id {p}")
+        offsets = list(call.offsets) if call.offsets is not None else [None] * len(parents)
+        if len(offsets) != len(parents):
+            raise InvalidCallError(
+                f"offsets length {len(offsets)} != parents length {len(parents)}")
+        prev_end = 0
+        for p, plen, off in zip(parents, lens, offsets):
+            o = prev_end if off is None else int(off)
+            if o < 0:
+                raise InvalidCallError(f"negative offset {o} for parent {p}")
+            if o + plen > window:
+                raise WindowOverflowError(f"parent {p} (len {plen}) does not fit at offset {o}")
+            if p in agreed and agreed[p] != o:
+                raise OffsetConflictError(
+                    f"parent {p} placed at both {agreed[p]} and {o} in one batch")
+            agreed[p] = o
+            prev_end = o + plen
+        new_off = int(call.new_offset) if call.new_offset is not None else prev_end
+        if new_off < 0:
+            raise InvalidCallError(f"negative new_offset {new_off}")
+        if new_off + new_len > window:
+            raise WindowOverflowError(f"new message (len {new_len}) does not fit at offset {new_off}")
+        layouts.append((parents, new_off))
+    return agreed, layouts
+
+
 class _Dec:
     """Per-message decode progress (engine.py:109-130)."""
 
@@ -196,41 +240,8 @@ class Engine:
     # -- validation and layout (engine.py:203-258) ---------------------------------------
 
     def _resolve_calls(self, calls, new_lens):
-        window = self.config.context_window
-        agreed: dict[int, int] = {}
-        layouts = []
-        for call, new_len in zip(calls, new_lens):
-            parents = [int(p) for p in call.parents]
-            if len(set(parents)) != len(parents):
-                raise InvalidCallError(f"duplicate parents {parents}")
-            for p in parents:
-                if p not in self.cache:
-                    raise UnknownMessageError(f"unknown parent id {p}")
-            offsets = list(call.offsets) if call.offsets is not None else [None] * len(parents)
-            if len(offsets) != len(parents):
-                raise InvalidCallError(
-                    f"offsets length {len(offsets)} != parents length {len(parents)}")
-            prev_end = 0
-            for p, off in zip(parents, offsets):
-                o = prev_end if off is None else int(off)
-                if o < 0:
-                    raise InvalidCallError(f"negative offset {o} for parent {p}")
-                plen = self.cache.message_length(p)
-                if o + plen > window:
-                    raise WindowOverflowError(f"parent {p} (len {plen}) does not fit at offset {o}")
-                if p in agreed and agreed[p] != o:
-                    raise OffsetConflictError(
-                        f"parent {p} placed at both {agreed[p]} and {o} in one batch")
-                agreed[p] = o
-                prev_end = o + plen
-            new_off = int(call.new_offset) if call.new_offset is not None else prev_end
-            if new_off < 0:
-                raise InvalidCallError(f"negative new_offset {new_off}")
-            if new_off + new_len > window:
-                raise WindowOverflowError(
-                    f"new message (len {new_len}) does not fit at offset {new_off}")
-            layouts.append((parents, new_off))
-        return agreed, layouts
+        return resolve_calls(calls, new_lens, self.cache.message_length_or_none,
+                             self.config.context_window)
 
     def _check_capacity(self, n_tokens: int) -> None:
         if self.cache.token_count + n_tokens > self.cache.capacity:

@@ -1,0 +1,195 @@
+"""CPU-only checks: the C-ABI library loads and exports every declared symbol, and the
+host-side logic (layout resolution, K3 sizing, physical-order views, FLOP
+accounting, weights) matches the oracle.  No kernel is launched here."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import choreo_oracle as O
+
+import paper_2512_23049_b200 as P
+from paper_2512_23049_b200 import _native as nat
+from paper_2512_23049_b200.cache import DeviceKvCache, cdiv
+from paper_2512_23049_b200.engine import resolve_calls
+from paper_2512_23049_b200.model import CallRows, plan_counts
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "choreo_b200.h")
+
+
+def _prototypes():
+    text = re.sub(r"/\*.*?\*/", "", open(HEADER).read(), flags=re.S)
+    protos = {}
+    for m in re.finditer(r"\b(?:int|const char\*)\s+(choreo_\w+)\s*\(([^)]*)\)\s*;", text):
+        args = [a.strip() for a in m.group(2).split(",") if a.strip() and a.strip() != "void"]
+        protos[m.group(1)] = args
+    return protos
+
+
+def test_library_exports_every_declared_symbol():
+    protos = _prototypes()
+    assert len(protos) >= 11
+    lib = nat.load()
+    for name in protos:
+        assert hasattr(lib, name), name
+    assert lib.choreo_abi_version() == 100
+
+
+def test_ctypes_signatures_match_header():
+    protos = _prototypes()
+    for name, args in nat.SIGNATURES.items():
+        assert name in protos, name
+        assert len(args) == len(protos[name]), (name, len(args), len(protos[name]))
+    assert set(protos) == set(nat.SIGNATURES) | set(nat.EXTRA)
+
+
+def test_no_torch_types_in_abi():
+    text = open(HEADER).read()
+    assert "torch" not in re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+
+
+def test_missing_library_fails_loudly(monkeypatch, tmp_path):
+    monkeypatch.setattr(nat, "_lib", None)
+    monkeypatch.setattr(nat, "LIB_PATH", str(tmp_path / "nope.so"))
+    with pytest.raises(P.NativeError):
+        nat.load()
+
+
+class _C:
+    def __init__(self, parents, offsets=None, new_offset=None):
+        self.parents, self.offsets, self.new_offset = parents, offsets, new_offset
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_resolve_calls_matches_oracle(seed):
+    rng = np.random.default_rng(seed)
+    W = 256
+    lens = {m: int(rng.integers(1, 60)) for m in range(8)}
+    calls = []
+    for _ in range(int(rng.integers(1, 4))):
+        par = [int(p) for p in rng.choice(10, size=int(rng.integers(0, 5)), replace=bool(rng.random() < 0.1))]
+        offs = None if rng.random() < 0.4 else [
+            None if rng.random() < 0.3 else int(rng.integers(-2, 200)) for _ in par]
+        if offs is not None and rng.random() < 0.05:
+            offs = offs + [0]
+        no = None if rng.random() < 0.5 else int(rng.integers(-1, 250))
+        calls.append(_C(par, offs, no))
+    new_lens = [int(rng.integers(1, 30)) for _ in calls]
+    ora = O.Oracle.__new__(O.Oracle)
+    ora.shape = O.Shape(context_window=W)
+    ora.store = O.Store(ora.shape, 100)
+    for m, n in lens.items():
+        ora.store.msgs[m] = O.Msg("prefilled", 0, "", None, list(range(n)))
+    want = got = None
+    try:
+        want = ora.resolve([{"parents": c.parents, "offsets": c.offsets, "new_offset": c.new_offset}
+                            for c in calls], new_lens)
+    except O.OracleError as e:
+        want = e.kind
+    try:
+        got = resolve_calls(calls, new_lens, lens.get, W)
+    except P.ChoreoError as e:
+        got = type(e).__name__
+    assert got == want
+
+
+def _cache_cpu(cfg=None):
+    cfg = cfg or P.ModelConfig(n_layers=2, n_heads=2, head_dim=8, context_window=256)
+    return DeviceKvCache(cfg, capacity=4096, dtype=torch.float32, device="cpu")
+
+
+def test_interleaved_physical_order_matches_reference_pattern():
+    c = _cache_cpu()
+    for m in (0, 1, 2):
+        c.register_message(m, "decoded", 0)
+    lens = [4, 7, 2]
+    for m, n in enumerate(lens):
+        c.reserve_slots(m, list(range(n)))
+    c.log_interleaved([0, 1, 2], [0, 0, 0], lens)
+    expected = [m for t in range(max(lens)) for m in range(3) if lens[m] > t]
+    assert c.msg_ids.tolist() == expected
+    assert c.message_span(1).physical.tolist() == [i for i, m in enumerate(expected) if m == 1]
+
+
+def test_pages_belong_to_one_message_and_views():
+    c = _cache_cpu()
+    c.register_message(0, "prefilled", 5, max_tokens=70)
+    c.register_message(1, "decoded", 0)
+    p0, s0 = c.reserve_slots(0, list(range(70)))
+    p1, s1 = c.reserve_slots(1, [7] * 10)
+    assert set(p0.tolist()).isdisjoint(p1.tolist())
+    assert s0.tolist() == [i % 64 for i in range(70)]
+    c.log_append(0, 0, 70)
+    c.log_append(1, 0, 10)
+    assert c.positions.tolist() == list(range(5, 75)) + list(range(10))
+    assert c.token_count == 80
+    with pytest.raises(P.CapacityError):
+        c.reserve_slots(1, [0] * 5000)
+
+
+def test_page_chain_relocates_when_reservation_is_exceeded():
+    c = _cache_cpu()
+    c.register_message(0, "decoded", 0, max_tokens=10)  # reserves one page-table entry
+    pages, _ = c.reserve_slots(0, list(range(200)))
+    e = c._messages[0]
+    assert len(e.pages) == 4 and e.pt_cap >= 4
+    assert c.page_table.host[e.pt:e.pt + 4].tolist() == e.pages
+    assert c.msg_pt.host[0] == e.pt
+
+
+def _brute_counts(calls, msg_len, P_, rpb, ppi):
+    v = it = pa = 0
+    for c in calls:
+        pp = sum(cdiv(msg_len[p], P_) for p in c.parents)
+        ts = [c.first_t + i for i in range(len(c.tokens))]
+        v += pp + ts[-1] // P_ + 1
+        blocks = [ts[i:i + rpb] for i in range(0, len(ts), rpb)]
+        for b in blocks:
+            ch = cdiv(pp + b[-1] // P_ + 1, ppi)
+            it += ch
+            pa += ch * len(b)
+    return v, it, pa
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_plan_counts(seed):
+    rng = np.random.default_rng(seed)
+    msg_len = rng.integers(1, 300, 20)
+    calls = [CallRows(int(rng.integers(20, 30)), [int(p) for p in rng.permutation(20)[:rng.integers(0, 6)]],
+                      int(rng.integers(0, 100)), [0] * int(rng.integers(1, 80)), None, None, 0)
+             for _ in range(int(rng.integers(1, 6)))]
+    for rpb, ppi in ((1, 1), (16, 3), (4, 1000)):
+        assert plan_counts(calls, msg_len, 64, rpb, ppi) == _brute_counts(calls, msg_len, 64, rpb, ppi)
+
+
+@pytest.mark.parametrize("shape", [O.TINY, O.Shape(n_layers=3, n_heads=8, n_kv_heads=2, head_dim=16,
+                                                    ffn_dim=64, vocab_size=300)])
+def test_encode_flops_matches_oracle(shape):
+    cfg = P.ModelConfig(**{k: getattr(shape, k) for k in shape.__dataclass_fields__})
+    for t, ctx, rows in ((1, 0, "all"), (19, 7, "none"), (5, 100, "last"), (0, 3, "all")):
+        assert P.encode_flops(cfg, t, ctx, rows) == sum(O.encode_flops(shape, t, ctx, rows).values())
+
+
+def test_product_init_weights_bitwise_oracle_and_device_layout():
+    ws = P.init_weights(P.DEFAULT_CONFIG)
+    ow = O.init_weights(O.TINY)
+    np.testing.assert_array_equal(ws.layers[3].w_up, ow["layers"][3]["w_up"])
+    np.testing.assert_array_equal(ws.out_head, ow["out_head"])
+    dw = P.DeviceWeights.from_host(ws, dtype=torch.float32, device="cpu")
+    l0 = ws.layers[0]
+    want = np.concatenate([l0.wq, l0.wk, l0.wv], axis=1).T.astype(np.float32)
+    np.testing.assert_array_equal(dw.layers[0]["w_qkv"].numpy(), want)
+    assert dw.out_head.shape == (512, 64)
+
+
+def test_config_roundtrip_and_presets():
+    assert P.DEFAULT_CONFIG.to_dict() == O.TINY.ref_dict()
+    cfg = P.LLAMA_3_1_8B
+    assert (cfg.model_dim, cfg.kv_dim, cfg.kv_heads) == (4096, 1024, 8)
+    assert P.ModelConfig.from_dict(cfg.to_dict()) == cfg
+    with pytest.raises(ValueError):
+        P.ModelConfig(n_heads=6, n_kv_heads=4)
