@@ -1,0 +1,382 @@
+"""Benchmark: choreographed multi-agent debate at the Llama-3.1-8B shape (BASELINE.json C3).
+
+One step = one complete debate workflow instance, laid out exactly as the
+reference's run_madpar (workflows.py:294-327): prefill a system prompt (64
+framed tokens) and a MATH-length question (160), then n_rounds rounds of
+``decode_parallel`` with n_agents agents; each agent sees sys, q and the other
+agents' previous-round replies, placed consecutively after q with explicit
+offsets (so shared parents are repositioned once per round by K2) and its own
+reply starts right after them.  Replies are teacher-forced to seeded lengths
+U(256, 512) (bench.py run_pair protocol, src/bench.py:94-109) so every run does
+identical work.  Weights: random-init Llama-3.1-8B shape, bf16, drawn on device.
+
+Reported (rank 0, one JSON line):
+  value    decode tokens/s over the timed workflows, device-busy time: the sum of
+           CUDA-event durations of every forward step (inputs staged in HBM; host
+           gaps between steps excluded).
+  e2e      the same tokens / CUDA-event time of the whole workflows through the
+           public Engine API (host strings and host token lists in, H2D of each
+           step's token/page metadata and D2H of results inside the timed region).
+  ttft_p50_ms  per-message TTFT (decode_parallel call start -> first token), p50.
+  roofline decode attention kernel (K5 split) vs measured HBM bandwidth.
+  cpu_baseline  the CPU oracle (NumPy restatement of the reference) on this host.
+Multi-GPU (torchrun): each rank runs its own independent workflow instances
+(seed = rank), no collectives on the data path; value = all ranks' tokens / max
+rank time ("scaling": "weak").
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import string
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "p50 per-message TTFT; choreographed decode tokens/s at Llama-3.1-8B shape"
+WORKLOAD = "C3: Llama-3.1-8B shape, multi-agent debate (madpar layout), 8 agents x 3 rounds"
+
+
+def random_text(rng, n_tokens: int) -> str:
+    """ASCII text whose framed encoding is exactly n_tokens long (src/bench.py:155-163)."""
+    n_bytes = max(1, n_tokens - 2)
+    letters = string.ascii_lowercase
+    chars: list = []
+    while len(chars) < n_bytes:
+        chars.extend(letters[i] for i in rng.integers(0, 26, size=8))
+        chars.append(" ")
+    return "".join(chars[:n_bytes]).strip().ljust(n_bytes, "x")
+
+
+def workflow_inputs(seed: int, n_agents: int, n_rounds: int):
+    rng = np.random.default_rng(seed)
+    sys_text = random_text(rng, 64)
+    question = random_text(rng, 160)
+    forced = [[rng.integers(97, 123, size=int(rng.integers(256, 513))).tolist()
+               for _ in range(n_agents)] for _ in range(n_rounds)]
+    return sys_text, question, forced
+
+
+def run_debate(engine, P, inputs, n_agents: int, n_rounds: int) -> dict:
+    """madpar layout (workflows.py:294-327) through the public Engine API."""
+    sys_text, question, forced = inputs
+    sys_id = engine.prefill(P.PrefillCall(sys_text))
+    q_id = engine.prefill(P.PrefillCall(question))
+    base = engine.message_token_count(sys_id) + engine.message_token_count(q_id)
+    prev: list = []
+    ttft, generated = [], 0
+    for r in range(n_rounds):
+        placed, cursor = {}, base
+        for m in prev:
+            placed[m] = cursor
+            cursor += engine.message_token_count(m)
+        calls = []
+        for i in range(n_agents):
+            others = [m for j, m in enumerate(prev) if j != i]
+            calls.append(P.DecodeCall(
+                f"Agent {i + 1}:", parents=[sys_id, q_id] + others,
+                offsets=[0, engine.message_token_count(sys_id)] + [placed[m] for m in others],
+                new_offset=cursor, sampling=P.SamplingParams(max_tokens=512)))
+        prev = engine.decode_parallel(calls, force_tokens=forced[r])
+        st = engine.last_stats
+        ttft += [st.ttft[m] for m in prev]
+        generated += sum(len(engine.generated_token_ids(m)) for m in prev)
+    return {"ttft": ttft, "generated": generated}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int) -> None:
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self) -> dict:
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows if len(r) >= 7
+                          for n, v in zip(names, r[3:7]) if v.lower() == "active"})
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def measured_peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh) | {"source": "measured"}
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback"}
+
+
+# ---------------------------------------------------------------------------- CPU side
+
+
+def cpu_reference_sample(n_agents: int, gen_tokens: int, seed: int = 0) -> dict:
+    """Time the CPU oracle (NumPy restatement of the reference engine) on a bounded
+    sample of the workload: one round-2 decode_parallel of n_agents agents over a
+    synthetic round-1 cache (sys 64 + q 160 + n_agents replies of ~384 tokens) with
+    gen_tokens forced tokens each, at the full 8B width (GQA 32/8) and the full
+    128256-row head.  The sample runs twice, with 1 and 2 layers, so per-forward time
+    is t(L) = a + b L; results are extrapolated to L = 32 and labelled so."""
+    from oracle import choreo_oracle as O
+
+    cores = len(os.sched_getaffinity(0))
+    L_FULL = 32
+    rng = np.random.default_rng(seed)
+    base = dict(n_heads=32, n_kv_heads=8, head_dim=128, ffn_dim=14336, vocab_size=128256,
+                context_window=32768, rope_base=500000.0)
+    d, dkv, f, v = 4096, 1024, 14336, 128256
+
+    def u(shp, fi, fo):
+        b = np.float32(np.sqrt(6.0 / (fi + fo)))
+        return (rng.random(shp, dtype=np.float32) * 2 - 1) * b
+
+    def layer():
+        return {"attn_norm": np.ones(d, np.float32), "wq": u((d, d), d, d),
+                "wk": u((d, dkv), d, dkv), "wv": u((d, dkv), d, dkv), "wo": u((d, d), d, d),
+                "ffn_norm": np.ones(d, np.float32), "w_gate": u((d, f), d, f),
+                "w_up": u((d, f), d, f), "w_down": u((f, d), f, d)}
+
+    shared = {"embed": u((v, d), v, d), "out_head": u((d, v), d, v),
+              "out_norm": np.ones(d, np.float32)}
+    layers = [layer(), layer()]
+    lens = [64, 160] + [int(rng.integers(256, 513)) + 10 for _ in range(n_agents)]
+    kvs = [rng.standard_normal((2, n, 8, 128), dtype=np.float32) for n in lens]
+
+    def run(n_layers: int):
+        shape = O.Shape(n_layers=n_layers, **base)
+        eng = O.Oracle(dict(shared, layers=layers[:n_layers]), shape, capacity=1 << 16)
+        st = eng.store
+        for m, n in enumerate(lens):
+            start = [0, 64][m] if m < 2 else 224
+            st.msgs[m] = O.Msg("prefilled", start, "", None)
+            st.append(m, [97] * n, np.arange(n) + start, kvs[m][:n_layers], kvs[m][:n_layers])
+        eng.next_id = len(lens)
+        prev = list(range(2, 2 + n_agents))
+        placed, cursor = {}, 224
+        for m in prev:
+            placed[m] = cursor
+            cursor += lens[m]
+        calls = []
+        for i in range(n_agents):
+            others = [m for j, m in enumerate(prev) if j != i]
+            calls.append({"header": f"Agent {i + 1}:", "parents": [0, 1] + others,
+                          "offsets": [0, 64] + [placed[m] for m in others], "new_offset": cursor,
+                          "sampling": O.Sampling(max_tokens=512)})
+        t0 = time.perf_counter()
+        eng.decode_batch(calls, [[97] * gen_tokens for _ in range(n_agents)])
+        t = time.perf_counter() - t0
+        st_ = eng.stats[-1]
+        return t, st_.tokens_encoded, sorted(st_.ttft.values())
+
+    t1, n_rows, ttft1 = run(1)
+    t2, _, ttft2 = run(2)
+    b_layer = max(t2 - t1, 0.0)
+    t_ext = t1 + (L_FULL - 1) * b_layer
+    ttft_ext = [x1 + (L_FULL - 1) * max(x2 - x1, 0.0) for x1, x2 in zip(ttft1, ttft2)]
+    # every encoded token of a parallel decode is one agent's decode step (header tokens are
+    # fed one per step by the reference), so encoded rows / time is its decode rate
+    return {"value": n_rows / t_ext, "unit": "tokens/s", "cores": cores, "kind": "port",
+            "extrapolated": True, "t_sample_s": t1 + t2,
+            "ttft_p50_ms": 1e3 * statistics.median(ttft_ext),
+            "sample": (f"oracle (NumPy f32, {cores} host threads): one round-2 decode_parallel of "
+                       f"{n_agents} agents x {gen_tokens} forced tokens (headers fed one token per "
+                       f"step, as the reference) over a synthetic {sum(lens)}-token cache, 8B width, "
+                       f"full 128256-row head, timed at 1 and 2 layers and extrapolated to 32")}
+
+
+def reference_arm(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = len(os.sched_getaffinity(0))
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores))
+    vals, ttfts, t_all = [], [], 0.0
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        res = cpu_reference_sample(args.agents, args.ref_tokens, seed=i)
+        if i >= args.warmup:
+            vals.append(res["value"])
+            ttfts.append(res["ttft_p50_ms"])
+            t_all += time.perf_counter() - t0
+    value = statistics.median(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * t_all / max(1, args.steps), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "ttft_p50_ms": statistics.median(ttfts),
+            "config": {"workload": WORKLOAD, "sample": res["sample"]},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
+                             "sample": res["sample"]},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------- GPU side
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--agents", type=int, default=8)
+    ap.add_argument("--rounds", type=int, default=3)
+    ap.add_argument("--ref-tokens", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--model", default="llama-3.1-8b")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        reference_arm(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2512_23049_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = P.PRESETS[args.model]
+    weights = P.DeviceWeights.random(cfg, dtype=torch.bfloat16, device="cuda", seed=cfg.seed + rank)
+    eng = P.Engine(weights, capacity=65536, seed=rank)
+    runner = eng._runner
+
+    def sync_all():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    for i in range(args.warmup):
+        eng.reset()
+        run_debate(eng, P, workflow_inputs(1000 * rank + i, args.agents, args.rounds),
+                   args.agents, args.rounds)
+    inputs = [workflow_inputs(1000 * rank + 100 + i, args.agents, args.rounds)
+              for i in range(args.steps)]
+
+    step_events, attn_events = [], []
+    runner.step_events = step_events
+    launches0, h2d0, d2h0 = runner.launches, runner.h2d_bytes, eng.d2h_bytes
+    ttft, generated = [], 0
+    sync_all()
+    with ClockSampler(local) as clocks:
+        ev_start = torch.cuda.Event(enable_timing=True)
+        ev_end = torch.cuda.Event(enable_timing=True)
+        ev_start.record()
+        for i in range(args.steps):
+            eng.reset()
+            runner.attn_events = attn_events if i == args.steps - 1 else None
+            res = run_debate(eng, P, inputs[i], args.agents, args.rounds)
+            ttft += res["ttft"]
+            generated += res["generated"]
+        runner.attn_events = None
+        ev_end.record()
+        sync_all()
+    runner.step_events = None
+    elapsed = ev_start.elapsed_time(ev_end) / 1e3
+    busy = sum(a.elapsed_time(b) for a, b in step_events) / 1e3
+    launches = runner.launches - launches0
+    h2d = (runner.h2d_bytes - h2d0) / args.steps
+    d2h = (eng.d2h_bytes - d2h0) / args.steps
+    if world > 1:
+        t = torch.tensor([elapsed, busy], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed, busy = t.tolist()
+        g = torch.tensor([generated], device="cuda", dtype=torch.float64)
+        dist.all_reduce(g)
+        generated_all = g.item()
+    else:
+        generated_all = generated
+
+    # decode attention (K5) roofline, from the events of the last timed workflow
+    peaks = measured_peaks()
+    a_ms = [a.elapsed_time(b) for a, b, _ in attn_events]
+    a_bytes = [nb for _, _, nb in attn_events]
+    roofline = None
+    if a_ms:
+        achieved = (sum(a_bytes) / len(a_bytes)) / (sum(a_ms) / len(a_ms) / 1e3) / 1e9
+        roofline = {"kernel": "choreo_attn_split (K5, decode split-KV)", "bound": "hbm",
+                    "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                    "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": None,
+                    "peak_source": peaks["source"],
+                    "avg_launch_us": round(1e3 * sum(a_ms) / len(a_ms), 2),
+                    "algorithmic_bytes_per_launch": int(sum(a_bytes) / len(a_bytes)),
+                    "launches_timed": len(a_ms)}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_reference_sample(args.agents, args.ref_tokens)
+        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    line = {
+        "metric": METRIC, "value": round(generated_all / busy, 2), "unit": "tokens/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * elapsed / args.steps, 2), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "ttft_p50_ms": round(1e3 * statistics.median(ttft), 3),
+        "ttft_p90_ms": round(1e3 * sorted(ttft)[int(0.9 * (len(ttft) - 1))], 3),
+        "config": {"workload": WORKLOAD, "model": args.model, "agents": args.agents,
+                   "rounds": args.rounds, "reply_tokens": "U(256,512) teacher-forced",
+                   "weights": "random-init bf16 (device draw)", "kv_cache": "paged bf16, P=64",
+                   "activations": "split hi/lo bf16 GEMM inputs, f32 residual",
+                   "value_definition": "generated tokens / sum of per-step device time",
+                   "l2": "inputs larger than L2 (16 GB of weights streamed per step)",
+                   "parallelism": f"replicas x{world} (independent workflows per GPU)"},
+        "e2e": {"value": round(generated_all / elapsed, 2), "unit": "tokens/s",
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": int(launches),
+        "generated_tokens": int(generated_all),
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "clocks": clocks.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -36,6 +36,15 @@ def cdiv(a: int, b: int) -> int:
     return -(-a // b)
 
 
+def h2d(arr: np.ndarray, device) -> torch.Tensor:
+    """Host array -> device tensor without a host sync: staged through pinned memory
+    (torch's caching host allocator keeps the buffer alive until the copy ran)."""
+    t = torch.from_numpy(np.ascontiguousarray(arr))
+    if torch.device(device).type != "cuda":
+        return t.clone()
+    return t.pin_memory().to(device, non_blocking=True)
+
+
 @dataclass
 class MessageSpan:
     """Where one message lives (reference cache.py:28-39)."""
@@ -113,8 +122,8 @@ class _Grow:
 
     def sync(self) -> None:
         if self.hi > self.lo:
-            self.dev[self.lo:self.hi].copy_(torch.from_numpy(self.host[self.lo:self.hi]),
-                                            non_blocking=False)
+            self.dev[self.lo:self.hi].copy_(h2d(self.host[self.lo:self.hi], self.device),
+                                            non_blocking=True)
             self.lo, self.hi = len(self.host), 0
 
 
@@ -316,7 +325,7 @@ class DeviceKvCache:
             moved += e.length
         if pages:
             self._views = None
-            arr = torch.from_numpy(np.asarray([pages, lens, deltas], dtype=np.int32)).to(self.device)
+            arr = h2d(np.asarray([pages, lens, deltas], dtype=np.int32), self.device)
             cfg = self.config
             nat.rerotate(self.k_pool.data_ptr(), nat.dtype_code(self.dtype), cfg.n_layers,
                          cfg.kv_heads, self.n_pages, P, cfg.head_dim, arr[0].data_ptr(),
@@ -395,6 +404,19 @@ class DeviceKvCache:
                 fh.write(json.dumps({"physical_index": i, "m": int(v["msg_ids"][i]),
                                      "j": int(v["positions"][i]),
                                      "token_id": int(v["token_ids"][i])}) + "\n")
+
+    def reset(self) -> None:
+        """Drop every message and free every page; pool storage is kept (no realloc)."""
+        self._free = list(range(self.n_pages - 1, -1, -1))
+        self._messages = {}
+        self.msg_len = _Grow(64, self.device)
+        self.msg_pt = _Grow(64, self.device)
+        self.page_table = _Grow(1024, self.device, fill=-1)
+        self._pt_next = 0
+        self.token_count = 0
+        self._log = []
+        self._nphys = 0
+        self._views = None
 
     def clone(self) -> "DeviceKvCache":
         """Deep copy: pools (device copy), page tables and host metadata."""

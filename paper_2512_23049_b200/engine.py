@@ -187,6 +187,7 @@ class Engine:
         self._generatable = generatable_mask(self.config.vocab_size)
         self._next_id = 0
         self.stats: list[CallStats] = []
+        self.d2h_bytes = 0
 
     # -- public API (engine.py:153-199) ------------------------------------------------
 
@@ -227,7 +228,17 @@ class Engine:
         other._generatable = self._generatable
         other._next_id = self._next_id
         other.stats = []
+        other.d2h_bytes = 0
         return other
+
+    def reset(self) -> None:
+        """Empty the cache and restart message ids (pool storage is reused).
+
+        Not in the reference API: lets benchmarks run many workflow instances on
+        one resident engine without reallocating the HBM pool."""
+        self.cache.reset()
+        self._next_id = 0
+        self.stats = []
 
     @property
     def last_stats(self) -> CallStats:
@@ -381,12 +392,16 @@ class Engine:
                                   torch.cuda.current_stream(self.device).cuda_stream)
                 self._runner.launches += 1
                 greedy_tok = out.cpu().numpy()
+                self.d2h_bytes += out.nbytes
             host_logits = None
             if self.record_logits or any(s.forced is None and s.call.sampling.mode != "greedy"
                                          for s in owners):
                 hl = logits.double().cpu().numpy()
+                self.d2h_bytes += logits.nbytes
                 host_logits = hl[:n_own] + hl[n_own:] if split else hl
-            else:
+            elif greedy_tok is None and any(s.sel == 0 for s in owners):
+                # all forced: the host already knows the tokens; synchronise only at a
+                # message's first selection so its TTFT is the time its logits exist
                 torch.cuda.current_stream(self.device).synchronize()
             for i, s in enumerate(owners):
                 if stats.logits is not None:

@@ -24,7 +24,7 @@ import numpy as np
 import torch
 
 from . import _native as nat
-from .cache import DeviceKvCache, RotationTableDevice, cdiv
+from .cache import DeviceKvCache, RotationTableDevice, cdiv, h2d
 from .weights import DeviceWeights
 
 RMS_EPS = 1e-6  # model.py:28
@@ -87,6 +87,11 @@ class Runner:
         G = self.cfg.n_heads // self.cfg.kv_heads
         self.rows_per_block = max(1, min(16, 64 // G))
         self.launches = 0  # our kernels launched (for bench accounting)
+        self.h2d_bytes = 0  # per-step metadata uploads (bench e2e accounting)
+        # When set to a list, attention launches are bracketed with CUDA events on the
+        # launching stream and (start, end, algorithmic_bytes) tuples are appended.
+        self.attn_events = None
+        self.step_events = None  # when a list: (start, end) events around each step's GPU work
         # bf16 engines carry GEMM activations as hi/lo bf16 pairs (see choreo_b200.h)
         self.split = self.dt == torch.bfloat16 and split_activations
 
@@ -94,6 +99,21 @@ class Runner:
         if out_f32 and a.dtype != torch.float32:
             return torch.mm(a, w.t(), out_dtype=torch.float32)
         return torch.mm(a, w.t())
+
+    def _attn_algorithmic_bytes(self, plan: StepPlan, msg_len, R: int, n_parts: int) -> int:
+        """unique KV bytes the step's attention must read (each visible
+        page once, valid slots only) + q read + partials written, for one layer."""
+        cfg, P = self.cfg, self.cache.page_size
+        seen: dict = {}
+        for c in plan.calls:
+            for p in c.parents:
+                seen[p] = int(msg_len[p])
+            own = c.first_t + len(c.tokens)
+            seen[c.msg] = max(seen.get(c.msg, 0), own)
+        toks = sum(seen.values())
+        elt = self.cache.k_pool.element_size()
+        return (2 * toks * cfg.kv_heads * cfg.head_dim * elt + R * cfg.n_heads * cfg.head_dim * 4
+                + n_parts * cfg.n_heads * (cfg.head_dim + 1) * 4)
 
     def forward(self, plan: StepPlan) -> torch.Tensor | None:
         """Run one step; returns f32 logits [S * n_logit_rows, V] (S = 2 when split:
@@ -131,7 +151,14 @@ class Runner:
         ints = np.concatenate([ids, row_t, pos, pages, slots, np.asarray(call_tab, np.int32),
                                np.asarray(parents + [0], np.int32),
                                np.asarray(plan.logit_rows, np.int32)])
-        dints = torch.from_numpy(ints).to(self.dev, non_blocking=False)
+        dints = h2d(ints, self.dev)
+        self.h2d_bytes += ints.nbytes
+        if self.step_events is not None:
+            sev0 = torch.cuda.Event(enable_timing=True)
+            sev0.record()
+        attn_bytes = 0
+        if self.attn_events is not None:
+            attn_bytes = self._attn_algorithmic_bytes(plan, msg_len, R, n_parts)
         o = 0
 
         def take(n):
@@ -178,11 +205,18 @@ class Runner:
                             cache.k_pool.data_ptr(), cache.v_pool.data_ptr(), self.pool_dtc, layer,
                             Hk, cache.n_pages, P, H, hd, self.rot.cos.data_ptr(),
                             self.rot.sin.data_ptr(), self.rot.max_delta, stream)
+            if self.attn_events is not None:
+                ev0 = torch.cuda.Event(enable_timing=True)
+                ev1 = torch.cuda.Event(enable_timing=True)
+                ev0.record()
             nat.attn_split(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(),
                            self.pool_dtc, layer, Hk, cache.n_pages, P, H, hd, rowt_d.data_ptr(),
                            vis[0].data_ptr(), vis[1].data_ptr(), vis[2].data_ptr(),
                            items.data_ptr(), counts.data_ptr(), n_items, part_o.data_ptr(),
                            part_lse.data_ptr(), 0, stream)
+            if self.attn_events is not None:
+                ev1.record()
+                self.attn_events.append((ev0, ev1, attn_bytes))
             nat.attn_combine(part_o.data_ptr(), part_lse.data_ptr(), row_part.data_ptr(), R, H,
                              hd, attn.data_ptr(), self.dtc, sp, stream)
             ao = self._mm(attn, lw["wo"], out_f32=True)
@@ -198,11 +232,16 @@ class Runner:
                              None, 0, 0, None, 0, stream)
         launches += 1
         self.launches += launches
-        if n_log == 0:
-            return None
-        xn = torch.empty(S * n_log, d, dtype=self.dt, device=self.dev)
-        nat.residual_rmsnorm(x.data_ptr(), None, 0, 0, self.w.out_norm.data_ptr(), self.dtc, R, d,
-                             RMS_EPS, xn.data_ptr(), self.dtc, sp, logit_d.data_ptr(), n_log,
-                             stream)
-        self.launches += 1
-        return self._mm(xn, self.w.out_head, out_f32=True)
+        logits = None
+        if n_log:
+            xn = torch.empty(S * n_log, d, dtype=self.dt, device=self.dev)
+            nat.residual_rmsnorm(x.data_ptr(), None, 0, 0, self.w.out_norm.data_ptr(), self.dtc,
+                                 R, d, RMS_EPS, xn.data_ptr(), self.dtc, sp, logit_d.data_ptr(),
+                                 n_log, stream)
+            self.launches += 1
+            logits = self._mm(xn, self.w.out_head, out_f32=True)
+        if self.step_events is not None:
+            sev1 = torch.cuda.Event(enable_timing=True)
+            sev1.record()
+            self.step_events.append((sev0, sev1))
+        return logits
