@@ -93,20 +93,26 @@ int choreo_rerotate(void* k_pool, int pool_dtype, int n_layers, int n_kv, int n_
                     const int32_t* delta, int n_list, const float* cos_t, const float* sin_t,
                     int max_delta, void* stream);
 
-/* K3 assemble: prompt assembly on device.  Inputs (device int32):
+/* K3 assemble: page-centric prompt assembly on device.  Inputs (device int32):
  *   msg_len[m], msg_pt[m] (offset of message m's page chain in page_table), page_table[]
  *   calls[5*c..]: {own msg, parent offset, parent count, row offset, row count}
  *   call_parents[]: parent message ids, in the call's parent order
  *   row_t[r]: the row's within-message token index (rows grouped by call, ascending t);
  *             the row sees its own message's tokens 0..t
  *   patch[2*i], patch[2*i+1]: page_table[patch[2i]] = patch[2i+1], applied first
+ * Work is grouped page-centrically: every distinct parent message of the step is one
+ * group whose viewers are all rows of all calls listing it (read once for all of
+ * them); each call's own pages form a causal group for its own rows.  Groups are
+ * split into items of <= rows_per_block rows x <= pages_per_item pages.
  * Outputs (device int32):
- *   vis_page[], vis_len[], vis_own[]: each call's visible page list — parent pages in
- *       parent order (vis_own = -1), then own pages up to the call's last row
- *       (vis_own = own token index of slot 0); pages past a block's last row are skipped
- *   items[6*i..]: {row_begin, n_rows, vis_begin, n_vis_pages, part_base, call}
- *   row_part[3*r..]: {first partial of the row, partial stride, partial count}
- *   counts[0..3] = {n_vis_pages, n_items, n_partials, status (0 ok, -1 over capacity)}
+ *   vis_page[], vis_len[], vis_own[]: visible pages (each distinct parent once, in
+ *       ascending message id, vis_own = -1; then each call's own pages up to its last
+ *       row, vis_own = own token index of slot 0)
+ *   blk_rows[]: row ids of every row block
+ *   items[6*i..]: {blk_rows offset, n_rows, vis offset, n_pages, partial base, group}
+ *       (group >= 0: parent group index; -1-c: own pages of call c)
+ *   row_part_off[n_rows + 1], row_part[]: per-row CSR list of the partial slots to merge
+ *   counts[0..3] = {n_vis_pages, n_items, n_partials, status (0 ok, <0 over capacity)}
  * Visibility is exactly reference masking.py:36-53 (parents' tokens + own tokens with
  * j <= query j) at page granularity; tests expand it to token level against the oracle.
  * Replaces engine.py:203-245 layout + masking.py:43-53 visible_cache_indices. */
@@ -114,27 +120,30 @@ int choreo_assemble(const int32_t* msg_len, const int32_t* msg_pt, int32_t* page
                     const int32_t* calls, const int32_t* call_parents, int n_calls,
                     const int32_t* row_t, int n_rows, const int32_t* patch, int n_patch,
                     int page_size, int rows_per_block, int pages_per_item, int32_t* vis_page,
-                    int32_t* vis_len, int32_t* vis_own, int32_t* items, int32_t* row_part,
-                    int32_t* counts, int cap_pages, int cap_items, int cap_parts, void* stream);
+                    int32_t* vis_len, int32_t* vis_own, int32_t* blk_rows, int32_t* items,
+                    int32_t* row_part_off, int32_t* row_part, int32_t* counts, int cap_vis,
+                    int cap_blk_rows, int cap_items, int cap_parts, void* stream);
 
 /* K5 split-KV attention over assembled work items (prefill and decode rows alike).
  * q: f32 [n_rows][n_heads][hd] (already rotated, K1).  For each item and KV head writes
  * per-(row, q-head) partials: part_o f32 [n_partials][n_heads][hd] (normalised) and
  * part_lse f32 [n_partials][n_heads] (natural-log sum-exp; -inf if nothing visible).
- * grid_ctas = number of persistent CTAs (0 = auto).  Replaces model.py:177-184 +
- * tensor.py:65-75 (gather, concat, scores, masked softmax, PV). */
+ * bf16 pools with page_size 64 and hd 64/128 run on tensor cores (mma.sync, cp.async
+ * 3-stage page pipeline); f32 pools run the SIMT f32 path.  grid_ctas = persistent CTAs
+ * (0 = auto).  Replaces model.py:177-184 + tensor.py:65-75 (gather, concat, scores,
+ * masked softmax, P.V). */
 int choreo_attn_split(const float* q, const void* k_pool, const void* v_pool, int pool_dtype,
                       int layer, int n_kv, int n_pages, int page_size, int n_heads, int head_dim,
                       const int32_t* row_t, const int32_t* vis_page, const int32_t* vis_len,
-                      const int32_t* vis_own, const int32_t* items, const int32_t* counts,
-                      int max_items, float* part_o, float* part_lse, int grid_ctas,
-                      void* stream);
+                      const int32_t* vis_own, const int32_t* blk_rows, const int32_t* items,
+                      const int32_t* counts, int max_items, float* part_o, float* part_lse,
+                      int grid_ctas, void* stream);
 
-/* Combine partials into out[r][h][:] (out_dtype; hi/lo pair if out_split) with the
- * LSE merge. */
-int choreo_attn_combine(const float* part_o, const float* part_lse, const int32_t* row_part,
-                        int n_rows, int n_heads, int head_dim, void* out, int out_dtype,
-                        int out_split, void* stream);
+/* Combine each row's partials (CSR row_part_off / row_part, <= 512 per row) into
+ * out[r][h][:] (out_dtype; hi/lo pair if out_split) with the LSE merge. */
+int choreo_attn_combine(const float* part_o, const float* part_lse, const int32_t* row_part_off,
+                        const int32_t* row_part, int n_rows, int n_heads, int head_dim, void* out,
+                        int out_dtype, int out_split, void* stream);
 
 /* K6 select: greedy argmax over generatable ids {0..255, 257} with first-index
  * tie-break, one row per logits row (engine.py:371, tokenizer.py:39-44). */

@@ -30,10 +30,10 @@ SIGNATURES: dict[str, list] = {
                            _I, _P, _P, _I, _P],
     "choreo_rerotate": [_P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _I, _P, _P, _I, _P],
     "choreo_assemble": [_P, _P, _P, _P, _P, _I, _P, _I, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P,
-                        _P, _I, _I, _I, _P],
-    "choreo_attn_split": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _P,
-                          _P, _I, _P],
-    "choreo_attn_combine": [_P, _P, _P, _I, _I, _I, _P, _I, _I, _P],
+                        _P, _P, _P, _I, _I, _I, _I, _P],
+    "choreo_attn_split": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P,
+                          _I, _P, _P, _I, _P],
+    "choreo_attn_combine": [_P, _P, _P, _P, _I, _I, _I, _P, _I, _I, _P],
     "choreo_select_greedy": [_P, _I, _I, _I, _I, _P, _P],
 }
 EXTRA = ["choreo_abi_version", "choreo_last_error"]

@@ -1,138 +1,285 @@
-// K3 assemble: prompt assembly on device.
+// K3 assemble: prompt assembly on device, page-centric.
 //
-// For every call of a step it emits the visible page list — the parents' pages in
-// parent order, then the call's own pages up to its last row — and splits each
-// row block's prefix of that list into split-KV work items.  This is the page-level
-// form of the reference's visibility (masking.py:36-53: a query sees all tokens of
-// every parent, plus its own message's tokens with j <= its own j) and of the
-// engine's per-call layout (engine.py:203-245, 277, 317).  Because every page holds
-// tokens of exactly one message, the visible set of a call is an exact page subset
-// plus a causal cut inside the own message; pages of the own message wholly after a
-// block's last row are skipped (whole-tile skip).
+// A step encodes new-token rows for several calls (messages).  The reference's
+// visibility (masking.py:36-53) says a row of call c sees every token of every
+// parent of c, plus the tokens of its own message up to its own j.  Since each
+// page holds tokens of one message, that is an exact page subset plus a causal
+// cut inside the own pages.  This kernel turns the step's calls into split-KV
+// work items that read each parent message ONCE per step for all the rows that
+// can see it (agents of a parallel decode share most parents):
+//
+//   group  = one distinct parent message p and its viewers (the rows of every call
+//            that lists p), split into blocks of <= rows_per_block rows;
+//   own    = one call's rows against its own pages (causal), same blocking;
+//   item   = (row block, run of <= pages_per_item pages of the group's / own list).
+//
+// Outputs: the visible page lists (each distinct parent's pages once, then each
+// call's own pages up to its last row), the row list of every block, the items,
+// and per row the list of partial-result slots the combine step merges.
+// Single CTA: steps have at most a few thousand (parent, call) pairs.
 #include "common.cuh"
 
 namespace choreo {
 
 constexpr int kMaxCalls = 1024;
+constexpr int kMaxPairs = 4096;
 constexpr int kCallFields = 5;  // msg, par_off, par_cnt, row_off, row_cnt
-
-struct CallPlan {
-  int parent_pages;  // pages of all parents
-  int vis;           // parent pages + own pages up to the call's last row
-  int items;
-  int parts;
-};
+constexpr int kThreads3 = 512;
 
 __device__ __forceinline__ int cdiv(int a, int b) { return (a + b - 1) / b; }
 
-__device__ void plan_call(const int32_t* call, const int32_t* call_parents,
-                          const int32_t* msg_len, const int32_t* row_t, int P, int rpb, int ppi,
-                          CallPlan& cp) {
-  const int par_off = call[1], par_cnt = call[2], row_off = call[3], row_cnt = call[4];
-  int pp = 0;
-  for (int i = 0; i < par_cnt; ++i) pp += cdiv(msg_len[call_parents[par_off + i]], P);
-  cp.parent_pages = pp;
-  cp.vis = cp.items = cp.parts = 0;
-  if (row_cnt <= 0) return;
-  cp.vis = pp + row_t[row_off + row_cnt - 1] / P + 1;
-  for (int b = 0; b * rpb < row_cnt; ++b) {
-    const int nr = min(rpb, row_cnt - b * rpb);
-    const int t_hi = row_t[row_off + b * rpb + nr - 1];
-    const int chunks = cdiv(pp + t_hi / P + 1, ppi);
-    cp.items += chunks;
-    cp.parts += chunks * nr;
+struct K3Params {
+  const int32_t* msg_len;
+  const int32_t* msg_pt;
+  int32_t* page_table;
+  const int32_t* calls;
+  const int32_t* call_parents;
+  int n_calls;
+  const int32_t* row_t;
+  int n_rows;
+  const int32_t* patch;
+  int n_patch;
+  int P, rpb, ppi;
+  int32_t* vis_page;
+  int32_t* vis_len;
+  int32_t* vis_own;
+  int32_t* blk_rows;
+  int32_t* items;
+  int32_t* row_part_off;  // [n_rows + 1]
+  int32_t* row_part;      // partial slots, CSR by row
+  int32_t* counts;
+  int cap_vis, cap_blk_rows, cap_items, cap_parts;
+};
+
+// smem-resident plan
+struct Shared {
+  uint32_t key[kMaxPairs];  // (parent << 11 | call) sorted
+  int n_pairs;
+  int n_groups;
+  int g_first[kMaxPairs];   // first pair index of group g
+  int g_vis[kMaxPairs], g_rows[kMaxPairs], g_item[kMaxPairs], g_part[kMaxPairs];
+  int c_vis[kMaxCalls], c_rows[kMaxCalls], c_item[kMaxCalls], c_part[kMaxCalls];
+  int tot_vis, tot_rows, tot_items, tot_parts, overflow;
+};
+
+__global__ void __launch_bounds__(kThreads3) assemble_kernel(K3Params p) {
+  extern __shared__ unsigned char smem_raw[];
+  Shared& S = *reinterpret_cast<Shared*>(smem_raw);
+  const int tid = threadIdx.x;
+  for (int i = tid; i < p.n_patch; i += blockDim.x) p.page_table[p.patch[2 * i]] = p.patch[2 * i + 1];
+  // ---- (parent, call) pairs, sorted by parent then call ----
+  if (tid == 0) {
+    int n = 0;
+    for (int c = 0; c < p.n_calls; ++c) n += p.calls[kCallFields * c + 2];
+    S.n_pairs = n;
+    S.overflow = n > kMaxPairs;
   }
-}
-
-__global__ void assemble_kernel(const int32_t* __restrict__ msg_len,
-                                const int32_t* __restrict__ msg_pt, int32_t* __restrict__ page_table,
-                                const int32_t* __restrict__ calls,
-                                const int32_t* __restrict__ call_parents, int n_calls,
-                                const int32_t* __restrict__ row_t, const int32_t* __restrict__ patch,
-                                int n_patch, int P, int rpb, int ppi, int32_t* __restrict__ vis_page,
-                                int32_t* __restrict__ vis_len, int32_t* __restrict__ vis_own,
-                                int32_t* __restrict__ items, int32_t* __restrict__ row_part,
-                                int32_t* __restrict__ counts, int cap_pages, int cap_items,
-                                int cap_parts) {
-  __shared__ CallPlan plan[kMaxCalls];
-  __shared__ int base_vis[kMaxCalls], base_item[kMaxCalls], base_part[kMaxCalls];
-  __shared__ int overflow;
-
-  for (int i = threadIdx.x; i < n_patch; i += blockDim.x) page_table[patch[2 * i]] = patch[2 * i + 1];
-  if (threadIdx.x == 0) overflow = 0;
   __syncthreads();
-
-  for (int c = threadIdx.x; c < n_calls; c += blockDim.x)
-    plan_call(calls + kCallFields * c, call_parents, msg_len, row_t, P, rpb, ppi, plan[c]);
+  if (S.overflow) {
+    if (tid == 0) { p.counts[1] = 0; p.counts[3] = -2; }
+    return;
+  }
+  const int NP = S.n_pairs;
+  for (int c = tid; c < p.n_calls; c += blockDim.x) {
+    const int32_t* cl = p.calls + kCallFields * c;
+    for (int i = 0; i < cl[2]; ++i)
+      S.key[cl[1] + i] = ((uint32_t)p.call_parents[cl[1] + i] << 11) | (uint32_t)c;
+  }
+  int np2 = 1;
+  while (np2 < NP) np2 <<= 1;
+  for (int i = NP + tid; i < np2; i += blockDim.x) S.key[i] = 0xffffffffu;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int v = 0, it = 0, pa = 0;
-    for (int c = 0; c < n_calls; ++c) {
-      base_vis[c] = v;
-      base_item[c] = it;
-      base_part[c] = pa;
-      v += plan[c].vis;
-      it += plan[c].items;
-      pa += plan[c].parts;
+  for (int k = 2; k <= np2; k <<= 1)  // bitonic sort
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < np2; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const uint32_t a = S.key[i], b = S.key[l];
+          if (((i & k) == 0) == (a > b)) { S.key[i] = b; S.key[l] = a; }
+        }
+      }
+      __syncthreads();
     }
-    overflow = (v > cap_pages) || (it > cap_items) || (pa > cap_parts);
-    counts[0] = v;
-    counts[1] = overflow ? 0 : it;  // an overflowing plan launches no attention work
-    counts[2] = pa;
-    counts[3] = overflow ? -1 : 0;
+  // ---- groups and per-group / per-call sizes ----
+  if (tid == 0) {
+    int g = 0;
+    for (int i = 0; i < NP; ++i)
+      if (i == 0 || (S.key[i] >> 11) != (S.key[i - 1] >> 11)) S.g_first[g++] = i;
+    S.g_first[g] = NP;
+    S.n_groups = g;
   }
   __syncthreads();
-  if (overflow) return;
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, n_warps = blockDim.x >> 5;
-  for (int c = warp; c < n_calls; c += n_warps) {
-    const int32_t* call = calls + kCallFields * c;
-    const int own_msg = call[0], par_off = call[1], par_cnt = call[2], row_off = call[3],
-              row_cnt = call[4];
+  const int NG = S.n_groups;
+  for (int g = tid; g < NG; g += blockDim.x) {
+    const int msg = S.key[S.g_first[g]] >> 11;
+    int rows = 0;
+    for (int i = S.g_first[g]; i < S.g_first[g + 1]; ++i) rows += p.calls[kCallFields * (S.key[i] & 2047) + 4];
+    const int pages = cdiv(p.msg_len[msg], p.P);
+    const int chunks = cdiv(pages, p.ppi);
+    S.g_vis[g] = pages;
+    S.g_rows[g] = rows;
+    S.g_item[g] = rows ? cdiv(rows, p.rpb) * chunks : 0;
+    S.g_part[g] = rows ? chunks * rows : 0;
+  }
+  for (int c = tid; c < p.n_calls; c += blockDim.x) {
+    const int32_t* cl = p.calls + kCallFields * c;
+    const int row_off = cl[3], row_cnt = cl[4];
+    S.c_vis[c] = S.c_rows[c] = S.c_item[c] = S.c_part[c] = 0;
     if (row_cnt <= 0) continue;
-    // visible page list: parents in order, then own pages
-    int w = base_vis[c];
-    for (int i = 0; i < par_cnt; ++i) {
-      const int p = call_parents[par_off + i];
-      const int len = msg_len[p], pt = msg_pt[p], np = cdiv(len, P);
-      for (int j = lane; j < np; j += 32) {
-        vis_page[w + j] = page_table[pt + j];
-        vis_len[w + j] = min(P, len - j * P);
-        vis_own[w + j] = -1;
-      }
-      w += np;
+    S.c_vis[c] = p.row_t[row_off + row_cnt - 1] / p.P + 1;
+    S.c_rows[c] = row_cnt;
+    for (int b = 0; b * p.rpb < row_cnt; ++b) {
+      const int nr = min(p.rpb, row_cnt - b * p.rpb);
+      const int ch = cdiv(p.row_t[row_off + b * p.rpb + nr - 1] / p.P + 1, p.ppi);
+      S.c_item[c] += ch;
+      S.c_part[c] += ch * nr;
     }
-    const int t_max = row_t[row_off + row_cnt - 1];
-    const int own_pages = t_max / P + 1, opt = msg_pt[own_msg];
+  }
+  __syncthreads();
+  // ---- exclusive scans (serial: groups + calls are small) ----
+  if (tid == 0) {
+    int v = 0, r = 0, it = 0, pa = 0;
+    for (int g = 0; g < NG; ++g) {
+      int t;
+      t = S.g_vis[g]; S.g_vis[g] = v; v += t;
+      t = S.g_rows[g]; S.g_rows[g] = r; r += t;
+      t = S.g_item[g]; S.g_item[g] = it; it += t;
+      t = S.g_part[g]; S.g_part[g] = pa; pa += t;
+    }
+    for (int c = 0; c < p.n_calls; ++c) {
+      int t;
+      t = S.c_vis[c]; S.c_vis[c] = v; v += t;
+      t = S.c_rows[c]; S.c_rows[c] = r; r += t;
+      t = S.c_item[c]; S.c_item[c] = it; it += t;
+      t = S.c_part[c]; S.c_part[c] = pa; pa += t;
+    }
+    S.tot_vis = v; S.tot_rows = r; S.tot_items = it; S.tot_parts = pa;
+    S.overflow = v > p.cap_vis || r > p.cap_blk_rows || it > p.cap_items || pa > p.cap_parts;
+    p.counts[0] = v;
+    p.counts[1] = S.overflow ? 0 : it;
+    p.counts[2] = pa;
+    p.counts[3] = S.overflow ? -1 : 0;
+  }
+  __syncthreads();
+  if (S.overflow) return;
+  // ---- per-row partial counts -> CSR offsets ----
+  // row r of call c: sum over parents p of chunks(p) + own chunks of its block
+  for (int c = tid; c < p.n_calls; c += blockDim.x) {
+    const int32_t* cl = p.calls + kCallFields * c;
+    int par_chunks = 0;
+    for (int i = 0; i < cl[2]; ++i) par_chunks += cdiv(cdiv(p.msg_len[p.call_parents[cl[1] + i]], p.P), p.ppi);
+    for (int b = 0; b * p.rpb < cl[4]; ++b) {
+      const int nr = min(p.rpb, cl[4] - b * p.rpb);
+      const int ch = cdiv(p.row_t[cl[3] + b * p.rpb + nr - 1] / p.P + 1, p.ppi);
+      for (int j = 0; j < nr; ++j) p.row_part_off[cl[3] + b * p.rpb + j + 1] = par_chunks + ch;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    p.row_part_off[0] = 0;
+    for (int r = 0; r < p.n_rows; ++r) p.row_part_off[r + 1] += p.row_part_off[r];
+  }
+  __syncthreads();
+  // fill cursor per row: reuse g_* / c_* are still needed; keep a per-row running
+  // position in the row_part array by walking groups in order (one warp per call
+  // would race), so groups are filled serially per row below.
+  const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+  // ---- groups: pages, block rows, items, partial slots ----
+  for (int g = warp; g < NG; g += nw) {
+    const int msg = S.key[S.g_first[g]] >> 11;
+    const int len = p.msg_len[msg], pt = p.msg_pt[msg], pages = cdiv(len, p.P);
+    const int vb = S.g_vis[g];
+    for (int j = lane; j < pages; j += 32) {
+      p.vis_page[vb + j] = p.page_table[pt + j];
+      p.vis_len[vb + j] = min(p.P, len - j * p.P);
+      p.vis_own[vb + j] = -1;
+    }
+    // block rows: concatenated row ranges of the viewer calls (ascending call)
+    int rb = S.g_rows[g], w = 0;
+    for (int i = S.g_first[g]; i < S.g_first[g + 1]; ++i) {
+      const int32_t* cl = p.calls + kCallFields * (S.key[i] & 2047);
+      for (int j = lane; j < cl[4]; j += 32) p.blk_rows[rb + w + j] = cl[3] + j;
+      w += cl[4];
+    }
+    const int rows = w, chunks = cdiv(pages, p.ppi), nb = cdiv(rows, p.rpb);
+    for (int k = lane; k < nb * chunks; k += 32) {
+      const int b = k / chunks, ch = k % chunks;
+      const int nr = min(p.rpb, rows - b * p.rpb);
+      int32_t* it = p.items + 6 * (S.g_item[g] + k);
+      it[0] = rb + b * p.rpb;
+      it[1] = nr;
+      it[2] = vb + ch * p.ppi;
+      it[3] = min(p.ppi, pages - ch * p.ppi);
+      it[4] = S.g_part[g] + ch * rows + b * p.rpb;
+      it[5] = g;
+    }
+  }
+  // ---- own pages, rows, items ----
+  for (int c = warp; c < p.n_calls; c += nw) {
+    const int32_t* cl = p.calls + kCallFields * c;
+    const int row_off = cl[3], row_cnt = cl[4];
+    if (row_cnt <= 0) continue;
+    const int t_max = p.row_t[row_off + row_cnt - 1];
+    const int own_pages = t_max / p.P + 1, opt = p.msg_pt[cl[0]], vb = S.c_vis[c];
     for (int j = lane; j < own_pages; j += 32) {
-      vis_page[w + j] = page_table[opt + j];
-      vis_len[w + j] = min(P, t_max + 1 - j * P);
-      vis_own[w + j] = j * P;
+      p.vis_page[vb + j] = p.page_table[opt + j];
+      p.vis_len[vb + j] = min(p.P, t_max + 1 - j * p.P);
+      p.vis_own[vb + j] = j * p.P;
     }
-    // row blocks -> split-KV items; partials of a block are [chunk][row]
-    const int pp = plan[c].parent_pages;
-    int it = base_item[c], pa = base_part[c];
-    const int n_blocks = cdiv(row_cnt, rpb);
-    for (int b = 0; b < n_blocks; ++b) {
-      const int r0 = row_off + b * rpb, nr = min(rpb, row_cnt - b * rpb);
-      const int nvis = pp + row_t[r0 + nr - 1] / P + 1;
-      const int chunks = cdiv(nvis, ppi);
-      for (int k = lane; k < chunks; k += 32) {
-        int32_t* item = items + 6 * (it + k);
-        item[0] = r0;
-        item[1] = nr;
-        item[2] = base_vis[c] + k * ppi;
-        item[3] = min(ppi, nvis - k * ppi);
-        item[4] = pa + k * nr;
-        item[5] = c;
+    const int rb = S.c_rows[c];
+    for (int j = lane; j < row_cnt; j += 32) p.blk_rows[rb + j] = row_off + j;
+    if (lane == 0) {
+      int it = S.c_item[c], pa = S.c_part[c];
+      for (int b = 0; b * p.rpb < row_cnt; ++b) {
+        const int nr = min(p.rpb, row_cnt - b * p.rpb);
+        const int nvis = p.row_t[row_off + b * p.rpb + nr - 1] / p.P + 1;
+        const int chunks = cdiv(nvis, p.ppi);
+        for (int ch = 0; ch < chunks; ++ch) {
+          int32_t* item = p.items + 6 * (it + ch);
+          item[0] = rb + b * p.rpb;
+          item[1] = nr;
+          item[2] = vb + ch * p.ppi;
+          item[3] = min(p.ppi, nvis - ch * p.ppi);
+          item[4] = pa + ch * nr;
+          item[5] = -1 - c;
+        }
+        it += chunks;
+        pa += chunks * nr;
       }
-      for (int r = lane; r < nr; r += 32) {
-        row_part[3 * (r0 + r)] = pa + r;
-        row_part[3 * (r0 + r) + 1] = nr;
-        row_part[3 * (r0 + r) + 2] = chunks;
+    }
+  }
+  __syncthreads();
+  // ---- per-row partial slot lists (CSR) ----
+  // Row r (call c, local index j in its call) gets, in order: for each group g
+  // viewing c (ascending parent id) its chunks' slots, then its own chunks' slots.
+  for (int c = warp; c < p.n_calls; c += nw) {
+    const int32_t* cl = p.calls + kCallFields * c;
+    const int row_off = cl[3], row_cnt = cl[4];
+    for (int j = lane; j < row_cnt; j += 32) {
+      const int r = row_off + j;
+      int w = p.row_part_off[r];
+      for (int g = 0; g < NG; ++g) {
+        // is call c a viewer of group g, and at which row index within the group?
+        int base = 0, found = -1;
+        for (int i = S.g_first[g]; i < S.g_first[g + 1]; ++i) {
+          const int cc = S.key[i] & 2047;
+          if (cc == c) { found = base; break; }
+          base += p.calls[kCallFields * cc + 4];
+        }
+        if (found < 0) continue;
+        const int msg = S.key[S.g_first[g]] >> 11;
+        const int chunks = cdiv(cdiv(p.msg_len[msg], p.P), p.ppi);
+        const int rows_g = (g + 1 < NG ? S.g_rows[g + 1] : S.c_rows[0]) - S.g_rows[g];
+        for (int ch = 0; ch < chunks; ++ch) p.row_part[w++] = S.g_part[g] + ch * rows_g + found + j;
       }
-      it += chunks;
-      pa += chunks * nr;
+      const int b = j / p.rpb, nr = min(p.rpb, row_cnt - b * p.rpb);
+      int pa = S.c_part[c];
+      for (int bb = 0; bb < b; ++bb) {
+        const int nrb = min(p.rpb, row_cnt - bb * p.rpb);
+        pa += cdiv(p.row_t[row_off + bb * p.rpb + nrb - 1] / p.P + 1, p.ppi) * nrb;
+      }
+      const int chunks = cdiv(p.row_t[row_off + b * p.rpb + nr - 1] / p.P + 1, p.ppi);
+      for (int ch = 0; ch < chunks; ++ch) p.row_part[w++] = pa + ch * nr + (j - b * p.rpb);
     }
   }
 }
@@ -146,17 +293,25 @@ extern "C" int choreo_assemble(const int32_t* msg_len, const int32_t* msg_pt, in
                                const int32_t* row_t, int n_rows, const int32_t* patch,
                                int n_patch, int page_size, int rows_per_block, int pages_per_item,
                                int32_t* vis_page, int32_t* vis_len, int32_t* vis_own,
-                               int32_t* items, int32_t* row_part, int32_t* counts,
-                               int cap_pages, int cap_items, int cap_parts, void* stream) {
+                               int32_t* blk_rows, int32_t* items, int32_t* row_part_off,
+                               int32_t* row_part, int32_t* counts, int cap_vis, int cap_blk_rows,
+                               int cap_items, int cap_parts, void* stream) {
   if (!msg_len || !msg_pt || !page_table || !calls || !row_t || !vis_page || !vis_len ||
-      !vis_own || !items || !row_part || !counts)
+      !vis_own || !blk_rows || !items || !row_part_off || !row_part || !counts)
     return CHOREO_EINVAL;
   if (n_calls < 0 || n_calls > kMaxCalls || n_rows < 0 || page_size <= 0 ||
       rows_per_block <= 0 || pages_per_item <= 0 || (n_patch > 0 && !patch))
     return CHOREO_EINVAL;
-  assemble_kernel<<<1, 256, 0, as_stream(stream)>>>(
-      msg_len, msg_pt, page_table, calls, call_parents, n_calls, row_t, patch, n_patch,
-      page_size, rows_per_block, pages_per_item, vis_page, vis_len, vis_own, items, row_part,
-      counts, cap_pages, cap_items, cap_parts);
+  K3Params p{msg_len, msg_pt, page_table, calls, call_parents, n_calls, row_t, n_rows, patch,
+             n_patch, page_size, rows_per_block, pages_per_item, vis_page, vis_len, vis_own,
+             blk_rows, items, row_part_off, row_part, counts, cap_vis, cap_blk_rows, cap_items,
+             cap_parts};
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(Shared));
+    attr = true;
+  }
+  assemble_kernel<<<1, kThreads3, sizeof(Shared), as_stream(stream)>>>(p);
   return launch_status("choreo_assemble");
 }

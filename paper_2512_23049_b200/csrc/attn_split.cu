@@ -1,23 +1,24 @@
-// K5 split-KV choreographed attention over assembled work items (SIMT f32 math).
+// K5 split-KV choreographed attention over K3 work items.
 //
-// A work item is (row block, run of visible pages) from K3; a CTA takes one
-// (item, kv head) pair and all G = n_heads / n_kv query heads of that KV head (GQA),
-// so each K/V page is read once per item for G*rows query vectors.  Scores, the
-// masked online softmax and P.V run in f32 (reference model.py:177-184,
-// tensor.py:65-75); K/V are read from the paged pool in their storage dtype.
+// A work item is (block of <= rows_per_block rows, run of visible pages); a CTA
+// takes one (item, kv head) and serves all G = n_heads / n_kv query heads of that
+// KV head (GQA), so each K/V page is read once per item for G * rows query
+// vectors.  Page-centric K3 items gather every row that sees a parent message, so
+// in a parallel decode a shared parent page is read once for all agents.
 // Masking: slot s of a page is visible to row r iff s < page_len and, for pages of
-// the row's own message, own_base + s <= row_t[r] (masking.py:36-40 restated on
-// pages).  Each (row, head) of an item emits a normalised partial + LSE; the
-// combine kernel merges a row's partials (flash-decoding split-KV).
+// the row's own message, own_base + s <= row_t[r] (masking.py:36-40 on pages).
+// Each (row, head) of an item emits a normalised partial + LSE (natural log); the
+// combine kernel merges a row's partials (reference model.py:177-184,
+// tensor.py:65-75: scores, masked softmax, P.V).
+//
+// bf16 pools: tensor-core path (mma.sync m16n8k16, f32 accumulate), pages staged by a
+// 3-stage cp.async pipeline.  Q and P enter the MMAs as hi/lo bf16 pairs, so the
+// only bf16 rounding is the K/V storage itself.  f32 pools (parity variant): SIMT.
 #include <math.h>
 
 #include "common.cuh"
 
 namespace choreo {
-
-constexpr int kThreads = 128;
-constexpr int kMaxM = 64;  // rows_per_block * G must not exceed this
-constexpr int kKT = 32;    // keys per smem tile
 
 struct SplitParams {
   const float* q;
@@ -28,6 +29,7 @@ struct SplitParams {
   const int32_t* vis_page;
   const int32_t* vis_len;
   const int32_t* vis_own;
+  const int32_t* blk_rows;
   const int32_t* items;
   const int32_t* counts;
   float* part_o;
@@ -35,19 +37,25 @@ struct SplitParams {
   float scale;
 };
 
+// ============================================================ SIMT path (f32 pools)
+constexpr int kThreads = 128;
+constexpr int kMaxM = 64;  // rows_per_block * G must not exceed this
+constexpr int kKT = 32;    // keys per smem tile
+
 template <typename T, int HD>
 __global__ void __launch_bounds__(kThreads) attn_split_simt(SplitParams p) {
-  constexpr int RPT = kMaxM * HD / kThreads;  // accumulator rows per thread
-  constexpr int GROUPS = kThreads / HD;       // row groups in the PV mapping
+  constexpr int RPT = kMaxM * HD / kThreads;
+  constexpr int GROUPS = kThreads / HD;
   extern __shared__ float smem[];
-  float* Qs = smem;                        // [kMaxM][HD]
-  float* Ks = Qs + kMaxM * HD;             // [kKT][HD + 1]
-  float* Vs = Ks + kKT * (HD + 1);         // [kKT][HD]
-  float* Ss = Vs + kKT * HD;               // [kMaxM][kKT + 1]
-  float* rmax = Ss + kMaxM * (kKT + 1);    // [kMaxM]
-  float* rsum = rmax + kMaxM;              // [kMaxM]
-  float* alpha = rsum + kMaxM;             // [kMaxM]
-  int* rt = reinterpret_cast<int*>(alpha + kMaxM);  // [kMaxM] row_t per local row
+  float* Qs = smem;
+  float* Ks = Qs + kMaxM * HD;
+  float* Vs = Ks + kKT * (HD + 1);
+  float* Ss = Vs + kKT * HD;
+  float* rmax = Ss + kMaxM * (kKT + 1);
+  float* rsum = rmax + kMaxM;
+  float* alpha = rsum + kMaxM;
+  int* rt = reinterpret_cast<int*>(alpha + kMaxM);
+  int* rid = rt + kMaxM;
 
   const int tid = threadIdx.x;
   const int G = p.n_heads / p.n_kv;
@@ -58,19 +66,22 @@ __global__ void __launch_bounds__(kThreads) attn_split_simt(SplitParams p) {
   for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
     const int32_t* it = p.items + 6 * (w / p.n_kv);
     const int kvh = w % p.n_kv;
-    const int r0 = it[0], nr = it[1], vb = it[2], nv = it[3], pbase = it[4];
+    const int rb = it[0], nr = it[1], vb = it[2], nv = it[3], pbase = it[4];
     const int M = nr * G;
-
+    for (int r = tid; r < nr; r += kThreads) {
+      rid[r] = p.blk_rows[rb + r];
+      rt[r] = p.row_t[rid[r]];
+    }
+    __syncthreads();
     for (int i = tid; i < M * HD; i += kThreads) {
       const int m = i / HD, d = i % HD;
       const int hq = kvh * G + (m % G);
-      Qs[i] = p.q[((int64_t)(r0 + m / G) * p.n_heads + hq) * HD + d] * p.scale;
+      Qs[i] = p.q[((int64_t)rid[m / G] * p.n_heads + hq) * HD + d] * p.scale;
     }
     for (int m = tid; m < M; m += kThreads) {
       rmax[m] = -INFINITY;
       rsum[m] = 0.f;
     }
-    for (int r = tid; r < nr; r += kThreads) rt[r] = p.row_t[r0 + r];
     float acc[RPT];
 #pragma unroll
     for (int j = 0; j < RPT; ++j) acc[j] = 0.f;
@@ -139,7 +150,6 @@ __global__ void __launch_bounds__(kThreads) attn_split_simt(SplitParams p) {
         __syncthreads();
       }
     }
-
     const int d = tid % HD;
 #pragma unroll
     for (int j = 0; j < RPT; ++j) {
@@ -156,40 +166,359 @@ __global__ void __launch_bounds__(kThreads) attn_split_simt(SplitParams p) {
   }
 }
 
+// ============================================================ tensor-core path (bf16)
+constexpr int kMmaThreads = 128;  // 4 warps
+constexpr int kStages = 3;
+constexpr int kPage = 64;         // keys per page (= page_size for this path)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(ptr));
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+// hi = bf16(x), lo = bf16(x - hi), packed pairs
+__device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  const float2 hf = __bfloat1622float2(h);
+  __nv_bfloat162 l = __floats2bfloat162_rn(a - hf.x, b - hf.y);
+  hi = *reinterpret_cast<uint32_t*>(&h);
+  lo = *reinterpret_cast<uint32_t*>(&l);
+}
+__device__ __forceinline__ void mma16816(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void ldsm_x4_trans(uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                              uint32_t& r3, const void* ptr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(smem_u32(ptr)));
+}
+
+// Warp roles: MT = m16 tiles needed (ceil(G*rows/16) <= 4); the KW = 4/MT warp groups
+// split each page's 64 keys; warp w owns m-tile (w % MT) and key slice (w / MT).
+template <int HD>
+__global__ void __launch_bounds__(kMmaThreads, 2) attn_split_mma(SplitParams p) {
+  constexpr int LD = HD + 8;  // padded smem row (bf16 elems): conflict-free fragments
+  constexpr int NT = HD / 8;  // n8 tiles over head dim
+  constexpr int KS = HD / 16; // k16 steps over head dim
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(smem_raw);     // [kStages][64][LD]
+  __nv_bfloat16* Vs = Ks + kStages * kPage * LD;                        // [kStages][64][LD]
+  float* red = reinterpret_cast<float*>(Vs + kStages * kPage * LD);     // merge scratch
+  __shared__ int s_rid[64], s_rt[64];
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int G = p.n_heads / p.n_kv;
+  const int n_work = p.counts[1] * p.n_kv;
+  const __nv_bfloat16* kp = reinterpret_cast<const __nv_bfloat16*>(p.k_pool);
+  const __nv_bfloat16* vp = reinterpret_cast<const __nv_bfloat16*>(p.v_pool);
+  const float sl2 = p.scale * 1.4426950408889634f;  // scores in log2 domain
+
+  for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+    const int32_t* it = p.items + 6 * (w / p.n_kv);
+    const int kvh = w % p.n_kv;
+    const int rb = it[0], nr = it[1], vb = it[2], nv = it[3], pbase = it[4];
+    const int M = nr * G;
+    const int MT = M <= 16 ? 1 : (M <= 32 ? 2 : 4);
+    const int KW = 4 / MT;
+    const int mt = warp % MT, kg = warp / MT;
+    const int kslice = kPage / KW;  // keys of each page handled by this warp
+    __syncthreads();
+    for (int r = tid; r < nr; r += kMmaThreads) {
+      s_rid[r] = p.blk_rows[rb + r];
+      s_rt[r] = p.row_t[s_rid[r]];
+    }
+    // page loader: stage s <- page index pi (K and V, zero-fill slots >= len)
+    auto load_page = [&](int stage, int pi) {
+      if (pi < vb + nv) {
+        const int page = p.vis_page[pi], len = p.vis_len[pi];
+        const int64_t base = pool_off(p.layer, kvh, page, 0, p.n_kv, p.n_pages, p.page_size, HD);
+        constexpr int CH = HD / 8;  // 16-byte chunks per row
+        for (int c = tid; c < kPage * CH; c += kMmaThreads) {
+          const int row = c / CH, col = (c % CH) * 8;
+          const int nb = row < len ? 16 : 0;
+          const int64_t src = base + (int64_t)(row < len ? row : 0) * HD + col;
+          cp_async16(Ks + (stage * kPage + row) * LD + col, kp + src, nb);
+          cp_async16(Vs + (stage * kPage + row) * LD + col, vp + src, nb);
+        }
+      }
+      cp_async_commit();
+    };
+    for (int s = 0; s < kStages - 1; ++s) load_page(s, vb + s);
+    __syncthreads();  // s_rid / s_rt visible
+
+    // Q fragments (hi/lo) for this warp's m-tile: rows m = mt*16 + {g, g+8}
+    uint32_t qh[KS][4], ql[KS][4];
+    int rowA = mt * 16 + g, rowB = rowA + 8;
+    const bool vA = rowA < M, vB = rowB < M;
+    const float* qA = vA ? p.q + ((int64_t)s_rid[rowA / G] * p.n_heads + kvh * G + rowA % G) * HD : nullptr;
+    const float* qB = vB ? p.q + ((int64_t)s_rid[rowB / G] * p.n_heads + kvh * G + rowB % G) * HD : nullptr;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int c0 = ks * 16 + 2 * t;
+      float2 a0 = vA ? *reinterpret_cast<const float2*>(qA + c0) : make_float2(0.f, 0.f);
+      float2 a1 = vB ? *reinterpret_cast<const float2*>(qB + c0) : make_float2(0.f, 0.f);
+      float2 a2 = vA ? *reinterpret_cast<const float2*>(qA + c0 + 8) : make_float2(0.f, 0.f);
+      float2 a3 = vB ? *reinterpret_cast<const float2*>(qB + c0 + 8) : make_float2(0.f, 0.f);
+      split2(a0.x * sl2, a0.y * sl2, qh[ks][0], ql[ks][0]);
+      split2(a1.x * sl2, a1.y * sl2, qh[ks][1], ql[ks][1]);
+      split2(a2.x * sl2, a2.y * sl2, qh[ks][2], ql[ks][2]);
+      split2(a3.x * sl2, a3.y * sl2, qh[ks][3], ql[ks][3]);
+    }
+    const int rtA = vA ? s_rt[rowA / G] : -1, rtB = vB ? s_rt[rowB / G] : -1;
+
+    float o[NT][4];
+#pragma unroll
+    for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+    float mA = -INFINITY, mB = -INFINITY, lA = 0.f, lB = 0.f;
+
+    for (int pi = vb; pi < vb + nv; ++pi) {
+      const int stage = (pi - vb) % kStages;
+      cp_async_wait<kStages - 2>();
+      __syncthreads();
+      load_page((pi - vb + kStages - 1) % kStages, pi + kStages - 1);
+      const int len = p.vis_len[pi], own = p.vis_own[pi];
+      const __nv_bfloat16* Kt = Ks + stage * kPage * LD;
+      const __nv_bfloat16* Vt = Vs + stage * kPage * LD;
+      const int k0 = kg * kslice;  // this warp's key slice [k0, k0 + kslice)
+      if (k0 < len) {
+        // ---- S = Q K^T over the slice (kslice/8 n8 tiles) ----
+        constexpr int MAXN = kPage / 8;
+        float s[MAXN][4];
+        const int nn = kslice / 8;
+#pragma unroll
+        for (int j = 0; j < MAXN; ++j) {
+          s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+          if (j < nn) {
+            const __nv_bfloat16* kr = Kt + (k0 + j * 8 + g) * LD + 2 * t;
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) {
+              const uint32_t b0 = *reinterpret_cast<const uint32_t*>(kr + ks * 16);
+              const uint32_t b1 = *reinterpret_cast<const uint32_t*>(kr + ks * 16 + 8);
+              mma16816(s[j], qh[ks], b0, b1);
+              mma16816(s[j], ql[ks], b0, b1);
+            }
+          }
+        }
+        // ---- mask + online softmax (rows A = g, B = g + 8 of the m-tile) ----
+        float tA = -INFINITY, tB = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < MAXN; ++j) {
+          if (j >= nn) continue;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int key = k0 + j * 8 + 2 * t + e;
+            const bool okA = vA && key < len && (own < 0 || own + key <= rtA);
+            const bool okB = vB && key < len && (own < 0 || own + key <= rtB);
+            s[j][e] = okA ? s[j][e] : -INFINITY;
+            s[j][2 + e] = okB ? s[j][2 + e] : -INFINITY;
+            tA = fmaxf(tA, s[j][e]);
+            tB = fmaxf(tB, s[j][2 + e]);
+          }
+        }
+        tA = fmaxf(tA, __shfl_xor_sync(0xffffffffu, tA, 1));
+        tA = fmaxf(tA, __shfl_xor_sync(0xffffffffu, tA, 2));
+        tB = fmaxf(tB, __shfl_xor_sync(0xffffffffu, tB, 1));
+        tB = fmaxf(tB, __shfl_xor_sync(0xffffffffu, tB, 2));
+        const float nA = fmaxf(mA, tA), nB = fmaxf(mB, tB);
+        const float aA = nA == -INFINITY ? 1.f : exp2f(mA - nA);
+        const float aB = nB == -INFINITY ? 1.f : exp2f(mB - nB);
+        float sumA = 0.f, sumB = 0.f;
+#pragma unroll
+        for (int j = 0; j < MAXN; ++j) {
+          if (j >= nn) continue;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            s[j][e] = s[j][e] == -INFINITY ? 0.f : exp2f(s[j][e] - nA);
+            s[j][2 + e] = s[j][2 + e] == -INFINITY ? 0.f : exp2f(s[j][2 + e] - nB);
+            sumA += s[j][e];
+            sumB += s[j][2 + e];
+          }
+        }
+        lA = lA * aA + sumA;
+        lB = lB * aB + sumB;
+        mA = nA;
+        mB = nB;
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          o[n][0] *= aA;
+          o[n][1] *= aA;
+          o[n][2] *= aB;
+          o[n][3] *= aB;
+        }
+        // ---- O += P V over the slice: k16 steps of keys, P as hi/lo A fragments ----
+#pragma unroll
+        for (int kk = 0; kk < MAXN / 2; ++kk) {
+          if (2 * kk >= nn) continue;
+          uint32_t ph[4], pl[4];
+          split2(s[2 * kk][0], s[2 * kk][1], ph[0], pl[0]);
+          split2(s[2 * kk][2], s[2 * kk][3], ph[1], pl[1]);
+          split2(s[2 * kk + 1][0], s[2 * kk + 1][1], ph[2], pl[2]);
+          split2(s[2 * kk + 1][2], s[2 * kk + 1][3], ph[3], pl[3]);
+          const int krow = k0 + kk * 16;
+#pragma unroll
+          for (int n = 0; n < NT; n += 2) {
+            // x4.trans: matrices (keys 0-7, dims n*8), (keys 8-15, n*8), (0-7, n*8+8), (8-15, n*8+8)
+            const int mi = lane >> 3;
+            const __nv_bfloat16* ptr = Vt + (krow + (mi & 1) * 8 + (lane & 7)) * LD + n * 8 + (mi >> 1) * 8;
+            uint32_t b0, b1, b2, b3;
+            ldsm_x4_trans(b0, b1, b2, b3, ptr);
+            mma16816(o[n], ph, b0, b1);
+            mma16816(o[n], pl, b0, b1);
+            mma16816(o[n + 1], ph, b2, b3);
+            mma16816(o[n + 1], pl, b2, b3);
+          }
+        }
+      }
+    }
+    cp_async_wait<0>();
+    // quad-reduce the row sums
+    lA += __shfl_xor_sync(0xffffffffu, lA, 1);
+    lA += __shfl_xor_sync(0xffffffffu, lA, 2);
+    lB += __shfl_xor_sync(0xffffffffu, lB, 1);
+    lB += __shfl_xor_sync(0xffffffffu, lB, 2);
+    __syncthreads();  // smem pages no longer needed: reuse as merge scratch
+    // ---- merge the KW key-slice warps of each m-tile (through smem) ----
+    // layout per warp: [16 rows][HD] o, then m[16], l[16]
+    float* my = red + warp * (16 * HD + 32);
+    if (KW > 1) {
+#pragma unroll
+      for (int n = 0; n < NT; ++n) {
+        my[g * HD + n * 8 + 2 * t] = o[n][0];
+        my[g * HD + n * 8 + 2 * t + 1] = o[n][1];
+        my[(g + 8) * HD + n * 8 + 2 * t] = o[n][2];
+        my[(g + 8) * HD + n * 8 + 2 * t + 1] = o[n][3];
+      }
+      if (t == 0) {
+        my[16 * HD + g] = mA;
+        my[16 * HD + g + 8] = mB;
+        my[16 * HD + 16 + g] = lA;
+        my[16 * HD + 16 + g + 8] = lB;
+      }
+    }
+    __syncthreads();
+    if (kg == 0) {
+      // final m, l over the key slices of this m-tile
+      float fmA = mA, fmB = mB;
+      for (int k = 1; k < KW; ++k) {
+        const float* ot = red + (warp + k * MT) * (16 * HD + 32);
+        fmA = fmaxf(fmA, ot[16 * HD + g]);
+        fmB = fmaxf(fmB, ot[16 * HD + g + 8]);
+      }
+      const float wA0 = fmA == -INFINITY ? 0.f : exp2f(mA - fmA);
+      const float wB0 = fmB == -INFINITY ? 0.f : exp2f(mB - fmB);
+      float LA = lA * wA0, LB = lB * wB0;
+#pragma unroll
+      for (int n = 0; n < NT; ++n) {
+        o[n][0] *= wA0;
+        o[n][1] *= wA0;
+        o[n][2] *= wB0;
+        o[n][3] *= wB0;
+      }
+      for (int k = 1; k < KW; ++k) {
+        const float* ot = red + (warp + k * MT) * (16 * HD + 32);
+        const float mk_A = ot[16 * HD + g], mk_B = ot[16 * HD + g + 8];
+        const float wA = fmA == -INFINITY ? 0.f : exp2f(mk_A - fmA);
+        const float wB = fmB == -INFINITY ? 0.f : exp2f(mk_B - fmB);
+        LA += ot[16 * HD + 16 + g] * wA;
+        LB += ot[16 * HD + 16 + g + 8] * wB;
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          o[n][0] += wA * ot[g * HD + n * 8 + 2 * t];
+          o[n][1] += wA * ot[g * HD + n * 8 + 2 * t + 1];
+          o[n][2] += wB * ot[(g + 8) * HD + n * 8 + 2 * t];
+          o[n][3] += wB * ot[(g + 8) * HD + n * 8 + 2 * t + 1];
+        }
+      }
+      // write normalised partials + natural-log LSE
+      const float ln2 = 0.6931471805599453f;
+      if (vA) {
+        const int64_t pidx = (int64_t)(pbase + rowA / G) * p.n_heads + kvh * G + rowA % G;
+        const float inv = LA > 0.f ? 1.f / LA : 0.f;
+#pragma unroll
+        for (int n = 0; n < NT; ++n)
+          *reinterpret_cast<float2*>(p.part_o + pidx * HD + n * 8 + 2 * t) =
+              make_float2(o[n][0] * inv, o[n][1] * inv);
+        if (t == 0) p.part_lse[pidx] = LA > 0.f ? (fmA + log2f(LA)) * ln2 : -INFINITY;
+      }
+      if (vB) {
+        const int64_t pidx = (int64_t)(pbase + rowB / G) * p.n_heads + kvh * G + rowB % G;
+        const float inv = LB > 0.f ? 1.f / LB : 0.f;
+#pragma unroll
+        for (int n = 0; n < NT; ++n)
+          *reinterpret_cast<float2*>(p.part_o + pidx * HD + n * 8 + 2 * t) =
+              make_float2(o[n][2] * inv, o[n][3] * inv);
+        if (t == 0) p.part_lse[pidx] = LB > 0.f ? (fmB + log2f(LB)) * ln2 : -INFINITY;
+      }
+    }
+  }
+}
+
+// ============================================================ combine
+// One CTA per (row, head): merge the row's partial slots (CSR) with the LSE rule.
 template <typename TO>
 __global__ void attn_combine_kernel(const float* __restrict__ part_o,
                                     const float* __restrict__ part_lse,
-                                    const int32_t* __restrict__ row_part, int n_heads, int hd,
-                                    int split, TO* __restrict__ out) {
-  const int r = blockIdx.x;
-  const int pb = row_part[3 * r], stride = row_part[3 * r + 1], n = row_part[3 * r + 2];
-  for (int i = threadIdx.x; i < n_heads * hd; i += blockDim.x) {
-    const int h = i / hd, d = i % hd;
-    float mx = -INFINITY;
-    for (int c = 0; c < n; ++c) mx = fmaxf(mx, part_lse[(int64_t)(pb + c * stride) * n_heads + h]);
-    float num = 0.f, den = 0.f;
-    if (mx != -INFINITY) {
-      for (int c = 0; c < n; ++c) {
-        const int64_t pi = (int64_t)(pb + c * stride) * n_heads + h;
-        const float l = part_lse[pi];
-        if (l == -INFINITY) continue;
-        const float wgt = expf(l - mx);
-        num += wgt * part_o[pi * hd + d];
-        den += wgt;
-      }
-    }
-    const float y = den > 0.f ? num / den : 0.f;
+                                    const int32_t* __restrict__ row_part_off,
+                                    const int32_t* __restrict__ row_part, int n_rows, int n_heads,
+                                    int hd, int split, TO* __restrict__ out) {
+  const int r = blockIdx.x / n_heads, h = blockIdx.x % n_heads;
+  const int b = row_part_off[r], e = row_part_off[r + 1];
+  __shared__ float wsh[512];
+  __shared__ float s_den;
+  float mx = -INFINITY;
+  for (int i = b + threadIdx.x; i < e; i += blockDim.x)
+    mx = fmaxf(mx, part_lse[(int64_t)row_part[i] * n_heads + h]);
+  mx = warp_max(mx);
+  __shared__ float s_mx[8];
+  if ((threadIdx.x & 31) == 0) s_mx[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  mx = -INFINITY;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) mx = fmaxf(mx, s_mx[i]);
+  for (int i = threadIdx.x; i < e - b && i < 512; i += blockDim.x) {
+    const float l = part_lse[(int64_t)row_part[b + i] * n_heads + h];
+    wsh[i] = (l == -INFINITY || mx == -INFINITY) ? 0.f : expf(l - mx);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float den = 0.f;
+    for (int i = 0; i < e - b && i < 512; ++i) den += wsh[i];
+    s_den = den;
+  }
+  __syncthreads();
+  const float inv = s_den > 0.f ? 1.f / s_den : 0.f;
+  for (int d = threadIdx.x; d < hd; d += blockDim.x) {
+    float num = 0.f;
+    for (int i = 0; i < e - b && i < 512; ++i)
+      if (wsh[i] != 0.f) num += wsh[i] * part_o[((int64_t)row_part[b + i] * n_heads + h) * hd + d];
+    const float y = num * inv;
     const int64_t oi = ((int64_t)r * n_heads + h) * hd + d;
     const TO hi = from_f32<TO>(y);
     out[oi] = hi;
-    if (split) out[(int64_t)gridDim.x * n_heads * hd + oi] = from_f32<TO>(y - to_f32(hi));
+    if (split) out[(int64_t)n_rows * n_heads * hd + oi] = from_f32<TO>(y - to_f32(hi));
   }
 }
 
 template <typename T, int HD>
-static int launch_split(const SplitParams& p, int grid, cudaStream_t s) {
+static int launch_simt(const SplitParams& p, int grid, cudaStream_t s) {
   const size_t smem = sizeof(float) * (kMaxM * HD + kKT * (HD + 1) + kKT * HD +
-                                       kMaxM * (kKT + 1) + 4 * kMaxM);
+                                       kMaxM * (kKT + 1) + 5 * kMaxM);
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(attn_split_simt<T, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -200,14 +529,29 @@ static int launch_split(const SplitParams& p, int grid, cudaStream_t s) {
   return launch_status("choreo_attn_split");
 }
 
+template <int HD>
+static int launch_mma(const SplitParams& p, int grid, cudaStream_t s) {
+  constexpr int LD = HD + 8;
+  const size_t pages = sizeof(__nv_bfloat16) * 2 * kStages * kPage * LD;
+  const size_t merge = sizeof(float) * 4 * (16 * HD + 32);
+  const size_t smem = pages > merge ? pages : merge;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(attn_split_mma<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set = true;
+  }
+  attn_split_mma<HD><<<grid, kMmaThreads, smem, s>>>(p);
+  return launch_status("choreo_attn_split");
+}
+
 template <typename T>
-static int dispatch_hd(int hd, const SplitParams& p, int grid, cudaStream_t s) {
+static int dispatch_simt(int hd, const SplitParams& p, int grid, cudaStream_t s) {
   switch (hd) {
-    case 8: return launch_split<T, 8>(p, grid, s);
-    case 16: return launch_split<T, 16>(p, grid, s);
-    case 32: return launch_split<T, 32>(p, grid, s);
-    case 64: return launch_split<T, 64>(p, grid, s);
-    case 128: return launch_split<T, 128>(p, grid, s);
+    case 8: return launch_simt<T, 8>(p, grid, s);
+    case 16: return launch_simt<T, 16>(p, grid, s);
+    case 32: return launch_simt<T, 32>(p, grid, s);
+    case 64: return launch_simt<T, 64>(p, grid, s);
+    case 128: return launch_simt<T, 128>(p, grid, s);
     default: return CHOREO_EUNSUPPORTED;
   }
 }
@@ -221,37 +565,44 @@ extern "C" {
 int choreo_attn_split(const float* q, const void* k_pool, const void* v_pool, int pool_dtype,
                       int layer, int n_kv, int n_pages, int page_size, int n_heads, int head_dim,
                       const int32_t* row_t, const int32_t* vis_page, const int32_t* vis_len,
-                      const int32_t* vis_own, const int32_t* items, const int32_t* counts,
-                      int max_items, float* part_o, float* part_lse, int grid_ctas,
-                      void* stream) {
-  if (!q || !k_pool || !v_pool || !row_t || !vis_page || !vis_len || !vis_own || !items ||
-      !counts || !part_o || !part_lse || !dtype_ok(pool_dtype) || n_kv <= 0 ||
+                      const int32_t* vis_own, const int32_t* blk_rows, const int32_t* items,
+                      const int32_t* counts, int max_items, float* part_o, float* part_lse,
+                      int grid_ctas, void* stream) {
+  if (!q || !k_pool || !v_pool || !row_t || !vis_page || !vis_len || !vis_own || !blk_rows ||
+      !items || !counts || !part_o || !part_lse || !dtype_ok(pool_dtype) || n_kv <= 0 ||
       n_heads % n_kv)
     return CHOREO_EINVAL;
   if (max_items <= 0) return CHOREO_OK;
   SplitParams p{q, k_pool, v_pool, layer, n_kv, n_pages, page_size, n_heads, row_t, vis_page,
-                vis_len, vis_own, items, counts, part_o, part_lse,
+                vis_len, vis_own, blk_rows, items, counts, part_o, part_lse,
                 1.0f / sqrtf((float)head_dim)};
-  int grid = grid_ctas > 0 ? grid_ctas : max_items * n_kv;
-  if (grid > 148 * 8) grid = 148 * 8;
   auto s = as_stream(stream);
-  return pool_dtype == CHOREO_BF16 ? dispatch_hd<__nv_bfloat16>(head_dim, p, grid, s)
-                                   : dispatch_hd<float>(head_dim, p, grid, s);
+  const bool mma = pool_dtype == CHOREO_BF16 && page_size == kPage &&
+                   (head_dim == 64 || head_dim == 128);
+  int grid = grid_ctas > 0 ? grid_ctas : max_items * n_kv;
+  const int cap = mma ? 148 * 2 : 148 * 8;
+  if (grid > cap) grid = cap;
+  if (mma) return head_dim == 128 ? launch_mma<128>(p, grid, s) : launch_mma<64>(p, grid, s);
+  return pool_dtype == CHOREO_BF16 ? dispatch_simt<__nv_bfloat16>(head_dim, p, grid, s)
+                                   : dispatch_simt<float>(head_dim, p, grid, s);
 }
 
-int choreo_attn_combine(const float* part_o, const float* part_lse, const int32_t* row_part,
-                        int n_rows, int n_heads, int head_dim, void* out, int out_dtype,
-                        int out_split, void* stream) {
-  if (!part_o || !part_lse || !row_part || !out || !dtype_ok(out_dtype)) return CHOREO_EINVAL;
+int choreo_attn_combine(const float* part_o, const float* part_lse, const int32_t* row_part_off,
+                        const int32_t* row_part, int n_rows, int n_heads, int head_dim, void* out,
+                        int out_dtype, int out_split, void* stream) {
+  if (!part_o || !part_lse || !row_part_off || !row_part || !out || !dtype_ok(out_dtype))
+    return CHOREO_EINVAL;
   if (out_split && out_dtype != CHOREO_BF16) return CHOREO_EINVAL;
   if (n_rows == 0) return CHOREO_OK;
   auto s = as_stream(stream);
+  const int threads = head_dim >= 128 ? 128 : 64;
   if (out_dtype == CHOREO_BF16)
-    attn_combine_kernel<__nv_bfloat16><<<n_rows, 256, 0, s>>>(part_o, part_lse, row_part, n_heads,
-                                                              head_dim, out_split, (__nv_bfloat16*)out);
+    attn_combine_kernel<__nv_bfloat16><<<n_rows * n_heads, threads, 0, s>>>(
+        part_o, part_lse, row_part_off, row_part, n_rows, n_heads, head_dim, out_split,
+        (__nv_bfloat16*)out);
   else
-    attn_combine_kernel<float><<<n_rows, 256, 0, s>>>(part_o, part_lse, row_part, n_heads,
-                                                      head_dim, 0, (float*)out);
+    attn_combine_kernel<float><<<n_rows * n_heads, threads, 0, s>>>(
+        part_o, part_lse, row_part_off, row_part, n_rows, n_heads, head_dim, 0, (float*)out);
   return launch_status("choreo_attn_combine");
 }
 

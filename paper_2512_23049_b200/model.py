@@ -53,22 +53,51 @@ class StepPlan:
         return sum(len(c.tokens) for c in self.calls)
 
 
-def plan_counts(calls: list, msg_len: np.ndarray, P: int, rpb: int, ppi: int):
-    """Host replica of K3's sizing (assemble.cu plan_call): (vis pages, items, partials)."""
-    v = it = pa = 0
+@dataclass
+class Plan:
+    """Host replica of K3's page-centric sizing (assemble.cu) for buffer capacities."""
+
+    n_vis: int
+    n_blk_rows: int
+    n_items: int
+    n_parts: int
+    max_row_parts: int
+    item_pages: int  # sum over items of pages (work estimate)
+
+
+def plan_counts(calls: list, msg_len: np.ndarray, P: int, rpb: int, ppi: int) -> Plan:
+    groups: dict = {}
     for c in calls:
-        pp = sum(cdiv(int(msg_len[p]), P) for p in c.parents)
+        for p in c.parents:
+            groups[p] = groups.get(p, 0) + len(c.tokens)
+    n_vis = n_blk = n_items = n_parts = item_pages = 0
+    for p, rows in groups.items():
+        pages = cdiv(int(msg_len[p]), P)
+        n_vis += pages
+        n_blk += rows
+        if rows:
+            ch = cdiv(pages, ppi)
+            n_items += cdiv(rows, rpb) * ch
+            n_parts += rows * ch
+            item_pages += cdiv(rows, rpb) * pages
+    max_row = 0
+    for c in calls:
         n = len(c.tokens)
         if n == 0:
             continue
-        t = c.first_t + np.arange(n)
-        v += pp + int(t[-1]) // P + 1
+        par_ch = sum(cdiv(cdiv(int(msg_len[p]), P), ppi) for p in c.parents)
+        t_last = c.first_t + n - 1
+        n_vis += t_last // P + 1
+        n_blk += n
         for b in range(0, n, rpb):
             nr = min(rpb, n - b)
-            ch = cdiv(pp + int(t[b + nr - 1]) // P + 1, ppi)
-            it += ch
-            pa += ch * nr
-    return v, it, pa
+            own_pages = (c.first_t + b + nr - 1) // P + 1
+            ch = cdiv(own_pages, ppi)
+            n_items += ch
+            n_parts += ch * nr
+            item_pages += own_pages
+            max_row = max(max_row, par_ch + ch)
+    return Plan(n_vis, n_blk, n_items, n_parts, max_row, item_pages)
 
 
 class Runner:
@@ -140,12 +169,16 @@ class Runner:
             row_off += len(c.tokens)
         n_calls = len(plan.calls)
         msg_len = cache.msg_len.host
-        total_pages = sum(
-            (sum(cdiv(int(msg_len[p]), P) for p in c.parents) + (c.first_t + len(c.tokens) - 1) // P + 1)
-            * cdiv(len(c.tokens), self.rows_per_block) for c in plan.calls)
-        target_items = max(1, (4 * 148) // Hk)
-        ppi = max(1, cdiv(total_pages, target_items))
-        n_vis, n_items, n_parts = plan_counts(plan.calls, msg_len, P, self.rows_per_block, ppi)
+        rpb = self.rows_per_block
+        # pages per item: about two waves of (2 CTAs/SM x 148 SMs) per layer, and at
+        # most 512 partials per row for the combine
+        work = plan_counts(plan.calls, msg_len, P, rpb, 1)
+        ppi = max(1, cdiv(work.item_pages * Hk, 2 * 2 * 148))
+        plan_ = plan_counts(plan.calls, msg_len, P, rpb, ppi)
+        while plan_.max_row_parts > 512:
+            ppi *= 2
+            plan_ = plan_counts(plan.calls, msg_len, P, rpb, ppi)
+        n_parts, n_items = plan_.n_parts, plan_.n_items
         n_log = len(plan.logit_rows)
 
         ints = np.concatenate([ids, row_t, pos, pages, slots, np.asarray(call_tab, np.int32),
@@ -172,16 +205,20 @@ class Runner:
         parents_d = take(len(parents) + 1)
         logit_d = take(n_log)
 
-        vis = torch.empty(3, max(n_vis, 1), dtype=torch.int32, device=self.dev)
+        vis = torch.empty(3, max(plan_.n_vis, 1), dtype=torch.int32, device=self.dev)
+        blk_rows = torch.empty(max(plan_.n_blk_rows, 1), dtype=torch.int32, device=self.dev)
         items = torch.empty(max(n_items, 1), 6, dtype=torch.int32, device=self.dev)
-        row_part = torch.empty(R, 3, dtype=torch.int32, device=self.dev)
+        row_part_off = torch.empty(R + 1, dtype=torch.int32, device=self.dev)
+        row_part = torch.empty(max(n_parts, 1), dtype=torch.int32, device=self.dev)
         counts = torch.empty(4, dtype=torch.int32, device=self.dev)
         nat.assemble(cache.msg_len.dev.data_ptr(), cache.msg_pt.dev.data_ptr(),
                      cache.page_table.dev.data_ptr(), calls_d.data_ptr(), parents_d.data_ptr(),
-                     n_calls, rowt_d.data_ptr(), R, None, 0, P, self.rows_per_block, ppi,
-                     vis[0].data_ptr(), vis[1].data_ptr(), vis[2].data_ptr(), items.data_ptr(),
-                     row_part.data_ptr(), counts.data_ptr(), n_vis, n_items, n_parts, stream)
+                     n_calls, rowt_d.data_ptr(), R, None, 0, P, rpb, ppi, vis[0].data_ptr(),
+                     vis[1].data_ptr(), vis[2].data_ptr(), blk_rows.data_ptr(), items.data_ptr(),
+                     row_part_off.data_ptr(), row_part.data_ptr(), counts.data_ptr(),
+                     plan_.n_vis, plan_.n_blk_rows, n_items, n_parts, stream)
         self.launches += 1
+        self.last_assembly = (vis, blk_rows, items, row_part_off, row_part, counts, plan_, rowt_d)
 
         S = 2 if self.split else 1  # stacked hi/lo activation rows
         sp = int(self.split)
@@ -212,13 +249,13 @@ class Runner:
             nat.attn_split(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(),
                            self.pool_dtc, layer, Hk, cache.n_pages, P, H, hd, rowt_d.data_ptr(),
                            vis[0].data_ptr(), vis[1].data_ptr(), vis[2].data_ptr(),
-                           items.data_ptr(), counts.data_ptr(), n_items, part_o.data_ptr(),
-                           part_lse.data_ptr(), 0, stream)
+                           blk_rows.data_ptr(), items.data_ptr(), counts.data_ptr(), n_items,
+                           part_o.data_ptr(), part_lse.data_ptr(), 0, stream)
             if self.attn_events is not None:
                 ev1.record()
                 self.attn_events.append((ev0, ev1, attn_bytes))
-            nat.attn_combine(part_o.data_ptr(), part_lse.data_ptr(), row_part.data_ptr(), R, H,
-                             hd, attn.data_ptr(), self.dtc, sp, stream)
+            nat.attn_combine(part_o.data_ptr(), part_lse.data_ptr(), row_part_off.data_ptr(),
+                             row_part.data_ptr(), R, H, hd, attn.data_ptr(), self.dtc, sp, stream)
             ao = self._mm(attn, lw["wo"], out_f32=True)
             nat.residual_rmsnorm(x.data_ptr(), ao.data_ptr(), nat.F32, sp,
                                  lw["ffn_norm"].data_ptr(), self.dtc, R, d, RMS_EPS, h.data_ptr(),

@@ -134,45 +134,58 @@ def _assemble(cache, calls, rpb, ppi):
         row_t += ts
         off += len(ts)
     cr = [CallRows(own, parents, ts[0], [0] * len(ts), None, None, 0) for own, parents, ts in calls]
-    n_vis, n_items, n_parts = plan_counts(cr, cache.msg_len.host, cache.page_size, rpb, ppi)
+    plan = plan_counts(cr, cache.msg_len.host, cache.page_size, rpb, ppi)
     cache.sync_tables()
     dev = lambda a: torch.tensor(a, dtype=torch.int32, device="cuda")  # noqa: E731
     tab_d, par_d, rt_d = dev(tab), dev(par + [0]), dev(row_t)
-    vis = torch.full((3, max(n_vis, 1)), -7, dtype=torch.int32, device="cuda")
-    items = torch.full((max(n_items, 1), 6), -7, dtype=torch.int32, device="cuda")
-    row_part = torch.empty(len(row_t), 3, dtype=torch.int32, device="cuda")
+    R = len(row_t)
+    vis = torch.full((3, max(plan.n_vis, 1)), -7, dtype=torch.int32, device="cuda")
+    blk = torch.full((max(plan.n_blk_rows, 1),), -7, dtype=torch.int32, device="cuda")
+    items = torch.full((max(plan.n_items, 1), 6), -7, dtype=torch.int32, device="cuda")
+    rpo = torch.full((R + 1,), -7, dtype=torch.int32, device="cuda")
+    rp = torch.full((max(plan.n_parts, 1),), -7, dtype=torch.int32, device="cuda")
     counts = torch.empty(4, dtype=torch.int32, device="cuda")
     nat.assemble(cache.msg_len.dev.data_ptr(), cache.msg_pt.dev.data_ptr(),
                  cache.page_table.dev.data_ptr(), tab_d.data_ptr(), par_d.data_ptr(), len(calls),
-                 rt_d.data_ptr(), len(row_t), None, 0, cache.page_size, rpb, ppi,
-                 vis[0].data_ptr(), vis[1].data_ptr(), vis[2].data_ptr(), items.data_ptr(),
-                 row_part.data_ptr(), counts.data_ptr(), n_vis, n_items, n_parts, _stream())
-    out = dict(vis=vis.cpu().numpy(), items=items.cpu().numpy(), row_part=row_part.cpu().numpy(),
-               counts=counts.cpu().numpy(), row_t=np.asarray(row_t), plan=(n_vis, n_items, n_parts))
-    return out, (rt_d, vis, items, row_part, counts)
+                 rt_d.data_ptr(), R, None, 0, cache.page_size, rpb, ppi,
+                 vis[0].data_ptr(), vis[1].data_ptr(), vis[2].data_ptr(), blk.data_ptr(),
+                 items.data_ptr(), rpo.data_ptr(), rp.data_ptr(), counts.data_ptr(),
+                 plan.n_vis, plan.n_blk_rows, plan.n_items, plan.n_parts, _stream())
+    out = dict(vis=vis.cpu().numpy(), blk=blk.cpu().numpy(), items=items.cpu().numpy(),
+               rpo=rpo.cpu().numpy(), rp=rp.cpu().numpy(), counts=counts.cpu().numpy(),
+               row_t=np.asarray(row_t), plan=plan)
+    return out, (rt_d, vis, blk, items, rpo, rp, counts)
 
 
 def _expand_rows(cache, out, n_rows):
-    """Token-level (msg, idx) visible sets per row, from K3 items; checks no duplicates."""
+    """Token-level (msg, idx) visible sets per row, from K3 items; checks that no token
+    is covered twice and that the per-row partial lists are exactly the items' slots."""
     page_owner = {}
     for m, e in cache._messages.items():
         for i, pg in enumerate(e.pages):
             page_owner[pg] = (m, i)
     P = cache.page_size
     sets = [[] for _ in range(n_rows)]
+    slots = [[] for _ in range(n_rows)]
     for it in out["items"][:out["counts"][1]]:
-        r0, nr, vb, nv = it[:4]
-        for r in range(r0, r0 + nr):
+        rb, nr, vb, nv, pbase = it[:5]
+        for jj in range(nr):
+            r = int(out["blk"][rb + jj])
+            slots[r].append(int(pbase + jj))
             t = out["row_t"][r]
             for k in range(vb, vb + nv):
                 pg, ln, own = out["vis"][:, k]
                 m, pi = page_owner[int(pg)]
-                for s in range(ln):
-                    if own < 0 or own + s <= t:
-                        sets[r].append((m, pi * P + s))
-    for s in sets:
-        assert len(s) == len(set(s)), "a token is covered twice"
-    return [sorted(s) for s in sets]
+                for s_ in range(ln):
+                    if own < 0 or own + s_ <= t:
+                        sets[r].append((m, pi * P + s_))
+    for r in range(n_rows):
+        assert len(sets[r]) == len(set(sets[r])), "a token is covered twice"
+        csr = out["rp"][out["rpo"][r]:out["rpo"][r + 1]].tolist()
+        assert sorted(csr) == sorted(slots[r]), f"row {r} partial list"
+    all_slots = sorted(x for s_ in slots for x in s_)
+    assert all_slots == list(range(out["plan"].n_parts)), "partial slots not a bijection"
+    return [sorted(s_) for s_ in sets]
 
 
 @pytest.mark.parametrize("rpb,ppi", [(1, 1), (4, 3), (16, 1000)])
@@ -194,7 +207,8 @@ def test_assemble_visible_sets_match_oracle(rpb, ppi):
         calls.append((own, parents, list(range(pre, pre + n_new))))
     out, _ = _assemble(cache, calls, rpb, ppi)
     assert out["counts"][3] == 0
-    assert tuple(out["counts"][:3]) == out["plan"]
+    pl = out["plan"]
+    assert tuple(out["counts"][:3]) == (pl.n_vis, pl.n_items, pl.n_parts)
     sets = _expand_rows(cache, out, len(out["row_t"]))
     # oracle: reference visibility over the physical store
     st = O.Store(O.Shape(n_layers=1, n_heads=2, head_dim=8), 1 << 16)
@@ -224,13 +238,22 @@ def test_attention_matches_dense_reference(dt, hd, H, Hk):
     cache.log_append(own, 0, 90)
     cache.k_pool.copy_(torch.randn_like(cache.k_pool))
     cache.v_pool.copy_(torch.randn_like(cache.v_pool))
-    calls = [(own, [3, 1, 6], list(range(60, 90))), (7, [], [int(lens[7]) - 1])]
+    cache.register_message(9, "decoded", 0)
+    cache.reserve_slots(9, [1] * 3)
+    cache.log_append(9, 0, 3)
+    cache.register_message(10, "decoded", 0)
+    cache.reserve_slots(10, [1] * 1)
+    cache.log_append(10, 0, 1)
+    cache.k_pool.copy_(torch.randn_like(cache.k_pool))
+    cache.v_pool.copy_(torch.randn_like(cache.v_pool))
+    calls = [(own, [3, 1, 6], list(range(60, 90))), (7, [], [int(lens[7]) - 1]),
+             (9, [6, 3, 0], [2]), (10, [1, 6, 2, 5, 4], [0])]
     G = H // Hk
     rpb = max(1, min(16, 64 // G))
-    out, (rt_d, vis, items, row_part, counts) = _assemble(cache, calls, rpb, 2)
+    out, (rt_d, vis, blk, items, rpo, rp, counts) = _assemble(cache, calls, rpb, 2)
     R = len(out["row_t"])
     q = torch.randn(R, H, hd, device="cuda")
-    n_parts = out["plan"][2]
+    n_parts = out["plan"].n_parts
     part_o = torch.empty(n_parts, H, hd, device="cuda")
     part_lse = torch.empty(n_parts, H, device="cuda")
     o = torch.empty(R, H * hd, dtype=torch.float32, device="cuda")
@@ -238,10 +261,10 @@ def test_attention_matches_dense_reference(dt, hd, H, Hk):
     nat.attn_split(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(),
                    nat.dtype_code(DT[dt]), L, Hk, cache.n_pages, cache.page_size, H, hd,
                    rt_d.data_ptr(), vis[0].data_ptr(), vis[1].data_ptr(), vis[2].data_ptr(),
-                   items.data_ptr(), counts.data_ptr(), out["plan"][1], part_o.data_ptr(),
-                   part_lse.data_ptr(), 0, _stream())
-    nat.attn_combine(part_o.data_ptr(), part_lse.data_ptr(), row_part.data_ptr(), R, H, hd,
-                     o.data_ptr(), nat.F32, 0, _stream())
+                   blk.data_ptr(), items.data_ptr(), counts.data_ptr(), out["plan"].n_items,
+                   part_o.data_ptr(), part_lse.data_ptr(), 0, _stream())
+    nat.attn_combine(part_o.data_ptr(), part_lse.data_ptr(), rpo.data_ptr(), rp.data_ptr(), R, H,
+                     hd, o.data_ptr(), nat.F32, 0, _stream())
     torch.cuda.synchronize()
     sets = _expand_rows(cache, out, R)
     K = cache.k_pool[L].float().cpu().numpy().astype(np.float64)  # (Hk, pages, P, hd)

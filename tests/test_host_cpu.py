@@ -142,28 +142,39 @@ def test_page_chain_relocates_when_reservation_is_exceeded():
 
 
 def _brute_counts(calls, msg_len, P_, rpb, ppi):
-    v = it = pa = 0
+    """Token-free restatement of K3's page-centric plan: one group per distinct parent
+    (viewers = rows of every call listing it), one causal own group per call."""
+    viewers = {}
     for c in calls:
-        pp = sum(cdiv(msg_len[p], P_) for p in c.parents)
+        for p in c.parents:
+            viewers.setdefault(p, []).extend([0] * len(c.tokens))
+    v = sum(cdiv(msg_len[p], P_) for p in viewers)
+    blk = sum(len(r) for r in viewers.values())
+    it = sum(cdiv(len(r), rpb) * cdiv(cdiv(msg_len[p], P_), ppi) for p, r in viewers.items() if r)
+    pa = sum(len(r) * cdiv(cdiv(msg_len[p], P_), ppi) for p, r in viewers.items())
+    for c in calls:
         ts = [c.first_t + i for i in range(len(c.tokens))]
-        v += pp + ts[-1] // P_ + 1
-        blocks = [ts[i:i + rpb] for i in range(0, len(ts), rpb)]
-        for b in blocks:
-            ch = cdiv(pp + b[-1] // P_ + 1, ppi)
+        v += ts[-1] // P_ + 1
+        blk += len(ts)
+        for i in range(0, len(ts), rpb):
+            b = ts[i:i + rpb]
+            ch = cdiv(b[-1] // P_ + 1, ppi)
             it += ch
             pa += ch * len(b)
-    return v, it, pa
+    return v, blk, it, pa
 
 
 @pytest.mark.parametrize("seed", range(10))
 def test_plan_counts(seed):
     rng = np.random.default_rng(seed)
     msg_len = rng.integers(1, 300, 20)
-    calls = [CallRows(int(rng.integers(20, 30)), [int(p) for p in rng.permutation(20)[:rng.integers(0, 6)]],
+    calls = [CallRows(int(20 + i), [int(p) for p in rng.permutation(20)[:rng.integers(0, 6)]],
                       int(rng.integers(0, 100)), [0] * int(rng.integers(1, 80)), None, None, 0)
-             for _ in range(int(rng.integers(1, 6)))]
+             for i in range(int(rng.integers(1, 6)))]
     for rpb, ppi in ((1, 1), (16, 3), (4, 1000)):
-        assert plan_counts(calls, msg_len, 64, rpb, ppi) == _brute_counts(calls, msg_len, 64, rpb, ppi)
+        pl = plan_counts(calls, msg_len, 64, rpb, ppi)
+        assert (pl.n_vis, pl.n_blk_rows, pl.n_items, pl.n_parts) == \
+            _brute_counts(calls, msg_len, 64, rpb, ppi)
 
 
 @pytest.mark.parametrize("shape", [O.TINY, O.Shape(n_layers=3, n_heads=8, n_kv_heads=2, head_dim=16,
