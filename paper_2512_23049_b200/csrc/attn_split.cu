@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(kMmaThreads, 2) attn_split_mma(SplitParams p) 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(smem_raw);     // [kStages][64][LD]
   __nv_bfloat16* Vs = Ks + kStages * kPage * LD;                        // [kStages][64][LD]
-  float* red = reinterpret_cast<float*>(Vs + kStages * kPage * LD);     // merge scratch
+  float* red = reinterpret_cast<float*>(smem_raw);  // merge scratch, reuses the page stages
   __shared__ int s_rid[64], s_rt[64];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
