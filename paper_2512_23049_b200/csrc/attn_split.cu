@@ -471,47 +471,89 @@ __global__ void __launch_bounds__(kMmaThreads, 2) attn_split_mma(SplitParams p) 
 }
 
 // ============================================================ combine
-// One CTA per (row, head): merge the row's partial slots (CSR) with the LSE rule.
+// One CTA (4 warps) per (row, head): lanes own 4 head dims each (float4), warps take
+// every 4th partial slot of the row's CSR list with the loads of 4 slots in flight,
+// then the warps' numerators/denominators are merged in smem (LSE rule).
 template <typename TO>
-__global__ void attn_combine_kernel(const float* __restrict__ part_o,
-                                    const float* __restrict__ part_lse,
-                                    const int32_t* __restrict__ row_part_off,
-                                    const int32_t* __restrict__ row_part, int n_rows, int n_heads,
-                                    int hd, int split, TO* __restrict__ out) {
+__global__ void __launch_bounds__(128) attn_combine_kernel(
+    const float* __restrict__ part_o, const float* __restrict__ part_lse,
+    const int32_t* __restrict__ row_part_off, const int32_t* __restrict__ row_part, int n_rows,
+    int n_heads, int hd, int split, TO* __restrict__ out) {
   const int r = blockIdx.x / n_heads, h = blockIdx.x % n_heads;
   const int b = row_part_off[r], e = row_part_off[r + 1];
-  __shared__ float wsh[512];
-  __shared__ float s_den;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ float s_mx[4];
+  __shared__ float4 s_num[4][32];
+  __shared__ float s_den[4];
   float mx = -INFINITY;
   for (int i = b + threadIdx.x; i < e; i += blockDim.x)
     mx = fmaxf(mx, part_lse[(int64_t)row_part[i] * n_heads + h]);
   mx = warp_max(mx);
-  __shared__ float s_mx[8];
-  if ((threadIdx.x & 31) == 0) s_mx[threadIdx.x >> 5] = mx;
+  if (lane == 0) s_mx[warp] = mx;
   __syncthreads();
-  mx = -INFINITY;
-  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) mx = fmaxf(mx, s_mx[i]);
-  for (int i = threadIdx.x; i < e - b && i < 512; i += blockDim.x) {
-    const float l = part_lse[(int64_t)row_part[b + i] * n_heads + h];
-    wsh[i] = (l == -INFINITY || mx == -INFINITY) ? 0.f : expf(l - mx);
+  mx = fmaxf(fmaxf(s_mx[0], s_mx[1]), fmaxf(s_mx[2], s_mx[3]));
+  const bool active = 4 * lane < hd;
+  float4 num = make_float4(0.f, 0.f, 0.f, 0.f);
+  float den = 0.f;
+  if (mx != -INFINITY) {
+    int i = b + warp;
+    for (; i + 12 < e; i += 16) {  // 4 slots per warp iteration, loads batched
+      int pi[4];
+      float l[4];
+      float4 o[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        pi[k] = row_part[i + 4 * k];
+        l[k] = part_lse[(int64_t)pi[k] * n_heads + h];
+        o[k] = active ? *reinterpret_cast<const float4*>(part_o + ((int64_t)pi[k] * n_heads + h) * hd + 4 * lane)
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float wgt = l[k] == -INFINITY ? 0.f : __expf(l[k] - mx);
+        den += wgt;
+        num.x += wgt * o[k].x;
+        num.y += wgt * o[k].y;
+        num.z += wgt * o[k].z;
+        num.w += wgt * o[k].w;
+      }
+    }
+    for (; i < e; i += 4) {
+      const int pi = row_part[i];
+      const float l = part_lse[(int64_t)pi * n_heads + h];
+      if (l == -INFINITY) continue;
+      const float wgt = __expf(l - mx);
+      den += wgt;
+      if (active) {
+        const float4 o = *reinterpret_cast<const float4*>(part_o + ((int64_t)pi * n_heads + h) * hd + 4 * lane);
+        num.x += wgt * o.x;
+        num.y += wgt * o.y;
+        num.z += wgt * o.z;
+        num.w += wgt * o.w;
+      }
+    }
   }
+  s_num[warp][lane] = num;
+  if (lane == 0) s_den[warp] = den;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    float den = 0.f;
-    for (int i = 0; i < e - b && i < 512; ++i) den += wsh[i];
-    s_den = den;
-  }
-  __syncthreads();
-  const float inv = s_den > 0.f ? 1.f / s_den : 0.f;
-  for (int d = threadIdx.x; d < hd; d += blockDim.x) {
-    float num = 0.f;
-    for (int i = 0; i < e - b && i < 512; ++i)
-      if (wsh[i] != 0.f) num += wsh[i] * part_o[((int64_t)row_part[b + i] * n_heads + h) * hd + d];
-    const float y = num * inv;
-    const int64_t oi = ((int64_t)r * n_heads + h) * hd + d;
-    const TO hi = from_f32<TO>(y);
-    out[oi] = hi;
-    if (split) out[(int64_t)n_rows * n_heads * hd + oi] = from_f32<TO>(y - to_f32(hi));
+  if (warp == 0 && active) {
+    float4 t = s_num[0][lane];
+    for (int k = 1; k < 4; ++k) {
+      t.x += s_num[k][lane].x;
+      t.y += s_num[k][lane].y;
+      t.z += s_num[k][lane].z;
+      t.w += s_num[k][lane].w;
+    }
+    const float dsum = s_den[0] + s_den[1] + s_den[2] + s_den[3];
+    const float inv = dsum > 0.f ? 1.f / dsum : 0.f;
+    const float y[4] = {t.x * inv, t.y * inv, t.z * inv, t.w * inv};
+    const int64_t oi = ((int64_t)r * n_heads + h) * hd + 4 * lane;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const TO hi = from_f32<TO>(y[k]);
+      out[oi + k] = hi;
+      if (split) out[(int64_t)n_rows * n_heads * hd + oi + k] = from_f32<TO>(y[k] - to_f32(hi));
+    }
   }
 }
 
@@ -595,7 +637,8 @@ int choreo_attn_combine(const float* part_o, const float* part_lse, const int32_
   if (out_split && out_dtype != CHOREO_BF16) return CHOREO_EINVAL;
   if (n_rows == 0) return CHOREO_OK;
   auto s = as_stream(stream);
-  const int threads = head_dim >= 128 ? 128 : 64;
+  if (head_dim % 4 || head_dim > 128) return CHOREO_EUNSUPPORTED;
+  const int threads = 128;
   if (out_dtype == CHOREO_BF16)
     attn_combine_kernel<__nv_bfloat16><<<n_rows * n_heads, threads, 0, s>>>(
         part_o, part_lse, row_part_off, row_part, n_rows, n_heads, head_dim, out_split,

@@ -73,6 +73,95 @@ __global__ void residual_rmsnorm_kernel(float* __restrict__ x, const void* __res
                 xr[i] * inv * load_any(w, w_dt, i), out_split);
 }
 
+// Vectorised variant (d % 4 == 0, f32 delta): every load of a row is issued before
+// the first use (CH float4 chunks per thread kept in registers across both passes),
+// so a row costs ~2 memory latencies instead of one per element.
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ float4 ld4_any(const void* p, int dt, int64_t i) {
+  if (dt == CHOREO_BF16) {
+    const uint2 u = *reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(p) + i);
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+    return make_float4(a.x, a.y, b.x, b.y);
+  }
+  return ld4(reinterpret_cast<const float*>(p) + i);
+}
+__device__ __forceinline__ void st4_split(void* out, int dt, int64_t i_hi, int64_t i_lo, float4 y,
+                                          int split) {
+  if (dt == CHOREO_BF16) {
+    const __nv_bfloat162 h0 = __floats2bfloat162_rn(y.x, y.y), h1 = __floats2bfloat162_rn(y.z, y.w);
+    uint2 u;
+    u.x = *reinterpret_cast<const uint32_t*>(&h0);
+    u.y = *reinterpret_cast<const uint32_t*>(&h1);
+    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(out) + i_hi) = u;
+    if (split) {
+      const float2 f0 = __bfloat1622float2(h0), f1 = __bfloat1622float2(h1);
+      const __nv_bfloat162 l0 = __floats2bfloat162_rn(y.x - f0.x, y.y - f0.y);
+      const __nv_bfloat162 l1 = __floats2bfloat162_rn(y.z - f1.x, y.w - f1.y);
+      u.x = *reinterpret_cast<const uint32_t*>(&l0);
+      u.y = *reinterpret_cast<const uint32_t*>(&l1);
+      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(out) + i_lo) = u;
+    }
+  } else {
+    *reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + i_hi) = y;
+  }
+}
+
+template <int CH>
+__global__ void residual_rmsnorm_vec(float* __restrict__ x, const float* __restrict__ delta,
+                                     int delta_split, int n_rows, const void* __restrict__ w,
+                                     int w_dt, int d, float eps, void* __restrict__ out, int out_dt,
+                                     int out_split, const int32_t* __restrict__ row_map) {
+  const int r_out = blockIdx.x;
+  const int r = row_map ? row_map[r_out] : r_out;
+  const int nvec = d >> 2;
+  float* xr = x + (int64_t)r * d;
+  float4 v[CH];
+  float ss = 0.f;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    const int i = threadIdx.x + c * blockDim.x;
+    v[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (i < nvec) {
+      v[c] = ld4(xr + 4 * i);
+      if (delta) {
+        const float4 a = ld4(delta + (int64_t)r * d + 4 * i);
+        float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (delta_split) b = ld4(delta + (int64_t)(n_rows + r) * d + 4 * i);
+        v[c].x += a.x + b.x;
+        v[c].y += a.y + b.y;
+        v[c].z += a.z + b.z;
+        v[c].w += a.w + b.w;
+        *reinterpret_cast<float4*>(xr + 4 * i) = v[c];
+      }
+    }
+    ss += v[c].x * v[c].x + v[c].y * v[c].y + v[c].z * v[c].z + v[c].w * v[c].w;
+  }
+  if (!out) return;
+  __shared__ float red[33];
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) red[32] = t;
+  }
+  __syncthreads();
+  const float inv = 1.0f / sqrtf(red[32] / (float)d + eps);
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    const int i = threadIdx.x + c * blockDim.x;
+    if (i < nvec) {
+      const float4 wv = ld4_any(w, w_dt, 4 * i);
+      const float4 y = make_float4(v[c].x * inv * wv.x, v[c].y * inv * wv.y, v[c].z * inv * wv.z,
+                                   v[c].w * inv * wv.w);
+      st4_split(out, out_dt, (int64_t)r_out * d + 4 * i, (int64_t)(gridDim.x + r_out) * d + 4 * i,
+                y, out_split);
+    }
+  }
+}
+
 __global__ void silu_mul_kernel(const void* __restrict__ gu, int dt, int in_split, int n_rows,
                                 int f, void* __restrict__ out, int out_dt, int out_split) {
   const int64_t n = (int64_t)n_rows * f, lo_in = (int64_t)n_rows * 2 * f;
@@ -142,6 +231,22 @@ int choreo_residual_rmsnorm(float* x, const void* delta, int delta_dtype, int de
   if (out_split && out_dtype != CHOREO_BF16) return CHOREO_EINVAL;
   const int rows = row_map ? n_out : n_rows;
   if (rows == 0) return CHOREO_OK;
+  if (d % 4 == 0 && (!delta || delta_dtype == CHOREO_F32) && d <= 4 * 4 * 1024) {
+    const int nvec = d / 4;
+    int threads = nvec < 1024 ? ((nvec + 31) / 32) * 32 : 1024;
+    if (nvec > 2048) threads = 1024;
+    const int ch = (nvec + threads - 1) / threads;
+    auto s = as_stream(stream);
+#define RMS_VEC(CH)                                                                            \
+  residual_rmsnorm_vec<CH><<<rows, threads, 0, s>>>(x, (const float*)delta, delta_split, n_rows, \
+                                                    w, w_dtype, d, eps, out, out_dtype,          \
+                                                    out_split, row_map)
+    if (ch == 1) RMS_VEC(1);
+    else if (ch == 2) RMS_VEC(2);
+    else RMS_VEC(4);
+#undef RMS_VEC
+    return launch_status("choreo_residual_rmsnorm");
+  }
   const int threads = d >= 2048 ? 512 : (d >= 256 ? 256 : 64);
   residual_rmsnorm_kernel<<<rows, threads, 0, as_stream(stream)>>>(
       x, delta, delta_dtype, delta_split, n_rows, w, w_dtype, d, eps, out, out_dtype, out_split,
