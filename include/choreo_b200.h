@@ -129,15 +129,16 @@ int choreo_assemble(const int32_t* msg_len, const int32_t* msg_pt, int32_t* page
  * per-(row, q-head) partials: part_o f32 [n_partials][n_heads][hd] (normalised) and
  * part_lse f32 [n_partials][n_heads] (natural-log sum-exp; -inf if nothing visible).
  * bf16 pools with page_size 64 and hd 64/128 run on tensor cores (mma.sync, cp.async
- * 3-stage page pipeline); f32 pools run the SIMT f32 path.  grid_ctas = persistent CTAs
- * (0 = auto).  Replaces model.py:177-184 + tensor.py:65-75 (gather, concat, scores,
+ * double-buffered page pipeline); f32 pools run the SIMT f32 path.  grid_ctas = persistent
+ * CTAs (0 = auto).  flags (tensor-core path): bit 0 = Q as a hi/lo bf16 pair, bit 1 = P as
+ * a hi/lo pair (each doubles that product's MMAs; 0 = plain bf16).  Replaces model.py:177-184 + tensor.py:65-75 (gather, concat, scores,
  * masked softmax, P.V). */
 int choreo_attn_split(const float* q, const void* k_pool, const void* v_pool, int pool_dtype,
                       int layer, int n_kv, int n_pages, int page_size, int n_heads, int head_dim,
                       const int32_t* row_t, const int32_t* vis_page, const int32_t* vis_len,
                       const int32_t* vis_own, const int32_t* blk_rows, const int32_t* items,
                       const int32_t* counts, int max_items, float* part_o, float* part_lse,
-                      int grid_ctas, void* stream);
+                      int grid_ctas, int flags, void* stream);
 
 /* Combine each row's partials (CSR row_part_off / row_part, <= 512 per row) into
  * out[r][h][:] (out_dtype; hi/lo pair if out_split) with the LSE merge. */

@@ -35,6 +35,7 @@ struct SplitParams {
   float* part_o;
   float* part_lse;
   float scale;
+  int q_split, p_split;  // carry Q / P as hi+lo bf16 pairs in the MMAs (1) or plain bf16 (0)
 };
 
 // ============================================================ SIMT path (f32 pools)
@@ -168,7 +169,7 @@ __global__ void __launch_bounds__(kThreads) attn_split_simt(SplitParams p) {
 
 // ============================================================ tensor-core path (bf16)
 constexpr int kMmaThreads = 128;  // 4 warps
-constexpr int kStages = 3;
+constexpr int kStages = 2;        // page double buffer (3 CTAs/SM at hd 128)
 constexpr int kPage = 64;         // keys per page (= page_size for this path)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
@@ -182,10 +183,6 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
-  return *reinterpret_cast<uint32_t*>(&v);
 }
 // hi = bf16(x), lo = bf16(x - hi), packed pairs
 __device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t& lo) {
@@ -209,264 +206,274 @@ __device__ __forceinline__ void ldsm_x4_trans(uint32_t& r0, uint32_t& r1, uint32
                : "r"(smem_u32(ptr)));
 }
 
-// Warp roles: MT = m16 tiles needed (ceil(G*rows/16) <= 4); the KW = 4/MT warp groups
-// split each page's 64 keys; warp w owns m-tile (w % MT) and key slice (w / MT).
-template <int HD>
-__global__ void __launch_bounds__(kMmaThreads, 2) attn_split_mma(SplitParams p) {
-  constexpr int LD = HD + 8;  // padded smem row (bf16 elems): conflict-free fragments
-  constexpr int NT = HD / 8;  // n8 tiles over head dim
-  constexpr int KS = HD / 16; // k16 steps over head dim
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(smem_raw);     // [kStages][64][LD]
-  __nv_bfloat16* Vs = Ks + kStages * kPage * LD;                        // [kStages][64][LD]
-  float* red = reinterpret_cast<float*>(smem_raw);  // merge scratch, reuses the page stages
-  __shared__ int s_rid[64], s_rt[64];
+// Per-item state shared by the warps of a CTA.
+struct ItemCtx {
+  int kvh, vb, nv, pbase, M, G;
+  int n_heads, n_kv, n_pages, page_size, layer;
+  const int* s_rid;
+  const int* s_rt;
+};
 
+// One work item on one KV head.  MT = m16 query tiles (G*rows <= 16*MT); the KW = 4/MT
+// warp groups split each page's 64 keys (warp w: m-tile w % MT, key slice w / MT) and
+// walk their slice in 16-key chunks with an online softmax.  Hi and lo halves of Q and
+// P run on separate accumulator chains so consecutive MMAs are independent.
+template <int HD, int MT>
+__device__ __forceinline__ void mma_item(const SplitParams& p, const ItemCtx& c,
+                                         __nv_bfloat16* Ks, __nv_bfloat16* Vs, float* red) {
+  constexpr int LD = HD + 8;
+  constexpr int NT = HD / 8;
+  constexpr int KS = HD / 16;
+  constexpr int KW = 4 / MT;
+  constexpr int SLICE = kPage / KW;  // keys per warp per page
+  constexpr int CHUNKS = SLICE / 16;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int G = p.n_heads / p.n_kv;
-  const int n_work = p.counts[1] * p.n_kv;
+  const int mt = warp % MT, kg = warp / MT;
   const __nv_bfloat16* kp = reinterpret_cast<const __nv_bfloat16*>(p.k_pool);
   const __nv_bfloat16* vp = reinterpret_cast<const __nv_bfloat16*>(p.v_pool);
-  const float sl2 = p.scale * 1.4426950408889634f;  // scores in log2 domain
 
+  auto load_page = [&](int stage, int pi) {
+    if (pi < c.vb + c.nv) {
+      const int page = p.vis_page[pi], len = p.vis_len[pi];
+      const int64_t base = pool_off(c.layer, c.kvh, page, 0, c.n_kv, c.n_pages, c.page_size, HD);
+      constexpr int CH = HD / 8;
+#pragma unroll 4
+      for (int q = tid; q < kPage * CH; q += kMmaThreads) {
+        const int row = q / CH, col = (q % CH) * 8;
+        const int nb = row < len ? 16 : 0;
+        const int64_t src = base + (int64_t)(row < len ? row : 0) * HD + col;
+        cp_async16(Ks + (stage * kPage + row) * LD + col, kp + src, nb);
+        cp_async16(Vs + (stage * kPage + row) * LD + col, vp + src, nb);
+      }
+    }
+    cp_async_commit();
+  };
+  load_page(0, c.vb);
+
+  // Q fragments (hi/lo), rows m = mt*16 + {g, g+8}, pre-scaled to the log2 domain
+  const float sl2 = p.scale * 1.4426950408889634f;
+  uint32_t qh[KS][4], ql[KS][4];
+  const int rowA = mt * 16 + g, rowB = rowA + 8;
+  const bool vA = rowA < c.M, vB = rowB < c.M;
+  const float* qA = p.q + ((int64_t)c.s_rid[vA ? rowA / c.G : 0] * c.n_heads + c.kvh * c.G + rowA % c.G) * HD;
+  const float* qB = p.q + ((int64_t)c.s_rid[vB ? rowB / c.G : 0] * c.n_heads + c.kvh * c.G + rowB % c.G) * HD;
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) {
+    const int c0 = ks * 16 + 2 * t;
+    const float2 z = make_float2(0.f, 0.f);
+    const float2 a0 = vA ? *reinterpret_cast<const float2*>(qA + c0) : z;
+    const float2 a1 = vB ? *reinterpret_cast<const float2*>(qB + c0) : z;
+    const float2 a2 = vA ? *reinterpret_cast<const float2*>(qA + c0 + 8) : z;
+    const float2 a3 = vB ? *reinterpret_cast<const float2*>(qB + c0 + 8) : z;
+    split2(a0.x * sl2, a0.y * sl2, qh[ks][0], ql[ks][0]);
+    split2(a1.x * sl2, a1.y * sl2, qh[ks][1], ql[ks][1]);
+    split2(a2.x * sl2, a2.y * sl2, qh[ks][2], ql[ks][2]);
+    split2(a3.x * sl2, a3.y * sl2, qh[ks][3], ql[ks][3]);
+  }
+  const int rtA = vA ? c.s_rt[rowA / c.G] : -1, rtB = vB ? c.s_rt[rowB / c.G] : -1;
+
+  float o[NT][4];
+#pragma unroll
+  for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+  float mA = -INFINITY, mB = -INFINITY, lA = 0.f, lB = 0.f;
+
+  for (int pi = c.vb; pi < c.vb + c.nv; ++pi) {
+    const int stage = (pi - c.vb) & 1;
+    load_page(stage ^ 1, pi + 1);  // prefetch next page into the other buffer
+    cp_async_wait<1>();
+    __syncthreads();
+    const int len = p.vis_len[pi], own = p.vis_own[pi];
+    const __nv_bfloat16* Kt = Ks + stage * kPage * LD;
+    const __nv_bfloat16* Vt = Vs + stage * kPage * LD;
+#pragma unroll
+    for (int ch = 0; ch < CHUNKS; ++ch) {
+      const int k0 = kg * SLICE + ch * 16;
+      if (k0 >= len) break;
+      float sh[2][4], sl[2][4];
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) sh[j][e] = sl[j][e] = 0.f;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const __nv_bfloat16* kr = Kt + (k0 + j * 8 + g) * LD + ks * 16 + 2 * t;
+          const uint32_t b0 = *reinterpret_cast<const uint32_t*>(kr);
+          const uint32_t b1 = *reinterpret_cast<const uint32_t*>(kr + 8);
+          mma16816(sh[j], qh[ks], b0, b1);
+          if (p.q_split) mma16816(sl[j], ql[ks], b0, b1);
+        }
+      }
+      float s[2][4];
+      float tA = -INFINITY, tB = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int key = k0 + j * 8 + 2 * t + e;
+          const bool okA = vA && key < len && (own < 0 || own + key <= rtA);
+          const bool okB = vB && key < len && (own < 0 || own + key <= rtB);
+          s[j][e] = okA ? sh[j][e] + sl[j][e] : -INFINITY;
+          s[j][2 + e] = okB ? sh[j][2 + e] + sl[j][2 + e] : -INFINITY;
+          tA = fmaxf(tA, s[j][e]);
+          tB = fmaxf(tB, s[j][2 + e]);
+        }
+      tA = fmaxf(tA, __shfl_xor_sync(0xffffffffu, tA, 1));
+      tA = fmaxf(tA, __shfl_xor_sync(0xffffffffu, tA, 2));
+      tB = fmaxf(tB, __shfl_xor_sync(0xffffffffu, tB, 1));
+      tB = fmaxf(tB, __shfl_xor_sync(0xffffffffu, tB, 2));
+      const float nA = fmaxf(mA, tA), nB = fmaxf(mB, tB);
+      const float aA = nA == -INFINITY ? 1.f : exp2f(mA - nA);
+      const float aB = nB == -INFINITY ? 1.f : exp2f(mB - nB);
+      float sumA = 0.f, sumB = 0.f;
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          s[j][e] = s[j][e] == -INFINITY ? 0.f : exp2f(s[j][e] - nA);
+          s[j][2 + e] = s[j][2 + e] == -INFINITY ? 0.f : exp2f(s[j][2 + e] - nB);
+          sumA += s[j][e];
+          sumB += s[j][2 + e];
+        }
+      lA = lA * aA + sumA;
+      lB = lB * aB + sumB;
+      mA = nA;
+      mB = nB;
+      uint32_t ph[4], pl[4];
+      split2(s[0][0], s[0][1], ph[0], pl[0]);
+      split2(s[0][2], s[0][3], ph[1], pl[1]);
+      split2(s[1][0], s[1][1], ph[2], pl[2]);
+      split2(s[1][2], s[1][3], ph[3], pl[3]);
+      const int mi = lane >> 3;
+      const __nv_bfloat16* vrow = Vt + (k0 + (mi & 1) * 8 + (lane & 7)) * LD + (mi >> 1) * 8;
+#pragma unroll
+      for (int n = 0; n < NT; n += 2) {
+        o[n][0] *= aA;
+        o[n][1] *= aA;
+        o[n][2] *= aB;
+        o[n][3] *= aB;
+        o[n + 1][0] *= aA;
+        o[n + 1][1] *= aA;
+        o[n + 1][2] *= aB;
+        o[n + 1][3] *= aB;
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4_trans(b0, b1, b2, b3, vrow + n * 8);
+        mma16816(o[n], ph, b0, b1);
+        mma16816(o[n + 1], ph, b2, b3);
+        if (p.p_split) {
+          mma16816(o[n], pl, b0, b1);
+          mma16816(o[n + 1], pl, b2, b3);
+        }
+      }
+    }
+    __syncthreads();  // everyone done with this stage before it is refilled
+  }
+  cp_async_wait<0>();
+  lA += __shfl_xor_sync(0xffffffffu, lA, 1);
+  lA += __shfl_xor_sync(0xffffffffu, lA, 2);
+  lB += __shfl_xor_sync(0xffffffffu, lB, 1);
+  lB += __shfl_xor_sync(0xffffffffu, lB, 2);
+  // ---- merge the KW key-slice warps of each m-tile through smem (reuses the pages) ----
+  float* my = red + warp * (16 * HD + 32);
+  if (KW > 1) {
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+      *reinterpret_cast<float2*>(my + g * HD + n * 8 + 2 * t) = make_float2(o[n][0], o[n][1]);
+      *reinterpret_cast<float2*>(my + (g + 8) * HD + n * 8 + 2 * t) = make_float2(o[n][2], o[n][3]);
+    }
+    if (t == 0) {
+      my[16 * HD + g] = mA;
+      my[16 * HD + g + 8] = mB;
+      my[16 * HD + 16 + g] = lA;
+      my[16 * HD + 16 + g + 8] = lB;
+    }
+  }
+  __syncthreads();
+  if (kg == 0) {
+    float fmA = mA, fmB = mB;
+#pragma unroll
+    for (int k = 1; k < KW; ++k) {
+      const float* ot = red + (warp + k * MT) * (16 * HD + 32);
+      fmA = fmaxf(fmA, ot[16 * HD + g]);
+      fmB = fmaxf(fmB, ot[16 * HD + g + 8]);
+    }
+    const float wA0 = fmA == -INFINITY ? 0.f : exp2f(mA - fmA);
+    const float wB0 = fmB == -INFINITY ? 0.f : exp2f(mB - fmB);
+    float LA = lA * wA0, LB = lB * wB0;
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+      o[n][0] *= wA0;
+      o[n][1] *= wA0;
+      o[n][2] *= wB0;
+      o[n][3] *= wB0;
+    }
+#pragma unroll
+    for (int k = 1; k < KW; ++k) {
+      const float* ot = red + (warp + k * MT) * (16 * HD + 32);
+      const float wA = fmA == -INFINITY ? 0.f : exp2f(ot[16 * HD + g] - fmA);
+      const float wB = fmB == -INFINITY ? 0.f : exp2f(ot[16 * HD + g + 8] - fmB);
+      LA += ot[16 * HD + 16 + g] * wA;
+      LB += ot[16 * HD + 16 + g + 8] * wB;
+#pragma unroll
+      for (int n = 0; n < NT; ++n) {
+        const float2 xa = *reinterpret_cast<const float2*>(ot + g * HD + n * 8 + 2 * t);
+        const float2 xb = *reinterpret_cast<const float2*>(ot + (g + 8) * HD + n * 8 + 2 * t);
+        o[n][0] += wA * xa.x;
+        o[n][1] += wA * xa.y;
+        o[n][2] += wB * xb.x;
+        o[n][3] += wB * xb.y;
+      }
+    }
+    const float ln2 = 0.6931471805599453f;
+    if (vA) {
+      const int64_t pidx = (int64_t)(c.pbase + rowA / c.G) * c.n_heads + c.kvh * c.G + rowA % c.G;
+      const float inv = LA > 0.f ? 1.f / LA : 0.f;
+#pragma unroll
+      for (int n = 0; n < NT; ++n)
+        *reinterpret_cast<float2*>(p.part_o + pidx * HD + n * 8 + 2 * t) =
+            make_float2(o[n][0] * inv, o[n][1] * inv);
+      if (t == 0) p.part_lse[pidx] = LA > 0.f ? (fmA + log2f(LA)) * ln2 : -INFINITY;
+    }
+    if (vB) {
+      const int64_t pidx = (int64_t)(c.pbase + rowB / c.G) * c.n_heads + c.kvh * c.G + rowB % c.G;
+      const float inv = LB > 0.f ? 1.f / LB : 0.f;
+#pragma unroll
+      for (int n = 0; n < NT; ++n)
+        *reinterpret_cast<float2*>(p.part_o + pidx * HD + n * 8 + 2 * t) =
+            make_float2(o[n][2] * inv, o[n][3] * inv);
+      if (t == 0) p.part_lse[pidx] = LB > 0.f ? (fmB + log2f(LB)) * ln2 : -INFINITY;
+    }
+  }
+}
+
+template <int HD>
+__global__ void __launch_bounds__(kMmaThreads, 3) attn_split_mma(SplitParams p) {
+  constexpr int LD = HD + 8;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(smem_raw);  // [kStages][64][LD]
+  __nv_bfloat16* Vs = Ks + kStages * kPage * LD;                     // [kStages][64][LD]
+  float* red = reinterpret_cast<float*>(smem_raw);  // merge scratch, reuses the page stages
+  __shared__ int s_rid[64], s_rt[64];
+  const int tid = threadIdx.x;
+  const int G = p.n_heads / p.n_kv;
+  const int n_work = p.counts[1] * p.n_kv;
   for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
     const int32_t* it = p.items + 6 * (w / p.n_kv);
-    const int kvh = w % p.n_kv;
-    const int rb = it[0], nr = it[1], vb = it[2], nv = it[3], pbase = it[4];
-    const int M = nr * G;
-    const int MT = M <= 16 ? 1 : (M <= 32 ? 2 : 4);
-    const int KW = 4 / MT;
-    const int mt = warp % MT, kg = warp / MT;
-    const int kslice = kPage / KW;  // keys of each page handled by this warp
-    __syncthreads();
+    const int rb = it[0], nr = it[1];
+    __syncthreads();  // previous item fully done with smem
     for (int r = tid; r < nr; r += kMmaThreads) {
-      s_rid[r] = p.blk_rows[rb + r];
-      s_rt[r] = p.row_t[s_rid[r]];
-    }
-    // page loader: stage s <- page index pi (K and V, zero-fill slots >= len)
-    auto load_page = [&](int stage, int pi) {
-      if (pi < vb + nv) {
-        const int page = p.vis_page[pi], len = p.vis_len[pi];
-        const int64_t base = pool_off(p.layer, kvh, page, 0, p.n_kv, p.n_pages, p.page_size, HD);
-        constexpr int CH = HD / 8;  // 16-byte chunks per row
-        for (int c = tid; c < kPage * CH; c += kMmaThreads) {
-          const int row = c / CH, col = (c % CH) * 8;
-          const int nb = row < len ? 16 : 0;
-          const int64_t src = base + (int64_t)(row < len ? row : 0) * HD + col;
-          cp_async16(Ks + (stage * kPage + row) * LD + col, kp + src, nb);
-          cp_async16(Vs + (stage * kPage + row) * LD + col, vp + src, nb);
-        }
-      }
-      cp_async_commit();
-    };
-    for (int s = 0; s < kStages - 1; ++s) load_page(s, vb + s);
-    __syncthreads();  // s_rid / s_rt visible
-
-    // Q fragments (hi/lo) for this warp's m-tile: rows m = mt*16 + {g, g+8}
-    uint32_t qh[KS][4], ql[KS][4];
-    int rowA = mt * 16 + g, rowB = rowA + 8;
-    const bool vA = rowA < M, vB = rowB < M;
-    const float* qA = vA ? p.q + ((int64_t)s_rid[rowA / G] * p.n_heads + kvh * G + rowA % G) * HD : nullptr;
-    const float* qB = vB ? p.q + ((int64_t)s_rid[rowB / G] * p.n_heads + kvh * G + rowB % G) * HD : nullptr;
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      const int c0 = ks * 16 + 2 * t;
-      float2 a0 = vA ? *reinterpret_cast<const float2*>(qA + c0) : make_float2(0.f, 0.f);
-      float2 a1 = vB ? *reinterpret_cast<const float2*>(qB + c0) : make_float2(0.f, 0.f);
-      float2 a2 = vA ? *reinterpret_cast<const float2*>(qA + c0 + 8) : make_float2(0.f, 0.f);
-      float2 a3 = vB ? *reinterpret_cast<const float2*>(qB + c0 + 8) : make_float2(0.f, 0.f);
-      split2(a0.x * sl2, a0.y * sl2, qh[ks][0], ql[ks][0]);
-      split2(a1.x * sl2, a1.y * sl2, qh[ks][1], ql[ks][1]);
-      split2(a2.x * sl2, a2.y * sl2, qh[ks][2], ql[ks][2]);
-      split2(a3.x * sl2, a3.y * sl2, qh[ks][3], ql[ks][3]);
-    }
-    const int rtA = vA ? s_rt[rowA / G] : -1, rtB = vB ? s_rt[rowB / G] : -1;
-
-    float o[NT][4];
-#pragma unroll
-    for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
-    float mA = -INFINITY, mB = -INFINITY, lA = 0.f, lB = 0.f;
-
-    for (int pi = vb; pi < vb + nv; ++pi) {
-      const int stage = (pi - vb) % kStages;
-      cp_async_wait<kStages - 2>();
-      __syncthreads();
-      load_page((pi - vb + kStages - 1) % kStages, pi + kStages - 1);
-      const int len = p.vis_len[pi], own = p.vis_own[pi];
-      const __nv_bfloat16* Kt = Ks + stage * kPage * LD;
-      const __nv_bfloat16* Vt = Vs + stage * kPage * LD;
-      const int k0 = kg * kslice;  // this warp's key slice [k0, k0 + kslice)
-      if (k0 < len) {
-        // ---- S = Q K^T over the slice (kslice/8 n8 tiles) ----
-        constexpr int MAXN = kPage / 8;
-        float s[MAXN][4];
-        const int nn = kslice / 8;
-#pragma unroll
-        for (int j = 0; j < MAXN; ++j) {
-          s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
-          if (j < nn) {
-            const __nv_bfloat16* kr = Kt + (k0 + j * 8 + g) * LD + 2 * t;
-#pragma unroll
-            for (int ks = 0; ks < KS; ++ks) {
-              const uint32_t b0 = *reinterpret_cast<const uint32_t*>(kr + ks * 16);
-              const uint32_t b1 = *reinterpret_cast<const uint32_t*>(kr + ks * 16 + 8);
-              mma16816(s[j], qh[ks], b0, b1);
-              mma16816(s[j], ql[ks], b0, b1);
-            }
-          }
-        }
-        // ---- mask + online softmax (rows A = g, B = g + 8 of the m-tile) ----
-        float tA = -INFINITY, tB = -INFINITY;
-#pragma unroll
-        for (int j = 0; j < MAXN; ++j) {
-          if (j >= nn) continue;
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int key = k0 + j * 8 + 2 * t + e;
-            const bool okA = vA && key < len && (own < 0 || own + key <= rtA);
-            const bool okB = vB && key < len && (own < 0 || own + key <= rtB);
-            s[j][e] = okA ? s[j][e] : -INFINITY;
-            s[j][2 + e] = okB ? s[j][2 + e] : -INFINITY;
-            tA = fmaxf(tA, s[j][e]);
-            tB = fmaxf(tB, s[j][2 + e]);
-          }
-        }
-        tA = fmaxf(tA, __shfl_xor_sync(0xffffffffu, tA, 1));
-        tA = fmaxf(tA, __shfl_xor_sync(0xffffffffu, tA, 2));
-        tB = fmaxf(tB, __shfl_xor_sync(0xffffffffu, tB, 1));
-        tB = fmaxf(tB, __shfl_xor_sync(0xffffffffu, tB, 2));
-        const float nA = fmaxf(mA, tA), nB = fmaxf(mB, tB);
-        const float aA = nA == -INFINITY ? 1.f : exp2f(mA - nA);
-        const float aB = nB == -INFINITY ? 1.f : exp2f(mB - nB);
-        float sumA = 0.f, sumB = 0.f;
-#pragma unroll
-        for (int j = 0; j < MAXN; ++j) {
-          if (j >= nn) continue;
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            s[j][e] = s[j][e] == -INFINITY ? 0.f : exp2f(s[j][e] - nA);
-            s[j][2 + e] = s[j][2 + e] == -INFINITY ? 0.f : exp2f(s[j][2 + e] - nB);
-            sumA += s[j][e];
-            sumB += s[j][2 + e];
-          }
-        }
-        lA = lA * aA + sumA;
-        lB = lB * aB + sumB;
-        mA = nA;
-        mB = nB;
-#pragma unroll
-        for (int n = 0; n < NT; ++n) {
-          o[n][0] *= aA;
-          o[n][1] *= aA;
-          o[n][2] *= aB;
-          o[n][3] *= aB;
-        }
-        // ---- O += P V over the slice: k16 steps of keys, P as hi/lo A fragments ----
-#pragma unroll
-        for (int kk = 0; kk < MAXN / 2; ++kk) {
-          if (2 * kk >= nn) continue;
-          uint32_t ph[4], pl[4];
-          split2(s[2 * kk][0], s[2 * kk][1], ph[0], pl[0]);
-          split2(s[2 * kk][2], s[2 * kk][3], ph[1], pl[1]);
-          split2(s[2 * kk + 1][0], s[2 * kk + 1][1], ph[2], pl[2]);
-          split2(s[2 * kk + 1][2], s[2 * kk + 1][3], ph[3], pl[3]);
-          const int krow = k0 + kk * 16;
-#pragma unroll
-          for (int n = 0; n < NT; n += 2) {
-            // x4.trans: matrices (keys 0-7, dims n*8), (keys 8-15, n*8), (0-7, n*8+8), (8-15, n*8+8)
-            const int mi = lane >> 3;
-            const __nv_bfloat16* ptr = Vt + (krow + (mi & 1) * 8 + (lane & 7)) * LD + n * 8 + (mi >> 1) * 8;
-            uint32_t b0, b1, b2, b3;
-            ldsm_x4_trans(b0, b1, b2, b3, ptr);
-            mma16816(o[n], ph, b0, b1);
-            mma16816(o[n], pl, b0, b1);
-            mma16816(o[n + 1], ph, b2, b3);
-            mma16816(o[n + 1], pl, b2, b3);
-          }
-        }
-      }
-    }
-    cp_async_wait<0>();
-    // quad-reduce the row sums
-    lA += __shfl_xor_sync(0xffffffffu, lA, 1);
-    lA += __shfl_xor_sync(0xffffffffu, lA, 2);
-    lB += __shfl_xor_sync(0xffffffffu, lB, 1);
-    lB += __shfl_xor_sync(0xffffffffu, lB, 2);
-    __syncthreads();  // smem pages no longer needed: reuse as merge scratch
-    // ---- merge the KW key-slice warps of each m-tile (through smem) ----
-    // layout per warp: [16 rows][HD] o, then m[16], l[16]
-    float* my = red + warp * (16 * HD + 32);
-    if (KW > 1) {
-#pragma unroll
-      for (int n = 0; n < NT; ++n) {
-        my[g * HD + n * 8 + 2 * t] = o[n][0];
-        my[g * HD + n * 8 + 2 * t + 1] = o[n][1];
-        my[(g + 8) * HD + n * 8 + 2 * t] = o[n][2];
-        my[(g + 8) * HD + n * 8 + 2 * t + 1] = o[n][3];
-      }
-      if (t == 0) {
-        my[16 * HD + g] = mA;
-        my[16 * HD + g + 8] = mB;
-        my[16 * HD + 16 + g] = lA;
-        my[16 * HD + 16 + g + 8] = lB;
-      }
+      const int rid = p.blk_rows[rb + r];
+      s_rid[r] = rid;
+      s_rt[r] = p.row_t[rid];
     }
     __syncthreads();
-    if (kg == 0) {
-      // final m, l over the key slices of this m-tile
-      float fmA = mA, fmB = mB;
-      for (int k = 1; k < KW; ++k) {
-        const float* ot = red + (warp + k * MT) * (16 * HD + 32);
-        fmA = fmaxf(fmA, ot[16 * HD + g]);
-        fmB = fmaxf(fmB, ot[16 * HD + g + 8]);
-      }
-      const float wA0 = fmA == -INFINITY ? 0.f : exp2f(mA - fmA);
-      const float wB0 = fmB == -INFINITY ? 0.f : exp2f(mB - fmB);
-      float LA = lA * wA0, LB = lB * wB0;
-#pragma unroll
-      for (int n = 0; n < NT; ++n) {
-        o[n][0] *= wA0;
-        o[n][1] *= wA0;
-        o[n][2] *= wB0;
-        o[n][3] *= wB0;
-      }
-      for (int k = 1; k < KW; ++k) {
-        const float* ot = red + (warp + k * MT) * (16 * HD + 32);
-        const float mk_A = ot[16 * HD + g], mk_B = ot[16 * HD + g + 8];
-        const float wA = fmA == -INFINITY ? 0.f : exp2f(mk_A - fmA);
-        const float wB = fmB == -INFINITY ? 0.f : exp2f(mk_B - fmB);
-        LA += ot[16 * HD + 16 + g] * wA;
-        LB += ot[16 * HD + 16 + g + 8] * wB;
-#pragma unroll
-        for (int n = 0; n < NT; ++n) {
-          o[n][0] += wA * ot[g * HD + n * 8 + 2 * t];
-          o[n][1] += wA * ot[g * HD + n * 8 + 2 * t + 1];
-          o[n][2] += wB * ot[(g + 8) * HD + n * 8 + 2 * t];
-          o[n][3] += wB * ot[(g + 8) * HD + n * 8 + 2 * t + 1];
-        }
-      }
-      // write normalised partials + natural-log LSE
-      const float ln2 = 0.6931471805599453f;
-      if (vA) {
-        const int64_t pidx = (int64_t)(pbase + rowA / G) * p.n_heads + kvh * G + rowA % G;
-        const float inv = LA > 0.f ? 1.f / LA : 0.f;
-#pragma unroll
-        for (int n = 0; n < NT; ++n)
-          *reinterpret_cast<float2*>(p.part_o + pidx * HD + n * 8 + 2 * t) =
-              make_float2(o[n][0] * inv, o[n][1] * inv);
-        if (t == 0) p.part_lse[pidx] = LA > 0.f ? (fmA + log2f(LA)) * ln2 : -INFINITY;
-      }
-      if (vB) {
-        const int64_t pidx = (int64_t)(pbase + rowB / G) * p.n_heads + kvh * G + rowB % G;
-        const float inv = LB > 0.f ? 1.f / LB : 0.f;
-#pragma unroll
-        for (int n = 0; n < NT; ++n)
-          *reinterpret_cast<float2*>(p.part_o + pidx * HD + n * 8 + 2 * t) =
-              make_float2(o[n][2] * inv, o[n][3] * inv);
-        if (t == 0) p.part_lse[pidx] = LB > 0.f ? (fmB + log2f(LB)) * ln2 : -INFINITY;
-      }
-    }
+    ItemCtx c{w % p.n_kv, it[2], it[3], it[4], nr * G, G, p.n_heads, p.n_kv, p.n_pages,
+              p.page_size, p.layer, s_rid, s_rt};
+    if (c.M <= 16) mma_item<HD, 1>(p, c, Ks, Vs, red);
+    else if (c.M <= 32) mma_item<HD, 2>(p, c, Ks, Vs, red);
+    else mma_item<HD, 4>(p, c, Ks, Vs, red);
   }
 }
 
@@ -574,7 +581,7 @@ static int launch_simt(const SplitParams& p, int grid, cudaStream_t s) {
 template <int HD>
 static int launch_mma(const SplitParams& p, int grid, cudaStream_t s) {
   constexpr int LD = HD + 8;
-  const size_t pages = sizeof(__nv_bfloat16) * 2 * kStages * kPage * LD;
+  const size_t pages = sizeof(__nv_bfloat16) * 2 * kStages * kPage * LD;  // 2 x 2 x 17 KiB
   const size_t merge = sizeof(float) * 4 * (16 * HD + 32);
   const size_t smem = pages > merge ? pages : merge;
   static bool attr_set = false;
@@ -609,7 +616,7 @@ int choreo_attn_split(const float* q, const void* k_pool, const void* v_pool, in
                       const int32_t* row_t, const int32_t* vis_page, const int32_t* vis_len,
                       const int32_t* vis_own, const int32_t* blk_rows, const int32_t* items,
                       const int32_t* counts, int max_items, float* part_o, float* part_lse,
-                      int grid_ctas, void* stream) {
+                      int grid_ctas, int flags, void* stream) {
   if (!q || !k_pool || !v_pool || !row_t || !vis_page || !vis_len || !vis_own || !blk_rows ||
       !items || !counts || !part_o || !part_lse || !dtype_ok(pool_dtype) || n_kv <= 0 ||
       n_heads % n_kv)
@@ -617,12 +624,12 @@ int choreo_attn_split(const float* q, const void* k_pool, const void* v_pool, in
   if (max_items <= 0) return CHOREO_OK;
   SplitParams p{q, k_pool, v_pool, layer, n_kv, n_pages, page_size, n_heads, row_t, vis_page,
                 vis_len, vis_own, blk_rows, items, counts, part_o, part_lse,
-                1.0f / sqrtf((float)head_dim)};
+                1.0f / sqrtf((float)head_dim), (flags & 1) ? 1 : 0, (flags & 2) ? 1 : 0};
   auto s = as_stream(stream);
   const bool mma = pool_dtype == CHOREO_BF16 && page_size == kPage &&
                    (head_dim == 64 || head_dim == 128);
   int grid = grid_ctas > 0 ? grid_ctas : max_items * n_kv;
-  const int cap = mma ? 148 * 2 : 148 * 8;
+  const int cap = mma ? 148 * 3 : 148 * 8;
   if (grid > cap) grid = cap;
   if (mma) return head_dim == 128 ? launch_mma<128>(p, grid, s) : launch_mma<64>(p, grid, s);
   return pool_dtype == CHOREO_BF16 ? dispatch_simt<__nv_bfloat16>(head_dim, p, grid, s)

@@ -18,6 +18,7 @@ cuBLAS GEMMs via torch (bf16 in, f32 accumulate); the residual stream is f32.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -123,6 +124,8 @@ class Runner:
         self.step_events = None  # when a list: (start, end) events around each step's GPU work
         # bf16 engines carry GEMM activations as hi/lo bf16 pairs (see choreo_b200.h)
         self.split = self.dt == torch.bfloat16 and split_activations
+        # K5 tensor-core precision: bit0 Q hi/lo, bit1 P hi/lo (env override for studies)
+        self.attn_flags = int(os.environ.get("CHOREO_ATTN_FLAGS", "3"))
 
     def _mm(self, a, w, out_f32: bool):
         if out_f32 and a.dtype != torch.float32:
@@ -250,7 +253,7 @@ class Runner:
                            self.pool_dtc, layer, Hk, cache.n_pages, P, H, hd, rowt_d.data_ptr(),
                            vis[0].data_ptr(), vis[1].data_ptr(), vis[2].data_ptr(),
                            blk_rows.data_ptr(), items.data_ptr(), counts.data_ptr(), n_items,
-                           part_o.data_ptr(), part_lse.data_ptr(), 0, stream)
+                           part_o.data_ptr(), part_lse.data_ptr(), 0, self.attn_flags, stream)
             if self.attn_events is not None:
                 ev1.record()
                 self.attn_events.append((ev0, ev1, attn_bytes))

@@ -262,7 +262,7 @@ def test_attention_matches_dense_reference(dt, hd, H, Hk):
                    nat.dtype_code(DT[dt]), L, Hk, cache.n_pages, cache.page_size, H, hd,
                    rt_d.data_ptr(), vis[0].data_ptr(), vis[1].data_ptr(), vis[2].data_ptr(),
                    blk.data_ptr(), items.data_ptr(), counts.data_ptr(), out["plan"].n_items,
-                   part_o.data_ptr(), part_lse.data_ptr(), 0, _stream())
+                   part_o.data_ptr(), part_lse.data_ptr(), 0, 3, _stream())
     nat.attn_combine(part_o.data_ptr(), part_lse.data_ptr(), rpo.data_ptr(), rp.data_ptr(), R, H,
                      hd, o.data_ptr(), nat.F32, 0, _stream())
     torch.cuda.synchronize()
