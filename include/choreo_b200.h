@@ -140,6 +140,20 @@ int choreo_attn_split(const float* q, const void* k_pool, const void* v_pool, in
                       const int32_t* counts, int max_items, float* part_o, float* part_lse,
                       int grid_ctas, int flags, void* stream);
 
+/* K4 choreographed prefill attention on tcgen05 tensor cores (bf16 pools, page_size 64,
+ * head_dim 64 or 128).  Same items / partials contract as choreo_attn_split, with items
+ * built for rows_per_block = 128 / (n_heads / n_kv) (one 128-row M tile of (row, head)
+ * query vectors per item).  Pages arrive by TMA (SW128 tensor maps over the pool, built
+ * here), S = Q K^T and O += P V accumulate in TMEM, the masked online softmax runs in
+ * registers, one query vector per TMEM lane.  Pool rows (layers*kv*pages*64) must fit in
+ * int32.  Replaces model.py:177-184 for prefill-sized steps. */
+int choreo_prefill_attn(const float* q, const void* k_pool, const void* v_pool, int pool_dtype,
+                        int n_layers, int layer, int n_kv, int n_pages, int page_size,
+                        int n_heads, int head_dim, const int32_t* row_t, const int32_t* vis_page,
+                        const int32_t* vis_len, const int32_t* vis_own, const int32_t* blk_rows,
+                        const int32_t* items, const int32_t* counts, int max_items, float* part_o,
+                        float* part_lse, int grid_ctas, void* stream);
+
 /* Combine each row's partials (CSR row_part_off / row_part, <= 512 per row) into
  * out[r][h][:] (out_dtype; hi/lo pair if out_split) with the LSE merge. */
 int choreo_attn_combine(const float* part_o, const float* part_lse, const int32_t* row_part_off,
@@ -150,6 +164,12 @@ int choreo_attn_combine(const float* part_o, const float* part_lse, const int32_
  * tie-break, one row per logits row (engine.py:371, tokenizer.py:39-44). */
 int choreo_select_greedy(const float* logits, int n_rows, int ld, int vocab, int split,
                          int32_t* out_tok, void* stream);
+
+/* Diagnostics: one-CTA tcgen05 GEMM over the UMMA primitives K4 uses.
+ * a: bf16 [128][64], b1: bf16 [64][64] (N x K), b2: bf16 [64][128] (K x N);
+ * c1 = a * b1^T (f32 [128][64]), c2 = a * b2 (f32 [128][128]). */
+int choreo_selftest_umma(const void* a, const void* b1, const void* b2, float* c1, float* c2,
+                         void* stream);
 
 #ifdef __cplusplus
 }

@@ -33,8 +33,11 @@ SIGNATURES: dict[str, list] = {
                         _P, _P, _P, _I, _I, _I, _I, _P],
     "choreo_attn_split": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P,
                           _I, _P, _P, _I, _I, _P],
+    "choreo_prefill_attn": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P,
+                            _P, _P, _I, _P, _P, _I, _P],
     "choreo_attn_combine": [_P, _P, _P, _P, _I, _I, _I, _P, _I, _I, _P],
     "choreo_select_greedy": [_P, _I, _I, _I, _I, _P, _P],
+    "choreo_selftest_umma": [_P, _P, _P, _P, _P, _P],
 }
 EXTRA = ["choreo_abi_version", "choreo_last_error"]
 
@@ -84,7 +87,9 @@ rerotate = _Caller("choreo_rerotate")
 assemble = _Caller("choreo_assemble")
 attn_split = _Caller("choreo_attn_split")
 attn_combine = _Caller("choreo_attn_combine")
+prefill_attn = _Caller("choreo_prefill_attn")
 select_greedy = _Caller("choreo_select_greedy")
+selftest_umma = _Caller("choreo_selftest_umma")
 
 
 def ptr(t) -> int | None:

@@ -172,11 +172,16 @@ class Runner:
             row_off += len(c.tokens)
         n_calls = len(plan.calls)
         msg_len = cache.msg_len.host
-        rpb = self.rows_per_block
+        # prefill-sized steps run K4 (tcgen05, 128-row M tiles); decode-sized steps K5
+        G = H // Hk
+        use_k4 = (self.pool_dtc == nat.BF16 and P == 64 and hd in (64, 128) and G <= 128
+                  and max(len(c.tokens) for c in plan.calls) >= 64
+                  and os.environ.get("CHOREO_PREFILL_K4", "1") != "0")
+        rpb = 128 // G if use_k4 else self.rows_per_block
         # pages per item: about two waves of (2 CTAs/SM x 148 SMs) per layer, and at
         # most 512 partials per row for the combine
         work = plan_counts(plan.calls, msg_len, P, rpb, 1)
-        ppi = max(1, cdiv(work.item_pages * Hk, 2 * 2 * 148))
+        ppi = max(1, cdiv(work.item_pages * Hk, (2 if use_k4 else 4) * 148))
         plan_ = plan_counts(plan.calls, msg_len, P, rpb, ppi)
         while plan_.max_row_parts > 512:
             ppi *= 2
@@ -249,11 +254,20 @@ class Runner:
                 ev0 = torch.cuda.Event(enable_timing=True)
                 ev1 = torch.cuda.Event(enable_timing=True)
                 ev0.record()
-            nat.attn_split(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(),
-                           self.pool_dtc, layer, Hk, cache.n_pages, P, H, hd, rowt_d.data_ptr(),
-                           vis[0].data_ptr(), vis[1].data_ptr(), vis[2].data_ptr(),
-                           blk_rows.data_ptr(), items.data_ptr(), counts.data_ptr(), n_items,
-                           part_o.data_ptr(), part_lse.data_ptr(), 0, self.attn_flags, stream)
+            if use_k4:
+                nat.prefill_attn(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(),
+                                 self.pool_dtc, cfg.n_layers, layer, Hk, cache.n_pages, P, H, hd,
+                                 rowt_d.data_ptr(), vis[0].data_ptr(), vis[1].data_ptr(),
+                                 vis[2].data_ptr(), blk_rows.data_ptr(), items.data_ptr(),
+                                 counts.data_ptr(), n_items, part_o.data_ptr(),
+                                 part_lse.data_ptr(), 0, stream)
+            else:
+                nat.attn_split(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(),
+                               self.pool_dtc, layer, Hk, cache.n_pages, P, H, hd,
+                               rowt_d.data_ptr(), vis[0].data_ptr(), vis[1].data_ptr(),
+                               vis[2].data_ptr(), blk_rows.data_ptr(), items.data_ptr(),
+                               counts.data_ptr(), n_items, part_o.data_ptr(), part_lse.data_ptr(),
+                               0, self.attn_flags, stream)
             if self.attn_events is not None:
                 ev1.record()
                 self.attn_events.append((ev0, ev1, attn_bytes))

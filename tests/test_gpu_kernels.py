@@ -283,3 +283,70 @@ def test_attention_matches_dense_reference(dt, hd, H, Hk):
             p = np.exp(s - s.max())
             p /= p.sum()
             np.testing.assert_allclose(got[r, h], p @ vv, rtol=1e-4, atol=1e-4)
+
+
+def test_umma_selftest_tcgen05_descriptors():
+    """tcgen05.mma with SW128 K-major and MN-major operands reproduces A@B in f32."""
+    g = torch.Generator(device="cuda").manual_seed(5)
+    a = torch.randn(128, 64, device="cuda", generator=g).to(torch.bfloat16)
+    b1 = torch.randn(64, 64, device="cuda", generator=g).to(torch.bfloat16)
+    b2 = torch.randn(64, 128, device="cuda", generator=g).to(torch.bfloat16)
+    c1 = torch.empty(128, 64, device="cuda")
+    c2 = torch.empty(128, 128, device="cuda")
+    nat.selftest_umma(a.data_ptr(), b1.data_ptr(), b2.data_ptr(), c1.data_ptr(), c2.data_ptr(),
+                      _stream())
+    torch.cuda.synchronize()
+    torch.testing.assert_close(c1, a.float() @ b1.float().t(), rtol=1e-4, atol=1e-3)
+    torch.testing.assert_close(c2, a.float() @ b2.float(), rtol=1e-4, atol=1e-3)
+
+
+@pytest.mark.parametrize("hd,H,Hk", [(128, 32, 8), (64, 8, 8), (128, 16, 2)])
+def test_prefill_tcgen05_matches_dense_reference(hd, H, Hk):
+    """K4 (tcgen05/TMEM/TMA) over page-centric items with 128-row M tiles: prefill rows of
+    two messages sharing reordered parents, causal own pages, partial tail pages."""
+    rng = np.random.default_rng(7)
+    cfg = ModelConfig(n_layers=2, n_heads=H, n_kv_heads=Hk, head_dim=hd)
+    cache, lens = _random_cache(cfg, rng, 6, dtype=torch.bfloat16)
+    for own, n in ((6, 150), (7, 41)):
+        cache.register_message(own, "prefilled", 0, max_tokens=n)
+        cache.reserve_slots(own, [1] * n)
+        cache.log_append(own, 0, n)
+    cache.k_pool.copy_(torch.randn_like(cache.k_pool))
+    cache.v_pool.copy_(torch.randn_like(cache.v_pool))
+    calls = [(6, [4, 1, 3], list(range(150))), (7, [3, 0], list(range(41)))]
+    G = H // Hk
+    out, (rt_d, vis, blk, items, rpo, rp, counts) = _assemble(cache, calls, 128 // G, 3)
+    R = len(out["row_t"])
+    q = torch.randn(R, H, hd, device="cuda")
+    n_parts = out["plan"].n_parts
+    part_o = torch.empty(n_parts, H, hd, device="cuda")
+    part_lse = torch.empty(n_parts, H, device="cuda")
+    o = torch.empty(R, H * hd, dtype=torch.float32, device="cuda")
+    L = 1
+    nat.prefill_attn(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(), nat.BF16,
+                     cfg.n_layers, L, Hk, cache.n_pages, cache.page_size, H, hd, rt_d.data_ptr(),
+                     vis[0].data_ptr(), vis[1].data_ptr(), vis[2].data_ptr(), blk.data_ptr(),
+                     items.data_ptr(), counts.data_ptr(), out["plan"].n_items, part_o.data_ptr(),
+                     part_lse.data_ptr(), 0, _stream())
+    nat.attn_combine(part_o.data_ptr(), part_lse.data_ptr(), rpo.data_ptr(), rp.data_ptr(), R, H,
+                     hd, o.data_ptr(), nat.F32, 0, _stream())
+    torch.cuda.synchronize()
+    sets = _expand_rows(cache, out, R)
+    K = cache.k_pool[L].float().cpu().numpy().astype(np.float64)
+    V = cache.v_pool[L].float().cpu().numpy().astype(np.float64)
+    # K4 rounds Q and P to bf16 (standard flash attention numerics)
+    qn = q.to(torch.bfloat16).float().cpu().numpy().astype(np.float64)
+    P_ = cache.page_size
+    got = o.cpu().numpy().reshape(R, H, hd)
+    worst = 0.0
+    for r in range(R):
+        toks = sets[r]
+        pg = np.array([cache._messages[m].pages[i // P_] for m, i in toks])
+        sl = np.array([i % P_ for m, i in toks])
+        for h in range(H):
+            kk, vv = K[h // G, pg, sl], V[h // G, pg, sl]
+            s = kk @ qn[r, h] / np.sqrt(hd)
+            p = np.exp(s - s.max())
+            p /= p.sum()
+            worst = max(worst, float(np.abs(got[r, h] - p @ vv).max()))
+    assert worst < 2e-2, worst
