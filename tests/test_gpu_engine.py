@@ -261,3 +261,38 @@ def test_keys_views_match_oracle_after_moves():
     np.testing.assert_allclose(eng.cache.keys, ref.store.K[:, :n], rtol=1e-5, atol=1e-5)
     np.testing.assert_allclose(eng.cache.values, ref.store.V[:, :n], rtol=1e-5, atol=1e-5)
     assert eng.cache.positions.tolist() == ref.store.pos[:n].tolist()
+
+
+@pytest.mark.parametrize("hd,H,Hk", [(128, 8, 2), (64, 8, 8)])
+def test_bf16_tensor_core_paths_match_oracle(hd, H, Hk):
+    """hd 64/128 bf16 engines run K4 (tcgen05 prefill, >= 64-row calls) and the mma.sync
+    decode path; teacher-forced on the oracle's tokens, logits stay within 2e-2."""
+    shape = O.Shape(n_layers=2, n_heads=H, n_kv_heads=Hk, head_dim=hd, ffn_dim=256,
+                    vocab_size=300, context_window=2048, rope_base=500000.0)
+    cfg = P.ModelConfig(**{k: getattr(shape, k) for k in shape.__dataclass_fields__})
+    ws = P.init_weights(cfg).rounded("bf16")
+    ref = O.Oracle(O.round_weights(O.init_weights(shape), "bf16"), shape, record_logits=True)
+    eng = P.Engine(P.DeviceWeights.from_host(ws, dtype=torch.bfloat16), record_logits=True)
+    rng = np.random.default_rng(0)
+    texts = ["".join(chr(97 + int(c)) for c in rng.integers(0, 26, n)) for n in (150, 90, 70)]
+    for t in texts:
+        ref.prefill({"message": t})
+    for t in texts:
+        eng.prefill(P.PrefillCall(t))
+    # a prefill that sees reordered, moved parents (K2 + K4), then a parallel decode (K5)
+    ref.prefill({"message": texts[1][:80], "parents": [2, 0], "offsets": [0, 100]})
+    eng.prefill(P.PrefillCall(texts[1][:80], parents=[2, 0], offsets=[0, 100]))
+    sp_o, sp_p = O.Sampling(max_tokens=10), P.SamplingParams(max_tokens=10)
+    ref.decode_batch([{"header": "A:", "parents": [3, 1], "sampling": sp_o},
+                      {"header": "Bee:", "parents": [0, 3], "offsets": [300, 0], "sampling": sp_o}])
+    forcing = [ref.generated(4), ref.generated(5)]
+    eng.decode_parallel([P.DecodeCall("A:", parents=[3, 1], sampling=sp_p),
+                         P.DecodeCall("Bee:", parents=[0, 3], offsets=[300, 0], sampling=sp_p)],
+                        force_tokens=forcing)
+    for m in (4, 5):
+        got = np.stack(eng.stats[-1].logits[m])
+        want = np.stack(ref.stats[-1].logits[m])
+        assert got.shape == want.shape
+        assert float(np.abs(got - want).max()) <= 2e-2
+    n = eng.cache.token_count
+    assert eng.cache.positions[:n].tolist() == ref.store.pos[:n].tolist()

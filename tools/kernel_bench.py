@@ -1,0 +1,247 @@
+"""Kernel microbenchmarks at the Llama-3.1-8B shape (SURVEY.md §8(d) roofline rows).
+
+Each returns a dict with the algorithmic work per launch, the CUDA-event time per
+launch (median of reps, on the launching stream, after warm-up) and the fraction of
+the measured peak (MEASURED_PEAKS.json; burst figures, kernels timed alone).
+
+  k2_rerotate : move 8192 cached tokens (all 32 layers);  bytes = tok*L*Hkv*hd*2B*2
+  k4_prefill  : prefill_parallel of 8 messages x 1024 tokens, each over a reordered
+                6144-token parent subset of a 32 x 256-token cache;
+                FLOPs = 4*hd*Hq*sum_rows |visible(row)| per layer (exact visible pairs)
+  k5_decode   : one decode step of N agents over shared parents (page-centric);
+                bytes = unique visible KV bytes + q + partials per layer
+Usage: python tools/kernel_bench.py [--json]
+"""
+from __future__ import annotations
+
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2512_23049_b200 import _native as nat  # noqa: E402
+from paper_2512_23049_b200.cache import DeviceKvCache, RotationTableDevice, cdiv  # noqa: E402
+from paper_2512_23049_b200.config import LLAMA_3_1_8B  # noqa: E402
+from paper_2512_23049_b200.model import CallRows, plan_counts  # noqa: E402
+
+
+def peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh) | {"source": "measured"}
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback"}
+
+
+def _time(fn, reps=20, warm=3) -> float:
+    s = torch.cuda.current_stream()
+    for _ in range(warm):
+        fn()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        fn()
+        b.record(s)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) / 1e3)
+    return statistics.median(ts)
+
+
+def _cache(cfg, n_tokens_capacity: int):
+    c = DeviceKvCache(cfg, capacity=n_tokens_capacity, dtype=torch.bfloat16, device="cuda")
+    c._grow_pool(cdiv(n_tokens_capacity, 64) + 64)
+    return c
+
+
+def _add(cache, mid, n):
+    cache.register_message(mid, "prefilled", 0, max_tokens=n)
+    cache.reserve_slots(mid, [97] * n)
+    cache.log_append(mid, 0, n)
+
+
+def _assemble(cache, calls, rpb, ppi):
+    """calls: (own, parents, first_t, n_rows)."""
+    tab, par, row_t, off = [], [], [], 0
+    cr = []
+    for own, parents, t0, n in calls:
+        tab += [own, len(par), len(parents), off, n]
+        par += parents
+        row_t += list(range(t0, t0 + n))
+        off += n
+        cr.append(CallRows(own, parents, t0, [0] * n, None, None, 0))
+    plan = plan_counts(cr, cache.msg_len.host, 64, rpb, ppi)
+    cache.sync_tables()
+    dev = lambda a: torch.tensor(a, dtype=torch.int32, device="cuda")  # noqa: E731
+    tab_d, par_d, rt_d = dev(tab), dev(par + [0]), dev(row_t)
+    R = len(row_t)
+    bufs = dict(vis=torch.empty(3, plan.n_vis, dtype=torch.int32, device="cuda"),
+                blk=torch.empty(plan.n_blk_rows, dtype=torch.int32, device="cuda"),
+                items=torch.empty(plan.n_items, 6, dtype=torch.int32, device="cuda"),
+                rpo=torch.empty(R + 1, dtype=torch.int32, device="cuda"),
+                rp=torch.empty(plan.n_parts, dtype=torch.int32, device="cuda"),
+                counts=torch.empty(4, dtype=torch.int32, device="cuda"), rt=rt_d)
+    v = bufs["vis"]
+    nat.assemble(cache.msg_len.dev.data_ptr(), cache.msg_pt.dev.data_ptr(),
+                 cache.page_table.dev.data_ptr(), tab_d.data_ptr(), par_d.data_ptr(), len(calls),
+                 rt_d.data_ptr(), R, None, 0, 64, rpb, ppi, v[0].data_ptr(), v[1].data_ptr(),
+                 v[2].data_ptr(), bufs["blk"].data_ptr(), bufs["items"].data_ptr(),
+                 bufs["rpo"].data_ptr(), bufs["rp"].data_ptr(), bufs["counts"].data_ptr(),
+                 plan.n_vis, plan.n_blk_rows, plan.n_items, plan.n_parts,
+                 torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert int(bufs["counts"][3]) == 0
+    return plan, bufs, R
+
+
+def k2_rerotate(tokens: int = 8192) -> dict:
+    cfg = LLAMA_3_1_8B
+    cache = _cache(cfg, tokens + 1024)
+    for m in range(tokens // 256):
+        _add(cache, m, 256)
+    cache.k_pool.normal_()
+    rot = RotationTableDevice(cfg, "cuda")
+    pages = [pg for m in range(tokens // 256) for pg in cache._messages[m].pages]
+    arr = torch.tensor([pages, [64] * len(pages), [37] * len(pages)], dtype=torch.int32, device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+
+    def run():
+        nat.rerotate(cache.k_pool.data_ptr(), nat.BF16, cfg.n_layers, cfg.kv_heads, cache.n_pages, 64,
+                     cfg.head_dim, arr[0].data_ptr(), arr[1].data_ptr(), arr[2].data_ptr(),
+                     len(pages), rot.cos.data_ptr(), rot.sin.data_ptr(), rot.max_delta, stream)
+    t = _time(run)
+    nbytes = tokens * cfg.n_layers * cfg.kv_heads * cfg.head_dim * 2 * 2
+    pk = peaks()
+    ach = nbytes / t / 1e9
+    return {"kernel": "choreo_rerotate (K2)", "bound": "hbm", "work": f"{tokens} tokens x 32 layers",
+            "algorithmic_bytes": nbytes, "us": round(t * 1e6, 2), "achieved": round(ach, 1),
+            "unit": "GB/s", "peak": pk["hbm_gbs"], "frac": round(ach / pk["hbm_gbs"], 4)}
+
+
+def k4_prefill(n_msgs: int = 8, rows: int = 1024, n_par: int = 24) -> dict:
+    cfg = LLAMA_3_1_8B
+    H, Hk, hd = cfg.n_heads, cfg.kv_heads, cfg.head_dim
+    G = H // Hk
+    cache = _cache(cfg, 32 * 256 + n_msgs * rows + 1024)
+    for m in range(32):
+        _add(cache, m, 256)
+    for i in range(n_msgs):
+        _add(cache, 32 + i, rows)
+    cache.k_pool.normal_()
+    cache.v_pool.normal_()
+    rng = np.random.default_rng(0)
+    calls = [(32 + i, [int(p) for p in rng.permutation(32)[:n_par]], 0, rows) for i in range(n_msgs)]
+    # items sized like the runner does for prefill (about two waves of 148 CTAs)
+    work = plan_counts([CallRows(c[0], c[1], 0, [0] * rows, None, None, 0) for c in calls],
+                       cache.msg_len.host, 64, 128 // G, 1)
+    ppi = max(1, cdiv(work.item_pages * Hk, 2 * 148))
+    plan, b, R = _assemble(cache, calls, 128 // G, ppi)
+    q = torch.randn(R, H, hd, device="cuda")
+    po = torch.empty(plan.n_parts, H, hd, device="cuda")
+    pl = torch.empty(plan.n_parts, H, device="cuda")
+    out = torch.empty(R, H * hd, dtype=torch.bfloat16, device="cuda")
+    v = b["vis"]
+    stream = torch.cuda.current_stream().cuda_stream
+
+    def run():
+        nat.prefill_attn(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(), nat.BF16,
+                         cfg.n_layers, 0, Hk, cache.n_pages, 64, H, hd, b["rt"].data_ptr(),
+                         v[0].data_ptr(), v[1].data_ptr(), v[2].data_ptr(), b["blk"].data_ptr(),
+                         b["items"].data_ptr(), b["counts"].data_ptr(), plan.n_items,
+                         po.data_ptr(), pl.data_ptr(), 0, stream)
+
+    def run_comb():
+        nat.attn_combine(po.data_ptr(), pl.data_ptr(), b["rpo"].data_ptr(), b["rp"].data_ptr(), R,
+                         H, hd, out.data_ptr(), nat.BF16, 0, stream)
+    t = _time(run, reps=10)
+    tc = _time(run_comb, reps=10)
+    pairs = n_msgs * (rows * n_par * 256 + rows * (rows + 1) // 2)
+    flops = 4 * hd * H * pairs
+    pk = peaks()
+    ach = flops / t / 1e12
+    return {"kernel": "choreo_prefill_attn (K4, tcgen05)", "bound": "tensor",
+            "work": f"{n_msgs} msgs x {rows} rows over {n_par * 256}-token reordered parents, 1 layer",
+            "algorithmic_flops": flops, "us": round(t * 1e6, 1), "combine_us": round(tc * 1e6, 1),
+            "achieved": round(ach, 1), "unit": "TFLOP/s", "peak": pk["bf16_tflops"],
+            "frac": round(ach / pk["bf16_tflops"], 4), "pages_per_item": ppi,
+            "items": plan.n_items}
+
+
+def k5_decode(n_workflows: int = 1, agents: int = 8) -> dict:
+    """One decode step of C3 round 2 (agents see sys, q and the other agents' replies)."""
+    cfg = LLAMA_3_1_8B
+    H, Hk, hd = cfg.n_heads, cfg.kv_heads, cfg.head_dim
+    rng = np.random.default_rng(1)
+    per = 2 + 2 * agents
+    cache = _cache(cfg, n_workflows * (224 + 2 * agents * 800) + 4096)
+    calls = []
+    for w in range(n_workflows):
+        b = w * per
+        _add(cache, b, 64)
+        _add(cache, b + 1, 160)
+        for a in range(agents):
+            _add(cache, b + 2 + a, int(rng.integers(266, 523)))
+        for a in range(agents):  # own round-2 replies, ~250 tokens in
+            _add(cache, b + 2 + agents + a, 260)
+            others = [b + 2 + j for j in range(agents) if j != a]
+            calls.append((b + 2 + agents + a, [b, b + 1] + others, 259, 1))
+    cache.k_pool.normal_()
+    cache.v_pool.normal_()
+    G = H // Hk
+    rpb = max(1, min(16, 64 // G))
+    work = plan_counts([CallRows(c[0], c[1], c[2], [0], None, None, 0) for c in calls],
+                       cache.msg_len.host, 64, rpb, 1)
+    ppi = max(1, cdiv(work.item_pages * Hk, 4 * 148))
+    plan, b, R = _assemble(cache, calls, rpb, ppi)
+    q = torch.randn(R, H, hd, device="cuda")
+    po = torch.empty(plan.n_parts, H, hd, device="cuda")
+    pl = torch.empty(plan.n_parts, H, device="cuda")
+    out = torch.empty(2 * R, H * hd, dtype=torch.bfloat16, device="cuda")
+    v = b["vis"]
+    stream = torch.cuda.current_stream().cuda_stream
+
+    def run():
+        nat.attn_split(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(), nat.BF16, 0,
+                       Hk, cache.n_pages, 64, H, hd, b["rt"].data_ptr(), v[0].data_ptr(),
+                       v[1].data_ptr(), v[2].data_ptr(), b["blk"].data_ptr(), b["items"].data_ptr(),
+                       b["counts"].data_ptr(), plan.n_items, po.data_ptr(), pl.data_ptr(), 0, 3,
+                       stream)
+
+    def run_comb():
+        nat.attn_combine(po.data_ptr(), pl.data_ptr(), b["rpo"].data_ptr(), b["rp"].data_ptr(), R,
+                         H, hd, out.data_ptr(), nat.BF16, 1, stream)
+    t = _time(run)
+    tc = _time(run_comb)
+    uniq = sum(cache.message_length(m) for m in set(p for c in calls for p in c[1]))
+    uniq += sum(c[2] + 1 for c in calls)
+    nbytes = 2 * uniq * Hk * hd * 2 + R * H * hd * 4 + plan.n_parts * H * (hd + 1) * 4
+    logical = sum(sum(cache.message_length(p) for p in c[1]) + c[2] + 1 for c in calls) * Hk * hd * 4
+    pk = peaks()
+    ach = nbytes / t / 1e9
+    return {"kernel": "choreo_attn_split (K5, page-centric decode)", "bound": "hbm",
+            "work": f"{n_workflows} workflow(s) x {agents} agents, 1 layer",
+            "algorithmic_bytes": nbytes, "logical_kv_bytes": logical, "us": round(t * 1e6, 2),
+            "combine_us": round(tc * 1e6, 2), "achieved": round(ach, 1), "unit": "GB/s",
+            "peak": pk["hbm_gbs"], "frac": round(ach / pk["hbm_gbs"], 4), "items": plan.n_items,
+            "pages_per_item": ppi}
+
+
+def run_all() -> list:
+    out = [k2_rerotate(), k4_prefill(), k5_decode(1), k5_decode(8)]
+    torch.cuda.empty_cache()
+    return out
+
+
+if __name__ == "__main__":
+    res = run_all()
+    if "--json" in sys.argv:
+        print(json.dumps(res))
+    else:
+        for r in res:
+            print(json.dumps(r))
