@@ -113,6 +113,9 @@ int choreo_rerotate(void* k_pool, int pool_dtype, int n_layers, int n_kv, int n_
  *       (group >= 0: parent group index; -1-c: own pages of call c)
  *   row_part_off[n_rows + 1], row_part[]: per-row CSR list of the partial slots to merge
  *   counts[0..3] = {n_vis_pages, n_items, n_partials, status (0 ok, <0 over capacity)}
+ * mode 0 = page-centric groups (decode-sized steps); mode 1 = per-call lists (prefill-sized
+ * steps: each call's parents' pages in parent order, then its own pages, items are row
+ * blocks x page chunks of that list; group field = -1-call).
  * Visibility is exactly reference masking.py:36-53 (parents' tokens + own tokens with
  * j <= query j) at page granularity; tests expand it to token level against the oracle.
  * Replaces engine.py:203-245 layout + masking.py:43-53 visible_cache_indices. */
@@ -122,7 +125,7 @@ int choreo_assemble(const int32_t* msg_len, const int32_t* msg_pt, int32_t* page
                     int page_size, int rows_per_block, int pages_per_item, int32_t* vis_page,
                     int32_t* vis_len, int32_t* vis_own, int32_t* blk_rows, int32_t* items,
                     int32_t* row_part_off, int32_t* row_part, int32_t* counts, int cap_vis,
-                    int cap_blk_rows, int cap_items, int cap_parts, void* stream);
+                    int cap_blk_rows, int cap_items, int cap_parts, int mode, void* stream);
 
 /* K5 split-KV attention over assembled work items (prefill and decode rows alike).
  * q: f32 [n_rows][n_heads][hd] (already rotated, K1).  For each item and KV head writes

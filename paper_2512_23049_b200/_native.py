@@ -30,7 +30,7 @@ SIGNATURES: dict[str, list] = {
                            _I, _P, _P, _I, _P],
     "choreo_rerotate": [_P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _I, _P, _P, _I, _P],
     "choreo_assemble": [_P, _P, _P, _P, _P, _I, _P, _I, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P,
-                        _P, _P, _P, _I, _I, _I, _I, _P],
+                        _P, _P, _P, _I, _I, _I, _I, _I, _P],
     "choreo_attn_split": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P,
                           _I, _P, _P, _I, _I, _P],
     "choreo_prefill_attn": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P,

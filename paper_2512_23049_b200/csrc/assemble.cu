@@ -56,7 +56,7 @@ struct Shared {
   uint32_t key[kMaxPairs];  // (parent << 11 | call) sorted
   int n_pairs;
   int n_groups;
-  int g_first[kMaxPairs];   // first pair index of group g
+  int g_first[kMaxPairs + 1];  // first pair index of group g
   int g_vis[kMaxPairs], g_rows[kMaxPairs], g_item[kMaxPairs], g_part[kMaxPairs];
   int c_vis[kMaxCalls], c_rows[kMaxCalls], c_item[kMaxCalls], c_part[kMaxCalls];
   int tot_vis, tot_rows, tot_items, tot_parts, overflow;
@@ -284,6 +284,105 @@ __global__ void __launch_bounds__(kThreads3) assemble_kernel(K3Params p) {
   }
 }
 
+// Per-call mode (prefill-sized steps): each call's visible list is its parents' pages
+// in parent order followed by its own pages up to its last row; a row block's items are
+// chunks of that list (pages past the block's last row are skipped).  A 128-row M tile
+// already comes from one call here, so sharing pages across calls would not enlarge it.
+__global__ void __launch_bounds__(kThreads3) assemble_percall_kernel(K3Params p) {
+  __shared__ int c_pp[kMaxCalls], c_vis[kMaxCalls], c_rows[kMaxCalls], c_item[kMaxCalls],
+      c_part[kMaxCalls];
+  __shared__ int overflow;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < p.n_patch; i += blockDim.x) p.page_table[p.patch[2 * i]] = p.patch[2 * i + 1];
+  __syncthreads();
+  for (int c = tid; c < p.n_calls; c += blockDim.x) {
+    const int32_t* cl = p.calls + kCallFields * c;
+    int pp = 0;
+    for (int i = 0; i < cl[2]; ++i) pp += cdiv(p.msg_len[p.call_parents[cl[1] + i]], p.P);
+    c_pp[c] = pp;
+    c_vis[c] = c_rows[c] = c_item[c] = c_part[c] = 0;
+    if (cl[4] <= 0) continue;
+    c_vis[c] = pp + p.row_t[cl[3] + cl[4] - 1] / p.P + 1;
+    c_rows[c] = cl[4];
+    for (int b = 0; b * p.rpb < cl[4]; ++b) {
+      const int nr = min(p.rpb, cl[4] - b * p.rpb);
+      const int ch = cdiv(pp + p.row_t[cl[3] + b * p.rpb + nr - 1] / p.P + 1, p.ppi);
+      c_item[c] += ch;
+      c_part[c] += ch * nr;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int v = 0, r = 0, it = 0, pa = 0;
+    for (int c = 0; c < p.n_calls; ++c) {
+      int t;
+      t = c_vis[c]; c_vis[c] = v; v += t;
+      t = c_rows[c]; c_rows[c] = r; r += t;
+      t = c_item[c]; c_item[c] = it; it += t;
+      t = c_part[c]; c_part[c] = pa; pa += t;
+    }
+    overflow = v > p.cap_vis || r > p.cap_blk_rows || it > p.cap_items || pa > p.cap_parts;
+    p.counts[0] = v;
+    p.counts[1] = overflow ? 0 : it;
+    p.counts[2] = pa;
+    p.counts[3] = overflow ? -1 : 0;
+    p.row_part_off[p.n_rows] = pa;
+  }
+  __syncthreads();
+  if (overflow) return;
+  const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+  for (int c = warp; c < p.n_calls; c += nw) {
+    const int32_t* cl = p.calls + kCallFields * c;
+    const int row_off = cl[3], row_cnt = cl[4];
+    if (row_cnt <= 0) continue;
+    int w = c_vis[c];
+    for (int i = 0; i < cl[2]; ++i) {
+      const int msg = p.call_parents[cl[1] + i];
+      const int len = p.msg_len[msg], pt = p.msg_pt[msg], np = cdiv(len, p.P);
+      for (int j = lane; j < np; j += 32) {
+        p.vis_page[w + j] = p.page_table[pt + j];
+        p.vis_len[w + j] = min(p.P, len - j * p.P);
+        p.vis_own[w + j] = -1;
+      }
+      w += np;
+    }
+    const int t_max = p.row_t[row_off + row_cnt - 1];
+    const int opt = p.msg_pt[cl[0]];
+    for (int j = lane; j <= t_max / p.P; j += 32) {
+      p.vis_page[w + j] = p.page_table[opt + j];
+      p.vis_len[w + j] = min(p.P, t_max + 1 - j * p.P);
+      p.vis_own[w + j] = j * p.P;
+    }
+    const int rb = c_rows[c];
+    for (int j = lane; j < row_cnt; j += 32) p.blk_rows[rb + j] = row_off + j;
+    int it = c_item[c], pa = c_part[c];
+    for (int b = 0; b * p.rpb < row_cnt; ++b) {
+      const int nr = min(p.rpb, row_cnt - b * p.rpb);
+      const int nvis = c_pp[c] + p.row_t[row_off + b * p.rpb + nr - 1] / p.P + 1;
+      const int chunks = cdiv(nvis, p.ppi);
+      for (int k = lane; k < chunks; k += 32) {
+        int32_t* item = p.items + 6 * (it + k);
+        item[0] = rb + b * p.rpb;
+        item[1] = nr;
+        item[2] = c_vis[c] + k * p.ppi;
+        item[3] = min(p.ppi, nvis - k * p.ppi);
+        item[4] = pa + k * nr;
+        item[5] = -1 - c;
+      }
+      // rows are contiguous per call and calls are in order, so row r's CSR entries
+      // start at this block's partial base + j * chunks
+      for (int j = lane; j < nr; j += 32) {
+        const int r = row_off + b * p.rpb + j;
+        const int o = pa + j * chunks;
+        p.row_part_off[r] = o;
+        for (int k = 0; k < chunks; ++k) p.row_part[o + k] = pa + k * nr + j;
+      }
+      it += chunks;
+      pa += chunks * nr;
+    }
+  }
+}
+
 }  // namespace choreo
 
 using namespace choreo;
@@ -295,7 +394,7 @@ extern "C" int choreo_assemble(const int32_t* msg_len, const int32_t* msg_pt, in
                                int32_t* vis_page, int32_t* vis_len, int32_t* vis_own,
                                int32_t* blk_rows, int32_t* items, int32_t* row_part_off,
                                int32_t* row_part, int32_t* counts, int cap_vis, int cap_blk_rows,
-                               int cap_items, int cap_parts, void* stream) {
+                               int cap_items, int cap_parts, int mode, void* stream) {
   if (!msg_len || !msg_pt || !page_table || !calls || !row_t || !vis_page || !vis_len ||
       !vis_own || !blk_rows || !items || !row_part_off || !row_part || !counts)
     return CHOREO_EINVAL;
@@ -306,6 +405,10 @@ extern "C" int choreo_assemble(const int32_t* msg_len, const int32_t* msg_pt, in
              n_patch, page_size, rows_per_block, pages_per_item, vis_page, vis_len, vis_own,
              blk_rows, items, row_part_off, row_part, counts, cap_vis, cap_blk_rows, cap_items,
              cap_parts};
+  if (mode == 1) {
+    assemble_percall_kernel<<<1, kThreads3, 0, as_stream(stream)>>>(p);
+    return launch_status("choreo_assemble");
+  }
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -66,7 +66,27 @@ class Plan:
     item_pages: int  # sum over items of pages (work estimate)
 
 
-def plan_counts(calls: list, msg_len: np.ndarray, P: int, rpb: int, ppi: int) -> Plan:
+def plan_counts(calls: list, msg_len: np.ndarray, P: int, rpb: int, ppi: int,
+                mode: int = 0) -> Plan:
+    """Host replica of K3's sizing; mode 0 page-centric, mode 1 per-call (assemble.cu)."""
+    if mode == 1:
+        n_vis = n_blk = n_items = n_parts = item_pages = max_row = 0
+        for c in calls:
+            n = len(c.tokens)
+            if n == 0:
+                continue
+            pp = sum(cdiv(int(msg_len[p]), P) for p in c.parents)
+            n_vis += pp + (c.first_t + n - 1) // P + 1
+            n_blk += n
+            for b in range(0, n, rpb):
+                nr = min(rpb, n - b)
+                nvis = pp + (c.first_t + b + nr - 1) // P + 1
+                ch = cdiv(nvis, ppi)
+                n_items += ch
+                n_parts += ch * nr
+                item_pages += nvis
+                max_row = max(max_row, ch)
+        return Plan(n_vis, n_blk, n_items, n_parts, max_row, item_pages)
     groups: dict = {}
     for c in calls:
         for p in c.parents:
@@ -180,12 +200,14 @@ class Runner:
         rpb = 128 // G if use_k4 else self.rows_per_block
         # pages per item: about two waves of (2 CTAs/SM x 148 SMs) per layer, and at
         # most 512 partials per row for the combine
-        work = plan_counts(plan.calls, msg_len, P, rpb, 1)
+        # prefill-sized steps: per-call page lists (a row block already fills an M tile)
+        mode = 1 if max(len(c.tokens) for c in plan.calls) >= 64 else 0
+        work = plan_counts(plan.calls, msg_len, P, rpb, 1, mode)
         ppi = max(1, cdiv(work.item_pages * Hk, (2 if use_k4 else 4) * 148))
-        plan_ = plan_counts(plan.calls, msg_len, P, rpb, ppi)
+        plan_ = plan_counts(plan.calls, msg_len, P, rpb, ppi, mode)
         while plan_.max_row_parts > 512:
             ppi *= 2
-            plan_ = plan_counts(plan.calls, msg_len, P, rpb, ppi)
+            plan_ = plan_counts(plan.calls, msg_len, P, rpb, ppi, mode)
         n_parts, n_items = plan_.n_parts, plan_.n_items
         n_log = len(plan.logit_rows)
 
@@ -224,7 +246,7 @@ class Runner:
                      n_calls, rowt_d.data_ptr(), R, None, 0, P, rpb, ppi, vis[0].data_ptr(),
                      vis[1].data_ptr(), vis[2].data_ptr(), blk_rows.data_ptr(), items.data_ptr(),
                      row_part_off.data_ptr(), row_part.data_ptr(), counts.data_ptr(),
-                     plan_.n_vis, plan_.n_blk_rows, n_items, n_parts, stream)
+                     plan_.n_vis, plan_.n_blk_rows, n_items, n_parts, mode, stream)
         self.launches += 1
         self.last_assembly = (vis, blk_rows, items, row_part_off, row_part, counts, plan_, rowt_d)
 

@@ -124,7 +124,7 @@ def _random_cache(cfg, rng, n_msgs, P=64, dtype=torch.float32):
     return cache, lens
 
 
-def _assemble(cache, calls, rpb, ppi):
+def _assemble(cache, calls, rpb, ppi, mode=0):
     """calls: list of (own msg, parents, row_t list).  Returns host copies of K3 outputs."""
     from paper_2512_23049_b200.model import plan_counts, CallRows
     tab, par, row_t, off = [], [], [], 0
@@ -134,7 +134,7 @@ def _assemble(cache, calls, rpb, ppi):
         row_t += ts
         off += len(ts)
     cr = [CallRows(own, parents, ts[0], [0] * len(ts), None, None, 0) for own, parents, ts in calls]
-    plan = plan_counts(cr, cache.msg_len.host, cache.page_size, rpb, ppi)
+    plan = plan_counts(cr, cache.msg_len.host, cache.page_size, rpb, ppi, mode)
     cache.sync_tables()
     dev = lambda a: torch.tensor(a, dtype=torch.int32, device="cuda")  # noqa: E731
     tab_d, par_d, rt_d = dev(tab), dev(par + [0]), dev(row_t)
@@ -150,7 +150,7 @@ def _assemble(cache, calls, rpb, ppi):
                  rt_d.data_ptr(), R, None, 0, cache.page_size, rpb, ppi,
                  vis[0].data_ptr(), vis[1].data_ptr(), vis[2].data_ptr(), blk.data_ptr(),
                  items.data_ptr(), rpo.data_ptr(), rp.data_ptr(), counts.data_ptr(),
-                 plan.n_vis, plan.n_blk_rows, plan.n_items, plan.n_parts, _stream())
+                 plan.n_vis, plan.n_blk_rows, plan.n_items, plan.n_parts, mode, _stream())
     out = dict(vis=vis.cpu().numpy(), blk=blk.cpu().numpy(), items=items.cpu().numpy(),
                rpo=rpo.cpu().numpy(), rp=rp.cpu().numpy(), counts=counts.cpu().numpy(),
                row_t=np.asarray(row_t), plan=plan)
@@ -188,8 +188,9 @@ def _expand_rows(cache, out, n_rows):
     return [sorted(s_) for s_ in sets]
 
 
+@pytest.mark.parametrize("mode", [0, 1])
 @pytest.mark.parametrize("rpb,ppi", [(1, 1), (4, 3), (16, 1000)])
-def test_assemble_visible_sets_match_oracle(rpb, ppi):
+def test_assemble_visible_sets_match_oracle(rpb, ppi, mode):
     rng = np.random.default_rng(3)
     cfg = ModelConfig(n_layers=1, n_heads=2, head_dim=8)
     cache, lens = _random_cache(cfg, rng, 12)
@@ -205,7 +206,7 @@ def test_assemble_visible_sets_match_oracle(rpb, ppi):
         cache.reserve_slots(own, [1] * (pre + n_new))
         cache.log_append(own, 0, pre + n_new)
         calls.append((own, parents, list(range(pre, pre + n_new))))
-    out, _ = _assemble(cache, calls, rpb, ppi)
+    out, _ = _assemble(cache, calls, rpb, ppi, mode)
     assert out["counts"][3] == 0
     pl = out["plan"]
     assert tuple(out["counts"][:3]) == (pl.n_vis, pl.n_items, pl.n_parts)
@@ -226,9 +227,10 @@ def test_assemble_visible_sets_match_oracle(rpb, ppi):
             r += 1
 
 
+@pytest.mark.parametrize("mode", [0, 1])
 @pytest.mark.parametrize("dt", ["f32", "bf16"])
 @pytest.mark.parametrize("hd,H,Hk", [(16, 4, 4), (128, 32, 8), (64, 8, 1)])
-def test_attention_matches_dense_reference(dt, hd, H, Hk):
+def test_attention_matches_dense_reference(dt, hd, H, Hk, mode):
     rng = np.random.default_rng(4)
     cfg = ModelConfig(n_layers=2, n_heads=H, n_kv_heads=Hk, head_dim=hd)
     cache, lens = _random_cache(cfg, rng, 8, dtype=DT[dt])
@@ -250,7 +252,7 @@ def test_attention_matches_dense_reference(dt, hd, H, Hk):
              (9, [6, 3, 0], [2]), (10, [1, 6, 2, 5, 4], [0])]
     G = H // Hk
     rpb = max(1, min(16, 64 // G))
-    out, (rt_d, vis, blk, items, rpo, rp, counts) = _assemble(cache, calls, rpb, 2)
+    out, (rt_d, vis, blk, items, rpo, rp, counts) = _assemble(cache, calls, rpb, 2, mode)
     R = len(out["row_t"])
     q = torch.randn(R, H, hd, device="cuda")
     n_parts = out["plan"].n_parts
@@ -315,7 +317,7 @@ def test_prefill_tcgen05_matches_dense_reference(hd, H, Hk):
     cache.v_pool.copy_(torch.randn_like(cache.v_pool))
     calls = [(6, [4, 1, 3], list(range(150))), (7, [3, 0], list(range(41)))]
     G = H // Hk
-    out, (rt_d, vis, blk, items, rpo, rp, counts) = _assemble(cache, calls, 128 // G, 3)
+    out, (rt_d, vis, blk, items, rpo, rp, counts) = _assemble(cache, calls, 128 // G, 3, 1)
     R = len(out["row_t"])
     q = torch.randn(R, H, hd, device="cuda")
     n_parts = out["plan"].n_parts

@@ -164,6 +164,21 @@ def _brute_counts(calls, msg_len, P_, rpb, ppi):
     return v, blk, it, pa
 
 
+def _brute_percall(calls, msg_len, P_, rpb, ppi):
+    v = blk = it = pa = 0
+    for c in calls:
+        pp = sum(cdiv(msg_len[p], P_) for p in c.parents)
+        ts = [c.first_t + i for i in range(len(c.tokens))]
+        v += pp + ts[-1] // P_ + 1
+        blk += len(ts)
+        for i in range(0, len(ts), rpb):
+            b = ts[i:i + rpb]
+            ch = cdiv(pp + b[-1] // P_ + 1, ppi)
+            it += ch
+            pa += ch * len(b)
+    return v, blk, it, pa
+
+
 @pytest.mark.parametrize("seed", range(10))
 def test_plan_counts(seed):
     rng = np.random.default_rng(seed)
@@ -172,6 +187,9 @@ def test_plan_counts(seed):
                       int(rng.integers(0, 100)), [0] * int(rng.integers(1, 80)), None, None, 0)
              for i in range(int(rng.integers(1, 6)))]
     for rpb, ppi in ((1, 1), (16, 3), (4, 1000)):
+        pm = plan_counts(calls, msg_len, 64, rpb, ppi, 1)
+        want = _brute_percall(calls, msg_len, 64, rpb, ppi)
+        assert (pm.n_vis, pm.n_blk_rows, pm.n_items, pm.n_parts) == want
         pl = plan_counts(calls, msg_len, 64, rpb, ppi)
         assert (pl.n_vis, pl.n_blk_rows, pl.n_items, pl.n_parts) == \
             _brute_counts(calls, msg_len, 64, rpb, ppi)

@@ -66,7 +66,7 @@ def _add(cache, mid, n):
     cache.log_append(mid, 0, n)
 
 
-def _assemble(cache, calls, rpb, ppi):
+def _assemble(cache, calls, rpb, ppi, mode=0):
     """calls: (own, parents, first_t, n_rows)."""
     tab, par, row_t, off = [], [], [], 0
     cr = []
@@ -76,7 +76,7 @@ def _assemble(cache, calls, rpb, ppi):
         row_t += list(range(t0, t0 + n))
         off += n
         cr.append(CallRows(own, parents, t0, [0] * n, None, None, 0))
-    plan = plan_counts(cr, cache.msg_len.host, 64, rpb, ppi)
+    plan = plan_counts(cr, cache.msg_len.host, 64, rpb, ppi, mode)
     cache.sync_tables()
     dev = lambda a: torch.tensor(a, dtype=torch.int32, device="cuda")  # noqa: E731
     tab_d, par_d, rt_d = dev(tab), dev(par + [0]), dev(row_t)
@@ -93,7 +93,7 @@ def _assemble(cache, calls, rpb, ppi):
                  rt_d.data_ptr(), R, None, 0, 64, rpb, ppi, v[0].data_ptr(), v[1].data_ptr(),
                  v[2].data_ptr(), bufs["blk"].data_ptr(), bufs["items"].data_ptr(),
                  bufs["rpo"].data_ptr(), bufs["rp"].data_ptr(), bufs["counts"].data_ptr(),
-                 plan.n_vis, plan.n_blk_rows, plan.n_items, plan.n_parts,
+                 plan.n_vis, plan.n_blk_rows, plan.n_items, plan.n_parts, mode,
                  torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     assert int(bufs["counts"][3]) == 0
@@ -139,9 +139,9 @@ def k4_prefill(n_msgs: int = 8, rows: int = 1024, n_par: int = 24) -> dict:
     calls = [(32 + i, [int(p) for p in rng.permutation(32)[:n_par]], 0, rows) for i in range(n_msgs)]
     # items sized like the runner does for prefill (about two waves of 148 CTAs)
     work = plan_counts([CallRows(c[0], c[1], 0, [0] * rows, None, None, 0) for c in calls],
-                       cache.msg_len.host, 64, 128 // G, 1)
+                       cache.msg_len.host, 64, 128 // G, 1, 1)
     ppi = max(1, cdiv(work.item_pages * Hk, 2 * 148))
-    plan, b, R = _assemble(cache, calls, 128 // G, ppi)
+    plan, b, R = _assemble(cache, calls, 128 // G, ppi, 1)
     q = torch.randn(R, H, hd, device="cuda")
     po = torch.empty(plan.n_parts, H, hd, device="cuda")
     pl = torch.empty(plan.n_parts, H, device="cuda")
