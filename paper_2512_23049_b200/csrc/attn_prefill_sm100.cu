@@ -49,18 +49,30 @@ struct PrefillParams {
 
 constexpr int kPfThreads = 192;
 constexpr int kPfStages = 4;
-constexpr int kPfKeys = 64;  // keys per page / per S tile
+constexpr int kPfKeys = 64;        // keys per page / per S tile
+constexpr float kRescaleTh = 8.f;  // lazy O rescale threshold (log2 units)
 
 template <int HD>
 struct PfSmem {
-  static constexpr int kRegions = HD / 64;                 // 64-column SW128 regions
-  static constexpr int kQBytes = 128 * 128 * kRegions;     // [128 rows][HD] bf16
+  static constexpr int kRegions = HD / 64;                  // 64-column SW128 regions
+  static constexpr int kQBytes = 128 * 128 * kRegions;      // [128 rows][HD] bf16
   static constexpr int kKVBytes = kPfKeys * 128 * kRegions; // one K (or V) page
   static constexpr int kStageBytes = 2 * kKVBytes;
   static constexpr int kPBytes = 128 * 128;                 // [128 rows][64 keys] bf16
-  static constexpr int kTotal = kQBytes + kPfStages * kStageBytes + kPBytes + 1024;
+  static constexpr int kTotal = kQBytes + kPfStages * kStageBytes + 2 * kPBytes + 1024;
 };
 
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// S tiles double-buffered in TMEM (cols [0,64) and [64,128)), O at [128, 128+HD);
+// P double-buffered in smem.  Per page g (global index over this CTA's items):
+//   MMA : S_{g+1} -> TMEM[(g+1)&1] is issued before PV_g, so the tensor core computes the
+//         next scores while the softmax warps work on S_g;
+//   SMX : ld S_g, release the S buffer, exp2, wait PV_{g-1}, write P_g, lazily rescale O.
 template <int HD>
 __global__ void __launch_bounds__(kPfThreads, 1)
     attn_prefill_sm100(PrefillParams p, const __grid_constant__ CUtensorMap tmK,
@@ -74,7 +86,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
   uint8_t* sKV = sQ + S::kQBytes;
   uint8_t* sP = sKV + kPfStages * S::kStageBytes;
   __shared__ uint64_t full_bar[kPfStages], empty_bar[kPfStages];
-  __shared__ uint64_t s_full, p_full, o_done, q_full, o_free;
+  __shared__ uint64_t s_full[2], s_free[2], p_full, o_done, q_full, o_free;
   __shared__ uint32_t tmem_base;
   __shared__ int s_rid[128], s_rt[128];
 
@@ -86,7 +98,10 @@ __global__ void __launch_bounds__(kPfThreads, 1)
       mbar_init(&full_bar[i], 1);
       mbar_init(&empty_bar[i], 1);
     }
-    mbar_init(&s_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], 128);
+    }
     mbar_init(&p_full, 128);
     mbar_init(&o_done, 1);
     mbar_init(&q_full, 128);
@@ -95,7 +110,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
   }
-  if (warp == 1) tmem_alloc(&tmem_base, 256);  // S: cols [0,64), O: cols [128, 128+HD)
+  if (warp == 1) tmem_alloc(&tmem_base, 256);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -110,9 +125,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         const int kvh = w % p.n_kv, vb = it[2], nv = it[3];
         for (int pi = vb; pi < vb + nv; ++pi, ++gp) {
           const int st = gp % kPfStages;
-          PF_DBG(0, 1000 + (int)gp);
           mbar_wait(&empty_bar[st], ((gp / kPfStages) & 1) ^ 1);
-          PF_DBG(0, 2000 + (int)gp);
           const int row0 = ((p.layer * p.n_kv + kvh) * p.n_pages + p.vis_page[pi]) * kPfKeys;
           uint8_t* dst = sKV + st * S::kStageBytes;
           mbar_arrive_expect_tx(&full_bar[st], S::kStageBytes);
@@ -129,44 +142,40 @@ __global__ void __launch_bounds__(kPfThreads, 1)
     if (lane == 0) {
       constexpr uint32_t idS = umma_idesc_bf16(128, kPfKeys, false);
       constexpr uint32_t idO = umma_idesc_bf16(128, HD, true);
+      const uint32_t qaddr = smem_addr(sQ);
+      auto issue_s = [&](uint32_t g) {
+        const int st = g % kPfStages, b = g & 1;
+        mbar_wait(&full_bar[st], (g / kPfStages) & 1);
+        mbar_wait(&s_free[b], ((g >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t kaddr = smem_addr(sKV + st * S::kStageBytes);
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k) {
+          const uint32_t off = (k & 3) * 32;
+          umma_bf16(tS + 64 * b, umma_desc_sw128(qaddr + (k >> 2) * 128 * 128 + off, 16, 1024),
+                    umma_desc_sw128(kaddr + (k >> 2) * kPfKeys * 128 + off, 16, 1024), idS, k > 0);
+        }
+        umma_commit(&s_full[b]);
+      };
       uint32_t gp = 0, ic = 0;
       for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++ic) {
-        const int32_t* it = p.items + 6 * (w / p.n_kv);
-        const int nv = it[3];
-        PF_DBG(1, 1000 + (int)ic);
+        const int nv = p.items[6 * (w / p.n_kv) + 3];
         mbar_wait(&q_full, ic & 1);
-        PF_DBG(1, 2000 + (int)ic);
         if (ic > 0) mbar_wait(&o_free, (ic - 1) & 1);
-        PF_DBG(1, 3000 + (int)ic);
         tc_fence_after();
+        issue_s(gp);
         for (int j = 0; j < nv; ++j, ++gp) {
+          if (j + 1 < nv) issue_s(gp + 1);
+          mbar_wait(&p_full, gp & 1);  // P_j written, O rescaled
+          tc_fence_after();
           const int st = gp % kPfStages;
-          PF_DBG(2, 1000 + (int)gp);
-          mbar_wait(&full_bar[st], (gp / kPfStages) & 1);
-          PF_DBG(2, 2000 + (int)gp);
-          tc_fence_after();
-          const uint32_t kaddr = smem_addr(sKV + st * S::kStageBytes);
-          const uint32_t vaddr = kaddr + S::kKVBytes;
-          const uint32_t qaddr = smem_addr(sQ);
+          const uint32_t vaddr = smem_addr(sKV + st * S::kStageBytes) + S::kKVBytes;
+          const uint32_t paddr = smem_addr(sP + (gp & 1) * S::kPBytes);
 #pragma unroll
-          for (int k = 0; k < HD / 16; ++k) {
-            const uint32_t off = (k >> 2) * 0 + (k & 3) * 32;
-            const uint64_t ad = umma_desc_sw128(qaddr + (k >> 2) * 128 * 128 + off, 16, 1024);
-            const uint64_t bd = umma_desc_sw128(kaddr + (k >> 2) * kPfKeys * 128 + off, 16, 1024);
-            umma_bf16(tS, ad, bd, idS, k > 0);
-          }
-          umma_commit(&s_full);
-          PF_DBG(2, 3000 + (int)gp);
-          mbar_wait(&p_full, gp & 1);  // softmax wrote P_j and rescaled O
-          PF_DBG(2, 4000 + (int)gp);
-          tc_fence_after();
-          const uint32_t paddr = smem_addr(sP);
-#pragma unroll
-          for (int k = 0; k < kPfKeys / 16; ++k) {
-            const uint64_t ad = umma_desc_sw128(paddr + k * 32, 16, 1024);
-            const uint64_t bd = umma_desc_sw128(vaddr + k * 2048, kPfKeys * 128, 1024);
-            umma_bf16(tO, ad, bd, idO, (j > 0 || k > 0) ? 1u : 0u);
-          }
+          for (int k = 0; k < kPfKeys / 16; ++k)
+            umma_bf16(tO, umma_desc_sw128(paddr + k * 32, 16, 1024),
+                      umma_desc_sw128(vaddr + k * 2048, kPfKeys * 128, 1024), idO,
+                      (j > 0 || k > 0) ? 1u : 0u);
           umma_commit(&empty_bar[st]);
           umma_commit(&o_done);
         }
@@ -174,29 +183,25 @@ __global__ void __launch_bounds__(kPfThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ softmax warps
-    const int quad = warp & 3;          // TMEM lane quadrant
-    const int m = quad * 32 + lane;     // query vector (TMEM lane) of this thread
+    const int quad = warp & 3;       // TMEM lane quadrant
+    const int m = quad * 32 + lane;  // query vector (TMEM lane) of this thread
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    const int st_tid = tid - 64;        // 0..127
+    const int st_tid = tid - 64;     // 0..127
     uint32_t gp = 0;
     for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
       const int32_t* it = p.items + 6 * (w / p.n_kv);
       const int kvh = w % p.n_kv, rb = it[0], nr = it[1], vb = it[2], nv = it[3], pbase = it[4];
       const int M = nr * G;
-      // rows of this block (warp-group barrier via named barrier 1, 128 threads)
       if (st_tid < nr) {
         const int rid = p.blk_rows[rb + st_tid];
         s_rid[st_tid] = rid;
         s_rt[st_tid] = p.row_t[rid];
       }
-      if (st_tid == 0) PF_DBG(4, 1000 + (int)gp);
       asm volatile("bar.sync 1, 128;\n" ::: "memory");
-      if (st_tid == 0) PF_DBG(4, 2000 + (int)gp);
       const bool valid = m < M;
       const int my_row = valid ? m / G : 0;
       const int my_t = valid ? s_rt[my_row] : -1;
-      // ---- stage Q (bf16, SW128 K-major, pre-scaled to the log2 domain) ----
-      {
+      {  // stage Q (bf16, SW128 K-major, pre-scaled to the log2 domain)
         const float* qr = p.q + ((int64_t)s_rid[my_row] * p.n_heads + kvh * G + (valid ? m % G : 0)) * HD;
 #pragma unroll
         for (int c = 0; c < HD / 8; ++c) {
@@ -205,11 +210,11 @@ __global__ void __launch_bounds__(kPfThreads, 1)
             a = *reinterpret_cast<const float4*>(qr + 8 * c);
             b = *reinterpret_cast<const float4*>(qr + 8 * c + 4);
           }
-          const float s = p.scale_log2;
-          __nv_bfloat162 h0 = __floats2bfloat162_rn(a.x * s, a.y * s);
-          __nv_bfloat162 h1 = __floats2bfloat162_rn(a.z * s, a.w * s);
-          __nv_bfloat162 h2 = __floats2bfloat162_rn(b.x * s, b.y * s);
-          __nv_bfloat162 h3 = __floats2bfloat162_rn(b.z * s, b.w * s);
+          const float sc = p.scale_log2;
+          __nv_bfloat162 h0 = __floats2bfloat162_rn(a.x * sc, a.y * sc);
+          __nv_bfloat162 h1 = __floats2bfloat162_rn(a.z * sc, a.w * sc);
+          __nv_bfloat162 h2 = __floats2bfloat162_rn(b.x * sc, b.y * sc);
+          __nv_bfloat162 h3 = __floats2bfloat162_rn(b.z * sc, b.w * sc);
           uint4 u;
           u.x = *reinterpret_cast<uint32_t*>(&h0);
           u.y = *reinterpret_cast<uint32_t*>(&h1);
@@ -220,39 +225,39 @@ __global__ void __launch_bounds__(kPfThreads, 1)
       }
       fence_proxy_async_smem();
       mbar_arrive(&q_full);
-      float mrow = -INFINITY, lrow = 0.f;
+      float mrow = -INFINITY, lrow = 0.f;  // mrow = max used for the exponentials (lazy)
       for (int j = 0; j < nv; ++j, ++gp) {
         const int pi = vb + j;
         const int len = p.vis_len[pi], own = p.vis_own[pi];
-        if (st_tid == 0) PF_DBG(3, 1000 + (int)gp);
-        mbar_wait(&s_full, gp & 1);
-        if (st_tid == 0) PF_DBG(3, 2000 + (int)gp);
+        const int b = gp & 1;
+        mbar_wait(&s_full[b], (gp >> 1) & 1);
         tc_fence_after();
         float s[kPfKeys];
 #pragma unroll
-        for (int c = 0; c < kPfKeys / 16; ++c) tmem_ld16(tS + lane_off + c * 16, s + c * 16);
+        for (int c = 0; c < kPfKeys / 16; ++c) tmem_ld16(tS + 64 * b + lane_off + c * 16, s + c * 16);
         tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive(&s_free[b]);
+        // keys visible to this row: k < lim (own pages: causal cut at my_t)
+        int lim = valid ? len : 0;
+        if (own >= 0) lim = min(lim, my_t - own + 1);
         float tmax = -INFINITY;
 #pragma unroll
-        for (int k = 0; k < kPfKeys; ++k) {
-          const bool ok = valid && k < len && (own < 0 || own + k <= my_t);
-          s[k] = ok ? s[k] : -INFINITY;
-          tmax = fmaxf(tmax, s[k]);
+        for (int k = 0; k < kPfKeys; ++k) tmax = fmaxf(tmax, k < lim ? s[k] : -INFINITY);
+        float alpha = 1.f;
+        if (tmax > mrow + kRescaleTh || (mrow == -INFINITY && tmax != -INFINITY)) {
+          alpha = mrow == -INFINITY ? 0.f : ex2(mrow - tmax);
+          mrow = tmax;
         }
-        const float mnew = fmaxf(mrow, tmax);
-        const float alpha = (mrow == -INFINITY || mnew == -INFINITY) ? 1.f : exp2f(mrow - mnew);
         float sum = 0.f;
 #pragma unroll
         for (int k = 0; k < kPfKeys; ++k) {
-          s[k] = s[k] == -INFINITY ? 0.f : exp2f(s[k] - mnew);
+          s[k] = k < lim ? ex2(s[k] - mrow) : 0.f;
           sum += s[k];
         }
         lrow = lrow * alpha + sum;
-        mrow = mnew;
-        // P -> smem (SW128 K-major, one 128-byte row per query vector)
-        if (st_tid == 0) PF_DBG(3, 3000 + (int)gp);
-        if (j > 0) mbar_wait(&o_done, (gp - 1) & 1);  // PV_{j-1} done: O stable, P free
-        if (st_tid == 0) PF_DBG(3, 4000 + (int)gp);
+        if (j > 0) mbar_wait(&o_done, (gp - 1) & 1);  // PV_{g-1} done: O stable, P buffer free
+        uint8_t* pb = sP + b * S::kPBytes;
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           __nv_bfloat162 h0 = __floats2bfloat162_rn(s[8 * c], s[8 * c + 1]);
@@ -264,9 +269,8 @@ __global__ void __launch_bounds__(kPfThreads, 1)
           u.y = *reinterpret_cast<uint32_t*>(&h1);
           u.z = *reinterpret_cast<uint32_t*>(&h2);
           u.w = *reinterpret_cast<uint32_t*>(&h3);
-          *reinterpret_cast<uint4*>(sP + sw128_offset(m, 8 * c)) = u;
+          *reinterpret_cast<uint4*>(pb + sw128_offset(m, 8 * c)) = u;
         }
-        // rescale the running O in TMEM when this warp's max moved
         if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
           tc_fence_after();
 #pragma unroll
@@ -285,9 +289,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         mbar_arrive(&p_full);
       }
       // ---- epilogue: O / l -> partial, LSE (natural log) ----
-      if (st_tid == 0) PF_DBG(4, 3000 + (int)gp);
       mbar_wait(&o_done, (gp - 1) & 1);
-      if (st_tid == 0) PF_DBG(4, 4000 + (int)gp);
       tc_fence_after();
       {
         // tcgen05.ld is warp-collective: every lane loads, only valid lanes store
