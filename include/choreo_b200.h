@@ -145,17 +145,21 @@ int choreo_attn_split(const float* q, const void* k_pool, const void* v_pool, in
 
 /* K4 choreographed prefill attention on tcgen05 tensor cores (bf16 pools, page_size 64,
  * head_dim 64 or 128).  Same items / partials contract as choreo_attn_split, with items
- * built for rows_per_block = 128 / (n_heads / n_kv) (one 128-row M tile of (row, head)
- * query vectors per item).  Pages arrive by TMA (SW128 tensor maps over the pool, built
+ * built for rows_per_block = 256 / (n_heads / n_kv): two 128-vector M tiles of (row, head)
+ * query vectors per item that share every K/V page and ping-pong on the tensor core.  Pages arrive by TMA (SW128 tensor maps over the pool, built
  * here), S = Q K^T and O += P V accumulate in TMEM, the masked online softmax runs in
  * registers, one query vector per TMEM lane.  Pool rows (layers*kv*pages*64) must fit in
- * int32.  Replaces model.py:177-184 for prefill-sized steps. */
+ * int32.  out (optional, bf16 [n_rows (x2 if out_split)][n_heads*head_dim]): when every row
+ * has exactly one item, write the final normalised rows there (hi/lo pair if out_split)
+ * instead of partials, so no combine pass is needed.
+ * Replaces model.py:177-184 for prefill-sized steps. */
 int choreo_prefill_attn(const float* q, const void* k_pool, const void* v_pool, int pool_dtype,
                         int n_layers, int layer, int n_kv, int n_pages, int page_size,
                         int n_heads, int head_dim, const int32_t* row_t, const int32_t* vis_page,
                         const int32_t* vis_len, const int32_t* vis_own, const int32_t* blk_rows,
                         const int32_t* items, const int32_t* counts, int max_items, float* part_o,
-                        float* part_lse, int grid_ctas, void* stream);
+                        float* part_lse, int grid_ctas, void* out, int out_split, int n_rows,
+                        void* stream);
 
 /* Combine each row's partials (CSR row_part_off / row_part, <= 512 per row) into
  * out[r][h][:] (out_dtype; hi/lo pair if out_split) with the LSE merge. */

@@ -34,7 +34,7 @@ SIGNATURES: dict[str, list] = {
     "choreo_attn_split": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P,
                           _I, _P, _P, _I, _I, _P],
     "choreo_prefill_attn": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P,
-                            _P, _P, _I, _P, _P, _I, _P],
+                            _P, _P, _I, _P, _P, _I, _P, _I, _I, _P],
     "choreo_attn_combine": [_P, _P, _P, _P, _I, _I, _I, _P, _I, _I, _P],
     "choreo_select_greedy": [_P, _I, _I, _I, _I, _P, _P],
     "choreo_selftest_umma": [_P, _P, _P, _P, _P, _P],

@@ -17,6 +17,7 @@
 // warp % 4), which also stage Q (f32 -> bf16, pre-scaled by log2(e)/sqrt(hd)).
 #include <cudaTypedefs.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -37,6 +38,11 @@ struct PrefillParams {
   float* part_lse;
   float scale_log2;
   int* dbg;  // optional progress counters (mapped host memory) for pipeline debugging
+  // When out != nullptr every row has exactly one item: the epilogue writes the final
+  // normalised row out[row][head*hd + d] (bf16; hi/lo pair at rows r / n_rows + r when
+  // out_split) and no partials / combine are needed.
+  __nv_bfloat16* out;
+  int out_split, n_rows;
 };
 
 #define PF_DBG(i, v)                                     \
@@ -47,19 +53,20 @@ struct PrefillParams {
     }                                                    \
   } while (0)
 
-constexpr int kPfThreads = 192;
-constexpr int kPfStages = 4;
-constexpr int kPfKeys = 64;        // keys per page / per S tile
-constexpr float kRescaleTh = 8.f;  // lazy O rescale threshold (log2 units)
+constexpr int kPfThreads = 320;     // 10 warps: TMA, MMA, 2 x 4 softmax warps
+constexpr int kPfStages = 3;
+constexpr int kPfKeys = 64;         // keys per page / per S tile
+constexpr int kTileM = 128;         // query vectors per tile (TMEM lanes)
+constexpr float kRescaleTh = 8.f;   // lazy O rescale threshold (log2 units)
 
 template <int HD>
 struct PfSmem {
   static constexpr int kRegions = HD / 64;                  // 64-column SW128 regions
-  static constexpr int kQBytes = 128 * 128 * kRegions;      // [128 rows][HD] bf16
+  static constexpr int kQBytes = kTileM * 128 * kRegions;   // one tile's [128][HD] bf16
   static constexpr int kKVBytes = kPfKeys * 128 * kRegions; // one K (or V) page
   static constexpr int kStageBytes = 2 * kKVBytes;
-  static constexpr int kPBytes = 128 * 128;                 // [128 rows][64 keys] bf16
-  static constexpr int kTotal = kQBytes + kPfStages * kStageBytes + 2 * kPBytes + 1024;
+  static constexpr int kPBytes = kTileM * 128;              // [128][64 keys] bf16
+  static constexpr int kTotal = 2 * kQBytes + kPfStages * kStageBytes + 2 * kPBytes + 1024;
 };
 
 __device__ __forceinline__ float ex2(float x) {
@@ -67,13 +74,37 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// sm_100a packed / 3-input forms (FADD2, FMNMX3) halve the softmax instruction count.
+__device__ __forceinline__ float max3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  unsigned long long x = *reinterpret_cast<unsigned long long*>(&a), y = *reinterpret_cast<unsigned long long*>(&b), z;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(z) : "l"(x), "l"(y));
+  return *reinterpret_cast<float2*>(&z);
+}
 
-// S tiles double-buffered in TMEM (cols [0,64) and [64,128)), O at [128, 128+HD);
-// P double-buffered in smem.  Per page g (global index over this CTA's items):
-//   MMA : S_{g+1} -> TMEM[(g+1)&1] is issued before PV_g, so the tensor core computes the
-//         next scores while the softmax warps work on S_g;
-//   SMX : ld S_g, release the S buffer, exp2, wait PV_{g-1}, write P_g, lazily rescale O.
-template <int HD>
+// 2^x on the FMA/ALU pipes only (FA4-style offload of the SFU): round x to the nearest
+// integer n with the 1.5*2^23 magic number, fit 2^f on f in [-0.5, 0.5] with a cubic
+// (max rel. error 1.4e-4 < bf16 ulp), add n to the exponent bits.
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -125.f);
+  const float t = x + 12582912.f;
+  const float f = x - (t - 12582912.f);
+  const float p = fmaf(fmaf(fmaf(0.05502927f, f, 0.24225698f), f, 0.69325305f), f, 0.99995134f);
+  return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
+}
+
+// Two query tiles per CTA (M = 2 x 128 query vectors of one KV head) share every K/V
+// page, and their MMAs ping-pong on the tensor core: while softmax warpgroup t works on
+// S_t, the tensor core runs the other tile's S / PV.  TMEM (512 columns) per tile t:
+// S double buffer at [256t, 256t+128), O at [256t+128, 256t+128+HD).  Per page g:
+//   MMA : S_0(g+1), S_1(g+1) are issued before PV_0(g), PV_1(g);
+//   SMX_t: ld S_t(g), release it, exp2 (POLY of every 4 on the FMA pipe), wait PV_t(g-1),
+//          write P_t(g), lazily rescale O_t.
+template <int HD, int POLY>
 __global__ void __launch_bounds__(kPfThreads, 1)
     attn_prefill_sm100(PrefillParams p, const __grid_constant__ CUtensorMap tmK,
                        const __grid_constant__ CUtensorMap tmV) {
@@ -82,39 +113,41 @@ __global__ void __launch_bounds__(kPfThreads, 1)
   constexpr int R = S::kRegions;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = base;
-  uint8_t* sKV = sQ + S::kQBytes;
-  uint8_t* sP = sKV + kPfStages * S::kStageBytes;
+  uint8_t* sQ = base;                                  // [2][kQBytes]
+  uint8_t* sKV = sQ + 2 * S::kQBytes;                  // [stages][K | V]
+  uint8_t* sP = sKV + kPfStages * S::kStageBytes;      // [2][kPBytes]
   __shared__ uint64_t full_bar[kPfStages], empty_bar[kPfStages];
-  __shared__ uint64_t s_full[2], s_free[2], p_full, o_done, q_full, o_free;
+  __shared__ uint64_t s_full[2][2], s_free[2][2], p_full[2], o_done[2], q_full[2], o_free[2];
   __shared__ uint32_t tmem_base;
-  __shared__ int s_rid[128], s_rt[128];
+  __shared__ int s_rid[2][kTileM], s_rt[2][kTileM];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int G = p.n_heads / p.n_kv;
+  const int rows_per_tile = kTileM / G;
   const int n_work = p.counts[1] * p.n_kv;
   if (tid == 0) {
     for (int i = 0; i < kPfStages; ++i) {
       mbar_init(&full_bar[i], 1);
       mbar_init(&empty_bar[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 128);
+    for (int t = 0; t < 2; ++t) {
+      for (int i = 0; i < 2; ++i) {
+        mbar_init(&s_full[t][i], 1);
+        mbar_init(&s_free[t][i], 128);
+      }
+      mbar_init(&p_full[t], 128);
+      mbar_init(&o_done[t], 1);
+      mbar_init(&q_full[t], 128);
+      mbar_init(&o_free[t], 128);
     }
-    mbar_init(&p_full, 128);
-    mbar_init(&o_done, 1);
-    mbar_init(&q_full, 128);
-    mbar_init(&o_free, 128);
     fence_barrier_init();
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
   }
-  if (warp == 1) tmem_alloc(&tmem_base, 256);
+  if (warp == 1) tmem_alloc(&tmem_base, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tS = tmem_base, tO = tmem_base + 128;
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -140,69 +173,87 @@ __global__ void __launch_bounds__(kPfThreads, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idS = umma_idesc_bf16(128, kPfKeys, false);
-      constexpr uint32_t idO = umma_idesc_bf16(128, HD, true);
-      const uint32_t qaddr = smem_addr(sQ);
-      auto issue_s = [&](uint32_t g) {
+      constexpr uint32_t idS = umma_idesc_bf16(kTileM, kPfKeys, false);
+      constexpr uint32_t idO = umma_idesc_bf16(kTileM, HD, true);
+      auto issue_s = [&](int t, uint32_t g) {
         const int st = g % kPfStages, b = g & 1;
-        mbar_wait(&full_bar[st], (g / kPfStages) & 1);
-        mbar_wait(&s_free[b], ((g >> 1) & 1) ^ 1);
+        if (t == 0) mbar_wait(&full_bar[st], (g / kPfStages) & 1);
+        mbar_wait(&s_free[t][b], ((g >> 1) & 1) ^ 1);
         tc_fence_after();
+        const uint32_t qaddr = smem_addr(sQ + t * S::kQBytes);
         const uint32_t kaddr = smem_addr(sKV + st * S::kStageBytes);
+        const uint32_t dS = tmem_base + 256 * t + 64 * b;
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k) {
           const uint32_t off = (k & 3) * 32;
-          umma_bf16(tS + 64 * b, umma_desc_sw128(qaddr + (k >> 2) * 128 * 128 + off, 16, 1024),
+          umma_bf16(dS, umma_desc_sw128(qaddr + (k >> 2) * kTileM * 128 + off, 16, 1024),
                     umma_desc_sw128(kaddr + (k >> 2) * kPfKeys * 128 + off, 16, 1024), idS, k > 0);
         }
-        umma_commit(&s_full[b]);
+        umma_commit(&s_full[t][b]);
+      };
+      auto issue_pv = [&](int t, uint32_t g, bool first) {
+        mbar_wait(&p_full[t], g & 1);
+        tc_fence_after();
+        const uint32_t vaddr = smem_addr(sKV + (g % kPfStages) * S::kStageBytes) + S::kKVBytes;
+        const uint32_t paddr = smem_addr(sP + t * S::kPBytes);
+        const uint32_t dO = tmem_base + 256 * t + 128;
+#pragma unroll
+        for (int k = 0; k < kPfKeys / 16; ++k)
+          umma_bf16(dO, umma_desc_sw128(paddr + k * 32, 16, 1024),
+                    umma_desc_sw128(vaddr + k * 2048, kPfKeys * 128, 1024), idO,
+                    (!first || k > 0) ? 1u : 0u);
+        umma_commit(&o_done[t]);
       };
       uint32_t gp = 0, ic = 0;
       for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++ic) {
         const int nv = p.items[6 * (w / p.n_kv) + 3];
-        mbar_wait(&q_full, ic & 1);
-        if (ic > 0) mbar_wait(&o_free, (ic - 1) & 1);
+        for (int t = 0; t < 2; ++t) {
+          mbar_wait(&q_full[t], ic & 1);
+          if (ic > 0) mbar_wait(&o_free[t], (ic - 1) & 1);
+        }
         tc_fence_after();
-        issue_s(gp);
+        issue_s(0, gp);
+        issue_s(1, gp);
         for (int j = 0; j < nv; ++j, ++gp) {
-          if (j + 1 < nv) issue_s(gp + 1);
-          mbar_wait(&p_full, gp & 1);  // P_j written, O rescaled
-          tc_fence_after();
-          const int st = gp % kPfStages;
-          const uint32_t vaddr = smem_addr(sKV + st * S::kStageBytes) + S::kKVBytes;
-          const uint32_t paddr = smem_addr(sP + (gp & 1) * S::kPBytes);
-#pragma unroll
-          for (int k = 0; k < kPfKeys / 16; ++k)
-            umma_bf16(tO, umma_desc_sw128(paddr + k * 32, 16, 1024),
-                      umma_desc_sw128(vaddr + k * 2048, kPfKeys * 128, 1024), idO,
-                      (j > 0 || k > 0) ? 1u : 0u);
-          umma_commit(&empty_bar[st]);
-          umma_commit(&o_done);
+          if (j + 1 < nv) {
+            issue_s(0, gp + 1);
+            issue_s(1, gp + 1);
+          }
+          issue_pv(0, gp, j == 0);
+          issue_pv(1, gp, j == 0);
+          umma_commit(&empty_bar[gp % kPfStages]);
         }
       }
     }
   } else {
-    // ------------------------------------------------------------ softmax warps
-    const int quad = warp & 3;       // TMEM lane quadrant
-    const int m = quad * 32 + lane;  // query vector (TMEM lane) of this thread
+    // ------------------------------------------------------------ softmax warpgroups
+    const int t = (warp - 2) >> 2;      // tile of this warpgroup
+    const int quad = warp & 3;          // TMEM lane quadrant
+    const int m = quad * 32 + lane;     // query vector (TMEM lane) within the tile
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    const int st_tid = tid - 64;     // 0..127
+    const uint32_t tS = tmem_base + 256 * t, tO = tmem_base + 256 * t + 128;
+    const int wg_tid = tid - 64 - 128 * t;  // 0..127
+    uint8_t* myQ = sQ + t * S::kQBytes;
+    uint8_t* myP = sP + t * S::kPBytes;
     uint32_t gp = 0;
     for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
       const int32_t* it = p.items + 6 * (w / p.n_kv);
       const int kvh = w % p.n_kv, rb = it[0], nr = it[1], vb = it[2], nv = it[3], pbase = it[4];
-      const int M = nr * G;
-      if (st_tid < nr) {
-        const int rid = p.blk_rows[rb + st_tid];
-        s_rid[st_tid] = rid;
-        s_rt[st_tid] = p.row_t[rid];
+      const int r0 = t * rows_per_tile;                       // first block row of this tile
+      const int nr_t = max(0, min(rows_per_tile, nr - r0));   // rows of this tile
+      const int M = nr_t * G;
+      if (wg_tid < nr_t) {
+        const int rid = p.blk_rows[rb + r0 + wg_tid];
+        s_rid[t][wg_tid] = rid;
+        s_rt[t][wg_tid] = p.row_t[rid];
       }
-      asm volatile("bar.sync 1, 128;\n" ::: "memory");
+      asm volatile("bar.sync %0, 128;\n" ::"r"(1 + t) : "memory");
       const bool valid = m < M;
       const int my_row = valid ? m / G : 0;
-      const int my_t = valid ? s_rt[my_row] : -1;
+      const int my_t = valid ? s_rt[t][my_row] : -1;
       {  // stage Q (bf16, SW128 K-major, pre-scaled to the log2 domain)
-        const float* qr = p.q + ((int64_t)s_rid[my_row] * p.n_heads + kvh * G + (valid ? m % G : 0)) * HD;
+        const int rid = nr_t > 0 ? s_rid[t][my_row] : 0;
+        const float* qr = p.q + ((int64_t)rid * p.n_heads + kvh * G + (valid ? m % G : 0)) * HD;
 #pragma unroll
         for (int c = 0; c < HD / 8; ++c) {
           float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
@@ -220,44 +271,75 @@ __global__ void __launch_bounds__(kPfThreads, 1)
           u.y = *reinterpret_cast<uint32_t*>(&h1);
           u.z = *reinterpret_cast<uint32_t*>(&h2);
           u.w = *reinterpret_cast<uint32_t*>(&h3);
-          *reinterpret_cast<uint4*>(sQ + (c >> 3) * 128 * 128 + sw128_offset(m, (c & 7) * 8)) = u;
+          *reinterpret_cast<uint4*>(myQ + (c >> 3) * kTileM * 128 + sw128_offset(m, (c & 7) * 8)) = u;
         }
       }
       fence_proxy_async_smem();
-      mbar_arrive(&q_full);
+      mbar_arrive(&q_full[t]);
       float mrow = -INFINITY, lrow = 0.f;  // mrow = max used for the exponentials (lazy)
       for (int j = 0; j < nv; ++j, ++gp) {
         const int pi = vb + j;
         const int len = p.vis_len[pi], own = p.vis_own[pi];
         const int b = gp & 1;
-        mbar_wait(&s_full[b], (gp >> 1) & 1);
+        mbar_wait(&s_full[t][b], (gp >> 1) & 1);
         tc_fence_after();
         float s[kPfKeys];
 #pragma unroll
         for (int c = 0; c < kPfKeys / 16; ++c) tmem_ld16(tS + 64 * b + lane_off + c * 16, s + c * 16);
         tmem_wait_ld();
         tc_fence_before();
-        mbar_arrive(&s_free[b]);
-        // keys visible to this row: k < lim (own pages: causal cut at my_t)
-        int lim = valid ? len : 0;
+        mbar_arrive(&s_free[t][b]);
+        int lim = valid ? len : 0;  // keys k < lim are visible (own pages: causal cut)
         if (own >= 0) lim = min(lim, my_t - own + 1);
-        float tmax = -INFINITY;
+        // warp-uniform fast path: a full page visible to every row of the warp (most parent
+        // pages) needs no per-key mask
+        const bool full = __all_sync(0xffffffffu, lim >= kPfKeys);
+        float mx[8];
 #pragma unroll
-        for (int k = 0; k < kPfKeys; ++k) tmax = fmaxf(tmax, k < lim ? s[k] : -INFINITY);
+        for (int i = 0; i < 8; ++i) mx[i] = -INFINITY;
+        if (full) {
+#pragma unroll
+          for (int k = 0; k < kPfKeys; k += 2) mx[(k >> 1) & 7] = max3(mx[(k >> 1) & 7], s[k], s[k + 1]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < kPfKeys; ++k) mx[k & 7] = fmaxf(mx[k & 7], k < lim ? s[k] : -INFINITY);
+        }
+        const float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                 fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
         float alpha = 1.f;
         if (tmax > mrow + kRescaleTh || (mrow == -INFINITY && tmax != -INFINITY)) {
           alpha = mrow == -INFINITY ? 0.f : ex2(mrow - tmax);
           mrow = tmax;
         }
-        float sum = 0.f;
+        float sm[8];
 #pragma unroll
-        for (int k = 0; k < kPfKeys; ++k) {
-          s[k] = k < lim ? ex2(s[k] - mrow) : 0.f;
-          sum += s[k];
+        for (int i = 0; i < 8; ++i) sm[i] = 0.f;
+        if (full) {
+          const float2 nm = make_float2(-mrow, -mrow);
+          float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                           make_float2(0.f, 0.f)};
+#pragma unroll
+          for (int k = 0; k < kPfKeys; k += 2) {
+            float2 x = add2(make_float2(s[k], s[k + 1]), nm);
+            x.x = ((k & 3) < POLY) ? ex2_poly(x.x) : ex2(x.x);
+            x.y = ex2(x.y);
+            s[k] = x.x;
+            s[k + 1] = x.y;
+            acc[(k >> 1) & 3] = add2(acc[(k >> 1) & 3], x);
+          }
+          const float2 t2 = add2(add2(acc[0], acc[1]), add2(acc[2], acc[3]));
+          sm[0] = t2.x + t2.y;
+        } else {
+#pragma unroll
+          for (int k = 0; k < kPfKeys; ++k) {
+            const float x = s[k] - mrow;
+            const float e = ((k & 3) < POLY) ? ex2_poly(x) : ex2(x);
+            s[k] = k < lim ? e : 0.f;
+            sm[k & 7] += s[k];
+          }
         }
-        lrow = lrow * alpha + sum;
-        if (j > 0) mbar_wait(&o_done, (gp - 1) & 1);  // PV_{g-1} done: O stable, P buffer free
-        uint8_t* pb = sP + b * S::kPBytes;
+        lrow = lrow * alpha + ((sm[0] + sm[1]) + (sm[2] + sm[3])) + ((sm[4] + sm[5]) + (sm[6] + sm[7]));
+        if (j > 0) mbar_wait(&o_done[t], (gp - 1) & 1);  // PV_t(g-1) done: O stable, P free
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           __nv_bfloat162 h0 = __floats2bfloat162_rn(s[8 * c], s[8 * c + 1]);
@@ -269,7 +351,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
           u.y = *reinterpret_cast<uint32_t*>(&h1);
           u.z = *reinterpret_cast<uint32_t*>(&h2);
           u.w = *reinterpret_cast<uint32_t*>(&h3);
-          *reinterpret_cast<uint4*>(pb + sw128_offset(m, 8 * c)) = u;
+          *reinterpret_cast<uint4*>(myP + sw128_offset(m, 8 * c)) = u;
         }
         if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
           tc_fence_after();
@@ -286,37 +368,61 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         }
         fence_proxy_async_smem();
         tc_fence_before();
-        mbar_arrive(&p_full);
+        mbar_arrive(&p_full[t]);
       }
       // ---- epilogue: O / l -> partial, LSE (natural log) ----
-      mbar_wait(&o_done, (gp - 1) & 1);
+      mbar_wait(&o_done[t], (gp - 1) & 1);
       tc_fence_after();
       {
         // tcgen05.ld is warp-collective: every lane loads, only valid lanes store
-        const int64_t pidx = (int64_t)(pbase + (valid ? m / G : 0)) * p.n_heads + kvh * G + m % G;
+        const int head = kvh * G + m % G;
+        const int64_t pidx = (int64_t)(pbase + r0 + (valid ? m / G : 0)) * p.n_heads + head;
         const float inv = lrow > 0.f ? 1.f / lrow : 0.f;
         float* dst = p.part_o + pidx * HD;
+        __nv_bfloat16* od = p.out ? p.out + ((int64_t)(valid ? s_rid[t][my_row] : 0) * p.n_heads + head) * HD
+                                  : nullptr;
+        const int64_t lo_off = (int64_t)p.n_rows * p.n_heads * HD;
 #pragma unroll
         for (int c = 0; c < HD / 16; ++c) {
           float o[16];
           tmem_ld16(tO + lane_off + c * 16, o);
           tmem_wait_ld();
           if (valid) {
+            if (od) {
 #pragma unroll
-            for (int i = 0; i < 16; i += 4)
-              *reinterpret_cast<float4*>(dst + c * 16 + i) =
-                  make_float4(o[i] * inv, o[i + 1] * inv, o[i + 2] * inv, o[i + 3] * inv);
+              for (int i = 0; i < 16; i += 8) {
+                uint4 hi, lo;
+                uint32_t* hp = reinterpret_cast<uint32_t*>(&hi);
+                uint32_t* lp = reinterpret_cast<uint32_t*>(&lo);
+#pragma unroll
+                for (int q2 = 0; q2 < 4; ++q2) {
+                  const float a = o[i + 2 * q2] * inv, b = o[i + 2 * q2 + 1] * inv;
+                  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+                  const float2 hf = __bfloat1622float2(h);
+                  __nv_bfloat162 l = __floats2bfloat162_rn(a - hf.x, b - hf.y);
+                  hp[q2] = *reinterpret_cast<uint32_t*>(&h);
+                  lp[q2] = *reinterpret_cast<uint32_t*>(&l);
+                }
+                *reinterpret_cast<uint4*>(od + c * 16 + i) = hi;
+                if (p.out_split) *reinterpret_cast<uint4*>(od + lo_off + c * 16 + i) = lo;
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; i += 4)
+                *reinterpret_cast<float4*>(dst + c * 16 + i) =
+                    make_float4(o[i] * inv, o[i + 1] * inv, o[i + 2] * inv, o[i + 3] * inv);
+            }
           }
         }
-        if (valid) p.part_lse[pidx] = lrow > 0.f ? (mrow + log2f(lrow)) * 0.6931471805599453f : -INFINITY;
+        if (valid && !od) p.part_lse[pidx] = lrow > 0.f ? (mrow + log2f(lrow)) * 0.6931471805599453f : -INFINITY;
       }
       tc_fence_before();
-      mbar_arrive(&o_free);
+      mbar_arrive(&o_free[t]);
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem_base, 256);
+  if (warp == 1) tmem_dealloc(tmem_base, 512);
 }
 
 // ---------------------------------------------------------------- host side
@@ -346,7 +452,7 @@ static bool encode_pool_map(CUtensorMap* map, const void* pool, uint64_t rows, i
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int HD>
+template <int HD, int POLY>
 static int launch_prefill(const PrefillParams& p, const void* k_pool, const void* v_pool,
                           uint64_t rows, int grid, cudaStream_t s) {
   CUtensorMap mk, mv;
@@ -355,10 +461,11 @@ static int launch_prefill(const PrefillParams& p, const void* k_pool, const void
   const int smem = PfSmem<HD>::kTotal;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attn_prefill_sm100<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attn_prefill_sm100<HD, POLY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         smem);
     attr = true;
   }
-  attn_prefill_sm100<HD><<<grid, kPfThreads, smem, s>>>(p, mk, mv);
+  attn_prefill_sm100<HD, POLY><<<grid, kPfThreads, smem, s>>>(p, mk, mv);
   return launch_status("choreo_prefill_attn");
 }
 
@@ -373,7 +480,8 @@ extern "C" int choreo_prefill_attn_dbg(const float* q, const void* k_pool, const
                                        const int32_t* vis_len, const int32_t* vis_own,
                                        const int32_t* blk_rows, const int32_t* items,
                                        const int32_t* counts, int max_items, float* part_o,
-                                       float* part_lse, int grid_ctas, int* dbg, void* stream);
+                                       float* part_lse, int grid_ctas, int* dbg, void* out,
+                                       int out_split, int n_rows, void* stream);
 
 extern "C" int choreo_prefill_attn(const float* q, const void* k_pool, const void* v_pool,
                                    int pool_dtype, int n_layers, int layer, int n_kv, int n_pages,
@@ -381,11 +489,12 @@ extern "C" int choreo_prefill_attn(const float* q, const void* k_pool, const voi
                                    const int32_t* vis_page, const int32_t* vis_len,
                                    const int32_t* vis_own, const int32_t* blk_rows,
                                    const int32_t* items, const int32_t* counts, int max_items,
-                                   float* part_o, float* part_lse, int grid_ctas, void* stream) {
+                                   float* part_o, float* part_lse, int grid_ctas, void* out,
+                                   int out_split, int n_rows, void* stream) {
   return choreo_prefill_attn_dbg(q, k_pool, v_pool, pool_dtype, n_layers, layer, n_kv, n_pages,
                                  page_size, n_heads, head_dim, row_t, vis_page, vis_len, vis_own,
                                  blk_rows, items, counts, max_items, part_o, part_lse, grid_ctas,
-                                 nullptr, stream);
+                                 nullptr, out, out_split, n_rows, stream);
 }
 
 extern "C" int choreo_prefill_attn_dbg(const float* q, const void* k_pool, const void* v_pool,
@@ -395,22 +504,32 @@ extern "C" int choreo_prefill_attn_dbg(const float* q, const void* k_pool, const
                                    const int32_t* vis_own, const int32_t* blk_rows,
                                    const int32_t* items, const int32_t* counts, int max_items,
                                    float* part_o, float* part_lse, int grid_ctas, int* dbg,
-                                   void* stream) {
+                                   void* out, int out_split, int n_rows, void* stream) {
   if (!q || !k_pool || !v_pool || !row_t || !vis_page || !vis_len || !vis_own || !blk_rows ||
       !items || !counts || !part_o || !part_lse || n_kv <= 0 || n_heads % n_kv)
     return CHOREO_EINVAL;
   if (pool_dtype != CHOREO_BF16 || page_size != kPfKeys || (head_dim != 64 && head_dim != 128) ||
-      (n_heads / n_kv) > 128)
+      (n_heads / n_kv) > 128 || 128 % (n_heads / n_kv))
     return CHOREO_EUNSUPPORTED;
   if (max_items <= 0) return CHOREO_OK;
   PrefillParams p{q, layer, n_kv, n_pages, page_size, n_heads, row_t, vis_page, vis_len, vis_own,
                   blk_rows, items, counts, part_o, part_lse,
-                  1.4426950408889634f / sqrtf((float)head_dim), dbg};
+                  1.4426950408889634f / sqrtf((float)head_dim), dbg,
+                  reinterpret_cast<__nv_bfloat16*>(out), out_split, n_rows};
   int grid = grid_ctas > 0 ? grid_ctas : max_items * n_kv;
   if (grid > 148) grid = 148;
   const uint64_t rows = (uint64_t)n_layers * n_kv * n_pages * page_size;
   if (rows > 0x7fffffffull) return CHOREO_EUNSUPPORTED;
   auto s = as_stream(stream);
-  return head_dim == 128 ? launch_prefill<128>(p, k_pool, v_pool, rows, grid, s)
-                         : launch_prefill<64>(p, k_pool, v_pool, rows, grid, s);
+  static int poly = -1;
+  if (poly < 0) {
+    const char* e = getenv("CHOREO_K4_POLY");
+    poly = e ? atoi(e) : 0;
+  }
+  if (head_dim == 64) return launch_prefill<64, 1>(p, k_pool, v_pool, rows, grid, s);
+  switch (poly) {
+    case 0: return launch_prefill<128, 0>(p, k_pool, v_pool, rows, grid, s);
+    case 2: return launch_prefill<128, 2>(p, k_pool, v_pool, rows, grid, s);
+    default: return launch_prefill<128, 1>(p, k_pool, v_pool, rows, grid, s);
+  }
 }

@@ -197,7 +197,7 @@ class Runner:
         use_k4 = (self.pool_dtc == nat.BF16 and P == 64 and hd in (64, 128) and G <= 128
                   and max(len(c.tokens) for c in plan.calls) >= 64
                   and os.environ.get("CHOREO_PREFILL_K4", "1") != "0")
-        rpb = 128 // G if use_k4 else self.rows_per_block
+        rpb = 256 // G if use_k4 else self.rows_per_block  # K4: two 128-vector tiles
         # pages per item: about two waves of (2 CTAs/SM x 148 SMs) per layer, and at
         # most 512 partials per row for the combine
         # prefill-sized steps: per-call page lists (a row block already fills an M tile)
@@ -209,6 +209,8 @@ class Runner:
             ppi *= 2
             plan_ = plan_counts(plan.calls, msg_len, P, rpb, ppi, mode)
         n_parts, n_items = plan_.n_parts, plan_.n_items
+        # K4 writes final rows directly when no row is split across items
+        direct = use_k4 and plan_.max_row_parts == 1 and self.dt == torch.bfloat16
         n_log = len(plan.logit_rows)
 
         ints = np.concatenate([ids, row_t, pos, pages, slots, np.asarray(call_tab, np.int32),
@@ -282,7 +284,8 @@ class Runner:
                                  rowt_d.data_ptr(), vis[0].data_ptr(), vis[1].data_ptr(),
                                  vis[2].data_ptr(), blk_rows.data_ptr(), items.data_ptr(),
                                  counts.data_ptr(), n_items, part_o.data_ptr(),
-                                 part_lse.data_ptr(), 0, stream)
+                                 part_lse.data_ptr(), 0,
+                                 attn.data_ptr() if direct else None, sp, R, stream)
             else:
                 nat.attn_split(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(),
                                self.pool_dtc, layer, Hk, cache.n_pages, P, H, hd,
@@ -293,8 +296,10 @@ class Runner:
             if self.attn_events is not None:
                 ev1.record()
                 self.attn_events.append((ev0, ev1, attn_bytes))
-            nat.attn_combine(part_o.data_ptr(), part_lse.data_ptr(), row_part_off.data_ptr(),
-                             row_part.data_ptr(), R, H, hd, attn.data_ptr(), self.dtc, sp, stream)
+            if not direct:
+                nat.attn_combine(part_o.data_ptr(), part_lse.data_ptr(), row_part_off.data_ptr(),
+                                 row_part.data_ptr(), R, H, hd, attn.data_ptr(), self.dtc, sp,
+                                 stream)
             ao = self._mm(attn, lw["wo"], out_f32=True)
             nat.residual_rmsnorm(x.data_ptr(), ao.data_ptr(), nat.F32, sp,
                                  lw["ffn_norm"].data_ptr(), self.dtc, R, d, RMS_EPS, h.data_ptr(),

@@ -302,8 +302,9 @@ def test_umma_selftest_tcgen05_descriptors():
     torch.testing.assert_close(c2, a.float() @ b2.float(), rtol=1e-4, atol=1e-3)
 
 
+@pytest.mark.parametrize("ppi", [3, 100000])
 @pytest.mark.parametrize("hd,H,Hk", [(128, 32, 8), (64, 8, 8), (128, 16, 2)])
-def test_prefill_tcgen05_matches_dense_reference(hd, H, Hk):
+def test_prefill_tcgen05_matches_dense_reference(hd, H, Hk, ppi):
     """K4 (tcgen05/TMEM/TMA) over page-centric items with 128-row M tiles: prefill rows of
     two messages sharing reordered parents, causal own pages, partial tail pages."""
     rng = np.random.default_rng(7)
@@ -317,21 +318,28 @@ def test_prefill_tcgen05_matches_dense_reference(hd, H, Hk):
     cache.v_pool.copy_(torch.randn_like(cache.v_pool))
     calls = [(6, [4, 1, 3], list(range(150))), (7, [3, 0], list(range(41)))]
     G = H // Hk
-    out, (rt_d, vis, blk, items, rpo, rp, counts) = _assemble(cache, calls, 128 // G, 3, 1)
+    out, (rt_d, vis, blk, items, rpo, rp, counts) = _assemble(cache, calls, 256 // G, ppi, 1)
     R = len(out["row_t"])
     q = torch.randn(R, H, hd, device="cuda")
     n_parts = out["plan"].n_parts
     part_o = torch.empty(n_parts, H, hd, device="cuda")
     part_lse = torch.empty(n_parts, H, device="cuda")
     o = torch.empty(R, H * hd, dtype=torch.float32, device="cuda")
+    direct = out["plan"].max_row_parts == 1
+    assert direct == (ppi > 1000)
+    direct_out = torch.zeros(2 * R, H * hd, dtype=torch.bfloat16, device="cuda")
     L = 1
     nat.prefill_attn(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(), nat.BF16,
                      cfg.n_layers, L, Hk, cache.n_pages, cache.page_size, H, hd, rt_d.data_ptr(),
                      vis[0].data_ptr(), vis[1].data_ptr(), vis[2].data_ptr(), blk.data_ptr(),
                      items.data_ptr(), counts.data_ptr(), out["plan"].n_items, part_o.data_ptr(),
-                     part_lse.data_ptr(), 0, _stream())
-    nat.attn_combine(part_o.data_ptr(), part_lse.data_ptr(), rpo.data_ptr(), rp.data_ptr(), R, H,
-                     hd, o.data_ptr(), nat.F32, 0, _stream())
+                     part_lse.data_ptr(), 0, direct_out.data_ptr() if direct else None, 1, R,
+                     _stream())
+    if direct:  # final rows written by K4 as hi/lo bf16 pairs
+        o.copy_((direct_out[:R].float() + direct_out[R:].float()))
+    else:
+        nat.attn_combine(part_o.data_ptr(), part_lse.data_ptr(), rpo.data_ptr(), rp.data_ptr(), R,
+                         H, hd, o.data_ptr(), nat.F32, 0, _stream())
     torch.cuda.synchronize()
     sets = _expand_rows(cache, out, R)
     K = cache.k_pool[L].float().cpu().numpy().astype(np.float64)
