@@ -113,6 +113,9 @@ int choreo_rerotate(void* k_pool, int pool_dtype, int n_layers, int n_kv, int n_
  *       (group >= 0: parent group index; -1-c: own pages of call c)
  *   row_part_off[n_rows + 1], row_part[]: per-row CSR list of the partial slots to merge
  *   counts[0..3] = {n_vis_pages, n_items, n_partials, status (0 ok, <0 over capacity)}
+ * fat (optional, int32 [n_items][64]): self-contained item records for choreo_decode_attn:
+ *   {n_rows, n_pages, partial base, 0, row ids[16], row_t[16], page[8], page_len[8],
+ *    own_base[8], pad[4]}; requires rows_per_block <= 16 and pages_per_item <= 8.
  * mode 0 = page-centric groups (decode-sized steps); mode 1 = per-call lists (prefill-sized
  * steps: each call's parents' pages in parent order, then its own pages, items are row
  * blocks x page chunks of that list; group field = -1-call).
@@ -125,7 +128,8 @@ int choreo_assemble(const int32_t* msg_len, const int32_t* msg_pt, int32_t* page
                     int page_size, int rows_per_block, int pages_per_item, int32_t* vis_page,
                     int32_t* vis_len, int32_t* vis_own, int32_t* blk_rows, int32_t* items,
                     int32_t* row_part_off, int32_t* row_part, int32_t* counts, int cap_vis,
-                    int cap_blk_rows, int cap_items, int cap_parts, int mode, void* stream);
+                    int cap_blk_rows, int cap_items, int cap_parts, int mode, int32_t* fat,
+                    void* stream);
 
 /* K5 split-KV attention over assembled work items (prefill and decode rows alike).
  * q: f32 [n_rows][n_heads][hd] (already rotated, K1).  For each item and KV head writes
@@ -160,6 +164,19 @@ int choreo_prefill_attn(const float* q, const void* k_pool, const void* v_pool, 
                         const int32_t* items, const int32_t* counts, int max_items, float* part_o,
                         float* part_lse, int grid_ctas, void* out, int out_split, int n_rows,
                         void* stream);
+
+/* Fused decode attention (bf16 pools, page_size 64, head_dim 64/128): K5's tensor-core
+ * split-KV math over K3 fat items (one 256-byte record per item, no dependent lookups) with
+ * the LSE combine fused in: each (row, kv head) has an arrival counter in row_counters
+ * (int32 [n_rows * n_kv], all zero on entry, left zero on exit); the CTA that delivers a
+ * row's last partial merges them and writes out[row] (bf16, hi/lo pair if out_split).
+ * flags as choreo_attn_split.  Replaces model.py:177-184 for decode-sized steps. */
+int choreo_decode_attn(const float* q, const void* k_pool, const void* v_pool, int layer, int n_kv,
+                       int n_pages, int page_size, int n_heads, int head_dim,
+                       const int32_t* fat_items, const int32_t* counts, int max_items,
+                       const int32_t* row_part_off, const int32_t* row_part, float* part_o,
+                       float* part_lse, int32_t* row_counters, void* out, int out_split,
+                       int n_rows, int flags, int grid_ctas, void* stream);
 
 /* Combine each row's partials (CSR row_part_off / row_part, <= 512 per row) into
  * out[r][h][:] (out_dtype; hi/lo pair if out_split) with the LSE merge. */

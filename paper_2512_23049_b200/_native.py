@@ -30,7 +30,9 @@ SIGNATURES: dict[str, list] = {
                            _I, _P, _P, _I, _P],
     "choreo_rerotate": [_P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _I, _P, _P, _I, _P],
     "choreo_assemble": [_P, _P, _P, _P, _P, _I, _P, _I, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P,
-                        _P, _P, _P, _I, _I, _I, _I, _I, _P],
+                        _P, _P, _P, _I, _I, _I, _I, _I, _P, _P],
+    "choreo_decode_attn": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P, _I, _P, _P, _P, _P, _P, _P,
+                           _I, _I, _I, _I, _P],
     "choreo_attn_split": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P,
                           _I, _P, _P, _I, _I, _P],
     "choreo_prefill_attn": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P,
@@ -88,6 +90,7 @@ assemble = _Caller("choreo_assemble")
 attn_split = _Caller("choreo_attn_split")
 attn_combine = _Caller("choreo_attn_combine")
 prefill_attn = _Caller("choreo_prefill_attn")
+decode_attn = _Caller("choreo_decode_attn")
 select_greedy = _Caller("choreo_select_greedy")
 selftest_umma = _Caller("choreo_selftest_umma")
 

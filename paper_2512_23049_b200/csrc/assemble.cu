@@ -49,7 +49,38 @@ struct K3Params {
   int32_t* row_part;      // partial slots, CSR by row
   int32_t* counts;
   int cap_vis, cap_blk_rows, cap_items, cap_parts;
+  int32_t* fat;  // optional self-contained item records (kFatInts each), see write_fat
 };
+
+// Self-contained item record for the latency-bound decode kernel: one 256-byte load gives
+// a CTA everything it needs (no dependent lookups of rows, row_t or page descriptors).
+//   [0] n_rows  [1] n_pages  [2] partial base  [3] unused
+//   [4..19] row ids   [20..35] row_t   [36..43] page  [44..51] page_len  [52..59] own_base
+// Requires n_rows <= kFatRows and n_pages <= kFatPages (the host sizes items that way).
+constexpr int kFatInts = 64, kFatRows = 16, kFatPages = 8;
+
+__device__ void write_fat(const K3Params& p, int n_items) {
+  for (int i = threadIdx.x; i < n_items; i += blockDim.x) {
+    const int32_t* it = p.items + 6 * i;
+    int32_t* f = p.fat + kFatInts * i;
+    const int nr = min(it[1], kFatRows), nv = min(it[3], kFatPages);
+    f[0] = nr;
+    f[1] = nv;
+    f[2] = it[4];
+    f[3] = 0;
+    for (int r = 0; r < kFatRows; ++r) {
+      const int rid = r < nr ? p.blk_rows[it[0] + r] : 0;
+      f[4 + r] = rid;
+      f[20 + r] = r < nr ? p.row_t[rid] : -1;
+    }
+    for (int k = 0; k < kFatPages; ++k) {
+      const bool ok = k < nv;
+      f[36 + k] = ok ? p.vis_page[it[2] + k] : 0;
+      f[44 + k] = ok ? p.vis_len[it[2] + k] : 0;
+      f[52 + k] = ok ? p.vis_own[it[2] + k] : -1;
+    }
+  }
+}
 
 // smem-resident plan
 struct Shared {
@@ -282,6 +313,10 @@ __global__ void __launch_bounds__(kThreads3) assemble_kernel(K3Params p) {
       for (int ch = 0; ch < chunks; ++ch) p.row_part[w++] = pa + ch * nr + (j - b * p.rpb);
     }
   }
+  if (p.fat) {
+    __syncthreads();
+    write_fat(p, S.tot_items);
+  }
 }
 
 // Per-call mode (prefill-sized steps): each call's visible list is its parents' pages
@@ -381,6 +416,10 @@ __global__ void __launch_bounds__(kThreads3) assemble_percall_kernel(K3Params p)
       pa += chunks * nr;
     }
   }
+  if (p.fat) {
+    __syncthreads();
+    write_fat(p, p.counts[1]);
+  }
 }
 
 }  // namespace choreo
@@ -394,7 +433,8 @@ extern "C" int choreo_assemble(const int32_t* msg_len, const int32_t* msg_pt, in
                                int32_t* vis_page, int32_t* vis_len, int32_t* vis_own,
                                int32_t* blk_rows, int32_t* items, int32_t* row_part_off,
                                int32_t* row_part, int32_t* counts, int cap_vis, int cap_blk_rows,
-                               int cap_items, int cap_parts, int mode, void* stream) {
+                               int cap_items, int cap_parts, int mode, int32_t* fat,
+                               void* stream) {
   if (!msg_len || !msg_pt || !page_table || !calls || !row_t || !vis_page || !vis_len ||
       !vis_own || !blk_rows || !items || !row_part_off || !row_part || !counts)
     return CHOREO_EINVAL;
@@ -404,7 +444,7 @@ extern "C" int choreo_assemble(const int32_t* msg_len, const int32_t* msg_pt, in
   K3Params p{msg_len, msg_pt, page_table, calls, call_parents, n_calls, row_t, n_rows, patch,
              n_patch, page_size, rows_per_block, pages_per_item, vis_page, vis_len, vis_own,
              blk_rows, items, row_part_off, row_part, counts, cap_vis, cap_blk_rows, cap_items,
-             cap_parts};
+             cap_parts, fat};
   if (mode == 1) {
     assemble_percall_kernel<<<1, kThreads3, 0, as_stream(stream)>>>(p);
     return launch_status("choreo_assemble");

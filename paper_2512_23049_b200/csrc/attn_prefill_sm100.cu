@@ -175,10 +175,11 @@ __global__ void __launch_bounds__(kPfThreads, 1)
     if (lane == 0) {
       constexpr uint32_t idS = umma_idesc_bf16(kTileM, kPfKeys, false);
       constexpr uint32_t idO = umma_idesc_bf16(kTileM, HD, true);
-      auto issue_s = [&](int t, uint32_t g) {
-        const int st = g % kPfStages, b = g & 1;
+      // g = global page index (K/V ring), gt = this tile's page index (its barriers)
+      auto issue_s = [&](int t, uint32_t g, uint32_t gt) {
+        const int st = g % kPfStages, b = gt & 1;
         if (t == 0) mbar_wait(&full_bar[st], (g / kPfStages) & 1);
-        mbar_wait(&s_free[t][b], ((g >> 1) & 1) ^ 1);
+        mbar_wait(&s_free[t][b], ((gt >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t qaddr = smem_addr(sQ + t * S::kQBytes);
         const uint32_t kaddr = smem_addr(sKV + st * S::kStageBytes);
@@ -191,8 +192,8 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         }
         umma_commit(&s_full[t][b]);
       };
-      auto issue_pv = [&](int t, uint32_t g, bool first) {
-        mbar_wait(&p_full[t], g & 1);
+      auto issue_pv = [&](int t, uint32_t g, uint32_t gt, bool first) {
+        mbar_wait(&p_full[t], gt & 1);
         tc_fence_after();
         const uint32_t vaddr = smem_addr(sKV + (g % kPfStages) * S::kStageBytes) + S::kKVBytes;
         const uint32_t paddr = smem_addr(sP + t * S::kPBytes);
@@ -204,25 +205,34 @@ __global__ void __launch_bounds__(kPfThreads, 1)
                     (!first || k > 0) ? 1u : 0u);
         umma_commit(&o_done[t]);
       };
-      uint32_t gp = 0, ic = 0;
-      for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++ic) {
-        const int nv = p.items[6 * (w / p.n_kv) + 3];
-        for (int t = 0; t < 2; ++t) {
-          mbar_wait(&q_full[t], ic & 1);
-          if (ic > 0) mbar_wait(&o_free[t], (ic - 1) & 1);
+      uint32_t gp = 0, g1 = 0, ic0 = 0, ic1 = 0;
+      for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+        const int32_t* it = p.items + 6 * (w / p.n_kv);
+        const int nv = it[3];
+        const bool two = it[1] > rows_per_tile;  // second tile has rows in this item
+        mbar_wait(&q_full[0], ic0 & 1);
+        if (ic0 > 0) mbar_wait(&o_free[0], (ic0 - 1) & 1);
+        if (two) {
+          mbar_wait(&q_full[1], ic1 & 1);
+          if (ic1 > 0) mbar_wait(&o_free[1], (ic1 - 1) & 1);
         }
         tc_fence_after();
-        issue_s(0, gp);
-        issue_s(1, gp);
+        issue_s(0, gp, gp);
+        if (two) issue_s(1, gp, g1);
         for (int j = 0; j < nv; ++j, ++gp) {
           if (j + 1 < nv) {
-            issue_s(0, gp + 1);
-            issue_s(1, gp + 1);
+            issue_s(0, gp + 1, gp + 1);
+            if (two) issue_s(1, gp + 1, g1 + 1);
           }
-          issue_pv(0, gp, j == 0);
-          issue_pv(1, gp, j == 0);
+          issue_pv(0, gp, gp, j == 0);
+          if (two) {
+            issue_pv(1, gp, g1, j == 0);
+            ++g1;
+          }
           umma_commit(&empty_bar[gp % kPfStages]);
         }
+        ++ic0;
+        if (two) ++ic1;
       }
     }
   } else {
@@ -241,6 +251,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
       const int kvh = w % p.n_kv, rb = it[0], nr = it[1], vb = it[2], nv = it[3], pbase = it[4];
       const int r0 = t * rows_per_tile;                       // first block row of this tile
       const int nr_t = max(0, min(rows_per_tile, nr - r0));   // rows of this tile
+      if (nr_t == 0) continue;  // tile unused by this item (the MMA warp skips it too)
       const int M = nr_t * G;
       if (wg_tid < nr_t) {
         const int rid = p.blk_rows[rb + r0 + wg_tid];

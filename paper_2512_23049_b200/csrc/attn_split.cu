@@ -206,12 +206,16 @@ __device__ __forceinline__ void ldsm_x4_trans(uint32_t& r0, uint32_t& r1, uint32
                : "r"(smem_u32(ptr)));
 }
 
-// Per-item state shared by the warps of a CTA.
+// Per-item state shared by the warps of a CTA.  Page descriptors of the item are
+// pg[j], pl[j], po[j] for j < nv (global vis arrays offset by vb, or a fat record in smem).
 struct ItemCtx {
   int kvh, vb, nv, pbase, M, G;
   int n_heads, n_kv, n_pages, page_size, layer;
   const int* s_rid;
   const int* s_rt;
+  const int* pg;
+  const int* pl;
+  const int* po;
 };
 
 // One work item on one KV head.  MT = m16 query tiles (G*rows <= 16*MT); the KW = 4/MT
@@ -235,7 +239,7 @@ __device__ __forceinline__ void mma_item(const SplitParams& p, const ItemCtx& c,
 
   auto load_page = [&](int stage, int pi) {
     if (pi < c.vb + c.nv) {
-      const int page = p.vis_page[pi], len = p.vis_len[pi];
+      const int page = c.pg[pi - c.vb], len = c.pl[pi - c.vb];
       const int64_t base = pool_off(c.layer, c.kvh, page, 0, c.n_kv, c.n_pages, c.page_size, HD);
       constexpr int CH = HD / 8;
 #pragma unroll 4
@@ -283,7 +287,7 @@ __device__ __forceinline__ void mma_item(const SplitParams& p, const ItemCtx& c,
     load_page(stage ^ 1, pi + 1);  // prefetch next page into the other buffer
     cp_async_wait<1>();
     __syncthreads();
-    const int len = p.vis_len[pi], own = p.vis_own[pi];
+    const int len = c.pl[pi - c.vb], own = c.po[pi - c.vb];
     const __nv_bfloat16* Kt = Ks + stage * kPage * LD;
     const __nv_bfloat16* Vt = Vs + stage * kPage * LD;
 #pragma unroll
@@ -470,11 +474,131 @@ __global__ void __launch_bounds__(kMmaThreads, 3) attn_split_mma(SplitParams p) 
     }
     __syncthreads();
     ItemCtx c{w % p.n_kv, it[2], it[3], it[4], nr * G, G, p.n_heads, p.n_kv, p.n_pages,
-              p.page_size, p.layer, s_rid, s_rt};
+              p.page_size, p.layer, s_rid, s_rt, p.vis_page + it[2], p.vis_len + it[2],
+              p.vis_own + it[2]};
     if (c.M <= 16) mma_item<HD, 1>(p, c, Ks, Vs, red);
     else if (c.M <= 32) mma_item<HD, 2>(p, c, Ks, Vs, red);
     else mma_item<HD, 4>(p, c, Ks, Vs, red);
   }
+}
+
+// ============================================================ fused decode (fat items)
+// Same math as attn_split_mma, for decode-sized steps: each CTA loads one self-contained
+// 256-byte item record (K3 "fat" item) instead of chasing rows / row_t / page descriptors,
+// and the LSE combine is fused: after writing its partials a CTA bumps an arrival counter
+// per (row, kv head); the CTA that completes a row's count merges that row's partials for
+// the G query heads of the KV head and writes the final bf16 (hi/lo) output row.
+constexpr int kFatInts = 64;
+
+struct DecodeParams {
+  SplitParams sp;
+  const int32_t* fat;
+  const int32_t* row_part_off;
+  const int32_t* row_part;
+  int32_t* counters;  // [n_rows * n_kv], zero between launches (finalisers reset them)
+  __nv_bfloat16* out;
+  int out_split, n_rows;
+};
+
+template <int HD>
+__device__ void finalize_row(const DecodeParams& d, int rid, int kvh, int G) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = d.row_part_off[rid], e = d.row_part_off[rid + 1];
+  const int H = d.sp.n_heads;
+  const bool active = 4 * lane < HD;
+  for (int j = warp; j < G; j += 4) {
+    const int h = kvh * G + j;
+    float mx = -INFINITY;
+    for (int i = b + lane; i < e; i += 32) mx = fmaxf(mx, d.sp.part_lse[(int64_t)d.row_part[i] * H + h]);
+    mx = warp_max(mx);
+    float4 num = make_float4(0.f, 0.f, 0.f, 0.f);
+    float den = 0.f;
+    if (mx != -INFINITY) {
+      for (int i = b; i < e; ++i) {
+        const int pi = d.row_part[i];
+        const float l = d.sp.part_lse[(int64_t)pi * H + h];
+        if (l == -INFINITY) continue;
+        const float wgt = __expf(l - mx);
+        den += wgt;
+        if (active) {
+          const float4 o = *reinterpret_cast<const float4*>(d.sp.part_o + ((int64_t)pi * H + h) * HD + 4 * lane);
+          num.x += wgt * o.x;
+          num.y += wgt * o.y;
+          num.z += wgt * o.z;
+          num.w += wgt * o.w;
+        }
+      }
+    }
+    if (active) {
+      const float inv = den > 0.f ? 1.f / den : 0.f;
+      const float y[4] = {num.x * inv, num.y * inv, num.z * inv, num.w * inv};
+      const int64_t oi = ((int64_t)rid * H + h) * HD + 4 * lane;
+      uint32_t hv[2], lv[2];
+      for (int k = 0; k < 2; ++k) split2(y[2 * k], y[2 * k + 1], hv[k], lv[k]);
+      *reinterpret_cast<uint2*>(d.out + oi) = make_uint2(hv[0], hv[1]);
+      if (d.out_split)
+        *reinterpret_cast<uint2*>(d.out + (int64_t)d.n_rows * H * HD + oi) = make_uint2(lv[0], lv[1]);
+    }
+  }
+}
+
+template <int HD>
+__global__ void __launch_bounds__(kMmaThreads, 3) decode_attn_fused(DecodeParams d) {
+  constexpr int LD = HD + 8;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(smem_raw);
+  __nv_bfloat16* Vs = Ks + kStages * kPage * LD;
+  float* red = reinterpret_cast<float*>(smem_raw);
+  __shared__ int s_fat[kFatInts];
+  __shared__ int s_last[16];
+  const SplitParams& p = d.sp;
+  const int tid = threadIdx.x;
+  const int G = p.n_heads / p.n_kv;
+  const int n_work = p.counts[1] * p.n_kv;
+  for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+    const int kvh = w % p.n_kv;
+    __syncthreads();  // previous item fully done with smem
+    if (tid < kFatInts) s_fat[tid] = d.fat[(int64_t)(w / p.n_kv) * kFatInts + tid];
+    __syncthreads();
+    const int nr = s_fat[0];
+    ItemCtx c{kvh, 0, s_fat[1], s_fat[2], nr * G, G, p.n_heads, p.n_kv, p.n_pages, p.page_size,
+              p.layer, s_fat + 4, s_fat + 20, s_fat + 36, s_fat + 44, s_fat + 52};
+    if (c.M <= 16) mma_item<HD, 1>(p, c, Ks, Vs, red);
+    else if (c.M <= 32) mma_item<HD, 2>(p, c, Ks, Vs, red);
+    else mma_item<HD, 4>(p, c, Ks, Vs, red);
+    // ---- fused combine: arrival counters per (row, kv head) ----
+    __threadfence();
+    __syncthreads();
+    if (tid < nr) {
+      const int rid = s_fat[4 + tid];
+      const int total = d.row_part_off[rid + 1] - d.row_part_off[rid];
+      const int old = atomicAdd(&d.counters[rid * p.n_kv + kvh], 1);
+      s_last[tid] = (old == total - 1);
+    }
+    __syncthreads();
+    for (int r = 0; r < nr; ++r) {
+      if (!s_last[r]) continue;
+      __threadfence();
+      const int rid = s_fat[4 + r];
+      finalize_row<HD>(d, rid, kvh, G);
+      if (tid == 0) d.counters[rid * p.n_kv + kvh] = 0;
+    }
+  }
+}
+
+template <int HD>
+static int launch_decode(const DecodeParams& d, int grid, cudaStream_t s) {
+  constexpr int LD = HD + 8;
+  const size_t pages = sizeof(__nv_bfloat16) * 2 * kStages * kPage * LD;
+  const size_t merge = sizeof(float) * 4 * (16 * HD + 32);
+  const size_t smem = pages > merge ? pages : merge;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(decode_attn_fused<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set = true;
+  }
+  decode_attn_fused<HD><<<grid, kMmaThreads, smem, s>>>(d);
+  return launch_status("choreo_decode_attn");
 }
 
 // ============================================================ combine
@@ -634,6 +758,29 @@ int choreo_attn_split(const float* q, const void* k_pool, const void* v_pool, in
   if (mma) return head_dim == 128 ? launch_mma<128>(p, grid, s) : launch_mma<64>(p, grid, s);
   return pool_dtype == CHOREO_BF16 ? dispatch_simt<__nv_bfloat16>(head_dim, p, grid, s)
                                    : dispatch_simt<float>(head_dim, p, grid, s);
+}
+
+int choreo_decode_attn(const float* q, const void* k_pool, const void* v_pool, int layer, int n_kv,
+                       int n_pages, int page_size, int n_heads, int head_dim,
+                       const int32_t* fat_items, const int32_t* counts, int max_items,
+                       const int32_t* row_part_off, const int32_t* row_part, float* part_o,
+                       float* part_lse, int32_t* row_counters, void* out, int out_split,
+                       int n_rows, int flags, int grid_ctas, void* stream) {
+  if (!q || !k_pool || !v_pool || !fat_items || !counts || !row_part_off || !row_part ||
+      !part_o || !part_lse || !row_counters || !out || n_kv <= 0 || n_heads % n_kv)
+    return CHOREO_EINVAL;
+  if (page_size != kPage || (head_dim != 64 && head_dim != 128) || (n_heads / n_kv) * 16 > 64 * 16)
+    return CHOREO_EUNSUPPORTED;
+  if (max_items <= 0) return CHOREO_OK;
+  DecodeParams d{{q, k_pool, v_pool, layer, n_kv, n_pages, page_size, n_heads, nullptr, nullptr,
+                  nullptr, nullptr, nullptr, nullptr, counts, part_o, part_lse,
+                  1.0f / sqrtf((float)head_dim), (flags & 1) ? 1 : 0, (flags & 2) ? 1 : 0},
+                 fat_items, row_part_off, row_part, row_counters,
+                 reinterpret_cast<__nv_bfloat16*>(out), out_split, n_rows};
+  int grid = grid_ctas > 0 ? grid_ctas : max_items * n_kv;
+  if (grid > 148 * 3) grid = 148 * 3;
+  auto s = as_stream(stream);
+  return head_dim == 128 ? launch_decode<128>(d, grid, s) : launch_decode<64>(d, grid, s);
 }
 
 int choreo_attn_combine(const float* part_o, const float* part_lse, const int32_t* row_part_off,

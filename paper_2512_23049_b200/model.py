@@ -142,6 +142,7 @@ class Runner:
         # launching stream and (start, end, algorithmic_bytes) tuples are appended.
         self.attn_events = None
         self.step_events = None  # when a list: (start, end) events around each step's GPU work
+        self._counters = None  # fused decode arrival counters (zero between launches)
         # bf16 engines carry GEMM activations as hi/lo bf16 pairs (see choreo_b200.h)
         self.split = self.dt == torch.bfloat16 and split_activations
         # K5 tensor-core precision: bit0 Q hi/lo, bit1 P hi/lo (env override for studies)
@@ -202,8 +203,14 @@ class Runner:
         # most 512 partials per row for the combine
         # prefill-sized steps: per-call page lists (a row block already fills an M tile)
         mode = 1 if max(len(c.tokens) for c in plan.calls) >= 64 else 0
+        # decode-sized bf16 steps: fused K5 (fat items, in-kernel combine)
+        fused = (not use_k4 and mode == 0 and self.pool_dtc == nat.BF16 and P == 64
+                 and hd in (64, 128) and rpb <= 16
+                 and os.environ.get("CHOREO_FUSED_DECODE", "1") != "0")
         work = plan_counts(plan.calls, msg_len, P, rpb, 1, mode)
-        ppi = max(1, cdiv(work.item_pages * Hk, (2 if use_k4 else 4) * 148))
+        ppi = max(1, cdiv(work.item_pages * Hk, (2 if use_k4 else 3) * 148))
+        if fused:
+            ppi = min(ppi, 8)
         plan_ = plan_counts(plan.calls, msg_len, P, rpb, ppi, mode)
         while plan_.max_row_parts > 512:
             ppi *= 2
@@ -243,12 +250,15 @@ class Runner:
         row_part_off = torch.empty(R + 1, dtype=torch.int32, device=self.dev)
         row_part = torch.empty(max(n_parts, 1), dtype=torch.int32, device=self.dev)
         counts = torch.empty(4, dtype=torch.int32, device=self.dev)
+        fat = torch.empty(max(n_items, 1), 64, dtype=torch.int32, device=self.dev) if fused else None
+        if fused and (self._counters is None or self._counters.numel() < R * Hk):
+            self._counters = torch.zeros(max(R * Hk, 1024), dtype=torch.int32, device=self.dev)
         nat.assemble(cache.msg_len.dev.data_ptr(), cache.msg_pt.dev.data_ptr(),
                      cache.page_table.dev.data_ptr(), calls_d.data_ptr(), parents_d.data_ptr(),
                      n_calls, rowt_d.data_ptr(), R, None, 0, P, rpb, ppi, vis[0].data_ptr(),
                      vis[1].data_ptr(), vis[2].data_ptr(), blk_rows.data_ptr(), items.data_ptr(),
                      row_part_off.data_ptr(), row_part.data_ptr(), counts.data_ptr(),
-                     plan_.n_vis, plan_.n_blk_rows, n_items, n_parts, mode, stream)
+                     plan_.n_vis, plan_.n_blk_rows, n_items, n_parts, mode, nat.ptr(fat), stream)
         self.launches += 1
         self.last_assembly = (vis, blk_rows, items, row_part_off, row_part, counts, plan_, rowt_d)
 
@@ -278,7 +288,13 @@ class Runner:
                 ev0 = torch.cuda.Event(enable_timing=True)
                 ev1 = torch.cuda.Event(enable_timing=True)
                 ev0.record()
-            if use_k4:
+            if fused:
+                nat.decode_attn(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(), layer,
+                                Hk, cache.n_pages, P, H, hd, fat.data_ptr(), counts.data_ptr(),
+                                n_items, row_part_off.data_ptr(), row_part.data_ptr(),
+                                part_o.data_ptr(), part_lse.data_ptr(), self._counters.data_ptr(),
+                                attn.data_ptr(), sp, R, self.attn_flags, 0, stream)
+            elif use_k4:
                 nat.prefill_attn(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(),
                                  self.pool_dtc, cfg.n_layers, layer, Hk, cache.n_pages, P, H, hd,
                                  rowt_d.data_ptr(), vis[0].data_ptr(), vis[1].data_ptr(),
@@ -296,7 +312,7 @@ class Runner:
             if self.attn_events is not None:
                 ev1.record()
                 self.attn_events.append((ev0, ev1, attn_bytes))
-            if not direct:
+            if not direct and not fused:
                 nat.attn_combine(part_o.data_ptr(), part_lse.data_ptr(), row_part_off.data_ptr(),
                                  row_part.data_ptr(), R, H, hd, attn.data_ptr(), self.dtc, sp,
                                  stream)

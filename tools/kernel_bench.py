@@ -39,18 +39,31 @@ def peaks() -> dict:
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback"}
 
 
-def _time(fn, reps=20, warm=3) -> float:
+def _time(fn, reps=20, warm=3, burst=None) -> float:
+    """Median per-launch time.  Launches are issued in bursts between one event pair so
+    the GPU never idles waiting for host-side submission (which would otherwise dominate
+    the event interval of a microsecond-scale kernel)."""
     s = torch.cuda.current_stream()
     for _ in range(warm):
         fn()
-    ts = []
-    for _ in range(reps):
+    torch.cuda.synchronize()
+    if burst is None:
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(s)
         fn()
         b.record(s)
         torch.cuda.synchronize()
-        ts.append(a.elapsed_time(b) / 1e3)
+        burst = max(1, min(64, int(2e-3 / max(a.elapsed_time(b) / 1e3, 1e-6))))
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(2_000_000)  # ~1 ms of GPU work so the burst is queued behind it
+        a.record(s)
+        for _ in range(burst):
+            fn()
+        b.record(s)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) / 1e3 / burst)
     return statistics.median(ts)
 
 
@@ -86,7 +99,8 @@ def _assemble(cache, calls, rpb, ppi, mode=0):
                 items=torch.empty(plan.n_items, 6, dtype=torch.int32, device="cuda"),
                 rpo=torch.empty(R + 1, dtype=torch.int32, device="cuda"),
                 rp=torch.empty(plan.n_parts, dtype=torch.int32, device="cuda"),
-                counts=torch.empty(4, dtype=torch.int32, device="cuda"), rt=rt_d)
+                counts=torch.empty(4, dtype=torch.int32, device="cuda"), rt=rt_d,
+                fat=torch.empty(max(plan.n_items, 1), 64, dtype=torch.int32, device="cuda"))
     v = bufs["vis"]
     nat.assemble(cache.msg_len.dev.data_ptr(), cache.msg_pt.dev.data_ptr(),
                  cache.page_table.dev.data_ptr(), tab_d.data_ptr(), par_d.data_ptr(), len(calls),
@@ -94,7 +108,7 @@ def _assemble(cache, calls, rpb, ppi, mode=0):
                  v[2].data_ptr(), bufs["blk"].data_ptr(), bufs["items"].data_ptr(),
                  bufs["rpo"].data_ptr(), bufs["rp"].data_ptr(), bufs["counts"].data_ptr(),
                  plan.n_vis, plan.n_blk_rows, plan.n_items, plan.n_parts, mode,
-                 torch.cuda.current_stream().cuda_stream)
+                 bufs["fat"].data_ptr(), torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     assert int(bufs["counts"][3]) == 0
     return plan, bufs, R
@@ -176,7 +190,7 @@ def k4_prefill(n_msgs: int = 8, rows: int = 1024, n_par: int = 24) -> dict:
             "items": plan.n_items}
 
 
-def k5_decode(n_workflows: int = 1, agents: int = 8) -> dict:
+def k5_decode(n_workflows: int = 1, agents: int = 8, tc: bool = False, fused: bool = True) -> dict:
     """One decode step of C3 round 2 (agents see sys, q and the other agents' replies)."""
     cfg = LLAMA_3_1_8B
     H, Hk, hd = cfg.n_heads, cfg.kv_heads, cfg.head_dim
@@ -197,10 +211,14 @@ def k5_decode(n_workflows: int = 1, agents: int = 8) -> dict:
     cache.k_pool.normal_()
     cache.v_pool.normal_()
     G = H // Hk
-    rpb = max(1, min(16, 64 // G))
+    rpb = 256 // G if tc else max(1, min(16, 64 // G))
     work = plan_counts([CallRows(c[0], c[1], c[2], [0], None, None, 0) for c in calls],
                        cache.msg_len.host, 64, rpb, 1)
-    ppi = max(1, cdiv(work.item_pages * Hk, 4 * 148))
+    ppi = max(1, cdiv(work.item_pages * Hk, (1 if tc else 3) * 148))
+    ppi = int(os.environ.get("K5_PPI", ppi))
+    fused = fused and not tc
+    if fused:
+        ppi = min(ppi, 8)
     plan, b, R = _assemble(cache, calls, rpb, ppi)
     q = torch.randn(R, H, hd, device="cuda")
     po = torch.empty(plan.n_parts, H, hd, device="cuda")
@@ -209,39 +227,73 @@ def k5_decode(n_workflows: int = 1, agents: int = 8) -> dict:
     v = b["vis"]
     stream = torch.cuda.current_stream().cuda_stream
 
+    counters = torch.zeros(R * Hk + 1024, dtype=torch.int32, device="cuda")
+
     def run():
+        if fused:
+            nat.decode_attn(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(), 0, Hk,
+                            cache.n_pages, 64, H, hd, b["fat"].data_ptr(), b["counts"].data_ptr(),
+                            plan.n_items, b["rpo"].data_ptr(), b["rp"].data_ptr(), po.data_ptr(),
+                            pl.data_ptr(), counters.data_ptr(), out.data_ptr(), 1, R,
+                            int(os.environ.get("CHOREO_ATTN_FLAGS", "3")), 0, stream)
+            return
+        if tc:
+            nat.prefill_attn(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(),
+                             nat.BF16, cfg.n_layers, 0, Hk, cache.n_pages, 64, H, hd,
+                             b["rt"].data_ptr(), v[0].data_ptr(), v[1].data_ptr(), v[2].data_ptr(),
+                             b["blk"].data_ptr(), b["items"].data_ptr(), b["counts"].data_ptr(),
+                             plan.n_items, po.data_ptr(), pl.data_ptr(), 0, None, 0, R, stream)
+            return
         nat.attn_split(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(), nat.BF16, 0,
                        Hk, cache.n_pages, 64, H, hd, b["rt"].data_ptr(), v[0].data_ptr(),
                        v[1].data_ptr(), v[2].data_ptr(), b["blk"].data_ptr(), b["items"].data_ptr(),
-                       b["counts"].data_ptr(), plan.n_items, po.data_ptr(), pl.data_ptr(), 0, 3,
-                       stream)
+                       b["counts"].data_ptr(), plan.n_items, po.data_ptr(), pl.data_ptr(), 0,
+                       int(os.environ.get("CHOREO_ATTN_FLAGS", "3")), stream)
 
     def run_comb():
         nat.attn_combine(po.data_ptr(), pl.data_ptr(), b["rpo"].data_ptr(), b["rp"].data_ptr(), R,
                          H, hd, out.data_ptr(), nat.BF16, 1, stream)
     t = _time(run)
-    tc = _time(run_comb)
+    tcomb = 0.0 if fused else _time(run_comb)
     uniq = sum(cache.message_length(m) for m in set(p for c in calls for p in c[1]))
     uniq += sum(c[2] + 1 for c in calls)
     nbytes = 2 * uniq * Hk * hd * 2 + R * H * hd * 4 + plan.n_parts * H * (hd + 1) * 4
     logical = sum(sum(cache.message_length(p) for p in c[1]) + c[2] + 1 for c in calls) * Hk * hd * 4
     pk = peaks()
     ach = nbytes / t / 1e9
-    return {"kernel": "choreo_attn_split (K5, page-centric decode)", "bound": "hbm",
+    return {"kernel": ("choreo_prefill_attn on decode items (tcgen05)" if tc else
+                       "choreo_decode_attn (K5 fused, page-centric)" if fused
+                       else "choreo_attn_split (K5, page-centric decode)"), "bound": "hbm",
             "work": f"{n_workflows} workflow(s) x {agents} agents, 1 layer",
             "algorithmic_bytes": nbytes, "logical_kv_bytes": logical, "us": round(t * 1e6, 2),
-            "combine_us": round(tc * 1e6, 2), "achieved": round(ach, 1), "unit": "GB/s",
+            "combine_us": round(tcomb * 1e6, 2), "fused_combine": fused, "achieved": round(ach, 1),
+            "unit": "GB/s",
             "peak": pk["hbm_gbs"], "frac": round(ach / pk["hbm_gbs"], 4), "items": plan.n_items,
             "pages_per_item": ppi}
 
 
+def k5_sweep() -> list:
+    out = []
+    for tc in (False, True):
+        for ppi in (1, 2, 3, 4, 6, 8):
+            os.environ["K5_PPI"] = str(ppi)
+            r = k5_decode(1, tc=tc)
+            out.append((tc, ppi, r["us"], r["combine_us"], r["items"]))
+    os.environ.pop("K5_PPI")
+    return out
+
+
 def run_all() -> list:
-    out = [k2_rerotate(), k4_prefill(), k5_decode(1), k5_decode(8)]
+    out = [k2_rerotate(), k4_prefill(), k5_decode(1), k5_decode(8), k5_decode(1, fused=False),
+           k5_decode(8, fused=False)]
     torch.cuda.empty_cache()
     return out
 
 
 if __name__ == "__main__":
+    if "--k5-sweep" in sys.argv:
+        print(k5_sweep())
+        sys.exit(0)
     res = run_all()
     if "--json" in sys.argv:
         print(json.dumps(res))
