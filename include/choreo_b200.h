@@ -170,6 +170,7 @@ int choreo_prefill_attn(const float* q, const void* k_pool, const void* v_pool, 
  * the LSE combine fused in: each (row, kv head) has an arrival counter in row_counters
  * (int32 [n_rows * n_kv], all zero on entry, left zero on exit); the CTA that delivers a
  * row's last partial merges them and writes out[row] (bf16, hi/lo pair if out_split).
+ * row_counters == NULL: partials only (run choreo_attn_combine afterwards).
  * flags as choreo_attn_split.  Replaces model.py:177-184 for decode-sized steps. */
 int choreo_decode_attn(const float* q, const void* k_pool, const void* v_pool, int layer, int n_kv,
                        int n_pages, int page_size, int n_heads, int head_dim,

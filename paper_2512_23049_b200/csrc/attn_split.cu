@@ -328,23 +328,38 @@ __device__ __forceinline__ void mma_item(const SplitParams& p, const ItemCtx& c,
       tA = fmaxf(tA, __shfl_xor_sync(0xffffffffu, tA, 2));
       tB = fmaxf(tB, __shfl_xor_sync(0xffffffffu, tB, 1));
       tB = fmaxf(tB, __shfl_xor_sync(0xffffffffu, tB, 2));
-      const float nA = fmaxf(mA, tA), nB = fmaxf(mB, tB);
-      const float aA = nA == -INFINITY ? 1.f : exp2f(mA - nA);
-      const float aB = nB == -INFINITY ? 1.f : exp2f(mB - nB);
+      // lazy rescale: keep the running max unless it grows by more than 8 (log2 units),
+      // so the O accumulators are rescaled only rarely (warp-uniform decision)
+      float aA = 1.f, aB = 1.f;
+      if (tA > mA + 8.f || (mA == -INFINITY && tA != -INFINITY)) {
+        aA = mA == -INFINITY ? 0.f : exp2f(mA - tA);
+        mA = tA;
+      }
+      if (tB > mB + 8.f || (mB == -INFINITY && tB != -INFINITY)) {
+        aB = mB == -INFINITY ? 0.f : exp2f(mB - tB);
+        mB = tB;
+      }
       float sumA = 0.f, sumB = 0.f;
 #pragma unroll
       for (int j = 0; j < 2; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          s[j][e] = s[j][e] == -INFINITY ? 0.f : exp2f(s[j][e] - nA);
-          s[j][2 + e] = s[j][2 + e] == -INFINITY ? 0.f : exp2f(s[j][2 + e] - nB);
+          s[j][e] = s[j][e] == -INFINITY ? 0.f : exp2f(s[j][e] - mA);
+          s[j][2 + e] = s[j][2 + e] == -INFINITY ? 0.f : exp2f(s[j][2 + e] - mB);
           sumA += s[j][e];
           sumB += s[j][2 + e];
         }
       lA = lA * aA + sumA;
       lB = lB * aB + sumB;
-      mA = nA;
-      mB = nB;
+      if (__any_sync(0xffffffffu, aA != 1.f || aB != 1.f)) {
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          o[n][0] *= aA;
+          o[n][1] *= aA;
+          o[n][2] *= aB;
+          o[n][3] *= aB;
+        }
+      }
       uint32_t ph[4], pl[4];
       split2(s[0][0], s[0][1], ph[0], pl[0]);
       split2(s[0][2], s[0][3], ph[1], pl[1]);
@@ -354,14 +369,6 @@ __device__ __forceinline__ void mma_item(const SplitParams& p, const ItemCtx& c,
       const __nv_bfloat16* vrow = Vt + (k0 + (mi & 1) * 8 + (lane & 7)) * LD + (mi >> 1) * 8;
 #pragma unroll
       for (int n = 0; n < NT; n += 2) {
-        o[n][0] *= aA;
-        o[n][1] *= aA;
-        o[n][2] *= aB;
-        o[n][3] *= aB;
-        o[n + 1][0] *= aA;
-        o[n + 1][1] *= aA;
-        o[n + 1][2] *= aB;
-        o[n + 1][3] *= aB;
         uint32_t b0, b1, b2, b3;
         ldsm_x4_trans(b0, b1, b2, b3, vrow + n * 8);
         mma16816(o[n], ph, b0, b1);
@@ -567,6 +574,7 @@ __global__ void __launch_bounds__(kMmaThreads, 3) decode_attn_fused(DecodeParams
     else if (c.M <= 32) mma_item<HD, 2>(p, c, Ks, Vs, red);
     else mma_item<HD, 4>(p, c, Ks, Vs, red);
     // ---- fused combine: arrival counters per (row, kv head) ----
+    if (!d.counters) continue;  // caller runs choreo_attn_combine instead
     __threadfence();
     __syncthreads();
     if (tid < nr) {
@@ -767,7 +775,7 @@ int choreo_decode_attn(const float* q, const void* k_pool, const void* v_pool, i
                        float* part_lse, int32_t* row_counters, void* out, int out_split,
                        int n_rows, int flags, int grid_ctas, void* stream) {
   if (!q || !k_pool || !v_pool || !fat_items || !counts || !row_part_off || !row_part ||
-      !part_o || !part_lse || !row_counters || !out || n_kv <= 0 || n_heads % n_kv)
+      !part_o || !part_lse || (row_counters && !out) || n_kv <= 0 || n_heads % n_kv)
     return CHOREO_EINVAL;
   if (page_size != kPage || (head_dim != 64 && head_dim != 128) || (n_heads / n_kv) * 16 > 64 * 16)
     return CHOREO_EUNSUPPORTED;

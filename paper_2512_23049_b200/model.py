@@ -143,6 +143,9 @@ class Runner:
         self.attn_events = None
         self.step_events = None  # when a list: (start, end) events around each step's GPU work
         self._counters = None  # fused decode arrival counters (zero between launches)
+        # in-kernel LSE combine (arrival counters) vs the separate combine kernel; the
+        # separate kernel is faster today (the in-kernel finaliser runs serially in the tail)
+        self.fused_combine = os.environ.get("CHOREO_FUSED_COMBINE", "0") == "1"
         # bf16 engines carry GEMM activations as hi/lo bf16 pairs (see choreo_b200.h)
         self.split = self.dt == torch.bfloat16 and split_activations
         # K5 tensor-core precision: bit0 Q hi/lo, bit1 P hi/lo (env override for studies)
@@ -209,9 +212,13 @@ class Runner:
                  and os.environ.get("CHOREO_FUSED_DECODE", "1") != "0")
         work = plan_counts(plan.calls, msg_len, P, rpb, 1, mode)
         ppi = max(1, cdiv(work.item_pages * Hk, (2 if use_k4 else 3) * 148))
-        if fused:
-            ppi = min(ppi, 8)
         plan_ = plan_counts(plan.calls, msg_len, P, rpb, ppi, mode)
+        if fused:
+            # one wave of resident CTAs (3 per SM): a second item on a few CTAs would
+            # double the kernel's length
+            while plan_.n_items * Hk > 3 * 148 and ppi < 8:
+                ppi += 1
+                plan_ = plan_counts(plan.calls, msg_len, P, rpb, ppi, mode)
         while plan_.max_row_parts > 512:
             ppi *= 2
             plan_ = plan_counts(plan.calls, msg_len, P, rpb, ppi, mode)
@@ -292,7 +299,8 @@ class Runner:
                 nat.decode_attn(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(), layer,
                                 Hk, cache.n_pages, P, H, hd, fat.data_ptr(), counts.data_ptr(),
                                 n_items, row_part_off.data_ptr(), row_part.data_ptr(),
-                                part_o.data_ptr(), part_lse.data_ptr(), self._counters.data_ptr(),
+                                part_o.data_ptr(), part_lse.data_ptr(),
+                                self._counters.data_ptr() if self.fused_combine else None,
                                 attn.data_ptr(), sp, R, self.attn_flags, 0, stream)
             elif use_k4:
                 nat.prefill_attn(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(),
@@ -312,7 +320,7 @@ class Runner:
             if self.attn_events is not None:
                 ev1.record()
                 self.attn_events.append((ev0, ev1, attn_bytes))
-            if not direct and not fused:
+            if not direct and not (fused and self.fused_combine):
                 nat.attn_combine(part_o.data_ptr(), part_lse.data_ptr(), row_part_off.data_ptr(),
                                  row_part.data_ptr(), R, H, hd, attn.data_ptr(), self.dtc, sp,
                                  stream)

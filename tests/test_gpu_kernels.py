@@ -395,8 +395,9 @@ def test_fused_decode_matches_dense_reference(hd, H, Hk):
         off += len(ts)
     dev = lambda a: torch.tensor(a, dtype=torch.int32, device="cuda")  # noqa: E731
     pl_ = out["plan"]
+    tab_d, par_d = dev(tab), dev(par + [0])  # keep alive until the kernel ran
     nat.assemble(cache.msg_len.dev.data_ptr(), cache.msg_pt.dev.data_ptr(),
-                 cache.page_table.dev.data_ptr(), dev(tab).data_ptr(), dev(par + [0]).data_ptr(),
+                 cache.page_table.dev.data_ptr(), tab_d.data_ptr(), par_d.data_ptr(),
                  len(calls), rt_d.data_ptr(), R, None, 0, 64, rpb, 2, vis[0].data_ptr(),
                  vis[1].data_ptr(), vis[2].data_ptr(), blk.data_ptr(), items.data_ptr(),
                  rpo.data_ptr(), rp.data_ptr(), counts.data_ptr(), pl_.n_vis, pl_.n_blk_rows,

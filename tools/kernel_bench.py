@@ -217,8 +217,10 @@ def k5_decode(n_workflows: int = 1, agents: int = 8, tc: bool = False, fused: bo
     ppi = max(1, cdiv(work.item_pages * Hk, (1 if tc else 3) * 148))
     ppi = int(os.environ.get("K5_PPI", ppi))
     fused = fused and not tc
-    if fused:
-        ppi = min(ppi, 8)
+    if fused and "K5_PPI" not in os.environ:  # same one-wave fit as the runner
+        while plan_counts([CallRows(c[0], c[1], c[2], [0], None, None, 0) for c in calls],
+                          cache.msg_len.host, 64, rpb, ppi).n_items * Hk > 3 * 148 and ppi < 8:
+            ppi += 1
     plan, b, R = _assemble(cache, calls, rpb, ppi)
     q = torch.randn(R, H, hd, device="cuda")
     po = torch.empty(plan.n_parts, H, hd, device="cuda")
@@ -228,13 +230,15 @@ def k5_decode(n_workflows: int = 1, agents: int = 8, tc: bool = False, fused: bo
     stream = torch.cuda.current_stream().cuda_stream
 
     counters = torch.zeros(R * Hk + 1024, dtype=torch.int32, device="cuda")
+    in_kernel_combine = os.environ.get("K5_FUSED_COMBINE", "1") == "1"
 
     def run():
         if fused:
             nat.decode_attn(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(), 0, Hk,
                             cache.n_pages, 64, H, hd, b["fat"].data_ptr(), b["counts"].data_ptr(),
                             plan.n_items, b["rpo"].data_ptr(), b["rp"].data_ptr(), po.data_ptr(),
-                            pl.data_ptr(), counters.data_ptr(), out.data_ptr(), 1, R,
+                            pl.data_ptr(), counters.data_ptr() if in_kernel_combine else None,
+                            out.data_ptr(), 1, R,
                             int(os.environ.get("CHOREO_ATTN_FLAGS", "3")), 0, stream)
             return
         if tc:
@@ -254,7 +258,7 @@ def k5_decode(n_workflows: int = 1, agents: int = 8, tc: bool = False, fused: bo
         nat.attn_combine(po.data_ptr(), pl.data_ptr(), b["rpo"].data_ptr(), b["rp"].data_ptr(), R,
                          H, hd, out.data_ptr(), nat.BF16, 1, stream)
     t = _time(run)
-    tcomb = 0.0 if fused else _time(run_comb)
+    tcomb = 0.0 if (fused and in_kernel_combine) else _time(run_comb)
     uniq = sum(cache.message_length(m) for m in set(p for c in calls for p in c[1]))
     uniq += sum(c[2] + 1 for c in calls)
     nbytes = 2 * uniq * Hk * hd * 2 + R * H * hd * 4 + plan.n_parts * H * (hd + 1) * 4
