@@ -77,41 +77,54 @@ struct Vec16<float> {
   static constexpr int N = 4;
 };
 
-template <typename T>
-__global__ void rerotate_kernel(T* __restrict__ kp, int n_layers, int n_kv, int n_pages,
-                                int page_size, int hd, const int32_t* __restrict__ pages,
-                                const int32_t* __restrict__ page_len,
-                                const int32_t* __restrict__ delta, int n_list,
-                                const float* __restrict__ cos_t, const float* __restrict__ sin_t,
-                                int max_delta) {
-  constexpr int N = Vec16<T>::N;
-  const int vpr = hd / N;  // vectors per token row
-  const int half = hd >> 1;
-  const int64_t per_page = (int64_t)page_size * vpr;
-  const int64_t total = (int64_t)n_layers * n_kv * n_list * per_page;
-  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total;
-       u += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t lhi = u / per_page;
-    const int in_page = (int)(u % per_page);
-    const int i = (int)(lhi % n_list);
-    const int lh = (int)(lhi / n_list);
-    const int slot = in_page / vpr;
-    const int vec = in_page % vpr;
-    const int dl = delta[i];
-    if (dl == 0 || slot >= page_len[i]) continue;
-    const int layer = lh / n_kv, h = lh % n_kv;
-    T* p = kp + pool_off(layer, h, pages[i], slot, n_kv, n_pages, page_size, hd) + vec * N;
-    uint4 raw = *reinterpret_cast<const uint4*>(p);
-    T* x = reinterpret_cast<T*>(&raw);
-    const int64_t trow = (int64_t)(dl + max_delta) * half + vec * (N / 2);
+// One CTA per (layer, kv head, listed page): the page's valid rows are one contiguous
+// [len][hd] chunk, so the CTA reads it with 16-byte vectors, VPT vectors per thread all
+// in flight before any is used, rotates in registers and writes back in place.  The cos/
+// sin row of the page's delta is staged in shared memory once per CTA.
+template <typename T, int VPT>
+__global__ void __launch_bounds__(256) rerotate_kernel(
+    T* __restrict__ kp, int n_kv, int n_pages, int page_size, int hd,
+    const int32_t* __restrict__ pages, const int32_t* __restrict__ page_len,
+    const int32_t* __restrict__ delta, int n_list, const float* __restrict__ cos_t,
+    const float* __restrict__ sin_t, int max_delta) {
+  constexpr int N = Vec16<T>::N;  // elements per 16-byte vector
+  extern __shared__ float cs[];   // [hd/2] cos then [hd/2] sin
+  const int i = blockIdx.x % n_list;
+  const int lh = blockIdx.x / n_list;
+  const int dl = delta[i];
+  if (dl == 0) return;
+  const int len = page_len[i], half = hd >> 1;
+  const int64_t trow = (int64_t)(dl + max_delta) * half;
+  for (int j = threadIdx.x; j < half; j += blockDim.x) {
+    cs[j] = cos_t[trow + j];
+    cs[half + j] = sin_t[trow + j];
+  }
+  __syncthreads();
+  const int layer = lh / n_kv, h = lh % n_kv;
+  T* base = kp + pool_off(layer, h, pages[i], 0, n_kv, n_pages, page_size, hd);
+  const int vpr = hd / N, nvec = len * vpr;
+  for (int v0 = threadIdx.x; v0 < nvec; v0 += blockDim.x * VPT) {
+    uint4 raw[VPT];
 #pragma unroll
-    for (int j = 0; j < N / 2; ++j) {
-      const float c = __ldg(cos_t + trow + j), s = __ldg(sin_t + trow + j);
-      const float e = to_f32(x[2 * j]), o = to_f32(x[2 * j + 1]);
-      x[2 * j] = from_f32<T>(e * c - o * s);
-      x[2 * j + 1] = from_f32<T>(e * s + o * c);
+    for (int u = 0; u < VPT; ++u) {
+      const int v = v0 + u * blockDim.x;
+      if (v < nvec) raw[u] = *reinterpret_cast<const uint4*>(base + (int64_t)v * N);
     }
-    *reinterpret_cast<uint4*>(p) = raw;
+#pragma unroll
+    for (int u = 0; u < VPT; ++u) {
+      const int v = v0 + u * blockDim.x;
+      if (v >= nvec) continue;
+      T* x = reinterpret_cast<T*>(&raw[u]);
+      const int p0 = (v % vpr) * (N / 2);
+#pragma unroll
+      for (int j = 0; j < N / 2; ++j) {
+        const float c = cs[p0 + j], sn = cs[half + p0 + j];
+        const float e = to_f32(x[2 * j]), o = to_f32(x[2 * j + 1]);
+        x[2 * j] = from_f32<T>(e * c - o * sn);
+        x[2 * j + 1] = from_f32<T>(e * sn + o * c);
+      }
+      *reinterpret_cast<uint4*>(base + (int64_t)v * N) = raw[u];
+    }
   }
 }
 
@@ -162,17 +175,18 @@ int choreo_rerotate(void* k_pool, int pool_dtype, int n_layers, int n_kv, int n_
   const int vec = pool_dtype == CHOREO_BF16 ? 8 : 4;
   if (head_dim % vec) return CHOREO_EINVAL;
   if (n_list == 0) return CHOREO_OK;
-  const int64_t total = (int64_t)n_layers * n_kv * n_list * page_size * (head_dim / vec);
-  const int blocks = grid_for(total, 256);
+  const int64_t blocks = (int64_t)n_layers * n_kv * n_list;
+  if (blocks > 0x7fffffff) return CHOREO_EUNSUPPORTED;
   auto s = as_stream(stream);
+  const size_t smem = sizeof(float) * head_dim;
   if (pool_dtype == CHOREO_BF16)
-    rerotate_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(
-        (__nv_bfloat16*)k_pool, n_layers, n_kv, n_pages, page_size, head_dim, pages, page_len,
-        delta, n_list, cos_t, sin_t, max_delta);
+    rerotate_kernel<__nv_bfloat16, 4><<<(int)blocks, 256, smem, s>>>(
+        (__nv_bfloat16*)k_pool, n_kv, n_pages, page_size, head_dim, pages, page_len, delta, n_list,
+        cos_t, sin_t, max_delta);
   else
-    rerotate_kernel<float><<<blocks, 256, 0, s>>>((float*)k_pool, n_layers, n_kv, n_pages,
-                                                  page_size, head_dim, pages, page_len, delta,
-                                                  n_list, cos_t, sin_t, max_delta);
+    rerotate_kernel<float, 4><<<(int)blocks, 256, smem, s>>>((float*)k_pool, n_kv, n_pages, page_size,
+                                                            head_dim, pages, page_len, delta, n_list,
+                                                            cos_t, sin_t, max_delta);
   return launch_status("choreo_rerotate");
 }
 
