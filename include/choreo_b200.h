@@ -192,9 +192,10 @@ int choreo_select_greedy(const float* logits, int n_rows, int ld, int vocab, int
 
 /* Diagnostics: one-CTA tcgen05 GEMM over the UMMA primitives K4 uses.
  * a: bf16 [128][64], b1: bf16 [64][64] (N x K), b2: bf16 [64][128] (K x N);
- * c1 = a * b1^T (f32 [128][64]), c2 = a * b2 (f32 [128][128]). */
+ * c1 = a * b1^T (f32 [128][64]), c2 = a * b2 (f32 [128][128]) with both operands in shared
+ * memory, c3 = a * b2 with a staged in tensor memory (A-from-TMEM MMA form). */
 int choreo_selftest_umma(const void* a, const void* b1, const void* b2, float* c1, float* c2,
-                         void* stream);
+                         float* c3, void* stream);
 
 #ifdef __cplusplus
 }

@@ -39,7 +39,7 @@ SIGNATURES: dict[str, list] = {
                             _P, _P, _I, _P, _P, _I, _P, _I, _I, _P],
     "choreo_attn_combine": [_P, _P, _P, _P, _I, _I, _I, _P, _I, _I, _P],
     "choreo_select_greedy": [_P, _I, _I, _I, _I, _P, _P],
-    "choreo_selftest_umma": [_P, _P, _P, _P, _P, _P],
+    "choreo_selftest_umma": [_P, _P, _P, _P, _P, _P, _P],
 }
 EXTRA = ["choreo_abi_version", "choreo_last_error"]
 

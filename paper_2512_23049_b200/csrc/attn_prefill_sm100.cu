@@ -54,7 +54,7 @@ struct PrefillParams {
   } while (0)
 
 constexpr int kPfThreads = 320;     // 10 warps: TMA, MMA, 2 x 4 softmax warps
-constexpr int kPfStages = 3;
+constexpr int kPfStages = 4;
 constexpr int kPfKeys = 64;         // keys per page / per S tile
 constexpr int kTileM = 128;         // query vectors per tile (TMEM lanes)
 constexpr float kRescaleTh = 8.f;   // lazy O rescale threshold (log2 units)
@@ -65,8 +65,7 @@ struct PfSmem {
   static constexpr int kQBytes = kTileM * 128 * kRegions;   // one tile's [128][HD] bf16
   static constexpr int kKVBytes = kPfKeys * 128 * kRegions; // one K (or V) page
   static constexpr int kStageBytes = 2 * kKVBytes;
-  static constexpr int kPBytes = kTileM * 128;              // [128][64 keys] bf16
-  static constexpr int kTotal = 2 * kQBytes + kPfStages * kStageBytes + 2 * kPBytes + 1024;
+  static constexpr int kTotal = 2 * kQBytes + kPfStages * kStageBytes + 1024;
 };
 
 __device__ __forceinline__ float ex2(float x) {
@@ -115,9 +114,8 @@ __global__ void __launch_bounds__(kPfThreads, 1)
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = base;                                  // [2][kQBytes]
   uint8_t* sKV = sQ + 2 * S::kQBytes;                  // [stages][K | V]
-  uint8_t* sP = sKV + kPfStages * S::kStageBytes;      // [2][kPBytes]
   __shared__ uint64_t full_bar[kPfStages], empty_bar[kPfStages];
-  __shared__ uint64_t s_full[2][2], s_free[2][2], p_full[2], o_done[2], q_full[2], o_free[2];
+  __shared__ uint64_t s_full[2][2], p_full[2], o_done[2], q_full[2], o_free[2];
   __shared__ uint32_t tmem_base;
   __shared__ int s_rid[2][kTileM], s_rt[2][kTileM];
 
@@ -131,10 +129,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
       mbar_init(&empty_bar[i], 1);
     }
     for (int t = 0; t < 2; ++t) {
-      for (int i = 0; i < 2; ++i) {
-        mbar_init(&s_full[t][i], 1);
-        mbar_init(&s_free[t][i], 128);
-      }
+      for (int i = 0; i < 2; ++i) mbar_init(&s_full[t][i], 1);
       mbar_init(&p_full[t], 128);
       mbar_init(&o_done[t], 1);
       mbar_init(&q_full[t], 128);
@@ -175,11 +170,13 @@ __global__ void __launch_bounds__(kPfThreads, 1)
     if (lane == 0) {
       constexpr uint32_t idS = umma_idesc_bf16(kTileM, kPfKeys, false);
       constexpr uint32_t idO = umma_idesc_bf16(kTileM, HD, true);
-      // g = global page index (K/V ring), gt = this tile's page index (its barriers)
+      // g = global page index (K/V ring), gt = this tile's page index (its barriers).
+      // S(gt) goes to TMEM buffer gt&1; the softmax overwrites it with P(gt) (bf16 pairs),
+      // which PV(gt) reads as its A operand.  The tensor pipe executes in issue order, so
+      // S(gt+2) (same buffer) is issued only after PV(gt) — no extra handshake needed.
       auto issue_s = [&](int t, uint32_t g, uint32_t gt) {
         const int st = g % kPfStages, b = gt & 1;
         if (t == 0) mbar_wait(&full_bar[st], (g / kPfStages) & 1);
-        mbar_wait(&s_free[t][b], ((gt >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t qaddr = smem_addr(sQ + t * S::kQBytes);
         const uint32_t kaddr = smem_addr(sKV + st * S::kStageBytes);
@@ -196,13 +193,12 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         mbar_wait(&p_full[t], gt & 1);
         tc_fence_after();
         const uint32_t vaddr = smem_addr(sKV + (g % kPfStages) * S::kStageBytes) + S::kKVBytes;
-        const uint32_t paddr = smem_addr(sP + t * S::kPBytes);
+        const uint32_t aP = tmem_base + 256 * t + 64 * (gt & 1);
         const uint32_t dO = tmem_base + 256 * t + 128;
 #pragma unroll
         for (int k = 0; k < kPfKeys / 16; ++k)
-          umma_bf16(dO, umma_desc_sw128(paddr + k * 32, 16, 1024),
-                    umma_desc_sw128(vaddr + k * 2048, kPfKeys * 128, 1024), idO,
-                    (!first || k > 0) ? 1u : 0u);
+          umma_bf16_tmem_a(dO, aP + k * 8, umma_desc_sw128(vaddr + k * 2048, kPfKeys * 128, 1024),
+                           idO, (!first || k > 0) ? 1u : 0u);
         umma_commit(&o_done[t]);
       };
       uint32_t gp = 0, g1 = 0, ic0 = 0, ic1 = 0;
@@ -244,7 +240,6 @@ __global__ void __launch_bounds__(kPfThreads, 1)
     const uint32_t tS = tmem_base + 256 * t, tO = tmem_base + 256 * t + 128;
     const int wg_tid = tid - 64 - 128 * t;  // 0..127
     uint8_t* myQ = sQ + t * S::kQBytes;
-    uint8_t* myP = sP + t * S::kPBytes;
     uint32_t gp = 0;
     for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
       const int32_t* it = p.items + 6 * (w / p.n_kv);
@@ -298,8 +293,6 @@ __global__ void __launch_bounds__(kPfThreads, 1)
 #pragma unroll
         for (int c = 0; c < kPfKeys / 16; ++c) tmem_ld16(tS + 64 * b + lane_off + c * 16, s + c * 16);
         tmem_wait_ld();
-        tc_fence_before();
-        mbar_arrive(&s_free[t][b]);
         int lim = valid ? len : 0;  // keys k < lim are visible (own pages: causal cut)
         if (own >= 0) lim = min(lim, my_t - own + 1);
         // warp-uniform fast path: a full page visible to every row of the warp (most parent
@@ -350,21 +343,20 @@ __global__ void __launch_bounds__(kPfThreads, 1)
           }
         }
         lrow = lrow * alpha + ((sm[0] + sm[1]) + (sm[2] + sm[3])) + ((sm[4] + sm[5]) + (sm[6] + sm[7]));
-        if (j > 0) mbar_wait(&o_done[t], (gp - 1) & 1);  // PV_t(g-1) done: O stable, P free
+        // P(g) -> TMEM over the consumed S buffer (bf16 pairs, 32 columns of this lane)
+        {
+          uint32_t pk[32];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          __nv_bfloat162 h0 = __floats2bfloat162_rn(s[8 * c], s[8 * c + 1]);
-          __nv_bfloat162 h1 = __floats2bfloat162_rn(s[8 * c + 2], s[8 * c + 3]);
-          __nv_bfloat162 h2 = __floats2bfloat162_rn(s[8 * c + 4], s[8 * c + 5]);
-          __nv_bfloat162 h3 = __floats2bfloat162_rn(s[8 * c + 6], s[8 * c + 7]);
-          uint4 u;
-          u.x = *reinterpret_cast<uint32_t*>(&h0);
-          u.y = *reinterpret_cast<uint32_t*>(&h1);
-          u.z = *reinterpret_cast<uint32_t*>(&h2);
-          u.w = *reinterpret_cast<uint32_t*>(&h3);
-          *reinterpret_cast<uint4*>(myP + sw128_offset(m, 8 * c)) = u;
+          for (int c = 0; c < 32; ++c) {
+            __nv_bfloat162 h = __floats2bfloat162_rn(s[2 * c], s[2 * c + 1]);
+            pk[c] = *reinterpret_cast<uint32_t*>(&h);
+          }
+          tmem_st16u(tS + 64 * b + lane_off, pk);
+          tmem_st16u(tS + 64 * b + lane_off + 16, pk + 16);
         }
+        // rescale the running O only when this warp's reference max moved (rare)
         if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+          mbar_wait(&o_done[t], (gp - 1) & 1);  // PV_t(g-1) done before touching O
           tc_fence_after();
 #pragma unroll
           for (int c = 0; c < HD / 16; ++c) {
@@ -375,13 +367,15 @@ __global__ void __launch_bounds__(kPfThreads, 1)
             for (int i = 0; i < 16; ++i) o[i] *= alpha;
             tmem_st16(tO + lane_off + c * 16, o);
           }
-          tmem_wait_st();
         }
-        fence_proxy_async_smem();
+        tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&p_full[t]);
       }
       // ---- epilogue: O / l -> partial, LSE (natural log) ----
+      // PV_t(last-1) and PV_t(last) may both be pending: a parity wait only tells the
+      // current phase from the previous one, so wait for them in order
+      if (nv >= 2) mbar_wait(&o_done[t], (gp - 2) & 1);
       mbar_wait(&o_done[t], (gp - 1) & 1);
       tc_fence_after();
       {
@@ -532,15 +526,6 @@ extern "C" int choreo_prefill_attn_dbg(const float* q, const void* k_pool, const
   const uint64_t rows = (uint64_t)n_layers * n_kv * n_pages * page_size;
   if (rows > 0x7fffffffull) return CHOREO_EUNSUPPORTED;
   auto s = as_stream(stream);
-  static int poly = -1;
-  if (poly < 0) {
-    const char* e = getenv("CHOREO_K4_POLY");
-    poly = e ? atoi(e) : 0;
-  }
-  if (head_dim == 64) return launch_prefill<64, 1>(p, k_pool, v_pool, rows, grid, s);
-  switch (poly) {
-    case 0: return launch_prefill<128, 0>(p, k_pool, v_pool, rows, grid, s);
-    case 2: return launch_prefill<128, 2>(p, k_pool, v_pool, rows, grid, s);
-    default: return launch_prefill<128, 1>(p, k_pool, v_pool, rows, grid, s);
-  }
-}
+  return head_dim == 128 ? launch_prefill<128, 0>(p, k_pool, v_pool, rows, grid, s)
+                         : launch_prefill<64, 0>(p, k_pool, v_pool, rows, grid, s);
+}}

@@ -295,9 +295,11 @@ def test_umma_selftest_tcgen05_descriptors():
     b2 = torch.randn(64, 128, device="cuda", generator=g).to(torch.bfloat16)
     c1 = torch.empty(128, 64, device="cuda")
     c2 = torch.empty(128, 128, device="cuda")
+    c3 = torch.empty(128, 128, device="cuda")
     nat.selftest_umma(a.data_ptr(), b1.data_ptr(), b2.data_ptr(), c1.data_ptr(), c2.data_ptr(),
-                      _stream())
+                      c3.data_ptr(), _stream())
     torch.cuda.synchronize()
+    torch.testing.assert_close(c3, a.float() @ b2.float(), rtol=1e-4, atol=1e-3)
     torch.testing.assert_close(c1, a.float() @ b1.float().t(), rtol=1e-4, atol=1e-3)
     torch.testing.assert_close(c2, a.float() @ b2.float(), rtol=1e-4, atol=1e-3)
 
