@@ -528,4 +528,4 @@ extern "C" int choreo_prefill_attn_dbg(const float* q, const void* k_pool, const
   auto s = as_stream(stream);
   return head_dim == 128 ? launch_prefill<128, 0>(p, k_pool, v_pool, rows, grid, s)
                          : launch_prefill<64, 0>(p, k_pool, v_pool, rows, grid, s);
-}}
+}
