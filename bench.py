@@ -260,6 +260,8 @@ def main() -> None:
     ap.add_argument("--rounds", type=int, default=3)
     ap.add_argument("--ref-tokens", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-kernels", action="store_true",
+                    help="skip the K2/K4/K5 kernel microbenchmarks (tools/kernel_bench.py)")
     ap.add_argument("--model", default="llama-3.1-8b")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -335,7 +337,8 @@ def main() -> None:
     roofline = None
     if a_ms:
         achieved = (sum(a_bytes) / len(a_bytes)) / (sum(a_ms) / len(a_ms) / 1e3) / 1e9
-        roofline = {"kernel": "choreo_attn_split (K5, decode split-KV)", "bound": "hbm",
+        roofline = {"kernel": "choreo_decode_attn (K5: page-centric split-KV decode attention)",
+                    "bound": "hbm",
                     "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                     "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": None,
                     "peak_source": peaks["source"],
@@ -347,6 +350,14 @@ def main() -> None:
         if world > 1:
             dist.destroy_process_group()
         return
+    kernels = None
+    if world == 1 and not args.no_kernels:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import kernel_bench as kb
+
+        del eng, weights
+        torch.cuda.empty_cache()
+        kernels = [kb.k2_rerotate(), kb.k4_prefill(), kb.k5_decode(1), kb.k5_decode(8)]
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_reference_sample(args.agents, args.ref_tokens)
@@ -370,6 +381,7 @@ def main() -> None:
         "gpu_launches": int(launches),
         "generated_tokens": int(generated_all),
         "roofline": roofline,
+        "kernel_rooflines": kernels,
         "cpu_baseline": cpu,
         "clocks": clocks.summary(),
     }

@@ -169,21 +169,26 @@ class Engine:
 
     def __init__(self, weights, *, capacity: int = 65536, seed: int = 0,
                  record_logits: bool = False, dtype=None, device=None, page_size: int = 64,
-                 split_activations: bool = True) -> None:
+                 split_activations: bool = True, tp=None, tp_group=None) -> None:
+        """tp / tp_group: KV-head tensor parallelism (parallel.TPLayout); weights must then
+        be this rank's shard (parallel.shard_weights or DeviceWeights.random(tp=...))."""
         nat.load()  # fail loudly without the CUDA extension
         device = torch.device(device or "cuda")
         if isinstance(weights, WeightSet):
             dtype = dtype or torch.bfloat16
             weights = DeviceWeights.from_host(weights, dtype=dtype, device=device)
         self.weights: DeviceWeights = weights
-        self.config: ModelConfig = weights.config
+        self.config: ModelConfig = tp.config if tp is not None else weights.config
+        self.tp, self.tp_group = tp, tp_group
         self.seed = int(seed)
         self.record_logits = record_logits
         self.device = device
-        self.cache = DeviceKvCache(self.config, capacity=capacity, dtype=weights.torch_dtype,
+        cache_cfg = tp.local_config() if tp is not None else self.config
+        self.cache = DeviceKvCache(cache_cfg, capacity=capacity, dtype=weights.torch_dtype,
                                    device=device, page_size=page_size)
         self.rotation = RotationTableDevice(self.config, device)
-        self._runner = Runner(self.weights, self.cache, self.rotation, split_activations)
+        self._runner = Runner(self.weights, self.cache, self.rotation, split_activations, tp,
+                              tp_group)
         self._generatable = generatable_mask(self.config.vocab_size)
         self._next_id = 0
         self.stats: list[CallStats] = []
@@ -224,7 +229,9 @@ class Engine:
         other.record_logits, other.device = self.record_logits, self.device
         other.cache = self.cache.clone()
         other.rotation = self.rotation
-        other._runner = Runner(self.weights, other.cache, self.rotation, self._runner.split)
+        other.tp, other.tp_group = self.tp, self.tp_group
+        other._runner = Runner(self.weights, other.cache, self.rotation, self._runner.split,
+                               self.tp, self.tp_group)
         other._generatable = self._generatable
         other._next_id = self._next_id
         other.stats = []

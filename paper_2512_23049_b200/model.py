@@ -125,11 +125,17 @@ class Runner:
     """Executes StepPlans for one (weights, cache) pair on the current stream."""
 
     def __init__(self, weights: DeviceWeights, cache: DeviceKvCache,
-                 rotation: RotationTableDevice, split_activations: bool = True) -> None:
+                 rotation: RotationTableDevice, split_activations: bool = True,
+                 tp=None, tp_group=None) -> None:
+        """tp: parallel.TPLayout for KV-head tensor parallelism (None = whole model here);
+        the partial o_proj / down_proj outputs are all-reduced over tp_group (NCCL)."""
         self.w = weights
         self.cache = cache
         self.rot = rotation
-        self.cfg = weights.config
+        self.tp, self.tp_group = tp, tp_group
+        # self.cfg: this rank's slice (heads, kv heads, ffn); self.d: the global model dim
+        self.cfg = tp.local_config() if tp is not None else weights.config
+        self.d = tp.model_dim if tp is not None else weights.config.model_dim
         self.dt = weights.torch_dtype
         self.dtc = nat.dtype_code(self.dt)
         self.pool_dtc = nat.dtype_code(cache.dtype)
@@ -177,7 +183,7 @@ class Runner:
         cfg, cache = self.cfg, self.cache
         stream = torch.cuda.current_stream(self.dev).cuda_stream
         R = plan.n_rows
-        H, Hk, hd, d = cfg.n_heads, cfg.kv_heads, cfg.head_dim, cfg.model_dim
+        H, Hk, hd, d = cfg.n_heads, cfg.kv_heads, cfg.head_dim, self.d
         P = cache.page_size
         cache.sync_tables()
 
@@ -325,6 +331,8 @@ class Runner:
                                  row_part.data_ptr(), R, H, hd, attn.data_ptr(), self.dtc, sp,
                                  stream)
             ao = self._mm(attn, lw["wo"], out_f32=True)
+            if self.tp is not None and self.tp.size > 1:  # row-parallel o_proj: sum partials
+                torch.distributed.all_reduce(ao, group=self.tp_group)
             nat.residual_rmsnorm(x.data_ptr(), ao.data_ptr(), nat.F32, sp,
                                  lw["ffn_norm"].data_ptr(), self.dtc, R, d, RMS_EPS, h.data_ptr(),
                                  self.dtc, sp, None, 0, stream)
@@ -332,6 +340,8 @@ class Runner:
             nat.silu_mul(gu.data_ptr(), nat.F32, sp, R, cfg.ffn_dim, act.data_ptr(), self.dtc, sp,
                          stream)
             delta = self._mm(act, lw["w_down"], out_f32=True)
+            if self.tp is not None and self.tp.size > 1:  # row-parallel down_proj
+                torch.distributed.all_reduce(delta, group=self.tp_group)
             launches += 6
         nat.residual_rmsnorm(x.data_ptr(), delta.data_ptr(), nat.F32, sp, None, 0, R, d, RMS_EPS,
                              None, 0, 0, None, 0, stream)

@@ -167,17 +167,22 @@ class DeviceWeights:
                                              "out_head": up(ws.out_head.T), "layers": layers})
 
     @classmethod
-    def random(cls, config: ModelConfig, dtype=None, device=None, seed: int | None = None
-               ) -> "DeviceWeights":
-        """Device-side scaled-uniform init (same bounds/order as init_weights, torch Philox)."""
+    def random(cls, config: ModelConfig, dtype=None, device=None, seed: int | None = None,
+               tp=None) -> "DeviceWeights":
+        """Device-side scaled-uniform init (same bounds/order as init_weights, torch Philox).
+
+        With tp (parallel.TPLayout) only this rank's slice is drawn (bounds use the full
+        fan-in/fan-out; slices of different ranks come from different generator streams)."""
         import torch
 
         dtype = dtype or torch.bfloat16
         device = torch.device(device or "cuda")
         gen = torch.Generator(device=device)
-        gen.manual_seed(config.seed if seed is None else seed)
+        gen.manual_seed((config.seed if seed is None else seed) + (1000 * tp.rank if tp else 0))
         d, dkv, f, v, hd = (config.model_dim, config.kv_dim, config.ffn_dim, config.vocab_size,
                             config.head_dim)
+        if tp is not None:
+            return cls._random_tp(config, tp, dtype, device, gen)
 
         def draw(fan_in, fan_out, shape):
             b = math.sqrt(6.0 / (fan_in + fan_out))
@@ -199,3 +204,27 @@ class DeviceWeights:
         out_head = draw(d, v, (v, d))
         return cls(config, dtype, device, {"embed": embed, "out_norm": ones, "out_head": out_head,
                                            "layers": layers})
+
+    @classmethod
+    def _random_tp(cls, config, tp, dtype, device, gen) -> "DeviceWeights":
+        import torch
+
+        d, dkv, f, v = config.model_dim, config.kv_dim, config.ffn_dim, config.vocab_size
+        hq, hkv, fl = tp.n_heads * config.head_dim, tp.kv_heads * config.head_dim, tp.ffn_dim
+
+        def draw(fan_in, fan_out, shape):
+            b = math.sqrt(6.0 / (fan_in + fan_out))
+            t = torch.empty(shape, device=device, dtype=torch.float32)
+            t.uniform_(-b, b, generator=gen)
+            return t.to(dtype)
+
+        ones = torch.ones(d, device=device, dtype=dtype)
+        layers = []
+        for _ in range(config.n_layers):
+            w_qkv = torch.cat([draw(d, d, (hq, d)), draw(d, dkv, (hkv, d)), draw(d, dkv, (hkv, d))])
+            layers.append({"attn_norm": ones, "w_qkv": w_qkv, "wo": draw(d, d, (d, hq)),
+                           "ffn_norm": ones, "w_gu": torch.cat([draw(d, f, (fl, d)), draw(d, f, (fl, d))]),
+                           "w_down": draw(f, d, (d, fl))})
+        return cls(tp.local_config(), dtype, device,
+                   {"embed": draw(v, d, (v, d)), "out_norm": ones, "out_head": draw(d, v, (v, d)),
+                    "layers": layers})
