@@ -46,10 +46,12 @@ def _worker(rank, world, port, q):
         b = eng.prefill(P.PrefillCall("a question", parents=[a]))
         ids = eng.decode_parallel([
             P.DecodeCall("A1:", parents=[a, b], sampling=P.SamplingParams(max_tokens=6)),
-            P.DecodeCall("A2:", parents=[b, a], offsets=[0, 40],
+            P.DecodeCall("A2:", parents=[b, a], offsets=[37, 0], new_offset=90,
                          sampling=P.SamplingParams(max_tokens=6))])
         q.put((rank, {m: np.stack(eng.last_stats.logits[m]) for m in ids},
                {m: eng.generated_token_ids(m) for m in ids}))
+    except Exception as exc:  # surface worker failures instead of a queue timeout
+        q.put((rank, repr(exc), None))
     finally:
         dist.destroy_process_group()
 
@@ -61,7 +63,7 @@ def test_tensor_parallel_engine_matches_oracle():
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=300) for _ in range(world)]
+    res = [q.get(timeout=240) for _ in range(world)]
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -70,9 +72,10 @@ def test_tensor_parallel_engine_matches_oracle():
     b = ref.prefill({"message": "a question", "parents": [a]})
     ids = ref.decode_batch([
         {"header": "A1:", "parents": [a, b], "sampling": O.Sampling(max_tokens=6)},
-        {"header": "A2:", "parents": [b, a], "offsets": [0, 40],
+        {"header": "A2:", "parents": [b, a], "offsets": [37, 0], "new_offset": 90,
          "sampling": O.Sampling(max_tokens=6)}])
     for rank, logits, gen in res:
+        assert gen is not None, logits
         for m in ids:
             assert gen[m] == ref.generated(m)
             want = np.stack(ref.stats[-1].logits[m])
