@@ -20,6 +20,10 @@ Reported (rank 0, one JSON line):
   ttft_p50_ms  per-message TTFT (decode_parallel call start -> first token), p50.
   roofline decode attention kernel (K5 split) vs measured HBM bandwidth.
   cpu_baseline  the CPU oracle (NumPy restatement of the reference) on this host.
+  reencode_baseline  one instance of the same debate through the device
+           BaselineEngine (the paper's re-encoding comparator): TTFT and decode rate
+           beside ours on the same GPU and weights.
+  kernel_rooflines  K2 / K4 / K5 microbenchmarks (tools/kernel_bench.py).
 Multi-GPU (torchrun): each rank runs its own independent workflow instances
 (seed = rank), no collectives on the data path; value = all ranks' tokens / max
 rank time ("scaling": "weak").
@@ -250,6 +254,34 @@ def reference_arm(args) -> None:
 # ---------------------------------------------------------------------------- GPU side
 
 
+def reencode_baseline(P, weights, inputs, args, choreo_ttft, choreo_tps) -> dict:
+    """The paper's comparison on the same GPU and weights: one instance of the same
+    debate through the re-encoding BaselineEngine (parents concatenated in list order
+    and re-encoded per call behind an exact prefix trie, decode_parallel sequential,
+    reference baseline.py) — TTFT and decode rate beside the choreographed engine's."""
+    import torch
+
+    eng = P.BaselineEngine(weights, capacity=1 << 17)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = run_debate(eng, P, inputs, args.agents, args.rounds)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    hits = sum(s.cache_hit_tokens for s in eng.stats)
+    enc = sum(s.tokens_encoded for s in eng.stats)
+    p50 = statistics.median(res["ttft"])
+    out = {"engine": "BaselineEngine (device, re-encoding + prefix trie)", "workflows": 1,
+           "ttft_p50_ms": round(1e3 * p50, 3),
+           "ttft_p90_ms": round(1e3 * sorted(res["ttft"])[int(0.9 * (len(res["ttft"]) - 1))], 3),
+           "decode_tokens_per_s": round(res["generated"] / wall, 2),
+           "tokens_encoded": enc, "trie_hit_tokens": hits,
+           "ttft_p50_speedup": round(p50 / statistics.median(choreo_ttft), 2),
+           "decode_speedup_e2e": round(choreo_tps / (res["generated"] / wall), 2)}
+    del eng
+    torch.cuda.empty_cache()
+    return out
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -262,6 +294,8 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-kernels", action="store_true",
                     help="skip the K2/K4/K5 kernel microbenchmarks (tools/kernel_bench.py)")
+    ap.add_argument("--no-reencode", action="store_true",
+                    help="skip the re-encoding comparator (BaselineEngine) workflow")
     ap.add_argument("--model", default="llama-3.1-8b")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -350,6 +384,9 @@ def main() -> None:
         if world > 1:
             dist.destroy_process_group()
         return
+    reencode = None
+    if world == 1 and not args.no_reencode:
+        reencode = reencode_baseline(P, weights, inputs[0], args, ttft, generated_all / elapsed)
     kernels = None
     if world == 1 and not args.no_kernels:
         sys.path.insert(0, os.path.join(ROOT, "tools"))
@@ -382,6 +419,7 @@ def main() -> None:
         "generated_tokens": int(generated_all),
         "roofline": roofline,
         "kernel_rooflines": kernels,
+        "reencode_baseline": reencode,
         "cpu_baseline": cpu,
         "clocks": clocks.summary(),
     }

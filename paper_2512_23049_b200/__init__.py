@@ -7,6 +7,7 @@ choreographed prefill and parallel decode — PyTorch host code over hand-writte
 sm_100a kernels behind a C ABI (include/choreo_b200.h).  No CPU fallback.
 """
 
+from .baseline import BaselineEngine, PrefixTrie
 from .config import (BOS_MSG, DEFAULT_CONFIG, EOS_MSG, LLAMA_3_1_8B, LLAMA_3_1_70B, LLAMA_3_2_1B,
                      N_RESERVED, PRESETS, ModelConfig)
 from .engine import (CallStats, DecodeCall, Engine, PrefillCall, SamplingParams, encode_flops)
@@ -19,6 +20,7 @@ from .weights import (DeviceWeights, LayerWeights, WeightSet, init_weights, load
                       save_weights)
 
 __all__ = [
+    "BaselineEngine", "PrefixTrie",
     "BOS_MSG", "DEFAULT_CONFIG", "EOS_MSG", "LLAMA_3_1_8B", "LLAMA_3_1_70B", "LLAMA_3_2_1B",
     "N_RESERVED", "PRESETS", "ModelConfig", "CallStats", "DecodeCall", "Engine", "PrefillCall",
     "SamplingParams", "encode_flops", "AllMaskedError", "CapacityError", "ChoreoError",

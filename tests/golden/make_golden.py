@@ -11,6 +11,9 @@ tests/golden/ and is small:
   ref_runs_<variant>.json per-script reference traces + cache metadata
   ref_logits_<variant>.npz per-selection logits recorded by the reference
                           (record_logits=True), key "<script>/<message>"
+  ref_baseline_runs.json  the same scripts through the reference BaselineEngine
+  ref_baseline_logits.npz (re-encoding comparator, f64 weights): traces with its
+                          cost counters (flops, tokens encoded, trie hits) + logits
 
 variants: "f64"  = init_weights(DEFAULT_CONFIG) as the reference builds it;
           "bf16" = the same weights rounded to bfloat16 (RNE) and upcast, the
@@ -34,7 +37,8 @@ HERE = Path(__file__).resolve().parent
 sys.path.insert(0, str(REF / "src"))
 sys.path.insert(0, str(HERE.parent.parent))
 
-from choreo.config import DEFAULT_CONFIG  # noqa: E402  (reference, read-only)
+from choreo.baseline import BaselineEngine  # noqa: E402  (reference, read-only)
+from choreo.config import DEFAULT_CONFIG  # noqa: E402
 from choreo.engine import DecodeCall, Engine, PrefillCall, SamplingParams  # noqa: E402
 from choreo.model import WeightSet, LayerWeights, init_weights  # noqa: E402
 from choreo.script import run_script  # noqa: E402
@@ -83,6 +87,20 @@ def run_c1(weights: WeightSet) -> dict:
             "logits": np.stack(eng.last_stats.logits[m])}
 
 
+def _trace_steps(trace, name: str, logits: dict) -> list:
+    steps = []
+    for s in trace.steps:
+        d = s.to_dict()
+        d.pop("wall", None)
+        lg = d.pop("logits", None) or {}
+        for msg_name, rows in lg.items():
+            logits[f"{name}/{msg_name}"] = np.asarray(rows, dtype=np.float64)
+        for m in d["messages"]:
+            m.pop("ttft", None)
+        steps.append(d)
+    return steps
+
+
 def run_variant(variant: str) -> tuple[dict, dict]:
     weights = ref_weights(variant)
     runs, logits = {}, {}
@@ -91,23 +109,25 @@ def run_variant(variant: str) -> tuple[dict, dict]:
         eng = Engine(weights, seed=0, record_logits=True)
         trace = run_script(eng, script)
         n = eng.cache.token_count
-        steps = []
-        for s in trace.steps:
-            d = s.to_dict()
-            d.pop("wall", None)
-            lg = d.pop("logits", None) or {}
-            for msg_name, rows in lg.items():
-                logits[f"{name}/{msg_name}"] = np.asarray(rows, dtype=np.float64)
-            for m in d["messages"]:
-                m.pop("ttft", None)
-            steps.append(d)
-        runs[name] = {"steps": steps,
+        runs[name] = {"steps": _trace_steps(trace, name, logits),
                       "msg_ids": eng.cache.msg_ids[:n].tolist(),
                       "positions": eng.cache.positions[:n].tolist(),
                       "token_ids": eng.cache.token_ids[:n].tolist()}
     c1 = run_c1(weights)
     logits["C1/answer"] = c1.pop("logits")
     runs["C1"] = c1
+    return runs, logits
+
+
+def run_baseline() -> tuple[dict, dict]:
+    weights = ref_weights("f64")
+    runs, logits = {}, {}
+    for name in SCRIPTS:
+        script = json.loads((REF / "fixtures" / "scripts" / f"{name}.json").read_text())
+        for cache in (True, False):
+            key = name if cache else f"{name}@nocache"
+            eng = BaselineEngine(weights, seed=0, prefix_cache=cache, record_logits=cache)
+            runs[key] = {"steps": _trace_steps(run_script(eng, script), key, logits)}
     return runs, logits
 
 
@@ -144,6 +164,10 @@ def main() -> None:
         (HERE / f"ref_runs_{variant}.json").write_text(json.dumps(runs, sort_keys=True) + "\n")
         np.savez_compressed(HERE / f"ref_logits_{variant}.npz", **logits)
         print(variant, "selections:", sum(len(v) for v in logits.values()))
+    runs, logits = run_baseline()
+    (HERE / "ref_baseline_runs.json").write_text(json.dumps(runs, sort_keys=True) + "\n")
+    np.savez_compressed(HERE / "ref_baseline_logits.npz", **logits)
+    print("baseline selections:", sum(len(v) for v in logits.values()))
     (HERE / "ref_pins.json").write_text(json.dumps(pins, sort_keys=True, indent=1) + "\n")
 
 
