@@ -366,8 +366,9 @@ def main() -> None:
 
     # decode attention (K5) roofline, from the events of the last timed workflow
     peaks = measured_peaks()
-    a_ms = [a.elapsed_time(b) for a, b, _ in attn_events]
-    a_bytes = [nb for _, _, nb in attn_events]
+    timed = runner.collect_attn_times()
+    a_ms = [m for m, _ in timed]
+    a_bytes = [nb for _, nb in timed]
     roofline = None
     if a_ms:
         achieved = (sum(a_bytes) / len(a_bytes)) / (sum(a_ms) / len(a_ms) / 1e3) / 1e9

@@ -190,6 +190,74 @@ int choreo_attn_combine(const float* part_o, const float* part_lse, const int32_
 int choreo_select_greedy(const float* logits, int n_rows, int ld, int vocab, int split,
                          int32_t* out_tok, void* stream);
 
+/* K7 decode-sized linear layer (weight streaming, tcgen05 + TMA, stream-K):
+ *   y[r][n] = sum_k x[r][k] * w[n][k]      x: bf16 [x_rows][k], w: bf16 [n][k] (out, in),
+ *                                          y: f32 [x_rows / (1 + split)][n].
+ * split = 1: x rows r and x_rows/2 + r are the hi/lo halves of one activation row and
+ * y row r is their sum.  x_rows <= 64 (<= 32 output rows when split), k % 8 == 0.
+ * workspace: f32 [148 * 2 * 64 * 128] partial tiles; tile_counters: int32 [ceil(n/128)],
+ * zero on entry, left zero on exit.  grid_ctas <= 0: one CTA per SM (148).
+ * Replaces the x @ W projections of model.py:172-174, 185-189 and the head at 193 for
+ * decode-sized steps (the reference runs them as NumPy matmuls). */
+int choreo_linear_skinny(const void* x, int x_rows, int split, const void* w, int n, int k,
+                         float* y, float* workspace, int* tile_counters, int grid_ctas,
+                         void* stream);
+
+/* Native decode-step executor: every layer of a decode-sized bf16 step (split hi/lo
+ * activations or plain bf16; page_size 64; fused K5 items from choreo_assemble with a
+ * fat buffer) issued in one call — per layer: residual_rmsnorm, K7 qkv, K1 rope_append,
+ * K5 decode attention, combine, K7 o_proj, residual_rmsnorm, K7 gate|up, silu_mul,
+ * K7 down.  Replaces the per-layer loop of model.py:169-189.  Weight arrays are HOST
+ * arrays of n_layers DEVICE pointers (bf16, (out, in) layout).  On return `delta` holds
+ * the last layer's down_proj output (the caller adds it and runs the final norm / head).
+ * attn_events: optional host array of 2 * n_layers cudaEvent_t recorded around each K5. */
+typedef struct {
+  int n_layers, d, n_heads, n_kv, head_dim, ffn_dim;
+  const void* const* attn_norm;
+  const void* const* w_qkv;
+  const void* const* wo;
+  const void* const* ffn_norm;
+  const void* const* w_gu;
+  const void* const* w_down;
+  float eps;
+  void* k_pool;
+  void* v_pool;
+  int n_pages, page_size;
+  const float* cos_t;
+  const float* sin_t;
+  int max_delta;
+  int n_rows, split, attn_flags, n_items;
+  const int32_t* pos;
+  const int32_t* page;
+  const int32_t* slot;
+  const int32_t* fat;
+  const int32_t* counts;
+  const int32_t* row_part_off;
+  const int32_t* row_part;
+  float* x;
+  const float* delta_in; /* added to x before layer 0's norm (NULL: none) */
+  void* h;
+  float* qkv;
+  float* q;
+  float* part_o;
+  float* part_lse;
+  void* attn;
+  float* ao;
+  float* gu;
+  void* act;
+  float* delta;
+  float* k7_ws;
+  int* k7_cnt;
+  void** attn_events;
+} ChoreoDecodeStep;
+
+int choreo_decode_layers(const ChoreoDecodeStep* step, void* stream);
+
+/* Timing-event helpers for attn_events (cudaEvent_t as void*). */
+int choreo_events_create(void** events, int n);
+int choreo_events_elapsed(void* const* events, int n_pairs, float* ms_out);
+int choreo_events_destroy(void* const* events, int n);
+
 /* Diagnostics: one-CTA tcgen05 GEMM over the UMMA primitives K4 uses.
  * a: bf16 [128][64], b1: bf16 [64][64] (N x K), b2: bf16 [64][128] (K x N);
  * c1 = a * b1^T (f32 [128][64]), c2 = a * b2 (f32 [128][128]) with both operands in shared

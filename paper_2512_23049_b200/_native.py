@@ -40,6 +40,11 @@ SIGNATURES: dict[str, list] = {
     "choreo_attn_combine": [_P, _P, _P, _P, _I, _I, _I, _P, _I, _I, _P],
     "choreo_select_greedy": [_P, _I, _I, _I, _I, _P, _P],
     "choreo_selftest_umma": [_P, _P, _P, _P, _P, _P, _P],
+    "choreo_linear_skinny": [_P, _I, _I, _P, _I, _I, _P, _P, _P, _I, _P],
+    "choreo_decode_layers": [_P, _P],
+    "choreo_events_create": [_P, _I],
+    "choreo_events_elapsed": [_P, _I, _P],
+    "choreo_events_destroy": [_P, _I],
 }
 EXTRA = ["choreo_abi_version", "choreo_last_error"]
 
@@ -93,6 +98,24 @@ prefill_attn = _Caller("choreo_prefill_attn")
 decode_attn = _Caller("choreo_decode_attn")
 select_greedy = _Caller("choreo_select_greedy")
 selftest_umma = _Caller("choreo_selftest_umma")
+linear_skinny = _Caller("choreo_linear_skinny")
+decode_layers = _Caller("choreo_decode_layers")
+events_create = _Caller("choreo_events_create")
+events_elapsed = _Caller("choreo_events_elapsed")
+events_destroy = _Caller("choreo_events_destroy")
+
+
+class DecodeStep(ctypes.Structure):
+    """Mirror of ChoreoDecodeStep (include/choreo_b200.h)."""
+
+    _fields_ = [(n, _I) for n in ("n_layers", "d", "n_heads", "n_kv", "head_dim", "ffn_dim")] + \
+        [(n, _P) for n in ("attn_norm", "w_qkv", "wo", "ffn_norm", "w_gu", "w_down")] + \
+        [("eps", _F), ("k_pool", _P), ("v_pool", _P), ("n_pages", _I), ("page_size", _I),
+         ("cos_t", _P), ("sin_t", _P), ("max_delta", _I), ("n_rows", _I), ("split", _I),
+         ("attn_flags", _I), ("n_items", _I)] + \
+        [(n, _P) for n in ("pos", "page", "slot", "fat", "counts", "row_part_off", "row_part",
+                           "x", "delta_in", "h", "qkv", "q", "part_o", "part_lse", "attn", "ao",
+                           "gu", "act", "delta", "k7_ws", "k7_cnt", "attn_events")]
 
 
 def ptr(t) -> int | None:

@@ -94,6 +94,8 @@ struct Shared {
 };
 
 __global__ void __launch_bounds__(kThreads3) assemble_kernel(K3Params p) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ unsigned char smem_raw[];
   Shared& S = *reinterpret_cast<Shared*>(smem_raw);
   const int tid = threadIdx.x;
@@ -324,6 +326,8 @@ __global__ void __launch_bounds__(kThreads3) assemble_kernel(K3Params p) {
 // chunks of that list (pages past the block's last row are skipped).  A 128-row M tile
 // already comes from one call here, so sharing pages across calls would not enlarge it.
 __global__ void __launch_bounds__(kThreads3) assemble_percall_kernel(K3Params p) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ int c_pp[kMaxCalls], c_vis[kMaxCalls], c_rows[kMaxCalls], c_item[kMaxCalls],
       c_part[kMaxCalls];
   __shared__ int overflow;
@@ -446,7 +450,7 @@ extern "C" int choreo_assemble(const int32_t* msg_len, const int32_t* msg_pt, in
              blk_rows, items, row_part_off, row_part, counts, cap_vis, cap_blk_rows, cap_items,
              cap_parts, fat};
   if (mode == 1) {
-    assemble_percall_kernel<<<1, kThreads3, 0, as_stream(stream)>>>(p);
+    launch_k(assemble_percall_kernel, 1, kThreads3, 0, as_stream(stream), p);
     return launch_status("choreo_assemble");
   }
   static bool attr = false;
@@ -455,6 +459,6 @@ extern "C" int choreo_assemble(const int32_t* msg_len, const int32_t* msg_pt, in
                          (int)sizeof(Shared));
     attr = true;
   }
-  assemble_kernel<<<1, kThreads3, sizeof(Shared), as_stream(stream)>>>(p);
+  launch_k(assemble_kernel, 1, kThreads3, sizeof(Shared), as_stream(stream), p);
   return launch_status("choreo_assemble");
 }

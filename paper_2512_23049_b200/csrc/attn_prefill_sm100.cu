@@ -107,6 +107,8 @@ template <int HD, int POLY>
 __global__ void __launch_bounds__(kPfThreads, 1)
     attn_prefill_sm100(PrefillParams p, const __grid_constant__ CUtensorMap tmK,
                        const __grid_constant__ CUtensorMap tmV) {
+  pdl_trigger();
+  pdl_wait();
   using namespace sm100;
   using S = PfSmem<HD>;
   constexpr int R = S::kRegions;
@@ -470,7 +472,7 @@ static int launch_prefill(const PrefillParams& p, const void* k_pool, const void
                          smem);
     attr = true;
   }
-  attn_prefill_sm100<HD, POLY><<<grid, kPfThreads, smem, s>>>(p, mk, mv);
+  launch_k(attn_prefill_sm100<HD, POLY>, grid, kPfThreads, smem, s, p, mk, mv);
   return launch_status("choreo_prefill_attn");
 }
 

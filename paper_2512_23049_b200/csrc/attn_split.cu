@@ -45,6 +45,8 @@ constexpr int kKT = 32;    // keys per smem tile
 
 template <typename T, int HD>
 __global__ void __launch_bounds__(kThreads) attn_split_simt(SplitParams p) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int RPT = kMaxM * HD / kThreads;
   constexpr int GROUPS = kThreads / HD;
   extern __shared__ float smem[];
@@ -461,6 +463,8 @@ __device__ __forceinline__ void mma_item(const SplitParams& p, const ItemCtx& c,
 
 template <int HD>
 __global__ void __launch_bounds__(kMmaThreads, 3) attn_split_mma(SplitParams p) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int LD = HD + 8;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(smem_raw);  // [kStages][64][LD]
@@ -551,6 +555,8 @@ __device__ void finalize_row(const DecodeParams& d, int rid, int kvh, int G) {
 
 template <int HD>
 __global__ void __launch_bounds__(kMmaThreads, 3) decode_attn_fused(DecodeParams d) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int LD = HD + 8;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(smem_raw);
@@ -605,7 +611,7 @@ static int launch_decode(const DecodeParams& d, int grid, cudaStream_t s) {
     cudaFuncSetAttribute(decode_attn_fused<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr_set = true;
   }
-  decode_attn_fused<HD><<<grid, kMmaThreads, smem, s>>>(d);
+  launch_k(decode_attn_fused<HD>, grid, kMmaThreads, smem, s, d);
   return launch_status("choreo_decode_attn");
 }
 
@@ -618,6 +624,8 @@ __global__ void __launch_bounds__(128) attn_combine_kernel(
     const float* __restrict__ part_o, const float* __restrict__ part_lse,
     const int32_t* __restrict__ row_part_off, const int32_t* __restrict__ row_part, int n_rows,
     int n_heads, int hd, int split, TO* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x / n_heads, h = blockIdx.x % n_heads;
   const int b = row_part_off[r], e = row_part_off[r + 1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -706,7 +714,7 @@ static int launch_simt(const SplitParams& p, int grid, cudaStream_t s) {
                          (int)smem);
     attr_set = true;
   }
-  attn_split_simt<T, HD><<<grid, kThreads, smem, s>>>(p);
+  launch_k(attn_split_simt<T, HD>, grid, kThreads, smem, s, p);
   return launch_status("choreo_attn_split");
 }
 
@@ -721,7 +729,7 @@ static int launch_mma(const SplitParams& p, int grid, cudaStream_t s) {
     cudaFuncSetAttribute(attn_split_mma<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr_set = true;
   }
-  attn_split_mma<HD><<<grid, kMmaThreads, smem, s>>>(p);
+  launch_k(attn_split_mma<HD>, grid, kMmaThreads, smem, s, p);
   return launch_status("choreo_attn_split");
 }
 
@@ -802,11 +810,11 @@ int choreo_attn_combine(const float* part_o, const float* part_lse, const int32_
   if (head_dim % 4 || head_dim > 128) return CHOREO_EUNSUPPORTED;
   const int threads = 128;
   if (out_dtype == CHOREO_BF16)
-    attn_combine_kernel<__nv_bfloat16><<<n_rows * n_heads, threads, 0, s>>>(
+    launch_k(attn_combine_kernel<__nv_bfloat16>, n_rows * n_heads, threads, 0, s, 
         part_o, part_lse, row_part_off, row_part, n_rows, n_heads, head_dim, out_split,
         (__nv_bfloat16*)out);
   else
-    attn_combine_kernel<float><<<n_rows * n_heads, threads, 0, s>>>(
+    launch_k(attn_combine_kernel<float>, n_rows * n_heads, threads, 0, s, 
         part_o, part_lse, row_part_off, row_part, n_rows, n_heads, head_dim, 0, (float*)out);
   return launch_status("choreo_attn_combine");
 }

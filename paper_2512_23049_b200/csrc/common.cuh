@@ -4,6 +4,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "../../include/choreo_b200.h"
 
@@ -45,6 +46,43 @@ __device__ __forceinline__ void store_any(void* p, int dtype, int64_t i, float v
     reinterpret_cast<__nv_bfloat16*>(p)[i] = __float2bfloat16_rn(v);
   else
     reinterpret_cast<float*>(p)[i] = v;
+}
+
+// Programmatic dependent launch: a kernel that precedes a weight-streaming GEMM lets the
+// GEMM (launched with the programmatic-serialization attribute) start its prologue and
+// weight prefetch while this kernel still runs; the GEMM waits (griddepcontrol.wait)
+// before it reads anything this kernel writes.  A no-op when no dependent is PDL-launched.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
+// Every library kernel is launched with the programmatic-serialization attribute
+// (env CHOREO_PDL=0 disables it) and starts with pdl_trigger(); pdl_wait() so the launch
+// and CTA rasterisation of kernel N+1 overlap kernel N's execution while its memory work
+// still starts after kernel N completed.
+inline bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("CHOREO_PDL");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
 inline bool dtype_ok(int dt) { return dt == CHOREO_F32 || dt == CHOREO_BF16; }

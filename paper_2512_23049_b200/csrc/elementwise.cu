@@ -16,6 +16,8 @@ void set_last_error(const char* where, cudaError_t err) {
 
 __global__ void embed_kernel(const void* __restrict__ embed, int dt, int d,
                              const int32_t* __restrict__ ids, float* __restrict__ x) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   const int64_t src = (int64_t)ids[r] * d;
   for (int i = threadIdx.x; i < d; i += blockDim.x) x[(int64_t)r * d + i] = load_any(embed, dt, src + i);
@@ -43,6 +45,8 @@ __global__ void residual_rmsnorm_kernel(float* __restrict__ x, const void* __res
                                         const void* __restrict__ w, int w_dt, int d,
                                         float eps, void* __restrict__ out, int out_dt,
                                         int out_split, const int32_t* __restrict__ row_map) {
+  pdl_trigger();
+  pdl_wait();
   const int r_out = blockIdx.x;
   const int r = row_map ? row_map[r_out] : r_out;
   float* xr = x + (int64_t)r * d;
@@ -112,6 +116,8 @@ __global__ void residual_rmsnorm_vec(float* __restrict__ x, const float* __restr
                                      int delta_split, int n_rows, const void* __restrict__ w,
                                      int w_dt, int d, float eps, void* __restrict__ out, int out_dt,
                                      int out_split, const int32_t* __restrict__ row_map) {
+  pdl_trigger();
+  pdl_wait();
   const int r_out = blockIdx.x;
   const int r = row_map ? row_map[r_out] : r_out;
   const int nvec = d >> 2;
@@ -164,6 +170,8 @@ __global__ void residual_rmsnorm_vec(float* __restrict__ x, const float* __restr
 
 __global__ void silu_mul_kernel(const void* __restrict__ gu, int dt, int in_split, int n_rows,
                                 int f, void* __restrict__ out, int out_dt, int out_split) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t n = (int64_t)n_rows * f, lo_in = (int64_t)n_rows * 2 * f;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -182,6 +190,8 @@ __global__ void silu_mul_kernel(const void* __restrict__ gu, int dt, int in_spli
 // lowest id, as np.argmax does (engine.py:371).
 __global__ void select_greedy_kernel(const float* __restrict__ logits, int n_rows, int64_t ld,
                                      int split, int32_t* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= n_rows) return;
@@ -216,7 +226,7 @@ int choreo_embed(const void* embed, int embed_dtype, int d, const int32_t* ids, 
                  float* x, void* stream) {
   if (!embed || !ids || !x || d <= 0 || n_rows < 0 || !dtype_ok(embed_dtype)) return CHOREO_EINVAL;
   if (n_rows == 0) return CHOREO_OK;
-  embed_kernel<<<n_rows, 256, 0, as_stream(stream)>>>(embed, embed_dtype, d, ids, x);
+  launch_k(embed_kernel, n_rows, 256, 0, as_stream(stream), embed, embed_dtype, d, ids, x);
   return launch_status("choreo_embed");
 }
 
@@ -238,7 +248,7 @@ int choreo_residual_rmsnorm(float* x, const void* delta, int delta_dtype, int de
     const int ch = (nvec + threads - 1) / threads;
     auto s = as_stream(stream);
 #define RMS_VEC(CH)                                                                            \
-  residual_rmsnorm_vec<CH><<<rows, threads, 0, s>>>(x, (const float*)delta, delta_split, n_rows, \
+  launch_k(residual_rmsnorm_vec<CH>, rows, threads, 0, s, x, (const float*)delta, delta_split, n_rows, \
                                                     w, w_dtype, d, eps, out, out_dtype,          \
                                                     out_split, row_map)
     if (ch == 1) RMS_VEC(1);
@@ -248,7 +258,7 @@ int choreo_residual_rmsnorm(float* x, const void* delta, int delta_dtype, int de
     return launch_status("choreo_residual_rmsnorm");
   }
   const int threads = d >= 2048 ? 512 : (d >= 256 ? 256 : 64);
-  residual_rmsnorm_kernel<<<rows, threads, 0, as_stream(stream)>>>(
+  launch_k(residual_rmsnorm_kernel, rows, threads, 0, as_stream(stream), 
       x, delta, delta_dtype, delta_split, n_rows, w, w_dtype, d, eps, out, out_dtype, out_split,
       row_map);
   return launch_status("choreo_residual_rmsnorm");
@@ -263,7 +273,7 @@ int choreo_silu_mul(const void* gu, int gu_dtype, int in_split, int n_rows, int 
   if (n == 0) return CHOREO_OK;
   int64_t blocks = (n + 255) / 256;
   if (blocks > 148 * 64) blocks = 148 * 64;
-  silu_mul_kernel<<<(int)blocks, 256, 0, as_stream(stream)>>>(gu, gu_dtype, in_split, n_rows, f,
+  launch_k(silu_mul_kernel, (int)blocks, 256, 0, as_stream(stream), gu, gu_dtype, in_split, n_rows, f,
                                                                out, out_dtype, out_split);
   return launch_status("choreo_silu_mul");
 }
@@ -273,7 +283,7 @@ int choreo_select_greedy(const float* logits, int n_rows, int ld, int vocab, int
   if (!logits || !out_tok || n_rows < 0 || vocab < 258 || ld < vocab) return CHOREO_EINVAL;
   if (n_rows == 0) return CHOREO_OK;
   const int warps = 4;
-  select_greedy_kernel<<<(n_rows + warps - 1) / warps, 32 * warps, 0, as_stream(stream)>>>(
+  launch_k(select_greedy_kernel, (n_rows + warps - 1) / warps, 32 * warps, 0, as_stream(stream), 
       logits, n_rows, ld, split, out_tok);
   return launch_status("choreo_select_greedy");
 }

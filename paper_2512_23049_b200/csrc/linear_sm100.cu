@@ -1,0 +1,319 @@
+// K7 weight-streaming linear layer for decode-sized steps (tcgen05 + TMEM + TMA, stream-K).
+//
+// A decode step multiplies a handful of activation rows (8 agents, as hi/lo bf16 pairs:
+// 16 rows) by every weight matrix of the model: y[r][n] = sum_k x[r][k] * w[n][k].  The
+// work is pure weight streaming (16 GB per step at the Llama-3.1-8B shape), so the kernel
+// is built to keep HBM busy, not the tensor core:
+//   * swap-AB: a 128-row weight tile is the UMMA A operand (M = 128), the activation rows
+//     are the B operand (N = NX = 16/32/64), accumulators live in TMEM (NX columns);
+//   * stream-K: the (tile, k-block) iteration space is cut into one equal contiguous range
+//     per CTA (one CTA per SM), so every SM streams the same number of weight bytes
+//     whatever the tile count (qkv: 48 tiles, o_proj/down: 32, gate|up: 224, head: 1002);
+//   * TMA producer warp with an 8-stage ring (16 KB of weights + the activation chunk per
+//     stage, ~150 KB in flight per SM), single-thread MMA issue, 4 epilogue warps;
+//   * a tile cut between CTAs is reduced deterministically: each piece is written to a
+//     per-CTA slot, the last piece to arrive sums all pieces in CTA order;
+//   * with split activations (x rows r and R + r are the hi/lo halves of one row) the
+//     halves are loaded to B rows r and NX/2 + r and the epilogue adds them: y has R rows.
+// Replaces the dense projections of reference model.py:172-174, 185-189, 193 at decode
+// sizes (the reference runs them as NumPy matmuls x @ W).
+#include <cudaTypedefs.h>
+#include <stdlib.h>
+
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace choreo {
+
+constexpr int kLnThreads = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
+constexpr int kLnTile = 128;     // weight rows per tile (UMMA M)
+constexpr int kLnKB = 64;        // k elements per block (one 128-byte SW128 row)
+
+struct LinearParams {
+  float* y;       // [out_rows][N]
+  float* ws;      // [grid][2][NX][128] partial tiles
+  int* counters;  // [n_tiles], zero between launches (reducers reset them)
+  int N, KB, iters, grid, out_rows, split;
+};
+
+template <int NX, int KSUB>
+struct LnCfg {
+  static constexpr int kWBytes = kLnTile * 128;  // one k-block of the weight tile
+  static constexpr int kXBytes = NX * 128;       // one k-block of the activations
+  static constexpr int kStageBytes = KSUB * (kWBytes + kXBytes);
+  static constexpr int kStages = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
+  static constexpr int kSmem = kStages * kStageBytes + 1024;
+  static constexpr int kTmemCols = 2 * NX < 32 ? 32 : 2 * NX;
+};
+
+__device__ __forceinline__ int ln_begin(int c, int iters, int grid) {
+  return (int)(((long long)c * iters) / grid);
+}
+// CTA whose range holds iteration i (every CTA owns >= 1 iteration: grid <= iters)
+__device__ __forceinline__ int ln_owner(int i, int iters, int grid) {
+  return (int)((((long long)i + 1) * grid - 1) / iters);
+}
+
+template <int NX, int KSUB>
+__global__ void __launch_bounds__(kLnThreads, 1)
+    linear_skinny_sm100(LinearParams p, const __grid_constant__ CUtensorMap tmW,
+                        const __grid_constant__ CUtensorMap tmX) {
+  using namespace sm100;
+  using C = LnCfg<NX, KSUB>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full_bar[C::kStages], empty_bar[C::kStages], acc_full[2], acc_empty[2];
+  __shared__ uint32_t tmem_base;
+  __shared__ int s_last;
+
+  pdl_trigger();  // the successor may launch now; it waits for this grid to complete
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int c = blockIdx.x;
+  const int b = ln_begin(c, p.iters, p.grid), e = ln_begin(c + 1, p.iters, p.grid);
+  if (tid == 0) {
+    for (int i = 0; i < C::kStages; ++i) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 128);
+    }
+    fence_barrier_init();
+    tma_prefetch_desc(&tmW);
+    tma_prefetch_desc(&tmX);
+  }
+  if (warp == 1) tmem_alloc(&tmem_base, C::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------------------------------------- TMA producer
+      auto load_w = [&](int i, int st) {
+        uint8_t* dst = base + st * C::kStageBytes;
+        const int t = i / p.KB, kb = (i % p.KB) * KSUB;
+        // the KSUB weight boxes go out back to back: 128 rows x KSUB*128 contiguous bytes
+#pragma unroll
+        for (int u = 0; u < KSUB; ++u)
+          tma_load_2d(dst + u * C::kWBytes, &tmW, &full_bar[st], (kb + u) * kLnKB, t * kLnTile);
+      };
+      auto load_x = [&](int i, int st) {
+        uint8_t* xd = base + st * C::kStageBytes + KSUB * C::kWBytes;
+        const int kb = (i % p.KB) * KSUB;
+#pragma unroll
+        for (int u = 0; u < KSUB; ++u) {
+          if (p.split) {  // hi rows -> smem rows [0, NX/2), lo rows -> [NX/2, NX)
+            tma_load_2d(xd + u * C::kXBytes, &tmX, &full_bar[st], (kb + u) * kLnKB, 0);
+            tma_load_2d(xd + u * C::kXBytes + C::kXBytes / 2, &tmX, &full_bar[st], (kb + u) * kLnKB,
+                        p.out_rows);
+          } else {
+            tma_load_2d(xd + u * C::kXBytes, &tmX, &full_bar[st], (kb + u) * kLnKB, 0);
+          }
+        }
+      };
+      // weights do not depend on the previous kernel: fill the ring with them before the
+      // programmatic-dependency wait, then add the activations (written by the predecessor)
+      const int pre = min(e - b, C::kStages);
+      for (int j = 0; j < pre; ++j) {
+        mbar_arrive_expect_tx(&full_bar[j], C::kStageBytes);
+        load_w(b + j, j);
+      }
+      pdl_wait();
+      for (int j = 0; j < pre; ++j) load_x(b + j, j);
+      for (int i = b + pre; i < e; ++i) {
+        const int j = i - b, st = j % C::kStages;
+        mbar_wait(&empty_bar[st], ((j / C::kStages) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full_bar[st], C::kStageBytes);
+        load_w(i, st);
+        load_x(i, st);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------------------------------------- MMA issuer
+      constexpr uint32_t idesc = umma_idesc_bf16(kLnTile, NX, false);
+      int seg = 0;
+      for (int i = b; i < e; ++i) {
+        const int j = i - b, st = j % C::kStages, kb = i % p.KB;
+        const bool first = (i == b) || kb == 0;
+        const bool last = (i == e - 1) || kb == p.KB - 1;
+        const int buf = seg & 1;
+        if (first && seg >= 2) mbar_wait(&acc_empty[buf], ((seg >> 1) - 1) & 1);
+        mbar_wait(&full_bar[st], (j / C::kStages) & 1);
+        tc_fence_after();
+        const uint32_t waddr = smem_addr(base + st * C::kStageBytes);
+        const uint32_t xaddr = waddr + KSUB * C::kWBytes;
+        const uint32_t d = tmem_base + buf * NX;
+#pragma unroll
+        for (int u = 0; u < KSUB; ++u)
+#pragma unroll
+          for (int k = 0; k < kLnKB / 16; ++k)
+            umma_bf16(d, umma_desc_sw128(waddr + u * C::kWBytes + k * 32, 16, 1024),
+                      umma_desc_sw128(xaddr + u * C::kXBytes + k * 32, 16, 1024), idesc,
+                      (first && u == 0 && k == 0) ? 0u : 1u);
+        umma_commit(&empty_bar[st]);
+        if (last) {
+          umma_commit(&acc_full[buf]);
+          ++seg;
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------------ epilogue
+    pdl_wait();  // y / workspace / counters are touched only after the predecessor is done
+    const int quad = warp & 3;
+    const int nl = quad * 32 + lane;  // weight row within the tile = TMEM lane
+    const int et = tid - 64;          // 0..127
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    int seg = 0;
+    for (int t = b / p.KB; t * p.KB < e; ++t, ++seg) {
+      const int buf = seg & 1;
+      const int lo = t * p.KB, hi = lo + p.KB;
+      const int c_lo = ln_owner(lo, p.iters, p.grid), c_hi = ln_owner(hi - 1, p.iters, p.grid);
+      mbar_wait(&acc_full[buf], (seg >> 1) & 1);
+      tc_fence_after();
+      float acc[NX];
+#pragma unroll
+      for (int q = 0; q < NX / 16; ++q) tmem_ld16(tmem_base + lane_off + buf * NX + q * 16, acc + q * 16);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&acc_empty[buf]);
+      const int n = t * kLnTile + nl;
+      if (c_lo != c_hi) {
+        // piece of a tile cut between CTAs: park it, the last piece reduces in CTA order
+        const int slot = (b >= lo) ? 0 : 1;
+        float* w = p.ws + ((size_t)(c * 2 + slot) * NX) * kLnTile + nl;
+#pragma unroll
+        for (int q = 0; q < NX; ++q) w[q * kLnTile] = acc[q];
+        __threadfence();
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        if (et == 0) {
+          const int old = atomicAdd(&p.counters[t], 1);
+          s_last = old == c_hi - c_lo;
+        }
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        if (!s_last) continue;
+        __threadfence();
+#pragma unroll
+        for (int q = 0; q < NX; ++q) acc[q] = 0.f;
+        for (int cc = c_lo; cc <= c_hi; ++cc) {
+          const int sl = (ln_begin(cc, p.iters, p.grid) >= lo) ? 0 : 1;
+          const volatile float* r = p.ws + ((size_t)(cc * 2 + sl) * NX) * kLnTile + nl;
+#pragma unroll
+          for (int q = 0; q < NX; ++q) acc[q] += r[q * kLnTile];
+        }
+        if (et == 0) p.counters[t] = 0;
+      }
+      if (n < p.N) {
+        if (p.split) {
+#pragma unroll
+          for (int r = 0; r < NX / 2; ++r)
+            if (r < p.out_rows) p.y[(size_t)r * p.N + n] = acc[r] + acc[NX / 2 + r];
+        } else {
+#pragma unroll
+          for (int r = 0; r < NX; ++r)
+            if (r < p.out_rows) p.y[(size_t)r * p.N + n] = acc[r];
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem_base, C::kTmemCols);
+}
+
+// ---------------------------------------------------------------- host side
+static PFN_cuTensorMapEncodeTiled_v12000 ln_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* ptr = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+// row-major [rows][cols] bf16, box = 64 cols x box_rows rows, SW128
+static bool ln_map(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols, int box_rows,
+                   CUtensorMapL2promotion l2) {
+  auto enc = ln_encode_fn();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  const cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, l2,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int NX, int KSUB>
+static int launch_linear(const LinearParams& p, const void* x, int x_rows, const void* w, int N,
+                         int K, cudaStream_t s) {
+  CUtensorMap mw, mx;
+  if (!ln_map(&mw, w, (uint64_t)N, (uint64_t)K, kLnTile, CU_TENSOR_MAP_L2_PROMOTION_L2_256B) ||
+      !ln_map(&mx, x, (uint64_t)x_rows, (uint64_t)K, p.split ? NX / 2 : NX,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_128B))
+    return CHOREO_ELAUNCH;
+  constexpr int smem = LnCfg<NX, KSUB>::kSmem;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(linear_skinny_sm100<NX, KSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         smem);
+    attr_set = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.grid);
+  cfg.blockDim = dim3(kLnThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, linear_skinny_sm100<NX, KSUB>, p, mw, mx);
+  return launch_status("choreo_linear_skinny");
+}
+
+}  // namespace choreo
+
+using namespace choreo;
+
+extern "C" int choreo_linear_skinny(const void* x, int x_rows, int split, const void* w, int n,
+                                    int k, float* y, float* workspace, int* tile_counters,
+                                    int grid_ctas, void* stream) {
+  if (!x || !w || !y || !workspace || !tile_counters || x_rows <= 0 || n <= 0 || k <= 0 ||
+      (split && (x_rows & 1)))
+    return CHOREO_EINVAL;
+  if (x_rows > 64 || k % 8) return CHOREO_EUNSUPPORTED;  // TMA: 16-byte row pitch
+  const int R = split ? x_rows / 2 : x_rows;  // output rows
+  const int NX = (split ? 2 * R : R) <= 16 ? 16 : (split ? 2 * R : R) <= 32 ? 32 : 64;
+  static int ksub = -1;
+  if (ksub < 0) {
+    const char* e = getenv("CHOREO_K7_KSUB");
+    ksub = e ? atoi(e) : 2;
+    if (ksub != 1 && ksub != 2 && ksub != 4) ksub = 2;
+  }
+  const int n_tiles = (n + kLnTile - 1) / kLnTile;
+  const int KB = (k + kLnKB * ksub - 1) / (kLnKB * ksub);  // iteration = ksub k-blocks
+  const int iters = n_tiles * KB;
+  int grid = grid_ctas > 0 ? grid_ctas : 148;
+  if (grid > iters) grid = iters;
+  LinearParams p{y, workspace, tile_counters, n, KB, iters, grid, split ? x_rows / 2 : x_rows,
+                 split};
+  auto s = as_stream(stream);
+#define LN_CASE(nx)                                                                       \
+  return ksub == 1   ? launch_linear<nx, 1>(p, x, x_rows, w, n, k, s)                     \
+         : ksub == 2 ? launch_linear<nx, 2>(p, x, x_rows, w, n, k, s)                     \
+                     : launch_linear<nx, 4>(p, x, x_rows, w, n, k, s);
+  switch (NX) {
+    case 16: LN_CASE(16)
+    case 32: LN_CASE(32)
+    default: LN_CASE(64)
+  }
+#undef LN_CASE
+}

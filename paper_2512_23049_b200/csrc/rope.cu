@@ -21,6 +21,8 @@ __global__ void rope_append_kernel(const TI* __restrict__ qkv, int ld, int n_row
                                    int n_pages, int page_size, int n_heads, int hd,
                                    const float* __restrict__ cos_t,
                                    const float* __restrict__ sin_t, int max_delta) {
+  pdl_trigger();
+  pdl_wait();
   const int half = hd >> 1;
   const int per_row = (n_heads + 2 * n_kv) * half;
   const int64_t total = (int64_t)n_rows * per_row;
@@ -87,6 +89,8 @@ __global__ void __launch_bounds__(256) rerotate_kernel(
     const int32_t* __restrict__ pages, const int32_t* __restrict__ page_len,
     const int32_t* __restrict__ delta, int n_list, const float* __restrict__ cos_t,
     const float* __restrict__ sin_t, int max_delta) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int N = Vec16<T>::N;  // elements per 16-byte vector
   extern __shared__ float cs[];   // [hd/2] cos then [hd/2] sin
   const int i = blockIdx.x % n_list;
@@ -155,7 +159,7 @@ int choreo_rope_append(const void* qkv, int qkv_dtype, int ld_qkv, int n_rows, i
   const int blocks = grid_for(total, 256);
   auto s = as_stream(stream);
 #define K1(TI, TP)                                                                               \
-  rope_append_kernel<TI, TP><<<blocks, 256, 0, s>>>(                                             \
+  launch_k(rope_append_kernel<TI, TP>, blocks, 256, 0, s,                                              \
       (const TI*)qkv, ld_qkv, n_rows, qkv_split, pos, dst_page, dst_slot, q_out, (TP*)k_pool, (TP*)v_pool, \
       layer, n_kv, n_pages, page_size, n_heads, head_dim, cos_t, sin_t, max_delta)
   if (qkv_dtype == CHOREO_F32 && pool_dtype == CHOREO_F32) K1(float, float);
@@ -180,11 +184,11 @@ int choreo_rerotate(void* k_pool, int pool_dtype, int n_layers, int n_kv, int n_
   auto s = as_stream(stream);
   const size_t smem = sizeof(float) * head_dim;
   if (pool_dtype == CHOREO_BF16)
-    rerotate_kernel<__nv_bfloat16, 4><<<(int)blocks, 256, smem, s>>>(
+    launch_k(rerotate_kernel<__nv_bfloat16, 4>, (int)blocks, 256, smem, s, 
         (__nv_bfloat16*)k_pool, n_kv, n_pages, page_size, head_dim, pages, page_len, delta, n_list,
         cos_t, sin_t, max_delta);
   else
-    rerotate_kernel<float, 4><<<(int)blocks, 256, smem, s>>>((float*)k_pool, n_kv, n_pages, page_size,
+    launch_k(rerotate_kernel<float, 4>, (int)blocks, 256, smem, s, (float*)k_pool, n_kv, n_pages, page_size,
                                                             head_dim, pages, page_len, delta, n_list,
                                                             cos_t, sin_t, max_delta);
   return launch_status("choreo_rerotate");

@@ -391,11 +391,10 @@ class Engine:
                 continue
             greedy_tok = None
             n_own = len(owners)
-            split = int(self._runner.split)
             if any(s.forced is None and s.call.sampling.mode == "greedy" for s in owners):
                 out = torch.empty(n_own, dtype=torch.int32, device=self.device)
                 nat.select_greedy(logits.data_ptr(), n_own, logits.shape[1], logits.shape[1],
-                                  split, out.data_ptr(),
+                                  0, out.data_ptr(),
                                   torch.cuda.current_stream(self.device).cuda_stream)
                 self._runner.launches += 1
                 greedy_tok = out.cpu().numpy()
@@ -405,7 +404,7 @@ class Engine:
                                          for s in owners):
                 hl = logits.double().cpu().numpy()
                 self.d2h_bytes += logits.nbytes
-                host_logits = hl[:n_own] + hl[n_own:] if split else hl
+                host_logits = hl
             elif greedy_tok is None and any(s.sel == 0 for s in owners):
                 # all forced: the host already knows the tokens; synchronise only at a
                 # message's first selection so its TTFT is the time its logits exist

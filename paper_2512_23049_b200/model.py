@@ -18,6 +18,7 @@ cuBLAS GEMMs via torch (bf16 in, f32 accumulate); the residual stream is f32.
 
 from __future__ import annotations
 
+import ctypes
 import os
 from dataclasses import dataclass
 
@@ -156,6 +157,59 @@ class Runner:
         self.split = self.dt == torch.bfloat16 and split_activations
         # K5 tensor-core precision: bit0 Q hi/lo, bit1 P hi/lo (env override for studies)
         self.attn_flags = int(os.environ.get("CHOREO_ATTN_FLAGS", "3"))
+        # K7 weight-streaming linear for decode-sized bf16 steps (cuBLAS above 64 GEMM rows)
+        self.k7 = self.dt == torch.bfloat16 and os.environ.get("CHOREO_K7", "1") != "0"
+        self._k7_ws = self._k7_cnt = None
+        # decode-sized bf16 steps run their layer loop in the native executor
+        # (choreo_decode_layers: one library call per step instead of ~11 per layer)
+        self.native_step = os.environ.get("CHOREO_NATIVE_STEP", "1") != "0"
+        self._wptrs = None
+        self._ev_free: list = []
+        self._ev_pending: list = []  # (event array, algorithmic bytes) awaiting readback
+        self.attn_times: list = []  # (ms, algorithmic bytes) per timed attention launch
+
+    def _weight_ptrs(self):
+        if self._wptrs is None:
+            L = len(self.w.layers)
+            self._wptrs = {n: (ctypes.c_void_p * L)(*[lw[n].data_ptr() for lw in self.w.layers])
+                           for n in ("attn_norm", "w_qkv", "wo", "ffn_norm", "w_gu", "w_down")}
+        return self._wptrs
+
+    def _retire_events(self, keep: int) -> None:
+        """Read back native K5 timing events older than `keep` steps (they completed long
+        ago, so this does not stall the launch pipeline) and recycle them."""
+        while len(self._ev_pending) > keep:
+            arr, nbytes = self._ev_pending.pop(0)
+            n = len(arr) // 2
+            ms = (ctypes.c_float * n)()
+            nat.events_elapsed(arr, n, ms)
+            self.attn_times.extend((float(m), nbytes) for m in ms)
+            self._ev_free.append(arr)
+
+    def collect_attn_times(self) -> list:
+        """(ms, algorithmic bytes) of every attention launch timed so far (both paths)."""
+        self._retire_events(0)
+        out = list(self.attn_times)
+        if self.attn_events:
+            out += [(a.elapsed_time(b), nb) for a, b, nb in self.attn_events]
+        return out
+
+    def _k7_ok(self, rows: int) -> bool:
+        """K7 takes the step when its stacked GEMM input has <= 64 rows."""
+        return self.k7 and (2 * rows if self.split else rows) <= 64
+
+    def _lin(self, a, w, rows: int):
+        """f32 [rows, N] = a @ w^T through K7; a holds the step's GEMM input rows (hi/lo
+        stacked when split; the halves are summed in K7's epilogue)."""
+        if self._k7_ws is None:
+            self._lin_buffers()
+        n, k = w.shape
+        y = torch.empty(rows, n, dtype=torch.float32, device=self.dev)
+        nat.linear_skinny(a.data_ptr(), a.shape[0], int(self.split), w.data_ptr(), n, k,
+                          y.data_ptr(), self._k7_ws.data_ptr(), self._k7_cnt.data_ptr(), 0,
+                          torch.cuda.current_stream(self.dev).cuda_stream)
+        self.launches += 1
+        return y
 
     def _mm(self, a, w, out_f32: bool):
         if out_f32 and a.dtype != torch.float32:
@@ -177,9 +231,60 @@ class Runner:
         return (2 * toks * cfg.kv_heads * cfg.head_dim * elt + R * cfg.n_heads * cfg.head_dim * 4
                 + n_parts * cfg.n_heads * (cfg.head_dim + 1) * 4)
 
+    def _native_layers(self, R, q, part_o, part_lse, attn, h, act, x, pos_d, page_d, slot_d, fat,
+                       counts, n_items, row_part_off, row_part, attn_bytes, stream):
+        """All layers of a decode-sized step through choreo_decode_layers; returns the last
+        layer's down_proj output (hi/lo summed)."""
+        cfg, cache, dev = self.cfg, self.cache, self.dev
+        L, d, hd = len(self.w.layers), self.d, cfg.head_dim
+        n_qkv = (cfg.n_heads + 2 * cfg.kv_heads) * hd
+        if self._k7_ws is None:
+            self._lin_buffers()
+        f32 = torch.float32
+        qkv = torch.empty(R, n_qkv, dtype=f32, device=dev)
+        ao = torch.empty(R, d, dtype=f32, device=dev)
+        gu = torch.empty(R, 2 * cfg.ffn_dim, dtype=f32, device=dev)
+        delta = torch.empty(R, d, dtype=f32, device=dev)
+        wp = self._weight_ptrs()
+        ev = None
+        if self.attn_events is not None:
+            ev = self._ev_free.pop() if self._ev_free else None
+            if ev is None:
+                ev = (ctypes.c_void_p * (2 * L))()
+                nat.events_create(ev, 2 * L)
+        st = nat.DecodeStep(
+            n_layers=L, d=d, n_heads=cfg.n_heads, n_kv=cfg.kv_heads, head_dim=hd,
+            ffn_dim=cfg.ffn_dim, attn_norm=ctypes.cast(wp["attn_norm"], ctypes.c_void_p),
+            w_qkv=ctypes.cast(wp["w_qkv"], ctypes.c_void_p), wo=ctypes.cast(wp["wo"], ctypes.c_void_p),
+            ffn_norm=ctypes.cast(wp["ffn_norm"], ctypes.c_void_p),
+            w_gu=ctypes.cast(wp["w_gu"], ctypes.c_void_p),
+            w_down=ctypes.cast(wp["w_down"], ctypes.c_void_p), eps=RMS_EPS,
+            k_pool=cache.k_pool.data_ptr(), v_pool=cache.v_pool.data_ptr(), n_pages=cache.n_pages,
+            page_size=cache.page_size, cos_t=self.rot.cos.data_ptr(), sin_t=self.rot.sin.data_ptr(),
+            max_delta=self.rot.max_delta, n_rows=R, split=int(self.split),
+            attn_flags=self.attn_flags, n_items=n_items, pos=pos_d.data_ptr(),
+            page=page_d.data_ptr(), slot=slot_d.data_ptr(), fat=fat.data_ptr(),
+            counts=counts.data_ptr(), row_part_off=row_part_off.data_ptr(),
+            row_part=row_part.data_ptr(), x=x.data_ptr(), delta_in=None, h=h.data_ptr(),
+            qkv=qkv.data_ptr(), q=q.data_ptr(), part_o=part_o.data_ptr(),
+            part_lse=part_lse.data_ptr(), attn=attn.data_ptr(), ao=ao.data_ptr(), gu=gu.data_ptr(),
+            act=act.data_ptr(), delta=delta.data_ptr(), k7_ws=self._k7_ws.data_ptr(),
+            k7_cnt=self._k7_cnt.data_ptr(),
+            attn_events=ctypes.cast(ev, ctypes.c_void_p) if ev is not None else None)
+        nat.decode_layers(ctypes.byref(st), stream)
+        if ev is not None:
+            self._ev_pending.append((ev, attn_bytes))
+            self._retire_events(8)
+        return delta
+
+    def _lin_buffers(self) -> None:
+        self._k7_ws = torch.empty(148 * 2 * 64 * 128, dtype=torch.float32, device=self.dev)
+        n_max = max(self.w.out_head.shape[0], self.w.layers[0]["w_gu"].shape[0],
+                    self.w.layers[0]["w_qkv"].shape[0], self.d)
+        self._k7_cnt = torch.zeros(cdiv(n_max, 128) + 1, dtype=torch.int32, device=self.dev)
+
     def forward(self, plan: StepPlan) -> torch.Tensor | None:
-        """Run one step; returns f32 logits [S * n_logit_rows, V] (S = 2 when split:
-        rows i and n + i are the hi/lo halves to be summed) or None."""
+        """Run one step; returns f32 logits [n_logit_rows, V] or None."""
         cfg, cache = self.cfg, self.cache
         stream = torch.cuda.current_stream(self.dev).cuda_stream
         R = plan.n_rows
@@ -277,6 +382,11 @@ class Runner:
 
         S = 2 if self.split else 1  # stacked hi/lo activation rows
         sp = int(self.split)
+        k7 = self._k7_ok(R)
+        # GEMM outputs: K7 already summed the hi/lo halves (isp = 0); cuBLAS outputs keep
+        # them stacked for the consumer to add (isp = sp)
+        isp = 0 if k7 else sp
+        mm = (lambda a, w: self._lin(a, w, R)) if k7 else (lambda a, w: self._mm(a, w, True))
         x = torch.empty(R, d, dtype=torch.float32, device=self.dev)
         nat.embed(self.w.embed.data_ptr(), self.dtc, d, ids_d.data_ptr(), R, x.data_ptr(), stream)
         q = torch.empty(R, H, hd, dtype=torch.float32, device=self.dev)
@@ -287,12 +397,19 @@ class Runner:
         act = torch.empty(S * R, cfg.ffn_dim, dtype=self.dt, device=self.dev)
         delta = None
         launches = 2
-        for layer, lw in enumerate(self.w.layers):
-            nat.residual_rmsnorm(x.data_ptr(), nat.ptr(delta), nat.F32, sp,
+        native = (fused and k7 and self.native_step and self.tp is None and not self.fused_combine
+                  and self.dt == torch.bfloat16)
+        if native:
+            delta = self._native_layers(R, q, part_o, part_lse, attn, h, act, x, pos_d, page_d,
+                                        slot_d, fat, counts, n_items, row_part_off, row_part,
+                                        attn_bytes, stream)
+            launches += 10 * len(self.w.layers)
+        for layer, lw in enumerate([] if native else self.w.layers):
+            nat.residual_rmsnorm(x.data_ptr(), nat.ptr(delta), nat.F32, isp,
                                  lw["attn_norm"].data_ptr(), self.dtc, R, d, RMS_EPS, h.data_ptr(),
                                  self.dtc, sp, None, 0, stream)
-            qkv = self._mm(h, lw["w_qkv"], out_f32=True)
-            nat.rope_append(qkv.data_ptr(), nat.F32, qkv.shape[1], R, sp, pos_d.data_ptr(),
+            qkv = mm(h, lw["w_qkv"])
+            nat.rope_append(qkv.data_ptr(), nat.F32, qkv.shape[1], R, isp, pos_d.data_ptr(),
                             page_d.data_ptr(), slot_d.data_ptr(), q.data_ptr(),
                             cache.k_pool.data_ptr(), cache.v_pool.data_ptr(), self.pool_dtc, layer,
                             Hk, cache.n_pages, P, H, hd, self.rot.cos.data_ptr(),
@@ -330,20 +447,20 @@ class Runner:
                 nat.attn_combine(part_o.data_ptr(), part_lse.data_ptr(), row_part_off.data_ptr(),
                                  row_part.data_ptr(), R, H, hd, attn.data_ptr(), self.dtc, sp,
                                  stream)
-            ao = self._mm(attn, lw["wo"], out_f32=True)
+            ao = mm(attn, lw["wo"])
             if self.tp is not None and self.tp.size > 1:  # row-parallel o_proj: sum partials
                 torch.distributed.all_reduce(ao, group=self.tp_group)
-            nat.residual_rmsnorm(x.data_ptr(), ao.data_ptr(), nat.F32, sp,
+            nat.residual_rmsnorm(x.data_ptr(), ao.data_ptr(), nat.F32, isp,
                                  lw["ffn_norm"].data_ptr(), self.dtc, R, d, RMS_EPS, h.data_ptr(),
                                  self.dtc, sp, None, 0, stream)
-            gu = self._mm(h, lw["w_gu"], out_f32=True)  # f32 pre-activations (parity)
-            nat.silu_mul(gu.data_ptr(), nat.F32, sp, R, cfg.ffn_dim, act.data_ptr(), self.dtc, sp,
+            gu = mm(h, lw["w_gu"])  # f32 pre-activations (parity)
+            nat.silu_mul(gu.data_ptr(), nat.F32, isp, R, cfg.ffn_dim, act.data_ptr(), self.dtc, sp,
                          stream)
-            delta = self._mm(act, lw["w_down"], out_f32=True)
+            delta = mm(act, lw["w_down"])
             if self.tp is not None and self.tp.size > 1:  # row-parallel down_proj
                 torch.distributed.all_reduce(delta, group=self.tp_group)
             launches += 6
-        nat.residual_rmsnorm(x.data_ptr(), delta.data_ptr(), nat.F32, sp, None, 0, R, d, RMS_EPS,
+        nat.residual_rmsnorm(x.data_ptr(), delta.data_ptr(), nat.F32, isp, None, 0, R, d, RMS_EPS,
                              None, 0, 0, None, 0, stream)
         launches += 1
         self.launches += launches
@@ -354,7 +471,12 @@ class Runner:
                                  R, d, RMS_EPS, xn.data_ptr(), self.dtc, sp, logit_d.data_ptr(),
                                  n_log, stream)
             self.launches += 1
-            logits = self._mm(xn, self.w.out_head, out_f32=True)
+            if self._k7_ok(n_log):
+                logits = self._lin(xn, self.w.out_head, n_log)
+            else:
+                logits = self._mm(xn, self.w.out_head, out_f32=True)
+                if self.split:
+                    logits = logits[:n_log] + logits[n_log:]
         if self.step_events is not None:
             sev1 = torch.cuda.Event(enable_timing=True)
             sev1.record()

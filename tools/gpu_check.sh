@@ -1,7 +1,8 @@
+# GPU gate: parity tests, smoke, bench (optionally BENCH_ARGS).
 set -x
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
 tail -5 gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -3 gpurun_out/smoke.log
-timeout 1200 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?"; tail -c 4000 gpurun_out/bench.log
+timeout 1200 python bench.py $BENCH_ARGS > gpurun_out/bench.log 2>&1; echo "bench rc=$?"; tail -c 4000 gpurun_out/bench.log

@@ -276,6 +276,52 @@ def k5_decode(n_workflows: int = 1, agents: int = 8, tc: bool = False, fused: bo
             "pages_per_item": ppi}
 
 
+def k7_linear(x_rows: int = 8, split: bool = True) -> list:
+    """K7 weight-streaming linear vs cuBLAS (torch.mm, f32 out) at the 8B decode shapes.
+    Each timed launch reads a different weight copy (copies total > 3x L2), so every
+    launch streams its weights from HBM.  bytes = weight bytes + activations + output."""
+    cfg = LLAMA_3_1_8B
+    d, f = cfg.model_dim, cfg.ffn_dim
+    shapes = {"qkv": ((cfg.n_heads + 2 * cfg.kv_heads) * cfg.head_dim, d), "o_proj": (d, d),
+              "gate_up": (2 * f, d), "down": (d, f), "head": (cfg.vocab_size, d)}
+    rows = 2 * x_rows if split else x_rows
+    ws = torch.empty(148 * 2 * 64 * 128, device="cuda")
+    pk = peaks()
+    out = []
+    stream = torch.cuda.current_stream().cuda_stream
+    for name, (n, k) in shapes.items():
+        ncopy = max(2, int(400e6 // (n * k * 2)) + 1)
+        ws_list = [torch.randn(n, k, device="cuda").to(torch.bfloat16) for _ in range(ncopy)]
+        x = torch.randn(rows, k, device="cuda").to(torch.bfloat16)
+        y = torch.empty(x_rows, n, device="cuda")
+        cnt = torch.zeros((n + 127) // 128, dtype=torch.int32, device="cuda")
+        it = [0]
+
+        def ours():
+            w = ws_list[it[0] % ncopy]
+            it[0] += 1
+            nat.linear_skinny(x.data_ptr(), rows, int(split), w.data_ptr(), n, k, y.data_ptr(),
+                              ws.data_ptr(), cnt.data_ptr(), 0, stream)
+
+        def cublas():
+            w = ws_list[it[0] % ncopy]
+            it[0] += 1
+            torch.mm(x, w.t(), out_dtype=torch.float32)
+        t_ours = _time(ours, burst=ncopy)
+        t_cb = _time(cublas, burst=ncopy)
+        nbytes = n * k * 2 + rows * k * 2 + x_rows * n * 4
+        ach = nbytes / t_ours / 1e9
+        out.append({"kernel": f"choreo_linear_skinny (K7) {name}", "bound": "hbm",
+                    "shape": f"{rows}x{k} @ {n}x{k}^T", "algorithmic_bytes": nbytes,
+                    "us": round(t_ours * 1e6, 2), "achieved": round(ach, 1), "unit": "GB/s",
+                    "peak": pk["hbm_gbs"], "frac": round(ach / pk["hbm_gbs"], 4),
+                    "cublas_us": round(t_cb * 1e6, 2),
+                    "cublas_frac": round(nbytes / t_cb / 1e9 / pk["hbm_gbs"], 4)})
+        del ws_list
+        torch.cuda.empty_cache()
+    return out
+
+
 def k5_sweep() -> list:
     out = []
     for tc in (False, True):
@@ -295,6 +341,10 @@ def run_all() -> list:
 
 
 if __name__ == "__main__":
+    if "--k7" in sys.argv:
+        for r in k7_linear():
+            print(json.dumps(r))
+        sys.exit(0)
     if "--k5-sweep" in sys.argv:
         print(k5_sweep())
         sys.exit(0)
