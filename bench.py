@@ -342,10 +342,12 @@ def main() -> None:
         for i in range(args.steps):
             eng.reset()
             runner.attn_events = attn_events if i == args.steps - 1 else None
+            runner.time_linear = i == args.steps - 1
             res = run_debate(eng, P, inputs[i], args.agents, args.rounds)
             ttft += res["ttft"]
             generated += res["generated"]
         runner.attn_events = None
+        runner.time_linear = False
         ev_end.record()
         sync_all()
     runner.step_events = None
@@ -369,10 +371,10 @@ def main() -> None:
     timed = runner.collect_attn_times()
     a_ms = [m for m, _ in timed]
     a_bytes = [nb for _, nb in timed]
-    roofline = None
+    attn_roofline = None
     if a_ms:
         achieved = (sum(a_bytes) / len(a_bytes)) / (sum(a_ms) / len(a_ms) / 1e3) / 1e9
-        roofline = {"kernel": "choreo_decode_attn (K5: page-centric split-KV decode attention)",
+        attn_roofline = {"kernel": "choreo_decode_attn_v2 (K5: page-centric split-KV decode attention, TMA page ring)",
                     "bound": "hbm",
                     "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                     "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": None,
@@ -380,6 +382,22 @@ def main() -> None:
                     "avg_launch_us": round(1e3 * sum(a_ms) / len(a_ms), 2),
                     "algorithmic_bytes_per_launch": int(sum(a_bytes) / len(a_bytes)),
                     "launches_timed": len(a_ms)}
+    # the decode step's dominant kernel: K7 weight streaming (4 launches per layer)
+    roofline = None
+    lin = runner.linear_times
+    if lin:
+        l_ms = sum(m for m, _ in lin) / len(lin)
+        l_b = sum(b for _, b in lin) / len(lin)
+        ach = l_b / (l_ms / 1e3) / 1e9
+        roofline = {"kernel": "choreo_linear_skinny (K7: tcgen05 stream-K weight-streaming "
+                              "linear, qkv / o_proj / gate|up / down of every decode layer)",
+                    "bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"],
+                    "unit": "GB/s", "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": None,
+                    "peak_source": peaks["source"], "avg_launch_us": round(1e3 * l_ms, 2),
+                    "algorithmic_bytes_per_launch": int(l_b), "launches_timed": len(lin),
+                    "note": "CUDA events on the launching stream around each launch of the last "
+                            "timed workflow; the brackets remove the launch's programmatic-"
+                            "dependent-launch overlap, so this is conservative"}
 
     if rank != 0:
         if world > 1:
@@ -395,7 +413,8 @@ def main() -> None:
 
         del eng, weights
         torch.cuda.empty_cache()
-        kernels = [kb.k2_rerotate(), kb.k4_prefill(), kb.k5_decode(1), kb.k5_decode(8)]
+        kernels = ([kb.k2_rerotate(), kb.k4_prefill(), kb.k5_decode(1, v2=True),
+                    kb.k5_decode(8, v2=True)] + kb.k7_linear())
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_reference_sample(args.agents, args.ref_tokens)
@@ -419,6 +438,7 @@ def main() -> None:
         "gpu_launches": int(launches),
         "generated_tokens": int(generated_all),
         "roofline": roofline,
+        "attention_roofline": attn_roofline,
         "kernel_rooflines": kernels,
         "reencode_baseline": reencode,
         "cpu_baseline": cpu,

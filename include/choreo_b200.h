@@ -190,6 +190,20 @@ int choreo_attn_combine(const float* part_o, const float* part_lse, const int32_
 int choreo_select_greedy(const float* logits, int n_rows, int ld, int vocab, int split,
                          int32_t* out_tok, void* stream);
 
+/* K5 v2 decode attention over K3 page-centric items (bf16 pools, page_size 64, head_dim
+ * 64/128, n_heads / n_kv <= 32, items built with rows_per_block <= 32 / G): persistent CTAs
+ * (grid_ctas <= 0: min(148, items * n_kv)), a TMA producer warp streaming K/V pages into a
+ * 5-slot shared-memory ring and 8 mma.sync consumer warps (4 key slices x 2 m16 tiles);
+ * plain bf16 Q and P, f32 accumulation.  Writes one normalised partial + LSE per
+ * (block row, head) like choreo_attn_split; merge with choreo_attn_combine.
+ * n_layers sizes the pool's TMA view.  Replaces model.py:177-184 for decode steps. */
+int choreo_decode_attn_v2(const float* q, const void* k_pool, const void* v_pool, int n_layers,
+                          int layer, int n_kv, int n_pages, int page_size, int n_heads,
+                          int head_dim, const int32_t* row_t, const int32_t* vis_page,
+                          const int32_t* vis_len, const int32_t* vis_own, const int32_t* blk_rows,
+                          const int32_t* items, const int32_t* counts, int max_items,
+                          float* part_o, float* part_lse, int grid_ctas, void* stream);
+
 /* K7 decode-sized linear layer (weight streaming, tcgen05 + TMA, stream-K):
  *   y[r][n] = sum_k x[r][k] * w[n][k]      x: bf16 [x_rows][k], w: bf16 [n][k] (out, in),
  *                                          y: f32 [x_rows / (1 + split)][n].
@@ -206,7 +220,7 @@ int choreo_linear_skinny(const void* x, int x_rows, int split, const void* w, in
 /* Native decode-step executor: every layer of a decode-sized bf16 step (split hi/lo
  * activations or plain bf16; page_size 64; fused K5 items from choreo_assemble with a
  * fat buffer) issued in one call — per layer: residual_rmsnorm, K7 qkv, K1 rope_append,
- * K5 decode attention, combine, K7 o_proj, residual_rmsnorm, K7 gate|up, silu_mul,
+ * K5 decode attention (v1 fused items or v2 TMA ring), combine, K7 o_proj, residual_rmsnorm, K7 gate|up, silu_mul,
  * K7 down.  Replaces the per-layer loop of model.py:169-189.  Weight arrays are HOST
  * arrays of n_layers DEVICE pointers (bf16, (out, in) layout).  On return `delta` holds
  * the last layer's down_proj output (the caller adds it and runs the final norm / head).
@@ -249,6 +263,18 @@ typedef struct {
   float* k7_ws;
   int* k7_cnt;
   void** attn_events;
+  /* attention kernel: 0 = choreo_decode_attn over `fat` items, 1 = choreo_decode_attn_v2
+   * over the K3 arrays below (row_t, vis_*, blk_rows, items) */
+  int attn_kernel;
+  const int32_t* row_t;
+  const int32_t* vis_page;
+  const int32_t* vis_len;
+  const int32_t* vis_own;
+  const int32_t* blk_rows;
+  const int32_t* items;
+  /* optional host array of 8 * n_layers cudaEvent_t recorded around the layer's four K7
+   * launches (qkv, o_proj, gate|up, down); NULL: none */
+  void** linear_events;
 } ChoreoDecodeStep;
 
 int choreo_decode_layers(const ChoreoDecodeStep* step, void* stream);

@@ -42,6 +42,8 @@ SIGNATURES: dict[str, list] = {
     "choreo_selftest_umma": [_P, _P, _P, _P, _P, _P, _P],
     "choreo_linear_skinny": [_P, _I, _I, _P, _I, _I, _P, _P, _P, _I, _P],
     "choreo_decode_layers": [_P, _P],
+    "choreo_decode_attn_v2": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P,
+                              _I, _P, _P, _I, _P],
     "choreo_events_create": [_P, _I],
     "choreo_events_elapsed": [_P, _I, _P],
     "choreo_events_destroy": [_P, _I],
@@ -100,6 +102,7 @@ select_greedy = _Caller("choreo_select_greedy")
 selftest_umma = _Caller("choreo_selftest_umma")
 linear_skinny = _Caller("choreo_linear_skinny")
 decode_layers = _Caller("choreo_decode_layers")
+decode_attn_v2 = _Caller("choreo_decode_attn_v2")
 events_create = _Caller("choreo_events_create")
 events_elapsed = _Caller("choreo_events_elapsed")
 events_destroy = _Caller("choreo_events_destroy")
@@ -115,7 +118,10 @@ class DecodeStep(ctypes.Structure):
          ("attn_flags", _I), ("n_items", _I)] + \
         [(n, _P) for n in ("pos", "page", "slot", "fat", "counts", "row_part_off", "row_part",
                            "x", "delta_in", "h", "qkv", "q", "part_o", "part_lse", "attn", "ao",
-                           "gu", "act", "delta", "k7_ws", "k7_cnt", "attn_events")]
+                           "gu", "act", "delta", "k7_ws", "k7_cnt", "attn_events")] + \
+        [("attn_kernel", _I)] + \
+        [(n, _P) for n in ("row_t", "vis_page", "vis_len", "vis_own", "blk_rows", "items",
+                           "linear_events")]
 
 
 def ptr(t) -> int | None:

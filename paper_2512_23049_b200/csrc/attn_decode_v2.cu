@@ -1,0 +1,499 @@
+// K5 (v2) choreographed decode attention: TMA page ring + FA2-style mma.sync consumers.
+//
+// Work unit = (K3 item, kv head): a block of <= 32 / G rows that all see a run of pages
+// (page-centric K3 items gather every agent that lists a parent message, so a shared
+// parent page is read from HBM once per step for all agents).  Per CTA (persistent, one
+// per SM):
+//   warp 8      TMA producer: streams each unit's K and V pages (2D tensor maps over the
+//               pool, SW128 boxes of 64 keys x 64 dims) into a 4-slot ring, mbarriers;
+//   warp 9      unit loader: stages the next unit's rows, page lengths and Q (cp.async) in smem;
+//   warps 0-7   consumers, warp = (key slice q4 in 0..3, m-tile mt in 0..1): every page's
+//               64 keys are split four ways (16 keys per warp), the <= 32 (row, query head)
+//               vectors in two m16 tiles; S = Q K^T and O += P V on mma.sync m16n8k16
+//               (bf16 in, f32 accumulate) with K / V fragments from ldmatrix on the swizzled
+//               tiles, online softmax in registers (lazy O rescale), no per-page CTA barrier;
+//   unit end    the four key-slice states of an m-tile are merged through shared memory
+//               (asynchronously: slices 1-3 hand over and move on) and one normalised
+//               partial + LSE per (row, head) is written for the combine.
+// Masking: slot s of a page is visible to row r iff s < page_len and, for the row's own
+// pages, own_base + s <= row_t[r] (reference masking.py:36-40, model.py:166-168, 177-184).
+#include <cudaTypedefs.h>
+#include <math.h>
+
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace choreo {
+
+constexpr int kDvSlots = 4;        // K/V page ring
+constexpr int kDvConsumers = 8;    // warps 0-7
+constexpr int kDvProducer = 8;     // warp 8: TMA
+constexpr int kDvLoader = 9;       // warp 9: unit metadata + Q staging
+constexpr int kDvThreads = 32 * 10;
+constexpr int kDvMaxPages = 32;    // pages per unit staged in the unit record (host: ppi <= 32)
+
+struct DvParams {
+  const float* q;
+  int layer, n_kv, n_pages, n_heads;
+  const int32_t* row_t;
+  const int32_t* vis_page;
+  const int32_t* vis_len;
+  const int32_t* vis_own;
+  const int32_t* blk_rows;
+  const int32_t* items;
+  const int32_t* counts;
+  float* part_o;
+  float* part_lse;
+  float scale_log2;
+};
+
+template <int HD>
+struct DvCfg {
+  static constexpr int kR = HD / 64;                      // 64-dim SW128 halves per page
+  static constexpr int kHalf = 64 * 128;                  // bytes of one [64][64] bf16 tile
+  static constexpr int kSlot = 2 * kR * kHalf;            // K + V of one page
+  static constexpr int kMergeRow = HD + 2;                // O row + m + l (floats)
+  static constexpr int kMerge = 3 * 2 * 16 * kMergeRow * 4;
+  static constexpr int kQLd = HD + 4;                     // padded f32 Q row
+  // unit record: ints [0] M [1] vb [2] nv [3] pbase [4] kvh, [8..40) row_t per vector,
+  // [40..72) page len, [72..104) own base; then Q f32 [32][kQLd] (cp.async from q)
+  static constexpr int kUnitInts = 128;
+  static constexpr int kUnit = kUnitInts * 4 + 32 * kQLd * 4;
+  static constexpr int kTotal = kDvSlots * kSlot + kMerge + 2 * kUnit + 1024;
+};
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                        uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                          uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void mma_bf16(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ float dv_ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// shared address of (key, 16-byte dim chunk c) in a page's K or V area (SW128 halves)
+__device__ __forceinline__ uint32_t dv_addr(uint32_t base, int key, int c) {
+  return base + (c >> 3) * (64 * 128) + key * 128 + ((((c & 7) ^ (key & 7))) << 4);
+}
+
+template <int HD>
+__global__ void __launch_bounds__(kDvThreads, 1)
+    decode_attn_v2(DvParams p, const __grid_constant__ CUtensorMap tmK,
+                   const __grid_constant__ CUtensorMap tmV) {
+  using namespace sm100;
+  using C = DvCfg<HD>;
+  constexpr int KS = HD / 16;  // k-steps of QK^T
+  constexpr int NT = HD / 8;   // n-tiles of O
+  pdl_trigger();
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* merge = reinterpret_cast<float*>(base + kDvSlots * C::kSlot);
+  uint8_t* units = base + kDvSlots * C::kSlot + C::kMerge;  // [2][kUnit]
+  __shared__ uint64_t full_bar[kDvSlots], empty_bar[kDvSlots];
+  __shared__ uint64_t unit_full[2], unit_empty[2], merge_full, merge_empty;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int G = p.n_heads / p.n_kv;
+  const int n_work = p.counts[1] * p.n_kv;
+  if (tid == 0) {
+    for (int i = 0; i < kDvSlots; ++i) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], kDvConsumers);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&unit_full[i], 32);
+      mbar_init(&unit_empty[i], kDvConsumers);
+    }
+    mbar_init(&merge_full, 6);
+    mbar_init(&merge_empty, 2);
+    fence_barrier_init();
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+  }
+  __syncthreads();
+  pdl_wait();
+
+  if (warp == kDvLoader) {
+    // ------------------------------------------------------------------ unit loader
+    // stages each unit's metadata and its Q vectors (bf16, pre-scaled to the log2 domain)
+    // one unit ahead of the consumers, so a unit boundary costs no dependent global loads
+    int u = 0;
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++u) {
+      const int sl = u & 1;
+      mbar_wait(&unit_empty[sl], ((u >> 1) & 1) ^ 1);
+      int* ui = reinterpret_cast<int*>(units + sl * C::kUnit);
+      float* qf = reinterpret_cast<float*>(units + sl * C::kUnit + C::kUnitInts * 4);
+      const int32_t* it = p.items + 6 * (w / p.n_kv);
+      const int iv = lane < 5 ? it[lane] : 0;
+      const int rb = __shfl_sync(0xffffffffu, iv, 0), nr = __shfl_sync(0xffffffffu, iv, 1);
+      const int vb = __shfl_sync(0xffffffffu, iv, 2), nv = __shfl_sync(0xffffffffu, iv, 3);
+      const int kvh = w % p.n_kv, M = nr * G;
+      const int rid = lane < M ? p.blk_rows[rb + lane / G] : 0;
+      // Q vectors of the unit straight into shared memory (f32, one round trip)
+      for (int m = 0; m < M; ++m) {  // warp-uniform loop: lane = 16-byte chunk of vector m
+        const int r = __shfl_sync(0xffffffffu, rid, m);
+        if (4 * lane < HD) {
+          const float* src = p.q + ((int64_t)r * p.n_heads + kvh * G + m % G) * HD + 4 * lane;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_addr(qf + m * C::kQLd + 4 * lane)),
+                       "l"(src));
+        }
+      }
+      asm volatile("cp.async.commit_group;\n" ::);
+      const int pbase = __shfl_sync(0xffffffffu, iv, 4);
+      if (lane == 0) {
+        ui[0] = M;
+        ui[1] = vb;
+        ui[2] = nv;
+        ui[3] = pbase;
+        ui[4] = kvh;
+      }
+      ui[8 + lane] = lane < M ? p.row_t[rid] : -1;
+      ui[40 + lane] = lane < nv ? p.vis_len[vb + lane] : 0;
+      ui[72 + lane] = lane < nv ? p.vis_own[vb + lane] : -1;
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      mbar_arrive(&unit_full[sl]);
+    }
+    return;
+  }
+  if (warp == kDvProducer) {
+    // ------------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      uint32_t gp = 0;
+      for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+        const int32_t* it = p.items + 6 * (w / p.n_kv);
+        const int kvh = w % p.n_kv, vb = it[2], nv = it[3];
+        for (int j = 0; j < nv; ++j, ++gp) {
+          const int st = gp % kDvSlots;
+          mbar_wait(&empty_bar[st], ((gp / kDvSlots) & 1) ^ 1);
+          const int row0 = ((p.layer * p.n_kv + kvh) * p.n_pages + p.vis_page[vb + j]) * 64;
+          uint8_t* dst = base + st * C::kSlot;
+          mbar_arrive_expect_tx(&full_bar[st], C::kSlot);
+#pragma unroll
+          for (int r = 0; r < C::kR; ++r) {
+            tma_load_2d(dst + r * C::kHalf, &tmK, &full_bar[st], r * 64, row0);
+            tma_load_2d(dst + (C::kR + r) * C::kHalf, &tmV, &full_bar[st], r * 64, row0);
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------------- consumers
+  const int q4 = warp >> 1, mt = warp & 1;  // key slice, m-tile
+  const int g = lane >> 2, t = lane & 3;
+  const int k0 = 16 * q4;                   // first key of this warp's slice
+  uint32_t gp = 0;
+  int u = 0;
+  for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++u) {
+    const int sl = u & 1;
+    mbar_wait(&unit_full[sl], (u >> 1) & 1);
+    const int* ui = reinterpret_cast<const int*>(units + sl * C::kUnit);
+    const float* qf = reinterpret_cast<const float*>(units + sl * C::kUnit + C::kUnitInts * 4);
+    const int M = ui[0], nv = ui[2], pbase = ui[3], kvh = ui[4];
+    const bool active = mt * 16 < M;  // warp-uniform: this m-tile has query vectors
+    const int mA = mt * 16 + g, mB = mA + 8;
+    const bool vA = mA < M, vB = mB < M;
+    const int rtA = ui[8 + mA], rtB = ui[8 + mB];
+    // Q as bf16 A fragments, pre-scaled to the log2 domain (rows past M are zero)
+    uint32_t qa[KS][4];
+    {
+      const float sc = p.scale_log2;
+      const float* qA = qf + (vA ? mA : 0) * C::kQLd;
+      const float* qB = qf + (vB ? mB : 0) * C::kQLd;
+      const float fa = vA ? sc : 0.f, fb = vB ? sc : 0.f;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const int c = 16 * ks + 2 * t;
+        const float2 a0 = *reinterpret_cast<const float2*>(qA + c);
+        const float2 a1 = *reinterpret_cast<const float2*>(qB + c);
+        const float2 a2 = *reinterpret_cast<const float2*>(qA + c + 8);
+        const float2 a3 = *reinterpret_cast<const float2*>(qB + c + 8);
+        qa[ks][0] = pack_bf16(a0.x * fa, a0.y * fa);
+        qa[ks][1] = pack_bf16(a1.x * fb, a1.y * fb);
+        qa[ks][2] = pack_bf16(a2.x * fa, a2.y * fa);
+        qa[ks][3] = pack_bf16(a3.x * fb, a3.y * fb);
+      }
+    }
+    float o[NT][4];
+#pragma unroll
+    for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+    float mxA = -INFINITY, mxB = -INFINITY, lA = 0.f, lB = 0.f;
+
+    for (int j = 0; j < nv; ++j, ++gp) {
+      const int st = gp % kDvSlots;
+      mbar_wait(&full_bar[st], (gp / kDvSlots) & 1);
+      if (active) {
+        const uint32_t kb = smem_addr(base + st * C::kSlot);
+        const uint32_t vbase = kb + C::kR * C::kHalf;
+        // ---- S = Q K^T over this warp's 16 keys (two n8 tiles, two chains each) ----
+        float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
+        float s0b[4] = {0.f, 0.f, 0.f, 0.f}, s1b[4] = {0.f, 0.f, 0.f, 0.f};
+        const int lk = k0 + ((lane >> 4) & 1) * 8 + (lane & 7);
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          uint32_t r0, r1, r2, r3;
+          ldsm_x4(dv_addr(kb, lk, 2 * ks + ((lane >> 3) & 1)), r0, r1, r2, r3);
+          if (ks & 1) {
+            mma_bf16(s0b, qa[ks], r0, r1);
+            mma_bf16(s1b, qa[ks], r2, r3);
+          } else {
+            mma_bf16(s0, qa[ks], r0, r1);
+            mma_bf16(s1, qa[ks], r2, r3);
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          s0[e] += s0b[e];
+          s1[e] += s1b[e];
+        }
+        // ---- mask (page length, causal cut of own pages) ----
+        const int len = ui[40 + j], own = ui[72 + j];
+        int limA = len, limB = len;
+        if (own >= 0) {
+          limA = min(limA, rtA - own + 1);
+          limB = min(limB, rtB - own + 1);
+        }
+        if (!__all_sync(0xffffffffu, limA >= k0 + 16 && limB >= k0 + 16)) {
+          const int ka = k0 + 2 * t;
+          s0[0] = ka < limA ? s0[0] : -INFINITY;
+          s0[1] = ka + 1 < limA ? s0[1] : -INFINITY;
+          s0[2] = ka < limB ? s0[2] : -INFINITY;
+          s0[3] = ka + 1 < limB ? s0[3] : -INFINITY;
+          s1[0] = ka + 8 < limA ? s1[0] : -INFINITY;
+          s1[1] = ka + 9 < limA ? s1[1] : -INFINITY;
+          s1[2] = ka + 8 < limB ? s1[2] : -INFINITY;
+          s1[3] = ka + 9 < limB ? s1[3] : -INFINITY;
+        }
+        // ---- online softmax (log2 domain, lazy rescale) ----
+        float tA = fmaxf(fmaxf(s0[0], s0[1]), fmaxf(s1[0], s1[1]));
+        float tB = fmaxf(fmaxf(s0[2], s0[3]), fmaxf(s1[2], s1[3]));
+        tA = fmaxf(tA, __shfl_xor_sync(0xffffffffu, tA, 1));
+        tA = fmaxf(tA, __shfl_xor_sync(0xffffffffu, tA, 2));
+        tB = fmaxf(tB, __shfl_xor_sync(0xffffffffu, tB, 1));
+        tB = fmaxf(tB, __shfl_xor_sync(0xffffffffu, tB, 2));
+        float aA = 1.f, aB = 1.f;
+        if (tA > mxA + 8.f || (mxA == -INFINITY && tA != -INFINITY)) {
+          aA = mxA == -INFINITY ? 0.f : dv_ex2(mxA - tA);
+          mxA = tA;
+        }
+        if (tB > mxB + 8.f || (mxB == -INFINITY && tB != -INFINITY)) {
+          aB = mxB == -INFINITY ? 0.f : dv_ex2(mxB - tB);
+          mxB = tB;
+        }
+        if (__any_sync(0xffffffffu, aA != 1.f || aB != 1.f)) {
+#pragma unroll
+          for (int n = 0; n < NT; ++n) {
+            o[n][0] *= aA;
+            o[n][1] *= aA;
+            o[n][2] *= aB;
+            o[n][3] *= aB;
+          }
+          lA *= aA;
+          lB *= aB;
+        }
+        const float nA = mxA == -INFINITY ? 0.f : mxA, nB = mxB == -INFINITY ? 0.f : mxB;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          s0[e] = dv_ex2(s0[e] - nA);
+          s1[e] = dv_ex2(s1[e] - nA);
+          s0[2 + e] = dv_ex2(s0[2 + e] - nB);
+          s1[2 + e] = dv_ex2(s1[2 + e] - nB);
+        }
+        lA += (s0[0] + s0[1]) + (s1[0] + s1[1]);
+        lB += (s0[2] + s0[3]) + (s1[2] + s1[3]);
+        uint32_t pa[4] = {pack_bf16(s0[0], s0[1]), pack_bf16(s0[2], s0[3]),
+                          pack_bf16(s1[0], s1[1]), pack_bf16(s1[2], s1[3])};
+        // ---- O += P V over the same 16 keys ----
+        const int lv = k0 + ((lane >> 3) & 1) * 8 + (lane & 7);
+#pragma unroll
+        for (int dp = 0; dp < HD / 16; ++dp) {
+          uint32_t r0, r1, r2, r3;
+          ldsm_x4_t(dv_addr(vbase, lv, 2 * dp + (lane >> 4)), r0, r1, r2, r3);
+          mma_bf16(o[2 * dp], pa, r0, r1);
+          mma_bf16(o[2 * dp + 1], pa, r2, r3);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[st]);
+    }
+
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&unit_empty[sl]);
+    // ---- merge the four key-slice states of each m-tile, write the partials ----
+    lA += __shfl_xor_sync(0xffffffffu, lA, 1);
+    lA += __shfl_xor_sync(0xffffffffu, lA, 2);
+    lB += __shfl_xor_sync(0xffffffffu, lB, 1);
+    lB += __shfl_xor_sync(0xffffffffu, lB, 2);
+    if (q4 > 0) {
+      if (u > 0) mbar_wait(&merge_empty, (u - 1) & 1);
+    }
+    if (q4 > 0 && active) {
+      float* sc = merge + ((q4 - 1) * 2 + mt) * 16 * C::kMergeRow;
+#pragma unroll
+      for (int n = 0; n < NT; ++n) {
+        *reinterpret_cast<float2*>(sc + g * C::kMergeRow + 8 * n + 2 * t) = make_float2(o[n][0], o[n][1]);
+        *reinterpret_cast<float2*>(sc + (g + 8) * C::kMergeRow + 8 * n + 2 * t) = make_float2(o[n][2], o[n][3]);
+      }
+      if (t == 0) {
+        sc[g * C::kMergeRow + HD] = mxA;
+        sc[g * C::kMergeRow + HD + 1] = lA;
+        sc[(g + 8) * C::kMergeRow + HD] = mxB;
+        sc[(g + 8) * C::kMergeRow + HD + 1] = lB;
+      }
+    }
+    if (q4 > 0) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&merge_full);
+      continue;
+    }
+    mbar_wait(&merge_full, u & 1);
+    if (active) {
+      float MA = mxA, MB = mxB;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const float* sc = merge + (k * 2 + mt) * 16 * C::kMergeRow;
+        MA = fmaxf(MA, sc[g * C::kMergeRow + HD]);
+        MB = fmaxf(MB, sc[(g + 8) * C::kMergeRow + HD]);
+      }
+      const float wA0 = MA == -INFINITY ? 0.f : dv_ex2(mxA - MA);
+      const float wB0 = MB == -INFINITY ? 0.f : dv_ex2(mxB - MB);
+      float LA = lA * wA0, LB = lB * wB0;
+#pragma unroll
+      for (int n = 0; n < NT; ++n) {
+        o[n][0] *= wA0;
+        o[n][1] *= wA0;
+        o[n][2] *= wB0;
+        o[n][3] *= wB0;
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const float* sc = merge + (k * 2 + mt) * 16 * C::kMergeRow;
+        const float mkA = sc[g * C::kMergeRow + HD], mkB = sc[(g + 8) * C::kMergeRow + HD];
+        const float wA = mkA == -INFINITY ? 0.f : dv_ex2(mkA - MA);
+        const float wB = mkB == -INFINITY ? 0.f : dv_ex2(mkB - MB);
+        LA += sc[g * C::kMergeRow + HD + 1] * wA;
+        LB += sc[(g + 8) * C::kMergeRow + HD + 1] * wB;
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          const float2 xa = *reinterpret_cast<const float2*>(sc + g * C::kMergeRow + 8 * n + 2 * t);
+          const float2 xb = *reinterpret_cast<const float2*>(sc + (g + 8) * C::kMergeRow + 8 * n + 2 * t);
+          o[n][0] += wA * xa.x;
+          o[n][1] += wA * xa.y;
+          o[n][2] += wB * xb.x;
+          o[n][3] += wB * xb.y;
+        }
+      }
+      const float ln2 = 0.6931471805599453f;
+      if (vA) {
+        const int64_t pidx = (int64_t)(pbase + mA / G) * p.n_heads + kvh * G + mA % G;
+        const float inv = LA > 0.f ? 1.f / LA : 0.f;
+#pragma unroll
+        for (int n = 0; n < NT; ++n)
+          *reinterpret_cast<float2*>(p.part_o + pidx * HD + 8 * n + 2 * t) =
+              make_float2(o[n][0] * inv, o[n][1] * inv);
+        if (t == 0) p.part_lse[pidx] = LA > 0.f ? (MA + log2f(LA)) * ln2 : -INFINITY;
+      }
+      if (vB) {
+        const int64_t pidx = (int64_t)(pbase + mB / G) * p.n_heads + kvh * G + mB % G;
+        const float inv = LB > 0.f ? 1.f / LB : 0.f;
+#pragma unroll
+        for (int n = 0; n < NT; ++n)
+          *reinterpret_cast<float2*>(p.part_o + pidx * HD + 8 * n + 2 * t) =
+              make_float2(o[n][2] * inv, o[n][3] * inv);
+        if (t == 0) p.part_lse[pidx] = LB > 0.f ? (MB + log2f(LB)) * ln2 : -INFINITY;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&merge_empty);
+  }
+}
+
+// ---------------------------------------------------------------- host side
+static PFN_cuTensorMapEncodeTiled_v12000 dv_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* ptr = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+static bool dv_pool_map(CUtensorMap* map, const void* pool, uint64_t rows, int hd) {
+  auto enc = dv_encode_fn();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)hd, rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)hd * 2};
+  const cuuint32_t box[2] = {64, 64};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(pool), dims, strides, box,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int HD>
+static int launch_dv(const DvParams& p, const void* k_pool, const void* v_pool, uint64_t rows,
+                     int grid, cudaStream_t s) {
+  CUtensorMap mk, mv;
+  if (!dv_pool_map(&mk, k_pool, rows, HD) || !dv_pool_map(&mv, v_pool, rows, HD))
+    return CHOREO_ELAUNCH;
+  constexpr int smem = DvCfg<HD>::kTotal;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(decode_attn_v2<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr_set = true;
+  }
+  launch_k(decode_attn_v2<HD>, grid, kDvThreads, smem, s, p, mk, mv);
+  return launch_status("choreo_decode_attn_v2");
+}
+
+}  // namespace choreo
+
+using namespace choreo;
+
+extern "C" int choreo_decode_attn_v2(const float* q, const void* k_pool, const void* v_pool,
+                                     int n_layers, int layer, int n_kv, int n_pages, int page_size,
+                                     int n_heads, int head_dim, const int32_t* row_t,
+                                     const int32_t* vis_page, const int32_t* vis_len,
+                                     const int32_t* vis_own, const int32_t* blk_rows,
+                                     const int32_t* items, const int32_t* counts, int max_items,
+                                     float* part_o, float* part_lse, int grid_ctas, void* stream) {
+  if (!q || !k_pool || !v_pool || !row_t || !vis_page || !vis_len || !vis_own || !blk_rows ||
+      !items || !counts || !part_o || !part_lse || n_kv <= 0 || n_heads % n_kv)
+    return CHOREO_EINVAL;
+  if (page_size != 64 || (head_dim != 64 && head_dim != 128) || n_heads / n_kv > 32)
+    return CHOREO_EUNSUPPORTED;  // items must also hold <= 32 / G rows and <= 32 pages
+  if (max_items <= 0) return CHOREO_OK;
+  const uint64_t rows = (uint64_t)n_layers * n_kv * n_pages * page_size;
+  if (rows > 0x7fffffffull) return CHOREO_EUNSUPPORTED;
+  DvParams p{q, layer, n_kv, n_pages, n_heads, row_t, vis_page, vis_len, vis_own, blk_rows, items,
+             counts, part_o, part_lse, 1.4426950408889634f / sqrtf((float)head_dim)};
+  int grid = grid_ctas > 0 ? grid_ctas : max_items * n_kv;
+  if (grid > 148) grid = 148;
+  auto s = as_stream(stream);
+  return head_dim == 128 ? launch_dv<128>(p, k_pool, v_pool, rows, grid, s)
+                         : launch_dv<64>(p, k_pool, v_pool, rows, grid, s);
+}

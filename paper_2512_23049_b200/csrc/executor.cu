@@ -26,6 +26,10 @@ extern "C" int choreo_decode_layers(const ChoreoDecodeStep* s, void* stream) {
   const int x_rows = sp ? 2 * R : R;
   const int n_qkv = (H + 2 * Hk) * hd;
   cudaEvent_t* ev = reinterpret_cast<cudaEvent_t*>(s->attn_events);
+  cudaEvent_t* lev = reinterpret_cast<cudaEvent_t*>(s->linear_events);
+  cudaStream_t cs = as_stream(stream);
+#define LIN_EV(i) \
+  if (lev) cudaEventRecord(lev[8 * l + (i)], cs)
   int rc;
 #define CHK(call)          \
   do {                     \
@@ -37,29 +41,45 @@ extern "C" int choreo_decode_layers(const ChoreoDecodeStep* s, void* stream) {
     CHK(choreo_residual_rmsnorm(s->x, l ? s->delta : s->delta_in, CHOREO_F32, 0, s->attn_norm[l],
                                 CHOREO_BF16, R, d, s->eps, s->h, CHOREO_BF16, sp, nullptr, 0,
                                 stream));
+    LIN_EV(0);
     CHK(choreo_linear_skinny(s->h, x_rows, sp, s->w_qkv[l], n_qkv, d, s->qkv, s->k7_ws, s->k7_cnt,
                              0, stream));
+    LIN_EV(1);
     CHK(choreo_rope_append(s->qkv, CHOREO_F32, n_qkv, R, 0, s->pos, s->page, s->slot, s->q,
                            s->k_pool, s->v_pool, CHOREO_BF16, l, Hk, s->n_pages, s->page_size, H,
                            hd, s->cos_t, s->sin_t, s->max_delta, stream));
     if (ev) cudaEventRecord(ev[2 * l], as_stream(stream));
-    CHK(choreo_decode_attn(s->q, s->k_pool, s->v_pool, l, Hk, s->n_pages, s->page_size, H, hd,
-                           s->fat, s->counts, s->n_items, s->row_part_off, s->row_part, s->part_o,
-                           s->part_lse, nullptr, s->attn, sp, R, s->attn_flags, 0, stream));
+    if (s->attn_kernel == 1)
+      CHK(choreo_decode_attn_v2(s->q, s->k_pool, s->v_pool, s->n_layers, l, Hk, s->n_pages,
+                                s->page_size, H, hd, s->row_t, s->vis_page, s->vis_len, s->vis_own,
+                                s->blk_rows, s->items, s->counts, s->n_items, s->part_o,
+                                s->part_lse, 0, stream));
+    else
+      CHK(choreo_decode_attn(s->q, s->k_pool, s->v_pool, l, Hk, s->n_pages, s->page_size, H, hd,
+                             s->fat, s->counts, s->n_items, s->row_part_off, s->row_part,
+                             s->part_o, s->part_lse, nullptr, s->attn, sp, R, s->attn_flags, 0,
+                             stream));
     if (ev) cudaEventRecord(ev[2 * l + 1], as_stream(stream));
     CHK(choreo_attn_combine(s->part_o, s->part_lse, s->row_part_off, s->row_part, R, H, hd,
                             s->attn, CHOREO_BF16, sp, stream));
+    LIN_EV(2);
     CHK(choreo_linear_skinny(s->attn, x_rows, sp, s->wo[l], d, H * hd, s->ao, s->k7_ws, s->k7_cnt,
                              0, stream));
+    LIN_EV(3);
     CHK(choreo_residual_rmsnorm(s->x, s->ao, CHOREO_F32, 0, s->ffn_norm[l], CHOREO_BF16, R, d,
                                 s->eps, s->h, CHOREO_BF16, sp, nullptr, 0, stream));
+    LIN_EV(4);
     CHK(choreo_linear_skinny(s->h, x_rows, sp, s->w_gu[l], 2 * F, d, s->gu, s->k7_ws, s->k7_cnt, 0,
                              stream));
+    LIN_EV(5);
     CHK(choreo_silu_mul(s->gu, CHOREO_F32, 0, R, F, s->act, CHOREO_BF16, sp, stream));
+    LIN_EV(6);
     CHK(choreo_linear_skinny(s->act, x_rows, sp, s->w_down[l], d, F, s->delta, s->k7_ws, s->k7_cnt,
                              0, stream));
+    LIN_EV(7);
   }
 #undef CHK
+#undef LIN_EV
   return CHOREO_OK;
 }
 

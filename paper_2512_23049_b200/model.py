@@ -165,8 +165,13 @@ class Runner:
         self.native_step = os.environ.get("CHOREO_NATIVE_STEP", "1") != "0"
         self._wptrs = None
         self._ev_free: list = []
-        self._ev_pending: list = []  # (event array, algorithmic bytes) awaiting readback
+        self._ev_pending: list = []  # (kind, event array, bytes per pair) awaiting readback
         self.attn_times: list = []  # (ms, algorithmic bytes) per timed attention launch
+        # When True (native decode steps only), the four K7 launches of every layer are
+        # bracketed with events too; (ms, bytes) land in linear_times.  The brackets cost the
+        # GEMM its programmatic-launch overlap, so these times are conservative.
+        self.time_linear = False
+        self.linear_times: list = []
 
     def _weight_ptrs(self):
         if self._wptrs is None:
@@ -179,11 +184,12 @@ class Runner:
         """Read back native K5 timing events older than `keep` steps (they completed long
         ago, so this does not stall the launch pipeline) and recycle them."""
         while len(self._ev_pending) > keep:
-            arr, nbytes = self._ev_pending.pop(0)
+            kind, arr, nbytes = self._ev_pending.pop(0)
             n = len(arr) // 2
             ms = (ctypes.c_float * n)()
             nat.events_elapsed(arr, n, ms)
-            self.attn_times.extend((float(m), nbytes) for m in ms)
+            dst = self.attn_times if kind == "attn" else self.linear_times
+            dst.extend((float(m), nbytes[i % len(nbytes)]) for i, m in enumerate(ms))
             self._ev_free.append(arr)
 
     def collect_attn_times(self) -> list:
@@ -232,7 +238,7 @@ class Runner:
                 + n_parts * cfg.n_heads * (cfg.head_dim + 1) * 4)
 
     def _native_layers(self, R, q, part_o, part_lse, attn, h, act, x, pos_d, page_d, slot_d, fat,
-                       counts, n_items, row_part_off, row_part, attn_bytes, stream):
+                       counts, n_items, row_part_off, row_part, attn_bytes, stream, v2=None):
         """All layers of a decode-sized step through choreo_decode_layers; returns the last
         layer's down_proj output (hi/lo summed)."""
         cfg, cache, dev = self.cfg, self.cache, self.dev
@@ -246,12 +252,15 @@ class Runner:
         gu = torch.empty(R, 2 * cfg.ffn_dim, dtype=f32, device=dev)
         delta = torch.empty(R, d, dtype=f32, device=dev)
         wp = self._weight_ptrs()
-        ev = None
-        if self.attn_events is not None:
-            ev = self._ev_free.pop() if self._ev_free else None
-            if ev is None:
-                ev = (ctypes.c_void_p * (2 * L))()
-                nat.events_create(ev, 2 * L)
+        def events(n):
+            for i, a in enumerate(self._ev_free):
+                if len(a) == n:
+                    return self._ev_free.pop(i)
+            a = (ctypes.c_void_p * n)()
+            nat.events_create(a, n)
+            return a
+        ev = events(2 * L) if self.attn_events is not None else None
+        lev = events(8 * L) if self.time_linear else None
         st = nat.DecodeStep(
             n_layers=L, d=d, n_heads=cfg.n_heads, n_kv=cfg.kv_heads, head_dim=hd,
             ffn_dim=cfg.ffn_dim, attn_norm=ctypes.cast(wp["attn_norm"], ctypes.c_void_p),
@@ -263,18 +272,31 @@ class Runner:
             page_size=cache.page_size, cos_t=self.rot.cos.data_ptr(), sin_t=self.rot.sin.data_ptr(),
             max_delta=self.rot.max_delta, n_rows=R, split=int(self.split),
             attn_flags=self.attn_flags, n_items=n_items, pos=pos_d.data_ptr(),
-            page=page_d.data_ptr(), slot=slot_d.data_ptr(), fat=fat.data_ptr(),
+            page=page_d.data_ptr(), slot=slot_d.data_ptr(), fat=nat.ptr(fat),
             counts=counts.data_ptr(), row_part_off=row_part_off.data_ptr(),
             row_part=row_part.data_ptr(), x=x.data_ptr(), delta_in=None, h=h.data_ptr(),
             qkv=qkv.data_ptr(), q=q.data_ptr(), part_o=part_o.data_ptr(),
             part_lse=part_lse.data_ptr(), attn=attn.data_ptr(), ao=ao.data_ptr(), gu=gu.data_ptr(),
             act=act.data_ptr(), delta=delta.data_ptr(), k7_ws=self._k7_ws.data_ptr(),
             k7_cnt=self._k7_cnt.data_ptr(),
-            attn_events=ctypes.cast(ev, ctypes.c_void_p) if ev is not None else None)
+            attn_events=ctypes.cast(ev, ctypes.c_void_p) if ev is not None else None,
+            linear_events=ctypes.cast(lev, ctypes.c_void_p) if lev is not None else None)
+        if v2 is not None:
+            _, rowt_d, vis, blk_rows, items = v2
+            st.attn_kernel = 1
+            st.row_t, st.vis_page, st.vis_len, st.vis_own = (
+                rowt_d.data_ptr(), vis[0].data_ptr(), vis[1].data_ptr(), vis[2].data_ptr())
+            st.blk_rows, st.items = blk_rows.data_ptr(), items.data_ptr()
         nat.decode_layers(ctypes.byref(st), stream)
         if ev is not None:
-            self._ev_pending.append((ev, attn_bytes))
-            self._retire_events(8)
+            self._ev_pending.append(("attn", ev, [attn_bytes]))
+        if lev is not None:
+            x_rows = (2 if self.split else 1) * R
+            lb = [w.numel() * w.element_size() + x_rows * w.shape[1] * 2 + R * w.shape[0] * 4
+                  for w in (self.w.layers[0][n] for n in ("w_qkv", "wo", "w_gu", "w_down"))]
+            self._ev_pending.append(("linear", lev, lb))
+        if ev is not None or lev is not None:
+            self._retire_events(16)
         return delta
 
     def _lin_buffers(self) -> None:
@@ -312,17 +334,23 @@ class Runner:
         use_k4 = (self.pool_dtc == nat.BF16 and P == 64 and hd in (64, 128) and G <= 128
                   and max(len(c.tokens) for c in plan.calls) >= 64
                   and os.environ.get("CHOREO_PREFILL_K4", "1") != "0")
-        rpb = 256 // G if use_k4 else self.rows_per_block  # K4: two 128-vector tiles
+        mode0 = max(len(c.tokens) for c in plan.calls) < 64
+        # decode-sized bf16 steps: K5 v2 (TMA page ring, <= 32 query vectors per item)
+        v2 = (not use_k4 and mode0 and self.pool_dtc == nat.BF16 and P == 64
+              and hd in (64, 128) and G <= 32 and os.environ.get("CHOREO_K5V2", "1") != "0")
+        rpb = 256 // G if use_k4 else max(1, 32 // G) if v2 else self.rows_per_block
         # pages per item: about two waves of (2 CTAs/SM x 148 SMs) per layer, and at
         # most 512 partials per row for the combine
         # prefill-sized steps: per-call page lists (a row block already fills an M tile)
         mode = 1 if max(len(c.tokens) for c in plan.calls) >= 64 else 0
         # decode-sized bf16 steps: fused K5 (fat items, in-kernel combine)
-        fused = (not use_k4 and mode == 0 and self.pool_dtc == nat.BF16 and P == 64
+        fused = (not use_k4 and not v2 and mode == 0 and self.pool_dtc == nat.BF16 and P == 64
                  and hd in (64, 128) and rpb <= 16
                  and os.environ.get("CHOREO_FUSED_DECODE", "1") != "0")
         work = plan_counts(plan.calls, msg_len, P, rpb, 1, mode)
-        ppi = max(1, cdiv(work.item_pages * Hk, (2 if use_k4 else 3) * 148))
+        ppi = max(1, cdiv(work.item_pages * Hk, (2 if use_k4 else 1 if v2 else 3) * 148))
+        if v2:  # persistent CTAs: about one (item, kv head) unit per SM; unit record <= 32 pages
+            ppi = min(max(ppi, 4), 32)
         plan_ = plan_counts(plan.calls, msg_len, P, rpb, ppi, mode)
         if fused:
             # one wave of resident CTAs (3 per SM): a second item on a few CTAs would
@@ -330,7 +358,7 @@ class Runner:
             while plan_.n_items * Hk > 3 * 148 and ppi < 8:
                 ppi += 1
                 plan_ = plan_counts(plan.calls, msg_len, P, rpb, ppi, mode)
-        while plan_.max_row_parts > 512:
+        while plan_.max_row_parts > 512 and not (v2 and ppi >= 32):
             ppi *= 2
             plan_ = plan_counts(plan.calls, msg_len, P, rpb, ppi, mode)
         n_parts, n_items = plan_.n_parts, plan_.n_items
@@ -397,12 +425,13 @@ class Runner:
         act = torch.empty(S * R, cfg.ffn_dim, dtype=self.dt, device=self.dev)
         delta = None
         launches = 2
-        native = (fused and k7 and self.native_step and self.tp is None and not self.fused_combine
+        native = ((fused or v2) and k7 and self.native_step and self.tp is None and not self.fused_combine
                   and self.dt == torch.bfloat16)
         if native:
             delta = self._native_layers(R, q, part_o, part_lse, attn, h, act, x, pos_d, page_d,
                                         slot_d, fat, counts, n_items, row_part_off, row_part,
-                                        attn_bytes, stream)
+                                        attn_bytes, stream,
+                                        (v2, rowt_d, vis, blk_rows, items) if v2 else None)
             launches += 10 * len(self.w.layers)
         for layer, lw in enumerate([] if native else self.w.layers):
             nat.residual_rmsnorm(x.data_ptr(), nat.ptr(delta), nat.F32, isp,
@@ -418,7 +447,14 @@ class Runner:
                 ev0 = torch.cuda.Event(enable_timing=True)
                 ev1 = torch.cuda.Event(enable_timing=True)
                 ev0.record()
-            if fused:
+            if v2:
+                nat.decode_attn_v2(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(),
+                                   cfg.n_layers, layer, Hk, cache.n_pages, P, H, hd,
+                                   rowt_d.data_ptr(), vis[0].data_ptr(), vis[1].data_ptr(),
+                                   vis[2].data_ptr(), blk_rows.data_ptr(), items.data_ptr(),
+                                   counts.data_ptr(), n_items, part_o.data_ptr(),
+                                   part_lse.data_ptr(), 0, stream)
+            elif fused:
                 nat.decode_attn(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(), layer,
                                 Hk, cache.n_pages, P, H, hd, fat.data_ptr(), counts.data_ptr(),
                                 n_items, row_part_off.data_ptr(), row_part.data_ptr(),

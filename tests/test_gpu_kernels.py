@@ -435,6 +435,64 @@ def test_fused_decode_matches_dense_reference(hd, H, Hk):
             np.testing.assert_allclose(got[r, h], p @ vv, rtol=1e-3, atol=1e-3)
 
 
+@pytest.mark.parametrize("ppi", [1, 2, 5])
+@pytest.mark.parametrize("hd,H,Hk", [(128, 32, 8), (64, 16, 2), (128, 8, 8)])
+def test_decode_v2_matches_dense_reference(hd, H, Hk, ppi):
+    """K5 v2 (TMA page ring + ldmatrix/mma.sync consumers, 4 key slices x 2 m-tiles) over
+    page-centric items: agents sharing reordered parents, causal own pages, ragged pages.
+    Plain bf16 Q and P with f32 accumulation: within 2e-2 of the f64 dense reference."""
+    rng = np.random.default_rng(12)
+    cfg = ModelConfig(n_layers=2, n_heads=H, n_kv_heads=Hk, head_dim=hd)
+    cache, lens = _random_cache(cfg, rng, 8, dtype=torch.bfloat16)
+    calls = []
+    for a in range(9):
+        own = 8 + a
+        n = int(rng.integers(1, 200))
+        cache.register_message(own, "decoded", 0)
+        cache.reserve_slots(own, [1] * n)
+        cache.log_append(own, 0, n)
+        parents = [int(p) for p in rng.permutation(8)[:int(rng.integers(0, 8))]]
+        calls.append((own, parents, [n - 1] if a != 3 else list(range(max(0, n - 5), n))))
+    cache.k_pool.copy_(torch.randn_like(cache.k_pool))
+    cache.v_pool.copy_(torch.randn_like(cache.v_pool))
+    G = H // Hk
+    rpb = max(1, 32 // G)
+    out, (rt_d, vis, blk, items, rpo, rp, counts) = _assemble(cache, calls, rpb, ppi, 0)
+    R = len(out["row_t"])
+    pl_ = out["plan"]
+    q = torch.randn(R, H, hd, device="cuda")
+    part_o = torch.empty(pl_.n_parts, H, hd, device="cuda")
+    part_lse = torch.empty(pl_.n_parts, H, device="cuda")
+    o = torch.empty(R, H * hd, dtype=torch.float32, device="cuda")
+    L = 1
+    for grid in (0, 5):  # persistent CTAs: many work units per CTA through one page ring
+        nat.decode_attn_v2(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(), 2, L,
+                           Hk, cache.n_pages, 64, H, hd, rt_d.data_ptr(), vis[0].data_ptr(),
+                           vis[1].data_ptr(), vis[2].data_ptr(), blk.data_ptr(), items.data_ptr(),
+                           counts.data_ptr(), pl_.n_items, part_o.data_ptr(), part_lse.data_ptr(),
+                           grid, _stream())
+        nat.attn_combine(part_o.data_ptr(), part_lse.data_ptr(), rpo.data_ptr(), rp.data_ptr(), R,
+                         H, hd, o.data_ptr(), nat.F32, 0, _stream())
+        torch.cuda.synchronize()
+        got = o.cpu().numpy().reshape(R, H, hd)
+        sets = _expand_rows(cache, out, R)
+        K = cache.k_pool[L].float().cpu().numpy().astype(np.float64)
+        V = cache.v_pool[L].float().cpu().numpy().astype(np.float64)
+        qn = q.cpu().numpy().astype(np.float64)
+        worst = 0.0
+        for r in range(R):
+            toks = sets[r]
+            pg = np.array([cache._messages[m].pages[i // 64] for m, i in toks])
+            sl = np.array([i % 64 for m, i in toks])
+            for h in range(H):
+                kk, vv = K[h // G, pg, sl], V[h // G, pg, sl]
+                s = kk @ qn[r, h] / np.sqrt(hd)
+                p = np.exp(s - s.max())
+                p /= p.sum()
+                worst = max(worst, float(np.abs(got[r, h] - p @ vv).max()))
+        assert worst < 2e-2, (grid, worst)
+
+
 def _linear(x, split, w, grid=0):
     rows = x.shape[0] // (2 if split else 1)
     y = torch.full((rows, w.shape[0]), float("nan"), device="cuda")

@@ -190,7 +190,8 @@ def k4_prefill(n_msgs: int = 8, rows: int = 1024, n_par: int = 24) -> dict:
             "items": plan.n_items}
 
 
-def k5_decode(n_workflows: int = 1, agents: int = 8, tc: bool = False, fused: bool = True) -> dict:
+def k5_decode(n_workflows: int = 1, agents: int = 8, tc: bool = False, fused: bool = True,
+              v2: bool = False) -> dict:
     """One decode step of C3 round 2 (agents see sys, q and the other agents' replies)."""
     cfg = LLAMA_3_1_8B
     H, Hk, hd = cfg.n_heads, cfg.kv_heads, cfg.head_dim
@@ -211,12 +212,14 @@ def k5_decode(n_workflows: int = 1, agents: int = 8, tc: bool = False, fused: bo
     cache.k_pool.normal_()
     cache.v_pool.normal_()
     G = H // Hk
-    rpb = 256 // G if tc else max(1, min(16, 64 // G))
+    rpb = 256 // G if tc else max(1, 32 // G) if v2 else max(1, min(16, 64 // G))
     work = plan_counts([CallRows(c[0], c[1], c[2], [0], None, None, 0) for c in calls],
                        cache.msg_len.host, 64, rpb, 1)
-    ppi = max(1, cdiv(work.item_pages * Hk, (1 if tc else 3) * 148))
+    ppi = max(1, cdiv(work.item_pages * Hk, (1 if tc else 1 if v2 else 3) * 148))
+    if v2:  # the runner's rule: about one (item, kv head) unit per SM, 4..32 pages
+        ppi = min(max(ppi, 4), 32)
     ppi = int(os.environ.get("K5_PPI", ppi))
-    fused = fused and not tc
+    fused = fused and not tc and not v2
     if fused and "K5_PPI" not in os.environ:  # same one-wave fit as the runner
         while plan_counts([CallRows(c[0], c[1], c[2], [0], None, None, 0) for c in calls],
                           cache.msg_len.host, 64, rpb, ppi).n_items * Hk > 3 * 148 and ppi < 8:
@@ -233,6 +236,13 @@ def k5_decode(n_workflows: int = 1, agents: int = 8, tc: bool = False, fused: bo
     in_kernel_combine = os.environ.get("K5_FUSED_COMBINE", "1") == "1"
 
     def run():
+        if v2:
+            nat.decode_attn_v2(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(),
+                               cfg.n_layers, 0, Hk, cache.n_pages, 64, H, hd, b["rt"].data_ptr(),
+                               v[0].data_ptr(), v[1].data_ptr(), v[2].data_ptr(),
+                               b["blk"].data_ptr(), b["items"].data_ptr(), b["counts"].data_ptr(),
+                               plan.n_items, po.data_ptr(), pl.data_ptr(), 0, stream)
+            return
         if fused:
             nat.decode_attn(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(), 0, Hk,
                             cache.n_pages, 64, H, hd, b["fat"].data_ptr(), b["counts"].data_ptr(),
@@ -265,7 +275,8 @@ def k5_decode(n_workflows: int = 1, agents: int = 8, tc: bool = False, fused: bo
     logical = sum(sum(cache.message_length(p) for p in c[1]) + c[2] + 1 for c in calls) * Hk * hd * 4
     pk = peaks()
     ach = nbytes / t / 1e9
-    return {"kernel": ("choreo_prefill_attn on decode items (tcgen05)" if tc else
+    return {"kernel": ("choreo_decode_attn_v2 (K5 v2: TMA page ring, page-centric)" if v2 else
+                       "choreo_prefill_attn on decode items (tcgen05)" if tc else
                        "choreo_decode_attn (K5 fused, page-centric)" if fused
                        else "choreo_attn_split (K5, page-centric decode)"), "bound": "hbm",
             "work": f"{n_workflows} workflow(s) x {agents} agents, 1 layer",
