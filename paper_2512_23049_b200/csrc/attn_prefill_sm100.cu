@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
   uint8_t* sQ = base;                                  // [2][kQBytes]
   uint8_t* sKV = sQ + 2 * S::kQBytes;                  // [stages][K | V]
   __shared__ uint64_t full_bar[kPfStages], empty_bar[kPfStages];
-  __shared__ uint64_t s_full[2][2], p_full[2], o_done[2], q_full[2], o_free[2];
+  __shared__ uint64_t s_full[2][2], p_full[2][2], o_done[2], q_full[2], o_free[2];
   __shared__ uint32_t tmem_base;
   __shared__ int s_rid[2][kTileM], s_rt[2][kTileM];
 
@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
     }
     for (int t = 0; t < 2; ++t) {
       for (int i = 0; i < 2; ++i) mbar_init(&s_full[t][i], 1);
-      mbar_init(&p_full[t], 128);
+      for (int i = 0; i < 2; ++i) mbar_init(&p_full[t][i], 128);
       mbar_init(&o_done[t], 1);
       mbar_init(&q_full[t], 128);
       mbar_init(&o_free[t], 128);
@@ -192,7 +192,10 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         umma_commit(&s_full[t][b]);
       };
       auto issue_pv = [&](int t, uint32_t g, uint32_t gt, bool first) {
-        mbar_wait(&p_full[t], gt & 1);
+        // P(gt) lives in S buffer gt & 1; one barrier per buffer: a softmax group may finish
+        // page gt + 1 before this wait runs (S(gt+1) is issued ahead of PV(gt)), so a single
+        // barrier could be two phases ahead and its parity wait would never return
+        mbar_wait(&p_full[t][gt & 1], (gt >> 1) & 1);
         tc_fence_after();
         const uint32_t vaddr = smem_addr(sKV + (g % kPfStages) * S::kStageBytes) + S::kKVBytes;
         const uint32_t aP = tmem_base + 256 * t + 64 * (gt & 1);
@@ -250,6 +253,8 @@ __global__ void __launch_bounds__(kPfThreads, 1)
       const int nr_t = max(0, min(rows_per_tile, nr - r0));   // rows of this tile
       if (nr_t == 0) continue;  // tile unused by this item (the MMA warp skips it too)
       const int M = nr_t * G;
+      // the previous item's epilogue (other warps of this group) may still read s_rid / s_rt
+      asm volatile("bar.sync %0, 128;\n" ::"r"(1 + t) : "memory");
       if (wg_tid < nr_t) {
         const int rid = p.blk_rows[rb + r0 + wg_tid];
         s_rid[t][wg_tid] = rid;
@@ -356,28 +361,34 @@ __global__ void __launch_bounds__(kPfThreads, 1)
           tmem_st16u(tS + 64 * b + lane_off, pk);
           tmem_st16u(tS + 64 * b + lane_off + 16, pk + 16);
         }
-        // rescale the running O only when this warp's reference max moved (rare)
-        if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+        // rescale the running O only when this warp's reference max moved (rare).  At the
+        // item's last page PV_t(g-1) is always awaited: here o_done is at phase g-1 or g
+        // (S(g) completing implies PV(g-2) did), so the parity wait is exact, and the
+        // epilogue then has only PV_t(g) to wait for.  (Waiting for PV(g-1) in the epilogue
+        // instead can deadlock: once PV(g-1) and PV(g) are both done, the barrier's current
+        // phase has PV(g-1)'s parity and the wait blocks for a phase that never comes.)
+        const bool resc = __any_sync(0xffffffffu, alpha != 1.f);
+        if (j > 0 && (resc || j == nv - 1)) {
           mbar_wait(&o_done[t], (gp - 1) & 1);  // PV_t(g-1) done before touching O
           tc_fence_after();
+          if (resc) {
 #pragma unroll
-          for (int c = 0; c < HD / 16; ++c) {
-            float o[16];
-            tmem_ld16(tO + lane_off + c * 16, o);
-            tmem_wait_ld();
+            for (int c = 0; c < HD / 16; ++c) {
+              float o[16];
+              tmem_ld16(tO + lane_off + c * 16, o);
+              tmem_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 16; ++i) o[i] *= alpha;
-            tmem_st16(tO + lane_off + c * 16, o);
+              for (int i = 0; i < 16; ++i) o[i] *= alpha;
+              tmem_st16(tO + lane_off + c * 16, o);
+            }
           }
         }
         tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(&p_full[t]);
+        mbar_arrive(&p_full[t][b]);
       }
       // ---- epilogue: O / l -> partial, LSE (natural log) ----
-      // PV_t(last-1) and PV_t(last) may both be pending: a parity wait only tells the
-      // current phase from the previous one, so wait for them in order
-      if (nv >= 2) mbar_wait(&o_done[t], (gp - 2) & 1);
+      // only PV_t(last) can still be pending (PV_t(last-1) was awaited at the last page)
       mbar_wait(&o_done[t], (gp - 1) & 1);
       tc_fence_after();
       {
@@ -528,6 +539,17 @@ extern "C" int choreo_prefill_attn_dbg(const float* q, const void* k_pool, const
   const uint64_t rows = (uint64_t)n_layers * n_kv * n_pages * page_size;
   if (rows > 0x7fffffffull) return CHOREO_EUNSUPPORTED;
   auto s = as_stream(stream);
-  return head_dim == 128 ? launch_prefill<128, 0>(p, k_pool, v_pool, rows, grid, s)
-                         : launch_prefill<64, 0>(p, k_pool, v_pool, rows, grid, s);
+  static int poly = -1;  // exp2 offload to the FMA pipe: elements with (k & 3) < poly
+  if (poly < 0) {
+    const char* e = getenv("CHOREO_K4_POLY");
+    poly = e ? atoi(e) : 0;
+  }
+  if (head_dim == 128) {
+    switch (poly) {
+      case 1: return launch_prefill<128, 1>(p, k_pool, v_pool, rows, grid, s);
+      case 3: return launch_prefill<128, 3>(p, k_pool, v_pool, rows, grid, s);
+      default: return launch_prefill<128, 0>(p, k_pool, v_pool, rows, grid, s);
+    }
+  }
+  return launch_prefill<64, 0>(p, k_pool, v_pool, rows, grid, s);
 }

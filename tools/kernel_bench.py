@@ -138,8 +138,11 @@ def k2_rerotate(tokens: int = 8192) -> dict:
             "unit": "GB/s", "peak": pk["hbm_gbs"], "frac": round(ach / pk["hbm_gbs"], 4)}
 
 
-def k4_prefill(n_msgs: int = 8, rows: int = 1024, n_par: int = 24) -> dict:
-    cfg = LLAMA_3_1_8B
+def k4_prefill(n_msgs: int = 8, rows: int = 1024, n_par: int = 24, n_layers: int = 32,
+               reps: int = 10) -> dict:
+    """n_layers < 32 shrinks the pool (profiling: ncu saves / restores device memory)."""
+    from dataclasses import replace
+    cfg = replace(LLAMA_3_1_8B, n_layers=n_layers)
     H, Hk, hd = cfg.n_heads, cfg.kv_heads, cfg.head_dim
     G = H // Hk
     cache = _cache(cfg, 32 * 256 + n_msgs * rows + 1024)
@@ -175,8 +178,8 @@ def k4_prefill(n_msgs: int = 8, rows: int = 1024, n_par: int = 24) -> dict:
     def run_comb():
         nat.attn_combine(po.data_ptr(), pl.data_ptr(), b["rpo"].data_ptr(), b["rp"].data_ptr(), R,
                          H, hd, out.data_ptr(), nat.BF16, 0, stream)
-    t = _time(run, reps=10)
-    tc = 0.0 if direct else _time(run_comb, reps=10)
+    t = _time(run, reps=reps, warm=min(3, reps), burst=1 if reps <= 2 else None)
+    tc = 0.0 if direct or reps <= 2 else _time(run_comb, reps=10)
     pairs = n_msgs * (rows * n_par * 256 + rows * (rows + 1) // 2)
     flops = 4 * hd * H * pairs
     pk = peaks()
