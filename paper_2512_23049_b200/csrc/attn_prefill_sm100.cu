@@ -53,7 +53,8 @@ struct PrefillParams {
     }                                                    \
   } while (0)
 
-constexpr int kPfThreads = 320;     // 10 warps: TMA, MMA, 2 x 4 softmax warps
+constexpr int kPfThreads = 352;     // 11 warps: TMA, MMA tile 0, 2 x 4 softmax, MMA tile 1
+constexpr int kPfMma1Warp = 10;
 constexpr int kPfStages = 4;
 constexpr int kPfKeys = 64;         // keys per page / per S tile
 constexpr int kTileM = 128;         // query vectors per tile (TMEM lanes)
@@ -100,7 +101,8 @@ __device__ __forceinline__ float ex2_poly(float x) {
 // page, and their MMAs ping-pong on the tensor core: while softmax warpgroup t works on
 // S_t, the tensor core runs the other tile's S / PV.  TMEM (512 columns) per tile t:
 // S double buffer at [256t, 256t+128), O at [256t+128, 256t+128+HD).  Per page g:
-//   MMA : S_0(g+1), S_1(g+1) are issued before PV_0(g), PV_1(g);
+//   MMA : one issuing thread per tile (warps 1 and 10), so a tile's S(g+1) goes out as
+//         soon as its PV(g-1) has, independent of the other tile's softmax progress;
 //   SMX_t: ld S_t(g), release it, exp2 (POLY of every 4 on the FMA pipe), wait PV_t(g-1),
 //          write P_t(g), lazily rescale O_t.
 template <int HD, int POLY>
@@ -128,7 +130,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
   if (tid == 0) {
     for (int i = 0; i < kPfStages; ++i) {
       mbar_init(&full_bar[i], 1);
-      mbar_init(&empty_bar[i], 1);
+      mbar_init(&empty_bar[i], 2);  // one release per tile issuer
     }
     for (int t = 0; t < 2; ++t) {
       for (int i = 0; i < 2; ++i) mbar_init(&s_full[t][i], 1);
@@ -167,18 +169,19 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
+  } else if (warp == 1 || warp == kPfMma1Warp) {
+    // ------------------------------------------------------------ MMA issuers (per tile)
     if (lane == 0) {
+      const int t = warp == 1 ? 0 : 1;
       constexpr uint32_t idS = umma_idesc_bf16(kTileM, kPfKeys, false);
       constexpr uint32_t idO = umma_idesc_bf16(kTileM, HD, true);
       // g = global page index (K/V ring), gt = this tile's page index (its barriers).
       // S(gt) goes to TMEM buffer gt&1; the softmax overwrites it with P(gt) (bf16 pairs),
       // which PV(gt) reads as its A operand.  The tensor pipe executes in issue order, so
       // S(gt+2) (same buffer) is issued only after PV(gt) — no extra handshake needed.
-      auto issue_s = [&](int t, uint32_t g, uint32_t gt) {
+      auto issue_s = [&](uint32_t g, uint32_t gt) {
         const int st = g % kPfStages, b = gt & 1;
-        if (t == 0) mbar_wait(&full_bar[st], (g / kPfStages) & 1);
+        mbar_wait(&full_bar[st], (g / kPfStages) & 1);
         tc_fence_after();
         const uint32_t qaddr = smem_addr(sQ + t * S::kQBytes);
         const uint32_t kaddr = smem_addr(sKV + st * S::kStageBytes);
@@ -191,7 +194,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         }
         umma_commit(&s_full[t][b]);
       };
-      auto issue_pv = [&](int t, uint32_t g, uint32_t gt, bool first) {
+      auto issue_pv = [&](uint32_t g, uint32_t gt, bool first) {
         // P(gt) lives in S buffer gt & 1; one barrier per buffer: a softmax group may finish
         // page gt + 1 before this wait runs (S(gt+1) is issued ahead of PV(gt)), so a single
         // barrier could be two phases ahead and its parity wait would never return
@@ -206,34 +209,30 @@ __global__ void __launch_bounds__(kPfThreads, 1)
                            idO, (!first || k > 0) ? 1u : 0u);
         umma_commit(&o_done[t]);
       };
-      uint32_t gp = 0, g1 = 0, ic0 = 0, ic1 = 0;
+      uint32_t gp = 0, gt = 0, ic = 0;  // ring page, this tile's page, this tile's item
       for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
         const int32_t* it = p.items + 6 * (w / p.n_kv);
         const int nv = it[3];
-        const bool two = it[1] > rows_per_tile;  // second tile has rows in this item
-        mbar_wait(&q_full[0], ic0 & 1);
-        if (ic0 > 0) mbar_wait(&o_free[0], (ic0 - 1) & 1);
-        if (two) {
-          mbar_wait(&q_full[1], ic1 & 1);
-          if (ic1 > 0) mbar_wait(&o_free[1], (ic1 - 1) & 1);
+        if (t == 1 && it[1] <= rows_per_tile) {
+          // tile 1 has no rows in this item: release each page once it has landed (waiting
+          // for full keeps this issuer from running a ring round ahead of tile 0)
+          for (int j = 0; j < nv; ++j, ++gp) {
+            const int st = gp % kPfStages;
+            mbar_wait(&full_bar[st], (gp / kPfStages) & 1);
+            mbar_arrive(&empty_bar[st]);
+          }
+          continue;
         }
+        mbar_wait(&q_full[t], ic & 1);
+        if (ic > 0) mbar_wait(&o_free[t], (ic - 1) & 1);
         tc_fence_after();
-        issue_s(0, gp, gp);
-        if (two) issue_s(1, gp, g1);
-        for (int j = 0; j < nv; ++j, ++gp) {
-          if (j + 1 < nv) {
-            issue_s(0, gp + 1, gp + 1);
-            if (two) issue_s(1, gp + 1, g1 + 1);
-          }
-          issue_pv(0, gp, gp, j == 0);
-          if (two) {
-            issue_pv(1, gp, g1, j == 0);
-            ++g1;
-          }
+        issue_s(gp, gt);
+        for (int j = 0; j < nv; ++j, ++gp, ++gt) {
+          if (j + 1 < nv) issue_s(gp + 1, gt + 1);
+          issue_pv(gp, gt, j == 0);
           umma_commit(&empty_bar[gp % kPfStages]);
         }
-        ++ic0;
-        if (two) ++ic1;
+        ++ic;
       }
     }
   } else {
