@@ -341,16 +341,20 @@ def main() -> None:
         ev_start.record()
         for i in range(args.steps):
             eng.reset()
-            runner.attn_events = attn_events if i == args.steps - 1 else None
-            runner.time_linear = i == args.steps - 1
             res = run_debate(eng, P, inputs[i], args.agents, args.rounds)
             ttft += res["ttft"]
             generated += res["generated"]
-        runner.attn_events = None
-        runner.time_linear = False
         ev_end.record()
         sync_all()
     runner.step_events = None
+    # per-kernel rooflines: one more instance of the same workflow right after the timed
+    # region with CUDA events around every K5 and K7 launch (kept out of the timed region:
+    # an event between two launches costs the second its programmatic-launch overlap)
+    eng.reset()
+    runner.attn_events, runner.time_linear = attn_events, True
+    run_debate(eng, P, inputs[0], args.agents, args.rounds)
+    runner.attn_events, runner.time_linear = None, False
+    torch.cuda.synchronize()
     elapsed = ev_start.elapsed_time(ev_end) / 1e3
     busy = sum(a.elapsed_time(b) for a, b in step_events) / 1e3
     launches = runner.launches - launches0
@@ -395,9 +399,10 @@ def main() -> None:
                     "unit": "GB/s", "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": None,
                     "peak_source": peaks["source"], "avg_launch_us": round(1e3 * l_ms, 2),
                     "algorithmic_bytes_per_launch": int(l_b), "launches_timed": len(lin),
-                    "note": "CUDA events on the launching stream around each launch of the last "
-                            "timed workflow; the brackets remove the launch's programmatic-"
-                            "dependent-launch overlap, so this is conservative"}
+                    "note": "CUDA events on the launching stream around each launch of one extra "
+                            "instance of the timed workflow run right after the timed region; "
+                            "the brackets remove the launch's programmatic-dependent-launch "
+                            "overlap, so this is conservative"}
 
     if rank != 0:
         if world > 1:
