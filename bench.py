@@ -347,6 +347,11 @@ def main() -> None:
         ev_end.record()
         sync_all()
     runner.step_events = None
+    elapsed = ev_start.elapsed_time(ev_end) / 1e3
+    busy = sum(a.elapsed_time(b) for a, b in step_events) / 1e3
+    launches = runner.launches - launches0
+    h2d = (runner.h2d_bytes - h2d0) / args.steps
+    d2h = (eng.d2h_bytes - d2h0) / args.steps
     # per-kernel rooflines: one more instance of the same workflow right after the timed
     # region with CUDA events around every K5 and K7 launch (kept out of the timed region:
     # an event between two launches costs the second its programmatic-launch overlap)
@@ -355,11 +360,6 @@ def main() -> None:
     run_debate(eng, P, inputs[0], args.agents, args.rounds)
     runner.attn_events, runner.time_linear = None, False
     torch.cuda.synchronize()
-    elapsed = ev_start.elapsed_time(ev_end) / 1e3
-    busy = sum(a.elapsed_time(b) for a, b in step_events) / 1e3
-    launches = runner.launches - launches0
-    h2d = (runner.h2d_bytes - h2d0) / args.steps
-    d2h = (eng.d2h_bytes - d2h0) / args.steps
     if world > 1:
         t = torch.tensor([elapsed, busy], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -5,7 +5,7 @@
 // work is pure weight streaming (16 GB per step at the Llama-3.1-8B shape), so the kernel
 // is built to keep HBM busy, not the tensor core:
 //   * swap-AB: a 128-row weight tile is the UMMA A operand (M = 128), the activation rows
-//     are the B operand (N = NX = 16/32/64), accumulators live in TMEM (NX columns);
+//     are the B operand (N = NX = 16/32/64/128), accumulators live in TMEM (NX columns);
 //   * stream-K: the (tile, k-block) iteration space is cut into one equal contiguous range
 //     per CTA (one CTA per SM), so every SM streams the same number of weight bytes
 //     whatever the tile count (qkv: 48 tiles, o_proj/down: 32, gate|up: 224, head: 1002);
@@ -31,7 +31,7 @@ constexpr int kLnKB = 64;        // k elements per block (one 128-byte SW128 row
 
 struct LinearParams {
   float* y;       // [out_rows][N]
-  float* ws;      // [grid][2][NX][128] partial tiles
+  float* ws;      // [grid][2][NX][128] partial tiles (NX <= 128)
   int* counters;  // [n_tiles], zero between launches (reducers reset them)
   int N, KB, iters, grid, out_rows, split;
 };
@@ -289,9 +289,10 @@ extern "C" int choreo_linear_skinny(const void* x, int x_rows, int split, const 
   if (!x || !w || !y || !workspace || !tile_counters || x_rows <= 0 || n <= 0 || k <= 0 ||
       (split && (x_rows & 1)))
     return CHOREO_EINVAL;
-  if (x_rows > 64 || k % 8) return CHOREO_EUNSUPPORTED;  // TMA: 16-byte row pitch
+  if (x_rows > 128 || k % 8) return CHOREO_EUNSUPPORTED;  // TMA: 16-byte row pitch
   const int R = split ? x_rows / 2 : x_rows;  // output rows
-  const int NX = (split ? 2 * R : R) <= 16 ? 16 : (split ? 2 * R : R) <= 32 ? 32 : 64;
+  const int xr = split ? 2 * R : R;
+  const int NX = xr <= 16 ? 16 : xr <= 32 ? 32 : xr <= 64 ? 64 : 128;
   static int ksub = -1;
   if (ksub < 0) {
     const char* e = getenv("CHOREO_K7_KSUB");
@@ -313,7 +314,8 @@ extern "C" int choreo_linear_skinny(const void* x, int x_rows, int split, const 
   switch (NX) {
     case 16: LN_CASE(16)
     case 32: LN_CASE(32)
-    default: LN_CASE(64)
+    case 64: LN_CASE(64)
+    default: LN_CASE(128)
   }
 #undef LN_CASE
 }

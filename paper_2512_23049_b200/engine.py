@@ -345,6 +345,10 @@ class Engine:
                 self.cache.log_interleaved([s.mid for s in states], firsts, counts)
             for s in states:
                 self.cache.set_text(s.mid, s.call.header + decode_tokens(s.generated))
+        # like the reference, a decode call returns with its messages fully encoded in the
+        # cache (teacher-forced steps never synchronise mid-call, so without this the next
+        # call's TTFT would absorb this call's queued steps)
+        torch.cuda.current_stream(self.device).synchronize()
         stats.wall = time.perf_counter() - t0
         self.stats.append(stats)
         return ids

@@ -157,7 +157,7 @@ class Runner:
         self.split = self.dt == torch.bfloat16 and split_activations
         # K5 tensor-core precision: bit0 Q hi/lo, bit1 P hi/lo (env override for studies)
         self.attn_flags = int(os.environ.get("CHOREO_ATTN_FLAGS", "3"))
-        # K7 weight-streaming linear for decode-sized bf16 steps (cuBLAS above 64 GEMM rows)
+        # K7 weight-streaming linear for decode-sized bf16 steps (cuBLAS above 128 GEMM rows)
         self.k7 = self.dt == torch.bfloat16 and os.environ.get("CHOREO_K7", "1") != "0"
         self._k7_ws = self._k7_cnt = None
         # decode-sized bf16 steps run their layer loop in the native executor
@@ -201,8 +201,8 @@ class Runner:
         return out
 
     def _k7_ok(self, rows: int) -> bool:
-        """K7 takes the step when its stacked GEMM input has <= 64 rows."""
-        return self.k7 and (2 * rows if self.split else rows) <= 64
+        """K7 takes the step when its stacked GEMM input has <= 128 rows."""
+        return self.k7 and (2 * rows if self.split else rows) <= 128
 
     def _lin(self, a, w, rows: int):
         """f32 [rows, N] = a @ w^T through K7; a holds the step's GEMM input rows (hi/lo
@@ -300,7 +300,7 @@ class Runner:
         return delta
 
     def _lin_buffers(self) -> None:
-        self._k7_ws = torch.empty(148 * 2 * 64 * 128, dtype=torch.float32, device=self.dev)
+        self._k7_ws = torch.empty(148 * 2 * 128 * 128, dtype=torch.float32, device=self.dev)
         n_max = max(self.w.out_head.shape[0], self.w.layers[0]["w_gu"].shape[0],
                     self.w.layers[0]["w_qkv"].shape[0], self.d)
         self._k7_cnt = torch.zeros(cdiv(n_max, 128) + 1, dtype=torch.int32, device=self.dev)

@@ -5,7 +5,7 @@ import torch
 import kernel_bench as kb
 from paper_2512_23049_b200 import _native as nat
 stream = torch.cuda.current_stream().cuda_stream
-ws = torch.empty(148 * 2 * 64 * 128, device="cuda")
+ws = torch.empty(148 * 2 * 128 * 128, device="cuda")
 for name, n, k in (("qkv", 6144, 4096), ("o", 4096, 4096), ("gu", 28672, 4096), ("down", 4096, 14336)):
     ncopy = max(2, int(400e6 // (n * k * 2)) + 1)
     wl = [torch.randn(n, k, device="cuda").to(torch.bfloat16) for _ in range(ncopy)]

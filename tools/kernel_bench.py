@@ -299,7 +299,7 @@ def k7_linear(x_rows: int = 8, split: bool = True) -> list:
     shapes = {"qkv": ((cfg.n_heads + 2 * cfg.kv_heads) * cfg.head_dim, d), "o_proj": (d, d),
               "gate_up": (2 * f, d), "down": (d, f), "head": (cfg.vocab_size, d)}
     rows = 2 * x_rows if split else x_rows
-    ws = torch.empty(148 * 2 * 64 * 128, device="cuda")
+    ws = torch.empty(148 * 2 * 128 * 128, device="cuda")
     pk = peaks()
     out = []
     stream = torch.cuda.current_stream().cuda_stream
