@@ -97,6 +97,46 @@ def run_debate(engine, P, inputs, n_agents: int, n_rounds: int) -> dict:
     return {"ttft": ttft, "generated": generated}
 
 
+def c4_workflow(engine, P, seed: int, n_prefill: int = 16, n_rounds: int = 4, n_dec: int = 4,
+                pre_len=(64, 513), dec_len=(128, 257)):
+    """BASELINE config C4, one workflow: n_prefill messages of U(64, 512)
+    framed tokens, then n_rounds rounds of n_dec parallel decodes teacher-forced to
+    U(128, 256) tokens.  Each round lays all prior messages out in a fresh random order
+    with random gaps U{0..32}, 25 % of them reusing the previous parent's offset (an
+    overlap); every call lists a random >= 50 % subset of them in its own random order at
+    the round's agreed offsets (shared parents must agree within a batch, reference
+    engine.py:233-235).  A generator for paper_2512_23049_b200.BatchScheduler."""
+    rng = np.random.default_rng(seed)
+    msgs = list((yield P.Prefill([P.PrefillCall(random_text(rng, int(rng.integers(*pre_len))))
+                                  for _ in range(n_prefill)])))
+    decoded = []
+    for r in range(n_rounds):
+        order = [msgs[i] for i in rng.permutation(len(msgs))]
+        offs, cursor, prev = {}, 0, None
+        for m in order:
+            if prev is not None and rng.random() < 0.25:
+                o = prev
+            else:
+                o = cursor + int(rng.integers(0, 33))
+            offs[m] = o
+            prev = o
+            cursor = max(cursor, o + engine.message_token_count(m))
+        new_off = cursor + int(rng.integers(0, 33))
+        calls, forced = [], []
+        for a in range(n_dec):
+            k = int(rng.integers((len(order) + 1) // 2, len(order) + 1))
+            parents = [order[i] for i in sorted(rng.permutation(len(order))[:k])]
+            parents = [parents[i] for i in rng.permutation(len(parents))]
+            calls.append(P.DecodeCall(f"W{seed}R{r}A{a}:", parents=parents,
+                                      offsets=[offs[m] for m in parents], new_offset=new_off,
+                                      sampling=P.SamplingParams(max_tokens=1024)))
+            forced.append(rng.integers(97, 123, size=int(rng.integers(*dec_len))).tolist())
+        ids = yield P.Decode(calls, force_tokens=forced)
+        msgs += list(ids)
+        decoded += list(ids)
+    return decoded
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -282,6 +322,35 @@ def reencode_baseline(P, weights, inputs, args, choreo_ttft, choreo_tps) -> dict
     return out
 
 
+def c4_batched(P, weights, rank: int, n_wf: int) -> dict:
+    """Config C4 on this GPU: n_wf C4 workflows batched per step by BatchScheduler (one
+    forward per step for all their agents) on one engine; one warm-up pass, then one timed
+    pass (CUDA events), decode tokens / time and per-message TTFT."""
+    import torch
+
+    eng = P.Engine(weights, capacity=1 << 17, seed=rank)
+    for rep in range(2):
+        eng.reset()
+        wfs = [c4_workflow(eng, P, 10_000 * rep + 100 * rank + k) for k in range(n_wf)]
+        sch = P.BatchScheduler(eng)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        res = sch.run(wfs)
+        b.record()
+        torch.cuda.synchronize()
+    secs = a.elapsed_time(b) / 1e3
+    gen = sum(len(eng.generated_token_ids(m)) for ids in res for m in ids)
+    ttft = [v for t in sch.ticks for v in t.ttft.values()]
+    out = {"workflows": n_wf, "generated_tokens": gen, "seconds": round(secs, 3),
+           "decode_tokens_per_s": round(gen / secs, 1),
+           "ttft_p50_ms": round(1e3 * statistics.median(ttft), 3),
+           "merged_ticks": sum(t.merged for t in sch.ticks), "ticks": len(sch.ticks)}
+    del eng
+    torch.cuda.empty_cache()
+    return out
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -297,6 +366,8 @@ def main() -> None:
     ap.add_argument("--no-reencode", action="store_true",
                     help="skip the re-encoding comparator (BaselineEngine) workflow")
     ap.add_argument("--model", default="llama-3.1-8b")
+    ap.add_argument("--no-c4", action="store_true",
+                    help="skip the config-C4 batched-workflows measurement (BatchScheduler)")
     args = ap.parse_args()
     if args.impl == "reference":
         reference_arm(args)
@@ -404,6 +475,23 @@ def main() -> None:
                             "the brackets remove the launch's programmatic-dependent-launch "
                             "overlap, so this is conservative"}
 
+    c4 = None
+    if not args.no_c4:  # every rank runs its own 8 workflows (C4: 64 over 8 GPUs)
+        c4_one = c4_batched(P, weights, rank, 1)
+        c4 = c4_batched(P, weights, rank, 8)
+        if world > 1:
+            t = torch.tensor([c4["seconds"], c4["generated_tokens"]], device="cuda",
+                             dtype=torch.float64)
+            mx = t.clone()
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+            dist.all_reduce(t)
+            c4["all_ranks_tokens_per_s"] = round(float(t[1] / mx[0]), 1)
+        c4 = {"workload": "C4: Llama-3.1-8B shape, 8 choreographed workflows per GPU batched per "
+                          "step (16 prefilled U(64,512) + 4 rounds x 4 decodes U(128,256), "
+                          "reordered parent subsets, gaps, 25% overlaps)",
+              "batched_8": c4, "single_workflow": c4_one,
+              "batching_speedup": round(c4["decode_tokens_per_s"] / c4_one["decode_tokens_per_s"], 2)}
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -446,6 +534,7 @@ def main() -> None:
         "attention_roofline": attn_roofline,
         "kernel_rooflines": kernels,
         "reencode_baseline": reencode,
+        "c4_batched_workflows": c4,
         "cpu_baseline": cpu,
         "clocks": clocks.summary(),
     }

@@ -15,12 +15,13 @@ from .errors import (AllMaskedError, CapacityError, ChoreoError, DeltaRangeError
                      EmptyHeaderError, InvalidCallError, NativeError, NondeterminismError,
                      OffsetConflictError, ScriptError, ShapeError, TraceMismatchError,
                      UnknownMessageError, WindowOverflowError)
+from .scheduler import BatchScheduler, Decode, Prefill
 from .tokenizer import decode_tokens, encode_text, frame_header, frame_message, generatable_mask
 from .weights import (DeviceWeights, LayerWeights, WeightSet, init_weights, load_weights,
                       save_weights)
 
 __all__ = [
-    "BaselineEngine", "PrefixTrie",
+    "BaselineEngine", "PrefixTrie", "BatchScheduler", "Decode", "Prefill",
     "BOS_MSG", "DEFAULT_CONFIG", "EOS_MSG", "LLAMA_3_1_8B", "LLAMA_3_1_70B", "LLAMA_3_2_1B",
     "N_RESERVED", "PRESETS", "ModelConfig", "CallStats", "DecodeCall", "Engine", "PrefillCall",
     "SamplingParams", "encode_flops", "AllMaskedError", "CapacityError", "ChoreoError",
