@@ -12,8 +12,10 @@ import json
 from dataclasses import asdict, dataclass, field
 from pathlib import Path
 
+import numpy as np
+
 from .engine import DecodeCall, PrefillCall, SamplingParams
-from .errors import ScriptError
+from .errors import ScriptError, TraceMismatchError
 
 OPS = ("prefill", "prefill_parallel", "decode", "decode_parallel")
 
@@ -79,6 +81,64 @@ class Trace:
                 d["logits"] = None if s.logits is None else {
                     k: [list(map(float, r)) for r in v] for k, v in s.logits.items()}
                 fh.write(json.dumps(d, sort_keys=True) + "\n")
+
+
+    @classmethod
+    def from_jsonl(cls, path) -> "Trace":
+        """Inverse of to_jsonl (reference script.py:235-262 reads the same layout)."""
+        lines = [json.loads(x) for x in Path(path).read_text(encoding="utf-8").splitlines() if x]
+        if not lines or lines[0].get("kind") != "trace":
+            raise ScriptError(f"{path}: not a trace file")
+        head = lines[0]
+        tr = cls(head["script"], head["engine"], head["seed"], head["config"])
+        for d in lines[1:]:
+            msgs = [MessageResult(**m) for m in d.pop("messages")]
+            tr.steps.append(StepRecord(messages=msgs, **d))
+        return tr
+
+
+def diff_traces(a: Trace, b: Trace, *, compare_logits: bool = False,
+                atol: float = 1e-9) -> list[str]:
+    """What two runs of one script disagree on (reference script.py:348-379).
+
+    Structural differences (other script, other steps / message names) raise
+    TraceMismatchError; engine kind, walls and cost counters are not compared.  Returns one
+    line per content difference (text, token count, generated ids, optionally logits
+    beyond ``atol``); empty when the runs are equivalent.
+    """
+    if a.script_name != b.script_name:
+        raise TraceMismatchError(f"scripts differ: {a.script_name!r} / {b.script_name!r}")
+    if len(a.steps) != len(b.steps):
+        raise TraceMismatchError(f"{len(a.steps)} vs {len(b.steps)} steps")
+    out: list[str] = []
+    for sa, sb in zip(a.steps, b.steps):
+        if (sa.name, sa.op) != (sb.name, sb.op) or len(sa.messages) != len(sb.messages):
+            raise TraceMismatchError(f"step {sa.index} differs in structure")
+        for ma, mb in zip(sa.messages, sb.messages):
+            if ma.name != mb.name:
+                raise TraceMismatchError(f"step {sa.name}: message {ma.name} vs {mb.name}")
+            if ma.text != mb.text:
+                out.append(f"{ma.name}: text {ma.text!r} != {mb.text!r}")
+            if ma.token_count != mb.token_count:
+                out.append(f"{ma.name}: token count {ma.token_count} != {mb.token_count}")
+            if list(ma.generated or []) != list(mb.generated or []):
+                out.append(f"{ma.name}: generated ids differ")
+        if compare_logits and (sa.logits is not None or sb.logits is not None):
+            if sa.logits is None or sb.logits is None:
+                out.append(f"{sa.name}: logits recorded on one side only")
+                continue
+            for name in sorted(set(sa.logits) | set(sb.logits)):
+                ra, rb = sa.logits.get(name), sb.logits.get(name)
+                if ra is None or rb is None or len(ra) != len(rb):
+                    out.append(f"{name}: logits row counts differ")
+                    continue
+                for i, (x, y) in enumerate(zip(ra, rb)):
+                    x, y = np.asarray(x, np.float64), np.asarray(y, np.float64)
+                    err = float(np.abs(x - y).max()) if x.shape == y.shape and x.size else 0.0
+                    if x.shape != y.shape or err > atol:
+                        out.append(f"{name}: logits row {i} differ (max abs {err:.3e})")
+                        break
+    return out
 
 
 def validate_script(script: dict) -> None:
