@@ -351,6 +351,55 @@ def c4_batched(P, weights, rank: int, n_wf: int) -> dict:
     return out
 
 
+def c2_agents(P, rank: int) -> dict:
+    """Config C2: Llama-3.2-1B shape, random-init bf16; a global cache of
+    32 messages x 256 tokens (4 prefill_parallel batches of 8), then ONE decode_parallel of
+    4 agents, each over 12 of the 32 messages (a random subset in random order) laid out
+    with gaps U{0..32} and 25 % overlaps at offsets shared by the batch; greedy, 256
+    tokens.  Timed with CUDA events around the decode call (one warm-up instance first)."""
+    import torch
+
+    cfg = P.PRESETS["llama-3.2-1b"]
+    w = P.DeviceWeights.random(cfg, dtype=torch.bfloat16, seed=cfg.seed + rank)
+    eng = P.Engine(w, capacity=16384, seed=rank)
+    for rep in range(2):
+        eng.reset()
+        rng = np.random.default_rng(1000 * rep + rank)
+        ids = []
+        for _ in range(4):
+            ids += eng.prefill_parallel([P.PrefillCall(random_text(rng, 256)) for _ in range(8)])
+        offs, cursor, prev = {}, 0, None
+        for i in rng.permutation(32):
+            o = prev if prev is not None and rng.random() < 0.25 else cursor + int(rng.integers(0, 33))
+            offs[ids[i]] = o
+            prev, cursor = o, max(cursor, o + 256)
+        calls = []
+        for a in range(4):
+            parents = [ids[j] for j in rng.permutation(32)[:12]]
+            calls.append(P.DecodeCall(f"Agent {a}:", parents=parents,
+                                      offsets=[offs[m] for m in parents],
+                                      new_offset=cursor + int(rng.integers(0, 33)),
+                                      sampling=P.SamplingParams(max_tokens=256)))
+        torch.cuda.synchronize()
+        a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_.record()
+        ms = eng.decode_parallel(calls)
+        b_.record()
+        torch.cuda.synchronize()
+    secs = a_.elapsed_time(b_) / 1e3
+    gen = sum(len(eng.generated_token_ids(m)) for m in ms)
+    st = eng.last_stats
+    out = {"workload": "C2: Llama-3.2-1B shape, 4 parallel agents (greedy, 256 tokens) over "
+                       "12-message reordered subsets of a shared 8K-token global cache",
+           "generated_tokens": gen, "seconds": round(secs, 4),
+           "decode_tokens_per_s": round(gen / secs, 1),
+           "ttft_p50_ms": round(1e3 * statistics.median(st.ttft.values()), 3),
+           "repositioned_tokens": st.repositioned_tokens, "cache_hit_tokens": st.cache_hit_tokens}
+    del eng, w
+    torch.cuda.empty_cache()
+    return out
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -366,6 +415,8 @@ def main() -> None:
     ap.add_argument("--no-reencode", action="store_true",
                     help="skip the re-encoding comparator (BaselineEngine) workflow")
     ap.add_argument("--model", default="llama-3.1-8b")
+    ap.add_argument("--no-c2", action="store_true",
+                    help="skip the config-C2 measurement (1B shape, 4 agents, 8K cache)")
     ap.add_argument("--no-c4", action="store_true",
                     help="skip the config-C4 batched-workflows measurement (BatchScheduler)")
     args = ap.parse_args()
@@ -508,6 +559,9 @@ def main() -> None:
         torch.cuda.empty_cache()
         kernels = ([kb.k2_rerotate(), kb.k4_prefill(), kb.k5_decode(1, v2=True),
                     kb.k5_decode(8, v2=True)] + kb.k7_linear())
+    c2 = None
+    if world == 1 and not args.no_c2:
+        c2 = c2_agents(P, rank)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_reference_sample(args.agents, args.ref_tokens)
@@ -535,6 +589,7 @@ def main() -> None:
         "kernel_rooflines": kernels,
         "reencode_baseline": reencode,
         "c4_batched_workflows": c4,
+        "c2_agents_1b": c2,
         "cpu_baseline": cpu,
         "clocks": clocks.summary(),
     }
