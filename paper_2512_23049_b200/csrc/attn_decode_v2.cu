@@ -6,7 +6,9 @@
 // per SM):
 //   warp 8      TMA producer: streams each unit's K and V pages (2D tensor maps over the
 //               pool, SW128 boxes of 64 keys x 64 dims) into a 4-slot ring, mbarriers;
-//   warp 9      unit loader: stages the next unit's rows, page lengths and Q (cp.async) in smem;
+//   warp 9      unit loader: stages the next unit's rows, page lengths and Q (bf16) in smem;
+//   warps 10-11 merge warps (one per m-tile): combine the four key-slice states of a unit
+//               and write its partials while the compute warps already stream the next unit;
 //   warps 0-7   consumers, warp = (key slice q4 in 0..3, m-tile mt in 0..1): every page's
 //               64 keys are split four ways (16 keys per warp), the <= 32 (row, query head)
 //               vectors in two m16 tiles; S = Q K^T and O += P V on mma.sync m16n8k16
@@ -29,7 +31,8 @@ constexpr int kDvSlots = 4;        // K/V page ring
 constexpr int kDvConsumers = 8;    // warps 0-7
 constexpr int kDvProducer = 8;     // warp 8: TMA
 constexpr int kDvLoader = 9;       // warp 9: unit metadata + Q staging
-constexpr int kDvThreads = 32 * 10;
+constexpr int kDvMerge = 10;       // warps 10, 11: merge the key-slice states of m-tile 0 / 1
+constexpr int kDvThreads = 32 * 12;
 constexpr int kDvMaxPages = 32;    // pages per unit staged in the unit record (host: ppi <= 32)
 
 struct DvParams {
@@ -52,13 +55,14 @@ struct DvCfg {
   static constexpr int kR = HD / 64;                      // 64-dim SW128 halves per page
   static constexpr int kHalf = 64 * 128;                  // bytes of one [64][64] bf16 tile
   static constexpr int kSlot = 2 * kR * kHalf;            // K + V of one page
-  static constexpr int kMergeRow = HD + 2;                // O row + m + l (floats)
-  static constexpr int kMerge = 3 * 2 * 16 * kMergeRow * 4;
-  static constexpr int kQLd = HD + 4;                     // padded f32 Q row
+  static constexpr int kMergeRow = HD + 4;                // O row + m + l (floats, 16-B rows)
+  // 4 key slices x 2 m-tiles x 16 rows, then a 4-int header (M, pbase, kvh)
+  static constexpr int kMerge = 4 * 2 * 16 * kMergeRow * 4 + 16;
+  static constexpr int kQLd = HD + 8;                     // padded bf16 Q row (conflict-free)
   // unit record: ints [0] M [1] vb [2] nv [3] pbase [4] kvh, [8..40) row_t per vector,
-  // [40..72) page len, [72..104) own base; then Q f32 [32][kQLd] (cp.async from q)
+  // [40..72) page len, [72..104) own base; then Q bf16 [32][kQLd], pre-scaled
   static constexpr int kUnitInts = 128;
-  static constexpr int kUnit = kUnitInts * 4 + 32 * kQLd * 4;
+  static constexpr int kUnit = kUnitInts * 4 + 32 * kQLd * 2;
   static constexpr int kTotal = kDvSlots * kSlot + kMerge + 2 * kUnit + 1024;
 };
 
@@ -96,6 +100,10 @@ __device__ __forceinline__ uint32_t dv_addr(uint32_t base, int key, int c) {
 }
 
 template <int HD>
+__device__ __forceinline__ void dv_merge_unit(const DvParams& p, const float* merge, int mt,
+                                              int lane, int G);
+
+template <int HD>
 __global__ void __launch_bounds__(kDvThreads, 1)
     decode_attn_v2(DvParams p, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV) {
@@ -123,7 +131,7 @@ __global__ void __launch_bounds__(kDvThreads, 1)
       mbar_init(&unit_full[i], 32);
       mbar_init(&unit_empty[i], kDvConsumers);
     }
-    mbar_init(&merge_full, 6);
+    mbar_init(&merge_full, kDvConsumers);
     mbar_init(&merge_empty, 2);
     fence_barrier_init();
     tma_prefetch_desc(&tmK);
@@ -141,23 +149,13 @@ __global__ void __launch_bounds__(kDvThreads, 1)
       const int sl = u & 1;
       mbar_wait(&unit_empty[sl], ((u >> 1) & 1) ^ 1);
       int* ui = reinterpret_cast<int*>(units + sl * C::kUnit);
-      float* qf = reinterpret_cast<float*>(units + sl * C::kUnit + C::kUnitInts * 4);
+      __nv_bfloat16* qs = reinterpret_cast<__nv_bfloat16*>(units + sl * C::kUnit + C::kUnitInts * 4);
       const int32_t* it = p.items + 6 * (w / p.n_kv);
       const int iv = lane < 5 ? it[lane] : 0;
       const int rb = __shfl_sync(0xffffffffu, iv, 0), nr = __shfl_sync(0xffffffffu, iv, 1);
       const int vb = __shfl_sync(0xffffffffu, iv, 2), nv = __shfl_sync(0xffffffffu, iv, 3);
       const int kvh = w % p.n_kv, M = nr * G;
       const int rid = lane < M ? p.blk_rows[rb + lane / G] : 0;
-      // Q vectors of the unit straight into shared memory (f32, one round trip)
-      for (int m = 0; m < M; ++m) {  // warp-uniform loop: lane = 16-byte chunk of vector m
-        const int r = __shfl_sync(0xffffffffu, rid, m);
-        if (4 * lane < HD) {
-          const float* src = p.q + ((int64_t)r * p.n_heads + kvh * G + m % G) * HD + 4 * lane;
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_addr(qf + m * C::kQLd + 4 * lane)),
-                       "l"(src));
-        }
-      }
-      asm volatile("cp.async.commit_group;\n" ::);
       const int pbase = __shfl_sync(0xffffffffu, iv, 4);
       if (lane == 0) {
         ui[0] = M;
@@ -169,8 +167,36 @@ __global__ void __launch_bounds__(kDvThreads, 1)
       ui[8 + lane] = lane < M ? p.row_t[rid] : -1;
       ui[40 + lane] = lane < nv ? p.vis_len[vb + lane] : 0;
       ui[72 + lane] = lane < nv ? p.vis_own[vb + lane] : -1;
-      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      // Q: lane = 4 dims of every vector; all loads in flight at once (one round trip),
+      // then scaled to the log2 domain and stored as bf16 (rows past M are zero)
+      const float sc = p.scale_log2;
+      float4 v[32];
+#pragma unroll
+      for (int m = 0; m < 32; ++m) {
+        const int r = __shfl_sync(0xffffffffu, rid, m);
+        v[m] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (m < M && 4 * lane < HD)
+          v[m] = *reinterpret_cast<const float4*>(p.q + ((int64_t)r * p.n_heads + kvh * G + m % G) * HD + 4 * lane);
+      }
+      if (4 * lane < HD) {
+#pragma unroll
+        for (int m = 0; m < 32; ++m)
+          *reinterpret_cast<uint2*>(qs + m * C::kQLd + 4 * lane) =
+              make_uint2(pack_bf16(v[m].x * sc, v[m].y * sc), pack_bf16(v[m].z * sc, v[m].w * sc));
+      }
       mbar_arrive(&unit_full[sl]);
+    }
+    return;
+  }
+  if (warp >= kDvMerge) {
+    // ------------------------------------------------------------------ merge warps
+    const int mt = warp - kDvMerge;
+    int u = 0;
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++u) {
+      mbar_wait(&merge_full, u & 1);
+      dv_merge_unit<HD>(p, merge, mt, lane, G);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&merge_empty);
     }
     return;
   }
@@ -208,31 +234,21 @@ __global__ void __launch_bounds__(kDvThreads, 1)
     const int sl = u & 1;
     mbar_wait(&unit_full[sl], (u >> 1) & 1);
     const int* ui = reinterpret_cast<const int*>(units + sl * C::kUnit);
-    const float* qf = reinterpret_cast<const float*>(units + sl * C::kUnit + C::kUnitInts * 4);
+    const __nv_bfloat16* qs = reinterpret_cast<const __nv_bfloat16*>(units + sl * C::kUnit + C::kUnitInts * 4);
     const int M = ui[0], nv = ui[2], pbase = ui[3], kvh = ui[4];
     const bool active = mt * 16 < M;  // warp-uniform: this m-tile has query vectors
     const int mA = mt * 16 + g, mB = mA + 8;
     const bool vA = mA < M, vB = mB < M;
     const int rtA = ui[8 + mA], rtB = ui[8 + mB];
-    // Q as bf16 A fragments, pre-scaled to the log2 domain (rows past M are zero)
+    // Q as bf16 A fragments (pre-scaled to the log2 domain; rows past M are zero)
     uint32_t qa[KS][4];
-    {
-      const float sc = p.scale_log2;
-      const float* qA = qf + (vA ? mA : 0) * C::kQLd;
-      const float* qB = qf + (vB ? mB : 0) * C::kQLd;
-      const float fa = vA ? sc : 0.f, fb = vB ? sc : 0.f;
 #pragma unroll
-      for (int ks = 0; ks < KS; ++ks) {
-        const int c = 16 * ks + 2 * t;
-        const float2 a0 = *reinterpret_cast<const float2*>(qA + c);
-        const float2 a1 = *reinterpret_cast<const float2*>(qB + c);
-        const float2 a2 = *reinterpret_cast<const float2*>(qA + c + 8);
-        const float2 a3 = *reinterpret_cast<const float2*>(qB + c + 8);
-        qa[ks][0] = pack_bf16(a0.x * fa, a0.y * fa);
-        qa[ks][1] = pack_bf16(a1.x * fb, a1.y * fb);
-        qa[ks][2] = pack_bf16(a2.x * fa, a2.y * fa);
-        qa[ks][3] = pack_bf16(a3.x * fb, a3.y * fb);
-      }
+    for (int ks = 0; ks < KS; ++ks) {
+      const int c = 16 * ks + 2 * t;
+      qa[ks][0] = *reinterpret_cast<const uint32_t*>(qs + mA * C::kQLd + c);
+      qa[ks][1] = *reinterpret_cast<const uint32_t*>(qs + mB * C::kQLd + c);
+      qa[ks][2] = *reinterpret_cast<const uint32_t*>(qs + mA * C::kQLd + c + 8);
+      qa[ks][3] = *reinterpret_cast<const uint32_t*>(qs + mB * C::kQLd + c + 8);
     }
     float o[NT][4];
 #pragma unroll
@@ -339,16 +355,14 @@ __global__ void __launch_bounds__(kDvThreads, 1)
 
     __syncwarp();
     if (lane == 0) mbar_arrive(&unit_empty[sl]);
-    // ---- merge the four key-slice states of each m-tile, write the partials ----
+    // ---- hand the key-slice state to the merge warps ----
     lA += __shfl_xor_sync(0xffffffffu, lA, 1);
     lA += __shfl_xor_sync(0xffffffffu, lA, 2);
     lB += __shfl_xor_sync(0xffffffffu, lB, 1);
     lB += __shfl_xor_sync(0xffffffffu, lB, 2);
-    if (q4 > 0) {
-      if (u > 0) mbar_wait(&merge_empty, (u - 1) & 1);
-    }
-    if (q4 > 0 && active) {
-      float* sc = merge + ((q4 - 1) * 2 + mt) * 16 * C::kMergeRow;
+    if (u > 0) mbar_wait(&merge_empty, (u - 1) & 1);  // the merge warps read unit u-1
+    if (active) {
+      float* sc = merge + (q4 * 2 + mt) * 16 * C::kMergeRow;
 #pragma unroll
       for (int n = 0; n < NT; ++n) {
         *reinterpret_cast<float2*>(sc + g * C::kMergeRow + 8 * n + 2 * t) = make_float2(o[n][0], o[n][1]);
@@ -361,71 +375,60 @@ __global__ void __launch_bounds__(kDvThreads, 1)
         sc[(g + 8) * C::kMergeRow + HD + 1] = lB;
       }
     }
-    if (q4 > 0) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&merge_full);
-      continue;
-    }
-    mbar_wait(&merge_full, u & 1);
-    if (active) {
-      float MA = mxA, MB = mxB;
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const float* sc = merge + (k * 2 + mt) * 16 * C::kMergeRow;
-        MA = fmaxf(MA, sc[g * C::kMergeRow + HD]);
-        MB = fmaxf(MB, sc[(g + 8) * C::kMergeRow + HD]);
-      }
-      const float wA0 = MA == -INFINITY ? 0.f : dv_ex2(mxA - MA);
-      const float wB0 = MB == -INFINITY ? 0.f : dv_ex2(mxB - MB);
-      float LA = lA * wA0, LB = lB * wB0;
-#pragma unroll
-      for (int n = 0; n < NT; ++n) {
-        o[n][0] *= wA0;
-        o[n][1] *= wA0;
-        o[n][2] *= wB0;
-        o[n][3] *= wB0;
-      }
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const float* sc = merge + (k * 2 + mt) * 16 * C::kMergeRow;
-        const float mkA = sc[g * C::kMergeRow + HD], mkB = sc[(g + 8) * C::kMergeRow + HD];
-        const float wA = mkA == -INFINITY ? 0.f : dv_ex2(mkA - MA);
-        const float wB = mkB == -INFINITY ? 0.f : dv_ex2(mkB - MB);
-        LA += sc[g * C::kMergeRow + HD + 1] * wA;
-        LB += sc[(g + 8) * C::kMergeRow + HD + 1] * wB;
-#pragma unroll
-        for (int n = 0; n < NT; ++n) {
-          const float2 xa = *reinterpret_cast<const float2*>(sc + g * C::kMergeRow + 8 * n + 2 * t);
-          const float2 xb = *reinterpret_cast<const float2*>(sc + (g + 8) * C::kMergeRow + 8 * n + 2 * t);
-          o[n][0] += wA * xa.x;
-          o[n][1] += wA * xa.y;
-          o[n][2] += wB * xb.x;
-          o[n][3] += wB * xb.y;
-        }
-      }
-      const float ln2 = 0.6931471805599453f;
-      if (vA) {
-        const int64_t pidx = (int64_t)(pbase + mA / G) * p.n_heads + kvh * G + mA % G;
-        const float inv = LA > 0.f ? 1.f / LA : 0.f;
-#pragma unroll
-        for (int n = 0; n < NT; ++n)
-          *reinterpret_cast<float2*>(p.part_o + pidx * HD + 8 * n + 2 * t) =
-              make_float2(o[n][0] * inv, o[n][1] * inv);
-        if (t == 0) p.part_lse[pidx] = LA > 0.f ? (MA + log2f(LA)) * ln2 : -INFINITY;
-      }
-      if (vB) {
-        const int64_t pidx = (int64_t)(pbase + mB / G) * p.n_heads + kvh * G + mB % G;
-        const float inv = LB > 0.f ? 1.f / LB : 0.f;
-#pragma unroll
-        for (int n = 0; n < NT; ++n)
-          *reinterpret_cast<float2*>(p.part_o + pidx * HD + 8 * n + 2 * t) =
-              make_float2(o[n][2] * inv, o[n][3] * inv);
-        if (t == 0) p.part_lse[pidx] = LB > 0.f ? (MB + log2f(LB)) * ln2 : -INFINITY;
-      }
+    if (warp == 0 && lane == 0) {
+      int* hdr = reinterpret_cast<int*>(merge + 4 * 2 * 16 * C::kMergeRow);
+      hdr[0] = M;
+      hdr[1] = pbase;
+      hdr[2] = kvh;
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&merge_empty);
+    if (lane == 0) mbar_arrive(&merge_full);
   }
+}
+
+// Merge warp of m-tile mt: lane = (row, 64-dim half); combines the four key slices' (O, m,
+// l) of each of the tile's 16 rows (LSE rule) and writes the normalised partial + LSE.
+template <int HD>
+__device__ __forceinline__ void dv_merge_unit(const DvParams& p, const float* merge, int mt,
+                                              int lane, int G) {
+  constexpr int MR = HD + 4;
+  constexpr int W = HD / 2;  // dims per lane
+  const int* hdr = reinterpret_cast<const int*>(merge + 4 * 2 * 16 * MR);
+  const int M = hdr[0], pbase = hdr[1], kvh = hdr[2];
+  const int row = lane >> 1, half = lane & 1;
+  const int m = mt * 16 + row;
+  if (mt * 16 >= M || m >= M) return;
+  float mk[4], lk[4], mx = -INFINITY;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float* sc = merge + (k * 2 + mt) * 16 * MR + row * MR;
+    mk[k] = sc[HD];
+    lk[k] = sc[HD + 1];
+    mx = fmaxf(mx, mk[k]);
+  }
+  float wk[4], L = 0.f;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    wk[k] = mk[k] == -INFINITY ? 0.f : dv_ex2(mk[k] - mx);
+    L += lk[k] * wk[k];
+  }
+  const float inv = L > 0.f ? 1.f / L : 0.f;
+  const int64_t pidx = (int64_t)(pbase + m / G) * p.n_heads + kvh * G + m % G;
+  float* dst = p.part_o + pidx * HD + half * W;
+#pragma unroll 4
+  for (int d = 0; d < W; d += 4) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float4 x = *reinterpret_cast<const float4*>(merge + (k * 2 + mt) * 16 * MR + row * MR + half * W + d);
+      acc.x += wk[k] * x.x;
+      acc.y += wk[k] * x.y;
+      acc.z += wk[k] * x.z;
+      acc.w += wk[k] * x.w;
+    }
+    *reinterpret_cast<float4*>(dst + d) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+  }
+  if (half == 0) p.part_lse[pidx] = L > 0.f ? (mx + log2f(L)) * 0.6931471805599453f : -INFINITY;
 }
 
 // ---------------------------------------------------------------- host side
