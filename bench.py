@@ -268,7 +268,11 @@ def reference_arm(args) -> None:
     if rank != 0:
         return
     cores = len(os.sched_getaffinity(0))
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores))
+    try:  # torchrun exports OMP_NUM_THREADS=1 before numpy loads: lift it for the CPU arm
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(limits=cores)
+    except ImportError:
+        pass
     vals, ttfts, t_all = [], [], 0.0
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
@@ -432,9 +436,14 @@ def main() -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    n_dev = torch.cuda.device_count()
+    local = local % n_dev  # > 1 rank per GPU only when testing the multi-rank path on one GPU
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if n_dev >= world:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:  # ranks sharing a GPU: NCCL refuses duplicate devices, gloo reduces CUDA tensors
+            dist.init_process_group("gloo")
     cfg = P.PRESETS[args.model]
     weights = P.DeviceWeights.random(cfg, dtype=torch.bfloat16, device="cuda", seed=cfg.seed + rank)
     eng = P.Engine(weights, capacity=65536, seed=rank)
