@@ -325,3 +325,43 @@ def test_native_decode_executor_bitwise_equals_python_loop(hd, H, Hk):
         assert np.array_equal(a, b)
     for a, b in zip(runs["native"], runs["cublas"]):
         assert float(np.abs(a - b).max()) <= 2e-2
+
+
+def test_llama8b_width_two_layers_matches_oracle():
+    """Full Llama-3.1-8B layer width (d 4096, 32 query / 8 KV heads, hd 128, ffn 14336), two
+    layers, small vocabulary: a reordered, moved-parent prefill (K2 + K4) and a parallel
+    decode whose header step and decode steps run K7 + K5 v2 through the native executor.
+    Teacher-forced on the oracle's tokens (bf16-rounded weights on both sides), logits
+    within the bf16 tolerance 2e-2; positions bit-exact."""
+    shape = O.Shape(n_layers=2, n_heads=32, n_kv_heads=8, head_dim=128, ffn_dim=14336,
+                    vocab_size=512, context_window=4096, rope_base=500000.0)
+    cfg = P.ModelConfig(**{k: getattr(shape, k) for k in shape.__dataclass_fields__})
+    ow = O.round_weights(O.init_weights(shape, dtype=np.float32), "bf16")
+    ref = O.Oracle(ow, shape, capacity=4096, record_logits=True)
+    ws = P.init_weights(cfg).rounded("bf16")
+    eng = P.Engine(P.DeviceWeights.from_host(ws, dtype=torch.bfloat16), capacity=4096,
+                   record_logits=True)
+    rng = np.random.default_rng(8)
+    texts = ["".join(chr(97 + int(c)) for c in rng.integers(0, 26, n)) for n in (120, 200, 90)]
+    for t in texts:
+        ref.prefill({"message": t})
+        eng.prefill(P.PrefillCall(t))
+    ref.prefill({"message": texts[0][:70], "parents": [2, 0], "offsets": [0, 150]})
+    eng.prefill(P.PrefillCall(texts[0][:70], parents=[2, 0], offsets=[0, 150]))
+    sp_o, sp_p = O.Sampling(max_tokens=12), P.SamplingParams(max_tokens=12)
+    calls = [("Agent one:", [3, 1], [0, 80]), ("Agent two:", [0, 3], [300, 0]),
+             ("Third:", [1, 2, 0], [80, 410, 300])]
+    ref.decode_batch([{"header": h, "parents": p, "offsets": o, "sampling": sp_o}
+                      for h, p, o in calls])
+    forcing = [ref.generated(m) for m in (4, 5, 6)]
+    eng.decode_parallel([P.DecodeCall(h, parents=p, offsets=o, sampling=sp_p) for h, p, o in calls],
+                        force_tokens=forcing)
+    worst = 0.0
+    for m in (4, 5, 6):
+        got = np.stack(eng.stats[-1].logits[m])
+        want = np.stack(ref.stats[-1].logits[m])
+        assert got.shape == want.shape
+        worst = max(worst, float(np.abs(got - want).max()))
+    assert worst <= 2e-2, worst
+    n = eng.cache.token_count
+    assert eng.cache.positions[:n].tolist() == ref.store.pos[:n].tolist()
