@@ -202,22 +202,33 @@ __global__ void __launch_bounds__(kDvThreads, 1)
   }
   if (warp == kDvProducer) {
     // ------------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      uint32_t gp = 0;
-      for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
-        const int32_t* it = p.items + 6 * (w / p.n_kv);
-        const int kvh = w % p.n_kv, vb = it[2], nv = it[3];
-        for (int j = 0; j < nv; ++j, ++gp) {
-          const int st = gp % kDvSlots;
-          mbar_wait(&empty_bar[st], ((gp / kDvSlots) & 1) ^ 1);
-          const int row0 = ((p.layer * p.n_kv + kvh) * p.n_pages + p.vis_page[vb + j]) * 64;
-          uint8_t* dst = base + st * C::kSlot;
-          mbar_arrive_expect_tx(&full_bar[st], C::kSlot);
+    // the whole warp fetches a unit's record and up to 32 page ids in one round trip each
+    // (a per-page dependent load would cap the ring at one page per L2 round trip); lane 0
+    // issues the TMA copies
+    uint32_t gp = 0;
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+      const int32_t* it = p.items + 6 * (w / p.n_kv);
+      const int iv = lane < 4 ? it[lane] : 0;
+      const int vb = __shfl_sync(0xffffffffu, iv, 2), nv = __shfl_sync(0xffffffffu, iv, 3);
+      const int kvh = w % p.n_kv;
+      for (int j0 = 0; j0 < nv; j0 += 32) {
+        const int pid = j0 + lane < nv ? p.vis_page[vb + j0 + lane] : 0;
+        const int nj = min(32, nv - j0);
+        for (int jj = 0; jj < nj; ++jj, ++gp) {
+          const int page = __shfl_sync(0xffffffffu, pid, jj);
+          if (lane == 0) {
+            const int st = gp % kDvSlots;
+            mbar_wait(&empty_bar[st], ((gp / kDvSlots) & 1) ^ 1);
+            const int row0 = ((p.layer * p.n_kv + kvh) * p.n_pages + page) * 64;
+            uint8_t* dst = base + st * C::kSlot;
+            mbar_arrive_expect_tx(&full_bar[st], C::kSlot);
 #pragma unroll
-          for (int r = 0; r < C::kR; ++r) {
-            tma_load_2d(dst + r * C::kHalf, &tmK, &full_bar[st], r * 64, row0);
-            tma_load_2d(dst + (C::kR + r) * C::kHalf, &tmV, &full_bar[st], r * 64, row0);
+            for (int r = 0; r < C::kR; ++r) {
+              tma_load_2d(dst + r * C::kHalf, &tmK, &full_bar[st], r * 64, row0);
+              tma_load_2d(dst + (C::kR + r) * C::kHalf, &tmV, &full_bar[st], r * 64, row0);
+            }
           }
+          __syncwarp();
         }
       }
     }
