@@ -284,6 +284,15 @@ int choreo_events_create(void** events, int n);
 int choreo_events_elapsed(void* const* events, int n_pairs, float* ms_out);
 int choreo_events_destroy(void* const* events, int n);
 
+/* K6b nucleus selection (temperature + top-p) on the device, the reference's f64 algorithm
+ * step for step (engine.py:374-392): one row per logits row; params = (temperature, top_p)
+ * per row (f64); keys = (engine_seed, sampling_seed, msg_id, sel_index) per row (u64), the
+ * Philox4x64-10 stream NumPy's Generator(Philox(counter=[sel, msg_id, 0, 0],
+ * key=[engine_seed, sampling_seed])).random() draws from.  vocab >= 258. */
+int choreo_select_nucleus(const float* logits, int n_rows, int ld, int vocab,
+                          const double* params, const uint64_t* keys, int32_t* out_tok,
+                          void* stream);
+
 /* Diagnostics: one-CTA tcgen05 GEMM over the UMMA primitives K4 uses.
  * a: bf16 [128][64], b1: bf16 [64][64] (N x K), b2: bf16 [64][128] (K x N);
  * c1 = a * b1^T (f32 [128][64]), c2 = a * b2 (f32 [128][128]) with both operands in shared

@@ -28,7 +28,7 @@ import numpy as np
 import torch
 
 from . import _native as nat
-from .cache import DeviceKvCache, RotationTableDevice
+from .cache import DeviceKvCache, RotationTableDevice, h2d
 from .config import EOS_MSG, ModelConfig
 from .errors import (CapacityError, EmptyHeaderError, InvalidCallError, OffsetConflictError,
                      UnknownMessageError, WindowOverflowError)
@@ -190,6 +190,8 @@ class Engine:
         self._runner = Runner(self.weights, self.cache, self.rotation, split_activations, tp,
                               tp_group)
         self._generatable = generatable_mask(self.config.vocab_size)
+        # temperature sampling on the device (K6b); False: the host NumPy sampler
+        self.device_sampling = self.config.vocab_size >= 258
         self._next_id = 0
         self.stats: list[CallStats] = []
         self.d2h_bytes = 0
@@ -233,6 +235,7 @@ class Engine:
         other._runner = Runner(self.weights, other.cache, self.rotation, self._runner.split,
                                self.tp, self.tp_group)
         other._generatable = self._generatable
+        other.device_sampling = self.device_sampling
         other._next_id = self._next_id
         other.stats = []
         other.d2h_bytes = 0
@@ -393,23 +396,39 @@ class Engine:
                     s.done = True
             if not owners:
                 continue
-            greedy_tok = None
+            greedy_tok = nucleus_tok = None
             n_own = len(owners)
-            if any(s.forced is None and s.call.sampling.mode == "greedy" for s in owners):
-                out = torch.empty(n_own, dtype=torch.int32, device=self.device)
-                nat.select_greedy(logits.data_ptr(), n_own, logits.shape[1], logits.shape[1],
-                                  0, out.data_ptr(),
-                                  torch.cuda.current_stream(self.device).cuda_stream)
-                self._runner.launches += 1
-                greedy_tok = out.cpu().numpy()
+            stream = torch.cuda.current_stream(self.device).cuda_stream
+            free = [s for s in owners if s.forced is None]
+            want_g = any(s.call.sampling.mode == "greedy" for s in free)
+            want_n = any(s.call.sampling.mode != "greedy" for s in free) and self.device_sampling
+            if want_g or want_n:
+                out = torch.empty(2, n_own, dtype=torch.int32, device=self.device)
+                if want_g:  # K6 greedy over every owner row (non-greedy rows ignored)
+                    nat.select_greedy(logits.data_ptr(), n_own, logits.shape[1], logits.shape[1],
+                                      0, out[0].data_ptr(), stream)
+                    self._runner.launches += 1
+                if want_n:  # K6b nucleus: the reference's f64 algorithm + Philox stream
+                    params = np.array([[s.call.sampling.temperature, s.call.sampling.top_p]
+                                       for s in owners], np.float64)
+                    m64 = 0xFFFFFFFFFFFFFFFF
+                    keys = np.array([[self.seed & m64, s.call.sampling.seed & m64, s.mid, s.sel]
+                                     for s in owners], np.uint64).view(np.int64)
+                    pd, kd = h2d(params, self.device), h2d(keys, self.device)
+                    nat.select_nucleus(logits.data_ptr(), n_own, logits.shape[1],
+                                       logits.shape[1], pd.data_ptr(), kd.data_ptr(),
+                                       out[1].data_ptr(), stream)
+                    self._runner.launches += 1
+                toks = out.cpu().numpy()
                 self.d2h_bytes += out.nbytes
+                greedy_tok, nucleus_tok = toks[0], (toks[1] if want_n else None)
             host_logits = None
-            if self.record_logits or any(s.forced is None and s.call.sampling.mode != "greedy"
-                                         for s in owners):
+            if self.record_logits or (not self.device_sampling and any(
+                    s.forced is None and s.call.sampling.mode != "greedy" for s in owners)):
                 hl = logits.double().cpu().numpy()
                 self.d2h_bytes += logits.nbytes
                 host_logits = hl
-            elif greedy_tok is None and any(s.sel == 0 for s in owners):
+            elif not (want_g or want_n) and any(s.sel == 0 for s in owners):
                 # all forced: the host already knows the tokens; synchronise only at a
                 # message's first selection so its TTFT is the time its logits exist
                 torch.cuda.current_stream(self.device).synchronize()
@@ -424,6 +443,8 @@ class Engine:
                     tok = s.forced[k] if k < len(s.forced) else None
                 elif s.call.sampling.mode == "greedy":
                     tok = int(greedy_tok[i])
+                elif nucleus_tok is not None:
+                    tok = int(nucleus_tok[i])
                 else:
                     tok = _sample_nucleus(host_logits[i], self._generatable, s.call.sampling,
                                           self.seed, s.mid, k)

@@ -365,3 +365,22 @@ def test_llama8b_width_two_layers_matches_oracle():
     assert worst <= 2e-2, worst
     n = eng.cache.token_count
     assert eng.cache.positions[:n].tolist() == ref.store.pos[:n].tolist()
+
+
+@pytest.mark.parametrize("mode", ["f32", "bf16"])
+def test_device_nucleus_sampling_matches_host_sampler(mode):
+    """Temperature / top-p decoding with the device sampler (K6b) generates exactly the
+    tokens of the host NumPy sampler (the reference's algorithm and Philox stream)."""
+    runs = []
+    for device_sampling in (True, False):
+        eng = _engine(mode)
+        eng.device_sampling = device_sampling
+        a = eng.prefill(P.PrefillCall("System: answer the question using the notes."))
+        b = eng.prefill(P.PrefillCall("Question: which river is long?"))
+        sp = [P.SamplingParams(mode="temperature", temperature=t, top_p=q, seed=s, max_tokens=24)
+              for t, q, s in ((0.7, 0.95, 1), (1.3, 0.5, 2), (0.9, 1.0, 3))]
+        ms = eng.decode_parallel([P.DecodeCall(f"A{i}:", parents=[b, a], offsets=[0, 40],
+                                               sampling=sp[i]) for i in range(3)])
+        runs.append([eng.generated_token_ids(m) for m in ms])
+    assert runs[0] == runs[1]
+    assert any(len(t) > 0 for t in runs[0])
