@@ -196,13 +196,16 @@ int choreo_select_greedy(const float* logits, int n_rows, int ld, int vocab, int
  * 5-slot shared-memory ring and 8 mma.sync consumer warps (4 key slices x 2 m16 tiles);
  * plain bf16 Q and P, f32 accumulation.  Writes one normalised partial + LSE per
  * (block row, head) like choreo_attn_split; merge with choreo_attn_combine.
- * n_layers sizes the pool's TMA view.  Replaces model.py:177-184 for decode steps. */
+ * n_layers sizes the pool's TMA view.  fat_items (optional, the `fat` output of
+ * choreo_assemble; used when 32 / G <= 16) lets the loader read a unit's rows in the same
+ * round trip as its item.  Replaces model.py:177-184 for decode steps. */
 int choreo_decode_attn_v2(const float* q, const void* k_pool, const void* v_pool, int n_layers,
                           int layer, int n_kv, int n_pages, int page_size, int n_heads,
                           int head_dim, const int32_t* row_t, const int32_t* vis_page,
                           const int32_t* vis_len, const int32_t* vis_own, const int32_t* blk_rows,
                           const int32_t* items, const int32_t* counts, int max_items,
-                          float* part_o, float* part_lse, int grid_ctas, void* stream);
+                          float* part_o, float* part_lse, const int32_t* fat_items,
+                          int grid_ctas, void* stream);
 
 /* K7 decode-sized linear layer (weight streaming, tcgen05 + TMA, stream-K):
  *   y[r][n] = sum_k x[r][k] * w[n][k]      x: bf16 [x_rows][k], w: bf16 [n][k] (out, in),

@@ -44,7 +44,7 @@ SIGNATURES: dict[str, list] = {
     "choreo_decode_layers": [_P, _P],
     "choreo_select_nucleus": [_P, _I, _I, _I, _P, _P, _P, _P],
     "choreo_decode_attn_v2": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P,
-                              _I, _P, _P, _I, _P],
+                              _I, _P, _P, _P, _I, _P],
     "choreo_events_create": [_P, _I],
     "choreo_events_elapsed": [_P, _I, _P],
     "choreo_events_destroy": [_P, _I],

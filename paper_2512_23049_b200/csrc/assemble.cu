@@ -54,7 +54,7 @@ struct K3Params {
 
 // Self-contained item record for the latency-bound decode kernel: one 256-byte load gives
 // a CTA everything it needs (no dependent lookups of rows, row_t or page descriptors).
-//   [0] n_rows  [1] n_pages  [2] partial base  [3] unused
+//   [0] n_rows  [1] n_pages  [2] partial base  [3] first vis index
 //   [4..19] row ids   [20..35] row_t   [36..43] page  [44..51] page_len  [52..59] own_base
 // Requires n_rows <= kFatRows and n_pages <= kFatPages (the host sizes items that way).
 constexpr int kFatInts = 64, kFatRows = 16, kFatPages = 8;
@@ -67,7 +67,7 @@ __device__ void write_fat(const K3Params& p, int n_items) {
     f[0] = nr;
     f[1] = nv;
     f[2] = it[4];
-    f[3] = 0;
+    f[3] = it[2];  // first vis index (K5 v2's loader reads the page lengths from there)
     for (int r = 0; r < kFatRows; ++r) {
       const int rid = r < nr ? p.blk_rows[it[0] + r] : 0;
       f[4 + r] = rid;

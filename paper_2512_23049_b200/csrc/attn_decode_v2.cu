@@ -33,6 +33,7 @@ constexpr int kDvProducer = 8;     // warp 8: TMA
 constexpr int kDvLoader = 9;       // warp 9: unit metadata + Q staging
 constexpr int kDvMerge = 10;       // warps 10, 11: merge the key-slice states of m-tile 0 / 1
 constexpr int kDvThreads = 32 * 12;
+constexpr int kDvUnits = 3;        // unit records the loader may run ahead by
 constexpr int kDvMaxPages = 32;    // pages per unit staged in the unit record (host: ppi <= 32)
 
 struct DvParams {
@@ -48,6 +49,7 @@ struct DvParams {
   float* part_o;
   float* part_lse;
   float scale_log2;
+  const int32_t* fat;  // optional K3 item records (rows <= 16): faster unit staging
 };
 
 template <int HD>
@@ -63,7 +65,7 @@ struct DvCfg {
   // [40..72) page len, [72..104) own base; then Q bf16 [32][kQLd], pre-scaled
   static constexpr int kUnitInts = 128;
   static constexpr int kUnit = kUnitInts * 4 + 32 * kQLd * 2;
-  static constexpr int kTotal = kDvSlots * kSlot + kMerge + 2 * kUnit + 1024;
+  static constexpr int kTotal = kDvSlots * kSlot + kMerge + kDvUnits * kUnit + 1024;
 };
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
@@ -115,9 +117,9 @@ __global__ void __launch_bounds__(kDvThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* merge = reinterpret_cast<float*>(base + kDvSlots * C::kSlot);
-  uint8_t* units = base + kDvSlots * C::kSlot + C::kMerge;  // [2][kUnit]
+  uint8_t* units = base + kDvSlots * C::kSlot + C::kMerge;  // [kDvUnits][kUnit]
   __shared__ uint64_t full_bar[kDvSlots], empty_bar[kDvSlots];
-  __shared__ uint64_t unit_full[2], unit_empty[2], merge_full, merge_empty;
+  __shared__ uint64_t unit_full[kDvUnits], unit_empty[kDvUnits], merge_full, merge_empty;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int G = p.n_heads / p.n_kv;
@@ -127,7 +129,7 @@ __global__ void __launch_bounds__(kDvThreads, 1)
       mbar_init(&full_bar[i], 1);
       mbar_init(&empty_bar[i], kDvConsumers);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kDvUnits; ++i) {
       mbar_init(&unit_full[i], 32);
       mbar_init(&unit_empty[i], kDvConsumers);
     }
@@ -146,17 +148,33 @@ __global__ void __launch_bounds__(kDvThreads, 1)
     // one unit ahead of the consumers, so a unit boundary costs no dependent global loads
     int u = 0;
     for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++u) {
-      const int sl = u & 1;
-      mbar_wait(&unit_empty[sl], ((u >> 1) & 1) ^ 1);
+      const int sl = u % kDvUnits;
+      mbar_wait(&unit_empty[sl], ((u / kDvUnits) & 1) ^ 1);
       int* ui = reinterpret_cast<int*>(units + sl * C::kUnit);
       __nv_bfloat16* qs = reinterpret_cast<__nv_bfloat16*>(units + sl * C::kUnit + C::kUnitInts * 4);
+      const int kvh = w % p.n_kv;
       const int32_t* it = p.items + 6 * (w / p.n_kv);
       const int iv = lane < 5 ? it[lane] : 0;
+      int rid, rt;
+      if (p.fat) {
+        // K3's self-contained item record supplies the rows and their row_t in the same
+        // round trip as the item ([4..20) rid, [20..36) row_t)
+        const int32_t* fr = p.fat + (int64_t)(w / p.n_kv) * 64;
+        const int f0 = fr[lane], f1 = fr[32 + lane];
+        const int rr = min(lane / G, 15);
+        rid = __shfl_sync(0xffffffffu, f0, 4 + rr);
+        const int t0 = __shfl_sync(0xffffffffu, f0, min(20 + rr, 31));
+        const int t1 = __shfl_sync(0xffffffffu, f1, max(rr - 12, 0));
+        rt = rr < 12 ? t0 : t1;
+      }
       const int rb = __shfl_sync(0xffffffffu, iv, 0), nr = __shfl_sync(0xffffffffu, iv, 1);
       const int vb = __shfl_sync(0xffffffffu, iv, 2), nv = __shfl_sync(0xffffffffu, iv, 3);
-      const int kvh = w % p.n_kv, M = nr * G;
-      const int rid = lane < M ? p.blk_rows[rb + lane / G] : 0;
       const int pbase = __shfl_sync(0xffffffffu, iv, 4);
+      if (!p.fat) {
+        rid = lane < nr * G ? p.blk_rows[rb + lane / G] : 0;
+        rt = lane < nr * G ? p.row_t[rid] : -1;
+      }
+      const int M = nr * G;
       if (lane == 0) {
         ui[0] = M;
         ui[1] = vb;
@@ -164,7 +182,7 @@ __global__ void __launch_bounds__(kDvThreads, 1)
         ui[3] = pbase;
         ui[4] = kvh;
       }
-      ui[8 + lane] = lane < M ? p.row_t[rid] : -1;
+      ui[8 + lane] = lane < M ? rt : -1;
       ui[40 + lane] = lane < nv ? p.vis_len[vb + lane] : 0;
       ui[72 + lane] = lane < nv ? p.vis_own[vb + lane] : -1;
       // Q: lane = 4 dims of every vector; all loads in flight at once (one round trip),
@@ -242,8 +260,8 @@ __global__ void __launch_bounds__(kDvThreads, 1)
   uint32_t gp = 0;
   int u = 0;
   for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++u) {
-    const int sl = u & 1;
-    mbar_wait(&unit_full[sl], (u >> 1) & 1);
+    const int sl = u % kDvUnits;
+    mbar_wait(&unit_full[sl], (u / kDvUnits) & 1);
     const int* ui = reinterpret_cast<const int*>(units + sl * C::kUnit);
     const __nv_bfloat16* qs = reinterpret_cast<const __nv_bfloat16*>(units + sl * C::kUnit + C::kUnitInts * 4);
     const int M = ui[0], nv = ui[2], pbase = ui[3], kvh = ui[4];
@@ -494,7 +512,8 @@ extern "C" int choreo_decode_attn_v2(const float* q, const void* k_pool, const v
                                      const int32_t* vis_page, const int32_t* vis_len,
                                      const int32_t* vis_own, const int32_t* blk_rows,
                                      const int32_t* items, const int32_t* counts, int max_items,
-                                     float* part_o, float* part_lse, int grid_ctas, void* stream) {
+                                     float* part_o, float* part_lse, const int32_t* fat_items,
+                                     int grid_ctas, void* stream) {
   if (!q || !k_pool || !v_pool || !row_t || !vis_page || !vis_len || !vis_own || !blk_rows ||
       !items || !counts || !part_o || !part_lse || n_kv <= 0 || n_heads % n_kv)
     return CHOREO_EINVAL;
@@ -503,8 +522,10 @@ extern "C" int choreo_decode_attn_v2(const float* q, const void* k_pool, const v
   if (max_items <= 0) return CHOREO_OK;
   const uint64_t rows = (uint64_t)n_layers * n_kv * n_pages * page_size;
   if (rows > 0x7fffffffull) return CHOREO_EUNSUPPORTED;
+  const int G = n_heads / n_kv;
   DvParams p{q, layer, n_kv, n_pages, n_heads, row_t, vis_page, vis_len, vis_own, blk_rows, items,
-             counts, part_o, part_lse, 1.4426950408889634f / sqrtf((float)head_dim)};
+             counts, part_o, part_lse, 1.4426950408889634f / sqrtf((float)head_dim),
+             32 / G <= 16 ? fat_items : nullptr};
   int grid = grid_ctas > 0 ? grid_ctas : max_items * n_kv;
   if (grid > 148) grid = 148;
   auto s = as_stream(stream);

@@ -53,7 +53,7 @@ extern "C" int choreo_decode_layers(const ChoreoDecodeStep* s, void* stream) {
       CHK(choreo_decode_attn_v2(s->q, s->k_pool, s->v_pool, s->n_layers, l, Hk, s->n_pages,
                                 s->page_size, H, hd, s->row_t, s->vis_page, s->vis_len, s->vis_own,
                                 s->blk_rows, s->items, s->counts, s->n_items, s->part_o,
-                                s->part_lse, 0, stream));
+                                s->part_lse, s->fat, 0, stream));
     else
       CHK(choreo_decode_attn(s->q, s->k_pool, s->v_pool, l, Hk, s->n_pages, s->page_size, H, hd,
                              s->fat, s->counts, s->n_items, s->row_part_off, s->row_part,

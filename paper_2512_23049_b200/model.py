@@ -396,7 +396,8 @@ class Runner:
         row_part_off = torch.empty(R + 1, dtype=torch.int32, device=self.dev)
         row_part = torch.empty(max(n_parts, 1), dtype=torch.int32, device=self.dev)
         counts = torch.empty(4, dtype=torch.int32, device=self.dev)
-        fat = torch.empty(max(n_items, 1), 64, dtype=torch.int32, device=self.dev) if fused else None
+        fat = (torch.empty(max(n_items, 1), 64, dtype=torch.int32, device=self.dev)
+               if fused or (v2 and rpb <= 16) else None)
         if fused and (self._counters is None or self._counters.numel() < R * Hk):
             self._counters = torch.zeros(max(R * Hk, 1024), dtype=torch.int32, device=self.dev)
         nat.assemble(cache.msg_len.dev.data_ptr(), cache.msg_pt.dev.data_ptr(),
@@ -453,7 +454,7 @@ class Runner:
                                    rowt_d.data_ptr(), vis[0].data_ptr(), vis[1].data_ptr(),
                                    vis[2].data_ptr(), blk_rows.data_ptr(), items.data_ptr(),
                                    counts.data_ptr(), n_items, part_o.data_ptr(),
-                                   part_lse.data_ptr(), 0, stream)
+                                   part_lse.data_ptr(), nat.ptr(fat), 0, stream)
             elif fused:
                 nat.decode_attn(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(), layer,
                                 Hk, cache.n_pages, P, H, hd, fat.data_ptr(), counts.data_ptr(),

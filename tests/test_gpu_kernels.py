@@ -470,7 +470,7 @@ def test_decode_v2_matches_dense_reference(hd, H, Hk, ppi):
                            Hk, cache.n_pages, 64, H, hd, rt_d.data_ptr(), vis[0].data_ptr(),
                            vis[1].data_ptr(), vis[2].data_ptr(), blk.data_ptr(), items.data_ptr(),
                            counts.data_ptr(), pl_.n_items, part_o.data_ptr(), part_lse.data_ptr(),
-                           grid, _stream())
+                           None, grid, _stream())
         nat.attn_combine(part_o.data_ptr(), part_lse.data_ptr(), rpo.data_ptr(), rp.data_ptr(), R,
                          H, hd, o.data_ptr(), nat.F32, 0, _stream())
         torch.cuda.synchronize()

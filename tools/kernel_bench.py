@@ -244,7 +244,8 @@ def k5_decode(n_workflows: int = 1, agents: int = 8, tc: bool = False, fused: bo
                                cfg.n_layers, 0, Hk, cache.n_pages, 64, H, hd, b["rt"].data_ptr(),
                                v[0].data_ptr(), v[1].data_ptr(), v[2].data_ptr(),
                                b["blk"].data_ptr(), b["items"].data_ptr(), b["counts"].data_ptr(),
-                               plan.n_items, po.data_ptr(), pl.data_ptr(), 0, stream)
+                               plan.n_items, po.data_ptr(), pl.data_ptr(),
+                               b["fat"].data_ptr(), 0, stream)
             return
         if fused:
             nat.decode_attn(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(), 0, Hk,
