@@ -352,6 +352,10 @@ class Runner:
         if v2:  # persistent CTAs: about one (item, kv head) unit per SM; unit record <= 32 pages
             ppi = min(max(ppi, 4), 32)
         plan_ = plan_counts(plan.calls, msg_len, P, rpb, ppi, mode)
+        if v2:  # grow items until the units fit one wave of CTAs (else a few CTAs run two)
+            while plan_.n_items * Hk > 148 and ppi < 32:
+                ppi = min(32, ppi + max(1, ppi // 4))
+                plan_ = plan_counts(plan.calls, msg_len, P, rpb, ppi, mode)
         if fused:
             # one wave of resident CTAs (3 per SM): a second item on a few CTAs would
             # double the kernel's length

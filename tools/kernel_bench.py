@@ -221,6 +221,9 @@ def k5_decode(n_workflows: int = 1, agents: int = 8, tc: bool = False, fused: bo
     ppi = max(1, cdiv(work.item_pages * Hk, (1 if tc else 1 if v2 else 3) * 148))
     if v2:  # the runner's rule: about one (item, kv head) unit per SM, 4..32 pages
         ppi = min(max(ppi, 4), 32)
+        while plan_counts([CallRows(c[0], c[1], c[2], [0], None, None, 0) for c in calls],
+                          cache.msg_len.host, 64, rpb, ppi).n_items * Hk > 148 and ppi < 32:
+            ppi = min(32, ppi + max(1, ppi // 4))
     ppi = int(os.environ.get("K5_PPI", ppi))
     fused = fused and not tc and not v2
     if fused and "K5_PPI" not in os.environ:  # same one-wave fit as the runner
