@@ -185,15 +185,18 @@ __global__ void __launch_bounds__(kLnThreads, 1)
         float* w = p.ws + ((size_t)(c * 2 + slot) * NX) * kLnTile + nl;
 #pragma unroll
         for (int q = 0; q < NX; ++q) w[q * kLnTile] = acc[q];
-        __threadfence();
+        // the group's barrier orders the 128 threads' partial stores before thread 0's
+        // GPU-scope release (one fence per piece instead of one per thread); the last piece
+        // acquires the others the same way before reading them
         asm volatile("bar.sync 1, 128;\n" ::: "memory");
         if (et == 0) {
+          asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
           const int old = atomicAdd(&p.counters[t], 1);
           s_last = old == c_hi - c_lo;
+          if (s_last) asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
         }
         asm volatile("bar.sync 1, 128;\n" ::: "memory");
         if (!s_last) continue;
-        __threadfence();
 #pragma unroll
         for (int q = 0; q < NX; ++q) acc[q] = 0.f;
         for (int cc = c_lo; cc <= c_hi; ++cc) {
