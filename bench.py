@@ -178,6 +178,16 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+def ncu_traffic() -> dict:
+    """Per-launch DRAM traffic of K7 / K5 v2 from the committed ncu capture of the same
+    decode step (profiles/r1_traffic.json, dram__bytes_read.sum + dram__bytes_write.sum)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as fh:
+            return json.load(fh)
+    except OSError:
+        return {}
+
+
 def measured_peaks() -> dict:
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -512,7 +522,8 @@ def main() -> None:
         attn_roofline = {"kernel": "choreo_decode_attn_v2 (K5: page-centric split-KV decode attention, TMA page ring)",
                     "bound": "hbm",
                     "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                    "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": None,
+                    "frac": round(achieved / peaks["hbm_gbs"], 4),
+                    "traffic": ncu_traffic().get("k5v2_dram_bytes_per_launch"),
                     "peak_source": peaks["source"],
                     "avg_launch_us": round(1e3 * sum(a_ms) / len(a_ms), 2),
                     "algorithmic_bytes_per_launch": int(sum(a_bytes) / len(a_bytes)),
@@ -527,7 +538,9 @@ def main() -> None:
         roofline = {"kernel": "choreo_linear_skinny (K7: tcgen05 stream-K weight-streaming "
                               "linear, qkv / o_proj / gate|up / down of every decode layer)",
                     "bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"],
-                    "unit": "GB/s", "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": None,
+                    "unit": "GB/s", "frac": round(ach / peaks["hbm_gbs"], 4),
+                    "traffic": ncu_traffic().get("k7_layer_gemm_dram_bytes_per_launch"),
+                    "traffic_source": ncu_traffic().get("source"),
                     "peak_source": peaks["source"], "avg_launch_us": round(1e3 * l_ms, 2),
                     "algorithmic_bytes_per_launch": int(l_b), "launches_timed": len(lin),
                     "note": "CUDA events on the launching stream around each launch of one extra "
