@@ -220,6 +220,15 @@ int choreo_linear_skinny(const void* x, int x_rows, int split, const void* w, in
                          float* y, float* workspace, int* tile_counters, int grid_ctas,
                          void* stream);
 
+/* K7 for the gate|up projection with the SwiGLU product fused into its epilogue:
+ * act[r][i] = silu(g) * u, g = x[r] . w_gu[i], u = x[r] . w_gu[f + i] (w_gu = [gate; up],
+ * (2f, d)), written as bf16 act [out_rows][f] (+ the lo halves at rows out_rows + r when
+ * split) — choreo_linear_skinny followed by choreo_silu_mul in one launch (each tile pairs
+ * 64 gate rows with the matching 64 up rows).  f % 64 == 0.  Replaces model.py:186-187. */
+int choreo_linear_gate_up_silu(const void* x, int x_rows, int split, const void* w_gu, int f,
+                               int d, void* act, float* workspace, int* tile_counters,
+                               void* stream);
+
 /* Native decode-step executor: every layer of a decode-sized bf16 step (split hi/lo
  * activations or plain bf16; page_size 64; fused K5 items from choreo_assemble with a
  * fat buffer) issued in one call — per layer: residual_rmsnorm, K7 qkv, K1 rope_append,

@@ -42,6 +42,7 @@ SIGNATURES: dict[str, list] = {
     "choreo_selftest_umma": [_P, _P, _P, _P, _P, _P, _P],
     "choreo_linear_skinny": [_P, _I, _I, _P, _I, _I, _P, _P, _P, _I, _P],
     "choreo_decode_layers": [_P, _P],
+    "choreo_linear_gate_up_silu": [_P, _I, _I, _P, _I, _I, _P, _P, _P, _P],
     "choreo_select_nucleus": [_P, _I, _I, _I, _P, _P, _P, _P],
     "choreo_decode_attn_v2": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P,
                               _I, _P, _P, _P, _I, _P],
@@ -103,6 +104,7 @@ select_greedy = _Caller("choreo_select_greedy")
 selftest_umma = _Caller("choreo_selftest_umma")
 linear_skinny = _Caller("choreo_linear_skinny")
 decode_layers = _Caller("choreo_decode_layers")
+linear_gate_up_silu = _Caller("choreo_linear_gate_up_silu")
 select_nucleus = _Caller("choreo_select_nucleus")
 decode_attn_v2 = _Caller("choreo_decode_attn_v2")
 events_create = _Caller("choreo_events_create")

@@ -9,7 +9,7 @@
 //   K5 decode attention over the K3 fat items (+ LSE combine)
 //   K7 ao = attn @ Wo^T
 //   residual_rmsnorm (x += ao; h = norm(x))
-//   K7 gu = h @ Wgu^T ; silu_mul ; K7 delta = act @ Wdown^T
+//   K7 act = silu(h @ Wg^T) * (h @ Wu^T) (SwiGLU in the epilogue) ; K7 delta = act @ Wdown^T
 // The final residual add, norm and head stay with the caller (they depend on which rows
 // need logits).  Every kernel is one of the library's C-ABI entry points, so results are
 // bit-identical to the Python-driven sequence.
@@ -69,10 +69,15 @@ extern "C" int choreo_decode_layers(const ChoreoDecodeStep* s, void* stream) {
     CHK(choreo_residual_rmsnorm(s->x, s->ao, CHOREO_F32, 0, s->ffn_norm[l], CHOREO_BF16, R, d,
                                 s->eps, s->h, CHOREO_BF16, sp, nullptr, 0, stream));
     LIN_EV(4);
-    CHK(choreo_linear_skinny(s->h, x_rows, sp, s->w_gu[l], 2 * F, d, s->gu, s->k7_ws, s->k7_cnt, 0,
-                             stream));
+    if (F % 64 == 0) {
+      CHK(choreo_linear_gate_up_silu(s->h, x_rows, sp, s->w_gu[l], F, d, s->act, s->k7_ws,
+                                     s->k7_cnt, stream));
+    } else {
+      CHK(choreo_linear_skinny(s->h, x_rows, sp, s->w_gu[l], 2 * F, d, s->gu, s->k7_ws,
+                               s->k7_cnt, 0, stream));
+      CHK(choreo_silu_mul(s->gu, CHOREO_F32, 0, R, F, s->act, CHOREO_BF16, sp, stream));
+    }
     LIN_EV(5);
-    CHK(choreo_silu_mul(s->gu, CHOREO_F32, 0, R, F, s->act, CHOREO_BF16, sp, stream));
     LIN_EV(6);
     CHK(choreo_linear_skinny(s->act, x_rows, sp, s->w_down[l], d, F, s->delta, s->k7_ws, s->k7_cnt,
                              0, stream));

@@ -30,10 +30,12 @@ constexpr int kLnTile = 128;     // weight rows per tile (UMMA M)
 constexpr int kLnKB = 64;        // k elements per block (one 128-byte SW128 row)
 
 struct LinearParams {
-  float* y;       // [out_rows][N]
+  float* y;       // [out_rows][N] (or, with silu_f > 0, act: bf16 [out_rows (x2 split)][silu_f])
   float* ws;      // [grid][2][NX][128] partial tiles (NX <= 128)
   int* counters;  // [n_tiles], zero between launches (reducers reset them)
   int N, KB, iters, grid, out_rows, split;
+  int silu_f;  // > 0: gate|up projection with SiLU(gate)*up fused (tile t = gate rows
+               // [64t, 64t+64) over up rows [F + 64t, ...)); N counts act columns (= F)
 };
 
 template <int NX, int KSUB>
@@ -45,6 +47,9 @@ struct LnCfg {
   static constexpr int kSmem = kStages * kStageBytes + 1024;
   static constexpr int kTmemCols = 2 * NX < 32 ? 32 : 2 * NX;
 };
+
+template <int NX>
+__host__ __device__ constexpr int p_split_rows() { return NX; }
 
 __device__ __forceinline__ int ln_begin(int c, int iters, int grid) {
   return (int)(((long long)c * iters) / grid);
@@ -65,6 +70,7 @@ __global__ void __launch_bounds__(kLnThreads, 1)
   __shared__ uint64_t full_bar[C::kStages], empty_bar[C::kStages], acc_full[2], acc_empty[2];
   __shared__ uint32_t tmem_base;
   __shared__ int s_last;
+  __shared__ float s_xch[16 * 64];  // SiLU epilogue: up values of 16 rows x 64 columns
 
   pdl_trigger();  // the successor may launch now; it waits for this grid to complete
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -96,7 +102,13 @@ __global__ void __launch_bounds__(kLnThreads, 1)
         // the KSUB weight boxes go out back to back: 128 rows x KSUB*128 contiguous bytes
 #pragma unroll
         for (int u = 0; u < KSUB; ++u)
-          tma_load_2d(dst + u * C::kWBytes, &tmW, &full_bar[st], (kb + u) * kLnKB, t * kLnTile);
+          if (p.silu_f) {  // 64 gate rows over the matching 64 up rows
+            tma_load_2d(dst + u * C::kWBytes, &tmW, &full_bar[st], (kb + u) * kLnKB, t * 64);
+            tma_load_2d(dst + u * C::kWBytes + 64 * 128, &tmW, &full_bar[st], (kb + u) * kLnKB,
+                        p.silu_f + t * 64);
+          } else {
+            tma_load_2d(dst + u * C::kWBytes, &tmW, &full_bar[st], (kb + u) * kLnKB, t * kLnTile);
+          }
       };
       auto load_x = [&](int i, int st) {
         uint8_t* xd = base + st * C::kStageBytes + KSUB * C::kWBytes;
@@ -207,7 +219,39 @@ __global__ void __launch_bounds__(kLnThreads, 1)
         }
         if (et == 0) p.counters[t] = 0;
       }
-      if (n < p.N) {
+      if (p.silu_f) {
+        // lanes 0-63 hold gate, 64-127 up of the same 64 ffn columns: exchange through smem
+        // in 16-row chunks, then act = silu(g) * u (the formula of choreo_silu_mul) as bf16
+        // (hi/lo rows r and out_rows + r when split)
+        const int j = t * 64 + (nl & 63);
+        __nv_bfloat16* act = reinterpret_cast<__nv_bfloat16*>(p.y);
+        const int64_t lo_off = (int64_t)p.out_rows * p.silu_f;
+#pragma unroll
+        for (int r0 = 0; r0 < (p_split_rows<NX>()); r0 += 16) {
+          asm volatile("bar.sync 1, 128;\n" ::: "memory");  // s_xch free
+          if (nl >= 64) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int r = r0 + i;
+              if (r < NX) s_xch[i * 64 + (nl - 64)] = p.split ? (r < NX / 2 ? acc[r] + acc[NX / 2 + r] : 0.f) : acc[r];
+            }
+          }
+          asm volatile("bar.sync 1, 128;\n" ::: "memory");
+          if (nl < 64) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int r = r0 + i;
+              if (r < p.out_rows && r < NX) {
+                const float g = p.split ? (r < NX / 2 ? acc[r] + acc[NX / 2 + r] : 0.f) : acc[r];
+                const float v = g / (1.0f + expf(-g)) * s_xch[i * 64 + nl];
+                const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+                act[(int64_t)r * p.silu_f + j] = hi;
+                if (p.split) act[lo_off + (int64_t)r * p.silu_f + j] = __float2bfloat16_rn(v - __bfloat162float(hi));
+              }
+            }
+          }
+        }
+      } else if (n < p.N) {
         if (p.split) {
 #pragma unroll
           for (int r = 0; r < NX / 2; ++r)
@@ -257,7 +301,8 @@ template <int NX, int KSUB>
 static int launch_linear(const LinearParams& p, const void* x, int x_rows, const void* w, int N,
                          int K, cudaStream_t s) {
   CUtensorMap mw, mx;
-  if (!ln_map(&mw, w, (uint64_t)N, (uint64_t)K, kLnTile, CU_TENSOR_MAP_L2_PROMOTION_L2_256B) ||
+  if (!ln_map(&mw, w, (uint64_t)(p.silu_f ? 2 * p.silu_f : N), (uint64_t)K,
+              p.silu_f ? 64 : kLnTile, CU_TENSOR_MAP_L2_PROMOTION_L2_256B) ||
       !ln_map(&mx, x, (uint64_t)x_rows, (uint64_t)K, p.split ? NX / 2 : NX,
               CU_TENSOR_MAP_L2_PROMOTION_L2_128B))
     return CHOREO_ELAUNCH;
@@ -286,13 +331,14 @@ static int launch_linear(const LinearParams& p, const void* x, int x_rows, const
 
 using namespace choreo;
 
-extern "C" int choreo_linear_skinny(const void* x, int x_rows, int split, const void* w, int n,
-                                    int k, float* y, float* workspace, int* tile_counters,
-                                    int grid_ctas, void* stream) {
+static int linear_impl(const void* x, int x_rows, int split, const void* w, int n, int k, void* y,
+                       float* workspace, int* tile_counters, int grid_ctas, int silu_f,
+                       void* stream) {
   if (!x || !w || !y || !workspace || !tile_counters || x_rows <= 0 || n <= 0 || k <= 0 ||
       (split && (x_rows & 1)))
     return CHOREO_EINVAL;
   if (x_rows > 128 || k % 8) return CHOREO_EUNSUPPORTED;  // TMA: 16-byte row pitch
+  if (silu_f && silu_f % 64) return CHOREO_EUNSUPPORTED;
   const int R = split ? x_rows / 2 : x_rows;  // output rows
   const int xr = split ? 2 * R : R;
   const int NX = xr <= 16 ? 16 : xr <= 32 ? 32 : xr <= 64 ? 64 : 128;
@@ -302,13 +348,13 @@ extern "C" int choreo_linear_skinny(const void* x, int x_rows, int split, const 
     ksub = e ? atoi(e) : 2;
     if (ksub != 1 && ksub != 2 && ksub != 4) ksub = 2;
   }
-  const int n_tiles = (n + kLnTile - 1) / kLnTile;
+  const int n_tiles = silu_f ? silu_f / 64 : (n + kLnTile - 1) / kLnTile;
   const int KB = (k + kLnKB * ksub - 1) / (kLnKB * ksub);  // iteration = ksub k-blocks
   const int iters = n_tiles * KB;
   int grid = grid_ctas > 0 ? grid_ctas : 148;
   if (grid > iters) grid = iters;
-  LinearParams p{y, workspace, tile_counters, n, KB, iters, grid, split ? x_rows / 2 : x_rows,
-                 split};
+  LinearParams p{reinterpret_cast<float*>(y), workspace, tile_counters, n, KB, iters, grid,
+                 split ? x_rows / 2 : x_rows, split, silu_f};
   auto s = as_stream(stream);
 #define LN_CASE(nx)                                                                       \
   return ksub == 1   ? launch_linear<nx, 1>(p, x, x_rows, w, n, k, s)                     \
@@ -321,4 +367,17 @@ extern "C" int choreo_linear_skinny(const void* x, int x_rows, int split, const 
     default: LN_CASE(128)
   }
 #undef LN_CASE
+}
+
+extern "C" int choreo_linear_skinny(const void* x, int x_rows, int split, const void* w, int n,
+                                    int k, float* y, float* workspace, int* tile_counters,
+                                    int grid_ctas, void* stream) {
+  return linear_impl(x, x_rows, split, w, n, k, y, workspace, tile_counters, grid_ctas, 0, stream);
+}
+
+extern "C" int choreo_linear_gate_up_silu(const void* x, int x_rows, int split, const void* w_gu,
+                                          int f, int d, void* act, float* workspace,
+                                          int* tile_counters, void* stream) {
+  if (f <= 0) return CHOREO_EINVAL;
+  return linear_impl(x, x_rows, split, w_gu, f, d, act, workspace, tile_counters, 0, f, stream);
 }

@@ -494,9 +494,15 @@ class Runner:
             nat.residual_rmsnorm(x.data_ptr(), ao.data_ptr(), nat.F32, isp,
                                  lw["ffn_norm"].data_ptr(), self.dtc, R, d, RMS_EPS, h.data_ptr(),
                                  self.dtc, sp, None, 0, stream)
-            gu = mm(h, lw["w_gu"])  # f32 pre-activations (parity)
-            nat.silu_mul(gu.data_ptr(), nat.F32, isp, R, cfg.ffn_dim, act.data_ptr(), self.dtc, sp,
-                         stream)
+            if k7 and cfg.ffn_dim % 64 == 0:  # K7 with SiLU(gate)*up in its epilogue
+                nat.linear_gate_up_silu(h.data_ptr(), h.shape[0], sp, lw["w_gu"].data_ptr(),
+                                        cfg.ffn_dim, d, act.data_ptr(), self._k7_ws.data_ptr(),
+                                        self._k7_cnt.data_ptr(), stream)
+                self.launches += 1
+            else:
+                gu = mm(h, lw["w_gu"])  # f32 pre-activations (parity)
+                nat.silu_mul(gu.data_ptr(), nat.F32, isp, R, cfg.ffn_dim, act.data_ptr(),
+                             self.dtc, sp, stream)
             delta = mm(act, lw["w_down"])
             if self.tp is not None and self.tp.size > 1:  # row-parallel down_proj
                 torch.distributed.all_reduce(delta, group=self.tp_group)

@@ -555,3 +555,35 @@ def test_select_nucleus_matches_host_sampler(vocab):
     nat.select_nucleus(lg.data_ptr(), n, vocab, vocab, params.data_ptr(), keys.data_ptr(),
                        out.data_ptr(), _stream())
     assert out.cpu().tolist() == want
+
+
+@pytest.mark.parametrize("rows,split", [(8, True), (3, True), (20, False), (64, True)])
+@pytest.mark.parametrize("f,d", [(14336, 4096), (256, 192)])
+def test_linear_gate_up_silu_matches_separate(rows, split, f, d):
+    """K7 with SwiGLU fused (tiles pair 64 gate rows with their 64 up rows) == K7 on
+    [gate; up] then choreo_silu_mul, up to f32 summation order (bf16 outputs within one
+    rounding); hi/lo halves when split."""
+    torch.manual_seed(rows + f)
+    xm = torch.randn(2 * rows if split else rows, d, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(2 * f, d, device="cuda") / d ** 0.5).to(torch.bfloat16)
+    S = 2 if split else 1
+    fused = torch.zeros(S * rows, f, dtype=torch.bfloat16, device="cuda")
+    sep = torch.zeros(S * rows, f, dtype=torch.bfloat16, device="cuda")
+    ws = torch.empty(148 * 2 * 128 * 128, device="cuda")
+    cnt = torch.zeros(2 * f // 128 + 2, dtype=torch.int32, device="cuda")
+    nat.linear_gate_up_silu(xm.data_ptr(), xm.shape[0], int(split), w.data_ptr(), f, d,
+                            fused.data_ptr(), ws.data_ptr(), cnt.data_ptr(), _stream())
+    gu = _linear(xm, split, w)
+    nat.silu_mul(gu.data_ptr(), nat.F32, 0, rows, f, sep.data_ptr(), nat.BF16, int(split),
+                 _stream())
+    torch.cuda.synchronize()
+    assert int(cnt.abs().sum()) == 0
+    a = fused[:rows].float() + (fused[rows:].float() if split else 0)
+    b = sep[:rows].float() + (sep[rows:].float() if split else 0)
+    tol = 2e-3 if split else 1e-2  # plain bf16 outputs: one bf16 ulp (<= 0.78 %) apart
+    torch.testing.assert_close(a, b, rtol=tol, atol=tol)
+    g = (xm.float() @ w[:f].float().t())
+    u = (xm.float() @ w[f:].float().t())
+    if split:
+        g, u = g[:rows] + g[rows:], u[:rows] + u[rows:]
+    torch.testing.assert_close(a, torch.nn.functional.silu(g) * u, rtol=1e-2, atol=1e-2)
