@@ -414,6 +414,58 @@ def c2_agents(P, rank: int) -> dict:
     return out
 
 
+def c5_tensor_parallel(P, rank: int, world: int) -> dict:
+    """Config C5 across the job's GPUs: Llama-3.1-70B shape, random-init bf16, KV heads (and
+    the MLP) sharded world-ways (parallel.TPLayout); every layer all-reduces the o_proj and
+    down_proj partial outputs over NCCL.  A 64 x 512-token global cache, then 8 agents
+    decoding 64 teacher-forced tokens over reordered 32-message subsets (~16K visible).
+    Decode time is CUDA events, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_23049_b200.parallel import TPLayout
+
+    cfg = P.PRESETS["llama-3.1-70b"]
+    lay = TPLayout(rank, world, cfg)
+    w = P.DeviceWeights.random(cfg, dtype=torch.bfloat16, tp=lay)
+    eng = P.Engine(w, capacity=36 * 1024, tp=lay, tp_group=dist.group.WORLD)
+    rng = np.random.default_rng(0)  # same layout on every rank
+    ids = []
+    for _ in range(8):
+        ids += eng.prefill_parallel([P.PrefillCall(random_text(rng, 512)) for _ in range(8)])
+    sel = [ids[i] for i in rng.permutation(64)[:32]]
+    offs, cursor, prev = {}, 0, None
+    for m in sel:
+        o = prev if prev is not None and rng.random() < 0.25 else cursor + int(rng.integers(0, 33))
+        offs[m] = o
+        prev, cursor = o, max(cursor, o + 512)
+    calls, forced = [], []
+    for a in range(8):
+        parents = [sel[j] for j in rng.permutation(32)]
+        calls.append(P.DecodeCall(f"Agent {a}:", parents=parents, offsets=[offs[m] for m in parents],
+                                  new_offset=cursor + 8, sampling=P.SamplingParams(max_tokens=512)))
+        forced.append(rng.integers(97, 123, size=64).tolist())
+    torch.cuda.synchronize()
+    dist.barrier()
+    a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a_.record()
+    ms = eng.decode_parallel(calls, force_tokens=forced)
+    b_.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([a_.elapsed_time(b_) / 1e3], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    gen = sum(len(eng.generated_token_ids(m)) for m in ms)
+    out = {"workload": f"C5: Llama-3.1-70B shape, KV heads sharded {world}-way (TP, NCCL "
+                       "all-reduce after o_proj and down_proj), 8 agents x 64 forced tokens over "
+                       "~16K visible tokens of a 32K global cache",
+           "tp": world, "decode_tokens_per_s": round(gen / float(t[0]), 1),
+           "ms_per_step": round(1e3 * float(t[0]) / 64, 2),
+           "ttft_p50_ms": round(1e3 * statistics.median(eng.last_stats.ttft.values()), 2)}
+    del eng, w
+    torch.cuda.empty_cache()
+    return out
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -431,6 +483,8 @@ def main() -> None:
     ap.add_argument("--model", default="llama-3.1-8b")
     ap.add_argument("--no-c2", action="store_true",
                     help="skip the config-C2 measurement (1B shape, 4 agents, 8K cache)")
+    ap.add_argument("--no-c5", action="store_true",
+                    help="skip the config-C5 tensor-parallel 70B measurement (N > 1 only)")
     ap.add_argument("--no-c4", action="store_true",
                     help="skip the config-C4 batched-workflows measurement (BatchScheduler)")
     args = ap.parse_args()
@@ -565,6 +619,15 @@ def main() -> None:
               "batched_8": c4, "single_workflow": c4_one,
               "batching_speedup": round(c4["decode_tokens_per_s"] / c4_one["decode_tokens_per_s"], 2)}
 
+    c5 = None
+    if world > 1 and 8 % world == 0 and not args.no_c5:
+        del eng, runner, weights  # the 70B shards need the room
+        torch.cuda.empty_cache()
+        try:
+            c5 = c5_tensor_parallel(P, rank, world)
+        except Exception as exc:  # report, never lose the main line
+            c5 = {"error": repr(exc)[:300]}
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -612,6 +675,7 @@ def main() -> None:
         "reencode_baseline": reencode,
         "c4_batched_workflows": c4,
         "c2_agents_1b": c2,
+        "c5_tensor_parallel_70b": c5,
         "cpu_baseline": cpu,
         "clocks": clocks.summary(),
     }

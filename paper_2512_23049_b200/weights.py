@@ -219,6 +219,16 @@ class DeviceWeights:
             return t.to(dtype)
 
         ones = torch.ones(d, device=device, dtype=dtype)
+        # replicated tensors (embedding, head) must be identical on every rank: own stream
+        rep = torch.Generator(device=device)
+        rep.manual_seed(config.seed)
+
+        def draw_rep(fan_in, fan_out, shape):
+            b = math.sqrt(6.0 / (fan_in + fan_out))
+            t = torch.empty(shape, device=device, dtype=torch.float32)
+            t.uniform_(-b, b, generator=rep)
+            return t.to(dtype)
+
         layers = []
         for _ in range(config.n_layers):
             w_qkv = torch.cat([draw(d, d, (hq, d)), draw(d, dkv, (hkv, d)), draw(d, dkv, (hkv, d))])
@@ -226,5 +236,6 @@ class DeviceWeights:
                            "ffn_norm": ones, "w_gu": torch.cat([draw(d, f, (fl, d)), draw(d, f, (fl, d))]),
                            "w_down": draw(f, d, (d, fl))})
         return cls(tp.local_config(), dtype, device,
-                   {"embed": draw(v, d, (v, d)), "out_norm": ones, "out_head": draw(d, v, (v, d)),
+                   {"embed": draw_rep(v, d, (v, d)), "out_norm": ones,
+                    "out_head": draw_rep(d, v, (v, d)),
                     "layers": layers})
