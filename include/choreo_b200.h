@@ -287,6 +287,11 @@ typedef struct {
   /* optional host array of 8 * n_layers cudaEvent_t recorded around the layer's four K7
    * launches (qkv, o_proj, gate|up, down); NULL: none */
   void** linear_events;
+  /* layers [layer_begin, layer_end) (layer_end 0: n_layers) and which part of each:
+   * 0 whole layers; 1 the attention half (first norm takes delta_in, ends with o_proj in
+   * `ao`); 2 the MLP half (norm of x += ao, ends with down_proj in `delta`).  Tensor
+   * parallel callers run part 1, all-reduce ao, part 2, all-reduce delta, per layer. */
+  int layer_begin, layer_end, part;
 } ChoreoDecodeStep;
 
 int choreo_decode_layers(const ChoreoDecodeStep* step, void* stream);

@@ -125,7 +125,8 @@ class DecodeStep(ctypes.Structure):
                            "gu", "act", "delta", "k7_ws", "k7_cnt", "attn_events")] + \
         [("attn_kernel", _I)] + \
         [(n, _P) for n in ("row_t", "vis_page", "vis_len", "vis_own", "blk_rows", "items",
-                           "linear_events")]
+                           "linear_events")] + \
+        [(n, _I) for n in ("layer_begin", "layer_end", "part")]
 
 
 def ptr(t) -> int | None:

@@ -123,7 +123,6 @@ __global__ void __launch_bounds__(kDvThreads, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int G = p.n_heads / p.n_kv;
-  const int n_work = p.counts[1] * p.n_kv;
   if (tid == 0) {
     for (int i = 0; i < kDvSlots; ++i) {
       mbar_init(&full_bar[i], 1);
@@ -141,6 +140,10 @@ __global__ void __launch_bounds__(kDvThreads, 1)
   }
   __syncthreads();
   pdl_wait();
+  // step data (K3's counts and items) only after the programmatic-dependency wait: with
+  // every kernel triggering its dependents at its start, a chain of launches can be
+  // resident long before this step's K3 finished
+  const int n_work = p.counts[1] * p.n_kv;
 
   if (warp == kDvLoader) {
     // ------------------------------------------------------------------ unit loader

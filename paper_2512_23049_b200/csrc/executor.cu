@@ -36,9 +36,12 @@ extern "C" int choreo_decode_layers(const ChoreoDecodeStep* s, void* stream) {
     rc = (call);           \
     if (rc != 0) return rc; \
   } while (0)
-  for (int l = 0; l < s->n_layers; ++l) {
+  const int l0 = s->layer_begin, l1 = s->layer_end > 0 ? s->layer_end : s->n_layers;
+  if (l0 < 0 || l1 > s->n_layers || l0 >= l1 || s->part < 0 || s->part > 2) return CHOREO_EINVAL;
+  for (int l = l0; l < l1; ++l) {
+   if (s->part != 2) {
     // delta: previous layer's down_proj output (K7 output, hi/lo already summed)
-    CHK(choreo_residual_rmsnorm(s->x, l ? s->delta : s->delta_in, CHOREO_F32, 0, s->attn_norm[l],
+    CHK(choreo_residual_rmsnorm(s->x, l > l0 ? s->delta : s->delta_in, CHOREO_F32, 0, s->attn_norm[l],
                                 CHOREO_BF16, R, d, s->eps, s->h, CHOREO_BF16, sp, nullptr, 0,
                                 stream));
     LIN_EV(0);
@@ -66,6 +69,8 @@ extern "C" int choreo_decode_layers(const ChoreoDecodeStep* s, void* stream) {
     CHK(choreo_linear_skinny(s->attn, x_rows, sp, s->wo[l], d, H * hd, s->ao, s->k7_ws, s->k7_cnt,
                              0, stream));
     LIN_EV(3);
+   }
+   if (s->part != 1) {
     CHK(choreo_residual_rmsnorm(s->x, s->ao, CHOREO_F32, 0, s->ffn_norm[l], CHOREO_BF16, R, d,
                                 s->eps, s->h, CHOREO_BF16, sp, nullptr, 0, stream));
     LIN_EV(4);
@@ -82,6 +87,7 @@ extern "C" int choreo_decode_layers(const ChoreoDecodeStep* s, void* stream) {
     CHK(choreo_linear_skinny(s->act, x_rows, sp, s->w_down[l], d, F, s->delta, s->k7_ws, s->k7_cnt,
                              0, stream));
     LIN_EV(7);
+   }
   }
 #undef CHK
 #undef LIN_EV

@@ -287,7 +287,19 @@ class Runner:
             st.row_t, st.vis_page, st.vis_len, st.vis_own = (
                 rowt_d.data_ptr(), vis[0].data_ptr(), vis[1].data_ptr(), vis[2].data_ptr())
             st.blk_rows, st.items = blk_rows.data_ptr(), items.data_ptr()
-        nat.decode_layers(ctypes.byref(st), stream)
+        if self.tp is not None and self.tp.size > 1:
+            # per layer: attention half, all-reduce o_proj partials, MLP half, all-reduce
+            # down_proj partials (the collectives stay with torch.distributed / NCCL)
+            for layer in range(L):
+                st.layer_begin, st.layer_end, st.part = layer, layer + 1, 1
+                st.delta_in = delta.data_ptr() if layer else None
+                nat.decode_layers(ctypes.byref(st), stream)
+                torch.distributed.all_reduce(ao, group=self.tp_group)
+                st.part = 2
+                nat.decode_layers(ctypes.byref(st), stream)
+                torch.distributed.all_reduce(delta, group=self.tp_group)
+        else:
+            nat.decode_layers(ctypes.byref(st), stream)
         if ev is not None:
             self._ev_pending.append(("attn", ev, [attn_bytes]))
         if lev is not None:
@@ -400,8 +412,9 @@ class Runner:
         row_part_off = torch.empty(R + 1, dtype=torch.int32, device=self.dev)
         row_part = torch.empty(max(n_parts, 1), dtype=torch.int32, device=self.dev)
         counts = torch.empty(4, dtype=torch.int32, device=self.dev)
+        v2_fat = v2 and rpb <= 16 and os.environ.get("CHOREO_K5V2_FAT", "1") != "0"
         fat = (torch.empty(max(n_items, 1), 64, dtype=torch.int32, device=self.dev)
-               if fused or (v2 and rpb <= 16) else None)
+               if fused or v2_fat else None)
         if fused and (self._counters is None or self._counters.numel() < R * Hk):
             self._counters = torch.zeros(max(R * Hk, 1024), dtype=torch.int32, device=self.dev)
         nat.assemble(cache.msg_len.dev.data_ptr(), cache.msg_pt.dev.data_ptr(),
@@ -430,7 +443,7 @@ class Runner:
         act = torch.empty(S * R, cfg.ffn_dim, dtype=self.dt, device=self.dev)
         delta = None
         launches = 2
-        native = ((fused or v2) and k7 and self.native_step and self.tp is None and not self.fused_combine
+        native = ((fused or v2) and k7 and self.native_step and not self.fused_combine
                   and self.dt == torch.bfloat16)
         if native:
             delta = self._native_layers(R, q, part_o, part_lse, attn, h, act, x, pos_d, page_d,

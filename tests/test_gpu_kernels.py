@@ -436,7 +436,7 @@ def test_fused_decode_matches_dense_reference(hd, H, Hk):
 
 
 @pytest.mark.parametrize("ppi", [1, 2, 5])
-@pytest.mark.parametrize("hd,H,Hk", [(128, 32, 8), (64, 16, 2), (128, 8, 8)])
+@pytest.mark.parametrize("hd,H,Hk", [(128, 32, 8), (64, 16, 2), (128, 8, 8), (64, 4, 2)])
 def test_decode_v2_matches_dense_reference(hd, H, Hk, ppi):
     """K5 v2 (TMA page ring + ldmatrix/mma.sync consumers, 4 key slices x 2 m-tiles) over
     page-centric items: agents sharing reordered parents, causal own pages, ragged pages.
