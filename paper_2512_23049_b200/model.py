@@ -450,7 +450,8 @@ class Runner:
                                         slot_d, fat, counts, n_items, row_part_off, row_part,
                                         attn_bytes, stream,
                                         (v2, rowt_d, vis, blk_rows, items) if v2 else None)
-            launches += 10 * len(self.w.layers)
+            # per layer: norm, K7 qkv, rope, K5, combine, K7 o, norm, K7 gate|up(+SwiGLU), K7 down
+            launches += (9 if cfg.ffn_dim % 64 == 0 else 10) * len(self.w.layers)
         for layer, lw in enumerate([] if native else self.w.layers):
             nat.residual_rmsnorm(x.data_ptr(), nat.ptr(delta), nat.F32, isp,
                                  lw["attn_norm"].data_ptr(), self.dtc, R, d, RMS_EPS, h.data_ptr(),
