@@ -194,7 +194,7 @@ int choreo_select_greedy(const float* logits, int n_rows, int ld, int vocab, int
  * 64/128, n_heads / n_kv <= 32, items built with rows_per_block <= 32 / G): persistent CTAs
  * (grid_ctas <= 0: min(148, items * n_kv)), a TMA producer warp streaming K/V pages into a
  * 5-slot shared-memory ring and 8 mma.sync consumer warps (4 key slices x 2 m16 tiles);
- * plain bf16 Q and P, f32 accumulation.  Writes one normalised partial + LSE per
+ * Q as a hi/lo bf16 pair, P bf16, f32 accumulation.  Writes one normalised partial + LSE per
  * (block row, head) like choreo_attn_split; merge with choreo_attn_combine.
  * n_layers sizes the pool's TMA view.  fat_items (optional, the `fat` output of
  * choreo_assemble; used when 32 / G <= 16) lets the loader read a unit's rows in the same

@@ -12,7 +12,8 @@
 //   warps 0-7   consumers, warp = (key slice q4 in 0..3, m-tile mt in 0..1): every page's
 //               64 keys are split four ways (16 keys per warp), the <= 32 (row, query head)
 //               vectors in two m16 tiles; S = Q K^T and O += P V on mma.sync m16n8k16
-//               (bf16 in, f32 accumulate) with K / V fragments from ldmatrix on the swizzled
+//               (Q as a hi/lo bf16 pair, P bf16, f32 accumulate) with K / V fragments from
+//               ldmatrix on the swizzled
 //               tiles, online softmax in registers (lazy O rescale), no per-page CTA barrier;
 //   unit end    the four key-slice states of an m-tile are merged through shared memory
 //               (asynchronously: slices 1-3 hand over and move on) and one normalised
@@ -21,6 +22,8 @@
 // pages, own_base + s <= row_t[r] (reference masking.py:36-40, model.py:166-168, 177-184).
 #include <cudaTypedefs.h>
 #include <math.h>
+
+#include <cuda_fp16.h>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -57,14 +60,19 @@ struct DvCfg {
   static constexpr int kR = HD / 64;                      // 64-dim SW128 halves per page
   static constexpr int kHalf = 64 * 128;                  // bytes of one [64][64] bf16 tile
   static constexpr int kSlot = 2 * kR * kHalf;            // K + V of one page
-  static constexpr int kMergeRow = HD + 4;                // O row + m + l (floats, 16-B rows)
-  // 4 key slices x 2 m-tiles x 16 rows, then a 4-int header (M, pbase, kvh)
-  static constexpr int kMerge = 4 * 2 * 16 * kMergeRow * 4 + 16;
+  // merge scratch: per (key slice, m-tile) 16 rows of the slice's NORMALISED O in f16
+  // (|O / l| <= max |v|: f16 range is safe, 11-bit mantissa) + (m, l) in f32, then a
+  // 4-int header (M, pbase, kvh)
+  static constexpr int kMergeRow = HD + 8;                // f16 elements per row (16-B rows)
+  static constexpr int kMergeO = 4 * 2 * 16 * kMergeRow * 2;
+  static constexpr int kMergeML = 4 * 2 * 16 * 8;
+  static constexpr int kMerge = kMergeO + kMergeML + 16;
   static constexpr int kQLd = HD + 8;                     // padded bf16 Q row (conflict-free)
   // unit record: ints [0] M [1] vb [2] nv [3] pbase [4] kvh, [8..40) row_t per vector,
-  // [40..72) page len, [72..104) own base; then Q bf16 [32][kQLd], pre-scaled
+  // [40..72) page len, [72..104) own base; then Q as a hi/lo bf16 pair (hi = bf16(q),
+  // lo = bf16(q - hi), pre-scaled): [2][32][kQLd]
   static constexpr int kUnitInts = 128;
-  static constexpr int kUnit = kUnitInts * 4 + 32 * kQLd * 2;
+  static constexpr int kUnit = kUnitInts * 4 + 2 * 32 * kQLd * 2;
   static constexpr int kTotal = kDvSlots * kSlot + kMerge + kDvUnits * kUnit + 1024;
 };
 
@@ -201,9 +209,15 @@ __global__ void __launch_bounds__(kDvThreads, 1)
       }
       if (4 * lane < HD) {
 #pragma unroll
-        for (int m = 0; m < 32; ++m)
+        for (int m = 0; m < 32; ++m) {
+          const float a0 = v[m].x * sc, a1 = v[m].y * sc, a2 = v[m].z * sc, a3 = v[m].w * sc;
+          const __nv_bfloat162 h01 = __floats2bfloat162_rn(a0, a1), h23 = __floats2bfloat162_rn(a2, a3);
+          const float2 f01 = __bfloat1622float2(h01), f23 = __bfloat1622float2(h23);
           *reinterpret_cast<uint2*>(qs + m * C::kQLd + 4 * lane) =
-              make_uint2(pack_bf16(v[m].x * sc, v[m].y * sc), pack_bf16(v[m].z * sc, v[m].w * sc));
+              make_uint2(*reinterpret_cast<const uint32_t*>(&h01), *reinterpret_cast<const uint32_t*>(&h23));
+          *reinterpret_cast<uint2*>(qs + (32 + m) * C::kQLd + 4 * lane) =
+              make_uint2(pack_bf16(a0 - f01.x, a1 - f01.y), pack_bf16(a2 - f23.x, a3 - f23.y));
+        }
       }
       mbar_arrive(&unit_full[sl]);
     }
@@ -272,7 +286,13 @@ __global__ void __launch_bounds__(kDvThreads, 1)
     const int mA = mt * 16 + g, mB = mA + 8;
     const bool vA = mA < M, vB = mB < M;
     const int rtA = ui[8 + mA], rtB = ui[8 + mB];
-    // Q as bf16 A fragments (pre-scaled to the log2 domain; rows past M are zero)
+    // Q as bf16 A fragments (pre-scaled to the log2 domain; rows past M are zero); the
+    // lo halves stay in shared memory (qlo) and are read per page
+    const __nv_bfloat16* qlo = qs + 32 * C::kQLd;
+    // ldmatrix row address of this lane for the m16 x k16 A fragments of Q lo
+    // (matrices: rows 0-7 / 8-15 x k 0-7 / 8-15; 272-byte rows are conflict-free)
+    const uint32_t qlo_lane = smem_addr(qlo + (mt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * C::kQLd +
+                                        (lane >> 4) * 8);
     uint32_t qa[KS][4];
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
@@ -297,17 +317,17 @@ __global__ void __launch_bounds__(kDvThreads, 1)
         float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
         float s0b[4] = {0.f, 0.f, 0.f, 0.f}, s1b[4] = {0.f, 0.f, 0.f, 0.f};
         const int lk = k0 + ((lane >> 4) & 1) * 8 + (lane & 7);
+        // hi and lo halves of Q on separate accumulator chains (the lo fragments come from
+        // shared memory each page, so Q costs no extra registers)
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
-          uint32_t r0, r1, r2, r3;
+          uint32_t r0, r1, r2, r3, ql[4];
           ldsm_x4(dv_addr(kb, lk, 2 * ks + ((lane >> 3) & 1)), r0, r1, r2, r3);
-          if (ks & 1) {
-            mma_bf16(s0b, qa[ks], r0, r1);
-            mma_bf16(s1b, qa[ks], r2, r3);
-          } else {
-            mma_bf16(s0, qa[ks], r0, r1);
-            mma_bf16(s1, qa[ks], r2, r3);
-          }
+          ldsm_x4(qlo_lane + 32 * ks, ql[0], ql[1], ql[2], ql[3]);  // A fragment of Q lo
+          mma_bf16(s0, qa[ks], r0, r1);
+          mma_bf16(s1, qa[ks], r2, r3);
+          mma_bf16(s0b, ql, r0, r1);
+          mma_bf16(s1b, ql, r2, r3);
         }
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -394,21 +414,24 @@ __global__ void __launch_bounds__(kDvThreads, 1)
     lB += __shfl_xor_sync(0xffffffffu, lB, 2);
     if (u > 0) mbar_wait(&merge_empty, (u - 1) & 1);  // the merge warps read unit u-1
     if (active) {
-      float* sc = merge + (q4 * 2 + mt) * 16 * C::kMergeRow;
+      __half* so = reinterpret_cast<__half*>(merge) + (q4 * 2 + mt) * 16 * C::kMergeRow;
+      float2* ml = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(merge) + C::kMergeO) +
+                   (q4 * 2 + mt) * 16;
+      const float iA = lA > 0.f ? 1.f / lA : 0.f, iB = lB > 0.f ? 1.f / lB : 0.f;
 #pragma unroll
       for (int n = 0; n < NT; ++n) {
-        *reinterpret_cast<float2*>(sc + g * C::kMergeRow + 8 * n + 2 * t) = make_float2(o[n][0], o[n][1]);
-        *reinterpret_cast<float2*>(sc + (g + 8) * C::kMergeRow + 8 * n + 2 * t) = make_float2(o[n][2], o[n][3]);
+        *reinterpret_cast<__half2*>(so + g * C::kMergeRow + 8 * n + 2 * t) =
+            __floats2half2_rn(o[n][0] * iA, o[n][1] * iA);
+        *reinterpret_cast<__half2*>(so + (g + 8) * C::kMergeRow + 8 * n + 2 * t) =
+            __floats2half2_rn(o[n][2] * iB, o[n][3] * iB);
       }
       if (t == 0) {
-        sc[g * C::kMergeRow + HD] = mxA;
-        sc[g * C::kMergeRow + HD + 1] = lA;
-        sc[(g + 8) * C::kMergeRow + HD] = mxB;
-        sc[(g + 8) * C::kMergeRow + HD + 1] = lB;
+        ml[g] = make_float2(mxA, lA);
+        ml[g + 8] = make_float2(mxB, lB);
       }
     }
     if (warp == 0 && lane == 0) {
-      int* hdr = reinterpret_cast<int*>(merge + 4 * 2 * 16 * C::kMergeRow);
+      int* hdr = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(merge) + C::kMergeO + C::kMergeML);
       hdr[0] = M;
       hdr[1] = pbase;
       hdr[2] = kvh;
@@ -423,42 +446,51 @@ __global__ void __launch_bounds__(kDvThreads, 1)
 template <int HD>
 __device__ __forceinline__ void dv_merge_unit(const DvParams& p, const float* merge, int mt,
                                               int lane, int G) {
-  constexpr int MR = HD + 4;
+  using C = DvCfg<HD>;
   constexpr int W = HD / 2;  // dims per lane
-  const int* hdr = reinterpret_cast<const int*>(merge + 4 * 2 * 16 * MR);
+  const uint8_t* mb = reinterpret_cast<const uint8_t*>(merge);
+  const int* hdr = reinterpret_cast<const int*>(mb + C::kMergeO + C::kMergeML);
   const int M = hdr[0], pbase = hdr[1], kvh = hdr[2];
   const int row = lane >> 1, half = lane & 1;
   const int m = mt * 16 + row;
-  if (mt * 16 >= M || m >= M) return;
+  if (m >= M) return;
+  const float2* ml = reinterpret_cast<const float2*>(mb + C::kMergeO);
   float mk[4], lk[4], mx = -INFINITY;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    const float* sc = merge + (k * 2 + mt) * 16 * MR + row * MR;
-    mk[k] = sc[HD];
-    lk[k] = sc[HD + 1];
+    const float2 v = ml[(k * 2 + mt) * 16 + row];
+    mk[k] = v.x;
+    lk[k] = v.y;
     mx = fmaxf(mx, mk[k]);
   }
   float wk[4], L = 0.f;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    wk[k] = mk[k] == -INFINITY ? 0.f : dv_ex2(mk[k] - mx);
-    L += lk[k] * wk[k];
+    wk[k] = (mk[k] == -INFINITY || lk[k] <= 0.f) ? 0.f : lk[k] * dv_ex2(mk[k] - mx);
+    L += wk[k];
   }
   const float inv = L > 0.f ? 1.f / L : 0.f;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) wk[k] *= inv;
   const int64_t pidx = (int64_t)(pbase + m / G) * p.n_heads + kvh * G + m % G;
   float* dst = p.part_o + pidx * HD + half * W;
-#pragma unroll 4
-  for (int d = 0; d < W; d += 4) {
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  const __half* so = reinterpret_cast<const __half*>(merge) + row * C::kMergeRow + half * W;
+#pragma unroll 2
+  for (int d = 0; d < W; d += 8) {
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const float4 x = *reinterpret_cast<const float4*>(merge + (k * 2 + mt) * 16 * MR + row * MR + half * W + d);
-      acc.x += wk[k] * x.x;
-      acc.y += wk[k] * x.y;
-      acc.z += wk[k] * x.z;
-      acc.w += wk[k] * x.w;
+      const uint4 x = *reinterpret_cast<const uint4*>(so + (k * 2 + mt) * 16 * C::kMergeRow + d);
+      const __half2* h = reinterpret_cast<const __half2*>(&x);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __half22float2(h[e]);
+        acc[2 * e] += wk[k] * f.x;
+        acc[2 * e + 1] += wk[k] * f.y;
+      }
     }
-    *reinterpret_cast<float4*>(dst + d) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+    *reinterpret_cast<float4*>(dst + d) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    *reinterpret_cast<float4*>(dst + d + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
   }
   if (half == 0) p.part_lse[pidx] = L > 0.f ? (mx + log2f(L)) * 0.6931471805599453f : -INFINITY;
 }

@@ -384,3 +384,36 @@ def test_device_nucleus_sampling_matches_host_sampler(mode):
         runs.append([eng.generated_token_ids(m) for m in ms])
     assert runs[0] == runs[1]
     assert any(len(t) > 0 for t in runs[0])
+
+
+def test_wide_header_step_matches_oracle():
+    """A parallel decode whose header step has >= 64 rows (8 agents x 14-token headers:
+    cuBLAS projections, page-centric K5 v2 over row blocks); logits within 2e-2 of the
+    oracle (bf16-rounded weights), teacher-forced on its tokens."""
+    shape = O.Shape(n_layers=2, n_heads=8, n_kv_heads=2, head_dim=128, ffn_dim=256,
+                    vocab_size=300, context_window=2048, rope_base=500000.0)
+    cfg = P.ModelConfig(**{k: getattr(shape, k) for k in shape.__dataclass_fields__})
+    ref = O.Oracle(O.round_weights(O.init_weights(shape), "bf16"), shape, record_logits=True)
+    eng = P.Engine(P.DeviceWeights.from_host(P.init_weights(cfg).rounded("bf16"),
+                                             dtype=torch.bfloat16), record_logits=True)
+    rng = np.random.default_rng(5)
+    texts = ["".join(chr(97 + int(c)) for c in rng.integers(0, 26, n)) for n in (150, 90, 200)]
+    for t in texts:
+        ref.prefill({"message": t})
+        eng.prefill(P.PrefillCall(t))
+    heads = [f"Agent {i:02d} says:" for i in range(8)]
+    sp_o, sp_p = O.Sampling(max_tokens=6), P.SamplingParams(max_tokens=6)
+    parents = [[2, 0, 1] if i % 2 else [0, 1] for i in range(8)]
+    offs = [[244, 0, 152] if i % 2 else [0, 152] for i in range(8)]
+    ref.decode_batch([{"header": h, "parents": p, "offsets": o, "new_offset": 500,
+                       "sampling": sp_o} for h, p, o in zip(heads, parents, offs)])
+    forcing = [ref.generated(3 + i) for i in range(8)]
+    ms = eng.decode_parallel([P.DecodeCall(h, parents=p, offsets=o, new_offset=500, sampling=sp_p)
+                              for h, p, o in zip(heads, parents, offs)], force_tokens=forcing)
+    worst = 0.0
+    for i, m in enumerate(ms):
+        got = np.stack(eng.stats[-1].logits[m])
+        want = np.stack(ref.stats[-1].logits[3 + i])
+        assert got.shape == want.shape
+        worst = max(worst, float(np.abs(got - want).max()))
+    assert worst <= 2e-2, worst

@@ -440,7 +440,7 @@ def test_fused_decode_matches_dense_reference(hd, H, Hk):
 def test_decode_v2_matches_dense_reference(hd, H, Hk, ppi):
     """K5 v2 (TMA page ring + ldmatrix/mma.sync consumers, 4 key slices x 2 m-tiles) over
     page-centric items: agents sharing reordered parents, causal own pages, ragged pages.
-    Plain bf16 Q and P with f32 accumulation: within 2e-2 of the f64 dense reference."""
+    Q as a hi/lo bf16 pair, P bf16, f32 accumulation: within 2e-2 of the f64 reference."""
     rng = np.random.default_rng(12)
     cfg = ModelConfig(n_layers=2, n_heads=H, n_kv_heads=Hk, head_dim=hd)
     cache, lens = _random_cache(cfg, rng, 8, dtype=torch.bfloat16)
