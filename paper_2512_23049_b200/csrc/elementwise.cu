@@ -117,10 +117,17 @@ __global__ void residual_rmsnorm_vec(float* __restrict__ x, const float* __restr
                                      int w_dt, int d, float eps, void* __restrict__ out, int out_dt,
                                      int out_split, const int32_t* __restrict__ row_map) {
   pdl_trigger();
+  // the norm weight is static: fetched before the dependency wait, off the critical path
+  const int nvec = d >> 2;
+  float4 wv[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    const int i = threadIdx.x + c * blockDim.x;
+    wv[c] = out && i < nvec ? ld4_any(w, w_dt, 4 * i) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   pdl_wait();
   const int r_out = blockIdx.x;
   const int r = row_map ? row_map[r_out] : r_out;
-  const int nvec = d >> 2;
   float* xr = x + (int64_t)r * d;
   float4 v[CH];
   float ss = 0.f;
@@ -159,9 +166,8 @@ __global__ void residual_rmsnorm_vec(float* __restrict__ x, const float* __restr
   for (int c = 0; c < CH; ++c) {
     const int i = threadIdx.x + c * blockDim.x;
     if (i < nvec) {
-      const float4 wv = ld4_any(w, w_dt, 4 * i);
-      const float4 y = make_float4(v[c].x * inv * wv.x, v[c].y * inv * wv.y, v[c].z * inv * wv.z,
-                                   v[c].w * inv * wv.w);
+      const float4 y = make_float4(v[c].x * inv * wv[c].x, v[c].y * inv * wv[c].y,
+                                   v[c].z * inv * wv[c].z, v[c].w * inv * wv[c].w);
       st4_split(out, out_dt, (int64_t)r_out * d + 4 * i, (int64_t)(gridDim.x + r_out) * d + 4 * i,
                 y, out_split);
     }

@@ -54,11 +54,12 @@ orig = eng._runner.forward
 
 def fwd(plan):
     Hook.n += 1
-    if Hook.n == 3:  # skip the header step and first decode step
+    first = 1 if os.environ.get("PROFILE_HEADER") else 3  # 1: the header step itself
+    if Hook.n == first:  # else skip the header step and the first decode step
         torch.cuda.synchronize()
         torch.cuda.cudart().cudaProfilerStart()
     out = orig(plan)
-    if Hook.n == 2 + args.steps:
+    if Hook.n == first - 1 + args.steps:
         torch.cuda.synchronize()
         torch.cuda.cudart().cudaProfilerStop()
     return out
