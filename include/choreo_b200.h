@@ -207,6 +207,17 @@ int choreo_decode_attn_v2(const float* q, const void* k_pool, const void* v_pool
                           float* part_o, float* part_lse, const int32_t* fat_items,
                           int grid_ctas, void* stream);
 
+/* Deferred K7 output ("pieces"): tiles owned by one CTA are complete in y ([rows][n] f32);
+ * tiles cut between CTAs (stream-K) are left as per-CTA partials in the workspace and summed
+ * by the consuming kernel in the order the K7 reducer uses, so the values are bit-identical
+ * to choreo_linear_skinny's y while the GEMM skips its cross-CTA fix-up (a GPU-scope
+ * atomic and a second pass over the partials at the end of the launch). */
+typedef struct {
+  const float* y;
+  const float* ws;
+  int n, kb, iters, grid, nx, split;
+} ChoreoK7Pieces;
+
 /* K7 decode-sized linear layer (weight streaming, tcgen05 + TMA, stream-K):
  *   y[r][n] = sum_k x[r][k] * w[n][k]      x: bf16 [x_rows][k], w: bf16 [n][k] (out, in),
  *                                          y: f32 [x_rows / (1 + split)][n].
@@ -219,6 +230,24 @@ int choreo_decode_attn_v2(const float* q, const void* k_pool, const void* v_pool
 int choreo_linear_skinny(const void* x, int x_rows, int split, const void* w, int n, int k,
                          float* y, float* workspace, int* tile_counters, int grid_ctas,
                          void* stream);
+
+/* choreo_linear_skinny that leaves cut tiles as pieces (see ChoreoK7Pieces, filled in
+ * `pieces`); consumers: choreo_rope_append_pieces, choreo_residual_rmsnorm_pieces. */
+int choreo_linear_skinny_pieces(const void* x, int x_rows, int split, const void* w, int n, int k,
+                                float* y, float* workspace, int* tile_counters, int grid_ctas,
+                                ChoreoK7Pieces* pieces, void* stream);
+
+/* choreo_rope_append (f32 qkv) reading a deferred K7 qkv projection. */
+int choreo_rope_append_pieces(const ChoreoK7Pieces* qkv, int n_rows, const int32_t* pos,
+                              const int32_t* dst_page, const int32_t* dst_slot, float* q_out,
+                              void* k_pool, void* v_pool, int pool_dtype, int layer, int n_kv,
+                              int n_pages, int page_size, int n_heads, int head_dim,
+                              const float* cos_t, const float* sin_t, int max_delta, void* stream);
+
+/* choreo_residual_rmsnorm with delta = a deferred K7 projection (x += delta; out = norm(x)). */
+int choreo_residual_rmsnorm_pieces(float* x, const ChoreoK7Pieces* delta, const void* w,
+                                   int w_dtype, int n_rows, int d, float eps, void* out,
+                                   int out_dtype, int out_split, void* stream);
 
 /* K7 for the gate|up projection with the SwiGLU product fused into its epilogue:
  * act[r][i] = silu(g) * u, g = x[r] . w_gu[i], u = x[r] . w_gu[f + i] (w_gu = [gate; up],

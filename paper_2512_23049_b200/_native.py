@@ -42,6 +42,10 @@ SIGNATURES: dict[str, list] = {
     "choreo_selftest_umma": [_P, _P, _P, _P, _P, _P, _P],
     "choreo_linear_skinny": [_P, _I, _I, _P, _I, _I, _P, _P, _P, _I, _P],
     "choreo_decode_layers": [_P, _P],
+    "choreo_linear_skinny_pieces": [_P, _I, _I, _P, _I, _I, _P, _P, _P, _I, _P, _P],
+    "choreo_rope_append_pieces": [_P, _I, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P,
+                                  _P, _I, _P],
+    "choreo_residual_rmsnorm_pieces": [_P, _P, _P, _I, _I, _I, _F, _P, _I, _I, _P],
     "choreo_linear_gate_up_silu": [_P, _I, _I, _P, _I, _I, _P, _P, _P, _P],
     "choreo_select_nucleus": [_P, _I, _I, _I, _P, _P, _P, _P],
     "choreo_decode_attn_v2": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P,
@@ -92,6 +96,16 @@ class _Caller:
 
 embed = _Caller("choreo_embed")
 residual_rmsnorm = _Caller("choreo_residual_rmsnorm")
+linear_skinny_pieces = _Caller("choreo_linear_skinny_pieces")
+rope_append_pieces = _Caller("choreo_rope_append_pieces")
+residual_rmsnorm_pieces = _Caller("choreo_residual_rmsnorm_pieces")
+
+
+class K7Pieces(ctypes.Structure):
+    """Mirror of ChoreoK7Pieces (include/choreo_b200.h): a deferred K7 output."""
+    _fields_ = [("y", ctypes.c_void_p), ("ws", ctypes.c_void_p), ("n", ctypes.c_int),
+                ("kb", ctypes.c_int), ("iters", ctypes.c_int), ("grid", ctypes.c_int),
+                ("nx", ctypes.c_int), ("split", ctypes.c_int)]
 silu_mul = _Caller("choreo_silu_mul")
 rope_append = _Caller("choreo_rope_append")
 rerotate = _Caller("choreo_rerotate")

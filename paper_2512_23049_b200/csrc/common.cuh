@@ -105,4 +105,42 @@ __device__ __forceinline__ float warp_max(float v) {
   return v;
 }
 
+// stream-K split of `iters` iterations over `grid` CTAs (K7): first iteration of CTA c, and
+// the CTA owning iteration i (every CTA owns >= 1 iteration: grid <= iters)
+__host__ __device__ __forceinline__ int ln_begin(int c, int iters, int grid) {
+  return (int)(((long long)c * iters) / grid);
+}
+__host__ __device__ __forceinline__ int ln_owner(int i, int iters, int grid) {
+  return (int)((((long long)i + 1) * grid - 1) / iters);
+}
+
+// element (r, n..n+W-1) of a deferred K7 output (ChoreoK7Pieces): y for tiles one CTA owns,
+// else the per-CTA partials of the tile summed in CTA order from 0 (the reducer's order; for
+// split activations hi and lo rows are summed separately, then added) -- bit-identical
+template <int W>
+__device__ __forceinline__ void k7_get(const ChoreoK7Pieces& v, int r, int n, float* out) {
+  const int t = n >> 7, nl = n & 127;
+  const int lo = t * v.kb, hi = lo + v.kb;
+  const int c_lo = ln_owner(lo, v.iters, v.grid), c_hi = ln_owner(hi - 1, v.iters, v.grid);
+  if (c_lo == c_hi) {
+#pragma unroll
+    for (int e = 0; e < W; ++e) out[e] = v.y[(size_t)r * v.n + n + e];
+    return;
+  }
+  float a[W], b[W];
+#pragma unroll
+  for (int e = 0; e < W; ++e) a[e] = b[e] = 0.f;
+  for (int cc = c_lo; cc <= c_hi; ++cc) {
+    const int sl = ln_begin(cc, v.iters, v.grid) >= lo ? 0 : 1;
+    const float* pc = v.ws + ((size_t)(cc * 2 + sl) * v.nx) * 128 + nl;
+#pragma unroll
+    for (int e = 0; e < W; ++e) {
+      a[e] += pc[r * 128 + e];
+      if (v.split) b[e] += pc[(v.nx / 2 + r) * 128 + e];
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < W; ++e) out[e] = v.split ? a[e] + b[e] : a[e];
+}
+
 }  // namespace choreo

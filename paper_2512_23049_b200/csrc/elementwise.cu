@@ -115,7 +115,8 @@ template <int CH>
 __global__ void residual_rmsnorm_vec(float* __restrict__ x, const float* __restrict__ delta,
                                      int delta_split, int n_rows, const void* __restrict__ w,
                                      int w_dt, int d, float eps, void* __restrict__ out, int out_dt,
-                                     int out_split, const int32_t* __restrict__ row_map) {
+                                     int out_split, const int32_t* __restrict__ row_map,
+                                     ChoreoK7Pieces pv) {
   pdl_trigger();
   // the norm weight is static: fetched before the dependency wait, off the critical path
   const int nvec = d >> 2;
@@ -138,7 +139,11 @@ __global__ void residual_rmsnorm_vec(float* __restrict__ x, const float* __restr
     if (i < nvec) {
       v[c] = ld4(xr + 4 * i);
       if (delta) {
-        const float4 a = ld4(delta + (int64_t)r * d + 4 * i);
+        float4 a;
+        if (pv.ws)
+          choreo::k7_get<4>(pv, r, 4 * i, &a.x);  // deferred K7 output
+        else
+          a = ld4(delta + (int64_t)r * d + 4 * i);
         float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
         if (delta_split) b = ld4(delta + (int64_t)(n_rows + r) * d + 4 * i);
         v[c].x += a.x + b.x;
@@ -256,7 +261,7 @@ int choreo_residual_rmsnorm(float* x, const void* delta, int delta_dtype, int de
 #define RMS_VEC(CH)                                                                            \
   launch_k(residual_rmsnorm_vec<CH>, rows, threads, 0, s, x, (const float*)delta, delta_split, n_rows, \
                                                     w, w_dtype, d, eps, out, out_dtype,          \
-                                                    out_split, row_map)
+                                                    out_split, row_map, ChoreoK7Pieces{})
     if (ch == 1) RMS_VEC(1);
     else if (ch == 2) RMS_VEC(2);
     else RMS_VEC(4);
@@ -268,6 +273,29 @@ int choreo_residual_rmsnorm(float* x, const void* delta, int delta_dtype, int de
       x, delta, delta_dtype, delta_split, n_rows, w, w_dtype, d, eps, out, out_dtype, out_split,
       row_map);
   return launch_status("choreo_residual_rmsnorm");
+}
+
+int choreo_residual_rmsnorm_pieces(float* x, const ChoreoK7Pieces* delta, const void* w,
+                                   int w_dtype, int n_rows, int d, float eps, void* out,
+                                   int out_dtype, int out_split, void* stream) {
+  if (!x || !delta || !delta->y || !delta->ws || !out || !w || d <= 0 || n_rows < 0 ||
+      delta->n != d || !dtype_ok(w_dtype) || !dtype_ok(out_dtype))
+    return CHOREO_EINVAL;
+  if (out_split && out_dtype != CHOREO_BF16) return CHOREO_EINVAL;
+  if (d % 4 || d > 4 * 4 * 1024) return CHOREO_EUNSUPPORTED;
+  if (n_rows == 0) return CHOREO_OK;
+  const int nvec = d / 4;
+  int threads = nvec < 1024 ? ((nvec + 31) / 32) * 32 : 1024;
+  const int ch = (nvec + threads - 1) / threads;
+  auto s = as_stream(stream);
+#define RMS_VEC(CH)                                                                           \
+  launch_k(residual_rmsnorm_vec<CH>, n_rows, threads, 0, s, x, delta->y, 0, n_rows, w, w_dtype, d, \
+           eps, out, out_dtype, out_split, (const int32_t*)nullptr, *delta)
+  if (ch == 1) RMS_VEC(1);
+  else if (ch == 2) RMS_VEC(2);
+  else RMS_VEC(4);
+#undef RMS_VEC
+  return launch_status("choreo_residual_rmsnorm_pieces");
 }
 
 int choreo_silu_mul(const void* gu, int gu_dtype, int in_split, int n_rows, int f, void* out,

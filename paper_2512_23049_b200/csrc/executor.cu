@@ -4,7 +4,8 @@
 //
 // Per layer, on `stream`:
 //   residual_rmsnorm (x += delta; h = norm(x) as hi/lo bf16)
-//   K7 qkv = h @ Wqkv^T                 (weights streamed; PDL prefetch under the norm)
+//   K7 qkv = h @ Wqkv^T                 (weights streamed; PDL prefetch under the norm;
+//                                        cut tiles left as pieces for RoPE, ChoreoK7Pieces)
 //   K1 rope_append (q rotated to f32, K/V written into the message pages)
 //   K5 decode attention over the K3 fat items (+ LSE combine)
 //   K7 ao = attn @ Wo^T
@@ -16,6 +17,15 @@
 #include "common.cuh"
 
 using namespace choreo;
+
+static bool k7_defer_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("CHOREO_K7_DEFER");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
+}
 
 extern "C" int choreo_decode_layers(const ChoreoDecodeStep* s, void* stream) {
   if (!s || !s->attn_norm || !s->w_qkv || !s->wo || !s->ffn_norm || !s->w_gu || !s->w_down ||
@@ -38,19 +48,39 @@ extern "C" int choreo_decode_layers(const ChoreoDecodeStep* s, void* stream) {
   } while (0)
   const int l0 = s->layer_begin, l1 = s->layer_end > 0 ? s->layer_end : s->n_layers;
   if (l0 < 0 || l1 > s->n_layers || l0 >= l1 || s->part < 0 || s->part > 2) return CHOREO_EINVAL;
+  // K7 outputs consumed inside this call are left deferred (ChoreoK7Pieces): the consumer
+  // (RoPE / residual+norm) sums the cut tiles, the GEMM skips its cross-CTA fix-up.  Outputs
+  // the caller reads (the last down_proj, the TP halves' o_proj / down_proj) are reduced.
+  const bool defer = k7_defer_enabled();
+  ChoreoK7Pieces pk{}, po{}, pd{};
+  bool pd_valid = false;
   for (int l = l0; l < l1; ++l) {
    if (s->part != 2) {
     // delta: previous layer's down_proj output (K7 output, hi/lo already summed)
-    CHK(choreo_residual_rmsnorm(s->x, l > l0 ? s->delta : s->delta_in, CHOREO_F32, 0, s->attn_norm[l],
-                                CHOREO_BF16, R, d, s->eps, s->h, CHOREO_BF16, sp, nullptr, 0,
-                                stream));
+    if (pd_valid && l > l0)
+      CHK(choreo_residual_rmsnorm_pieces(s->x, &pd, s->attn_norm[l], CHOREO_BF16, R, d, s->eps,
+                                         s->h, CHOREO_BF16, sp, stream));
+    else
+      CHK(choreo_residual_rmsnorm(s->x, l > l0 ? s->delta : s->delta_in, CHOREO_F32, 0,
+                                  s->attn_norm[l], CHOREO_BF16, R, d, s->eps, s->h, CHOREO_BF16,
+                                  sp, nullptr, 0, stream));
+    pd_valid = false;
     LIN_EV(0);
-    CHK(choreo_linear_skinny(s->h, x_rows, sp, s->w_qkv[l], n_qkv, d, s->qkv, s->k7_ws, s->k7_cnt,
-                             0, stream));
-    LIN_EV(1);
-    CHK(choreo_rope_append(s->qkv, CHOREO_F32, n_qkv, R, 0, s->pos, s->page, s->slot, s->q,
-                           s->k_pool, s->v_pool, CHOREO_BF16, l, Hk, s->n_pages, s->page_size, H,
-                           hd, s->cos_t, s->sin_t, s->max_delta, stream));
+    if (defer) {
+      CHK(choreo_linear_skinny_pieces(s->h, x_rows, sp, s->w_qkv[l], n_qkv, d, s->qkv, s->k7_ws,
+                                      s->k7_cnt, 0, &pk, stream));
+      LIN_EV(1);
+      CHK(choreo_rope_append_pieces(&pk, R, s->pos, s->page, s->slot, s->q, s->k_pool, s->v_pool,
+                                    CHOREO_BF16, l, Hk, s->n_pages, s->page_size, H, hd, s->cos_t,
+                                    s->sin_t, s->max_delta, stream));
+    } else {
+      CHK(choreo_linear_skinny(s->h, x_rows, sp, s->w_qkv[l], n_qkv, d, s->qkv, s->k7_ws,
+                               s->k7_cnt, 0, stream));
+      LIN_EV(1);
+      CHK(choreo_rope_append(s->qkv, CHOREO_F32, n_qkv, R, 0, s->pos, s->page, s->slot, s->q,
+                             s->k_pool, s->v_pool, CHOREO_BF16, l, Hk, s->n_pages, s->page_size,
+                             H, hd, s->cos_t, s->sin_t, s->max_delta, stream));
+    }
     if (ev) cudaEventRecord(ev[2 * l], as_stream(stream));
     if (s->attn_kernel == 1)
       CHK(choreo_decode_attn_v2(s->q, s->k_pool, s->v_pool, s->n_layers, l, Hk, s->n_pages,
@@ -66,13 +96,21 @@ extern "C" int choreo_decode_layers(const ChoreoDecodeStep* s, void* stream) {
     CHK(choreo_attn_combine(s->part_o, s->part_lse, s->row_part_off, s->row_part, R, H, hd,
                             s->attn, CHOREO_BF16, sp, stream));
     LIN_EV(2);
-    CHK(choreo_linear_skinny(s->attn, x_rows, sp, s->wo[l], d, H * hd, s->ao, s->k7_ws, s->k7_cnt,
-                             0, stream));
+    if (defer && s->part == 0)
+      CHK(choreo_linear_skinny_pieces(s->attn, x_rows, sp, s->wo[l], d, H * hd, s->ao, s->k7_ws,
+                                      s->k7_cnt, 0, &po, stream));
+    else
+      CHK(choreo_linear_skinny(s->attn, x_rows, sp, s->wo[l], d, H * hd, s->ao, s->k7_ws,
+                               s->k7_cnt, 0, stream));
     LIN_EV(3);
    }
    if (s->part != 1) {
-    CHK(choreo_residual_rmsnorm(s->x, s->ao, CHOREO_F32, 0, s->ffn_norm[l], CHOREO_BF16, R, d,
-                                s->eps, s->h, CHOREO_BF16, sp, nullptr, 0, stream));
+    if (defer && s->part == 0)
+      CHK(choreo_residual_rmsnorm_pieces(s->x, &po, s->ffn_norm[l], CHOREO_BF16, R, d, s->eps,
+                                         s->h, CHOREO_BF16, sp, stream));
+    else
+      CHK(choreo_residual_rmsnorm(s->x, s->ao, CHOREO_F32, 0, s->ffn_norm[l], CHOREO_BF16, R, d,
+                                  s->eps, s->h, CHOREO_BF16, sp, nullptr, 0, stream));
     LIN_EV(4);
     if (F % 64 == 0) {
       CHK(choreo_linear_gate_up_silu(s->h, x_rows, sp, s->w_gu[l], F, d, s->act, s->k7_ws,
@@ -84,8 +122,14 @@ extern "C" int choreo_decode_layers(const ChoreoDecodeStep* s, void* stream) {
     }
     LIN_EV(5);
     LIN_EV(6);
-    CHK(choreo_linear_skinny(s->act, x_rows, sp, s->w_down[l], d, F, s->delta, s->k7_ws, s->k7_cnt,
-                             0, stream));
+    if (defer && s->part == 0 && l < l1 - 1) {
+      CHK(choreo_linear_skinny_pieces(s->act, x_rows, sp, s->w_down[l], d, F, s->delta,
+                                      s->k7_ws, s->k7_cnt, 0, &pd, stream));
+      pd_valid = true;
+    } else {
+      CHK(choreo_linear_skinny(s->act, x_rows, sp, s->w_down[l], d, F, s->delta, s->k7_ws,
+                               s->k7_cnt, 0, stream));
+    }
     LIN_EV(7);
    }
   }

@@ -36,6 +36,7 @@ struct LinearParams {
   int N, KB, iters, grid, out_rows, split;
   int silu_f;  // > 0: gate|up projection with SiLU(gate)*up fused (tile t = gate rows
                // [64t, 64t+64) over up rows [F + 64t, ...)); N counts act columns (= F)
+  int defer;   // 1: cut tiles stay as pieces in ws for the consumer (ChoreoK7Pieces)
 };
 
 template <int NX, int KSUB>
@@ -51,13 +52,6 @@ struct LnCfg {
 template <int NX>
 __host__ __device__ constexpr int p_split_rows() { return NX; }
 
-__device__ __forceinline__ int ln_begin(int c, int iters, int grid) {
-  return (int)(((long long)c * iters) / grid);
-}
-// CTA whose range holds iteration i (every CTA owns >= 1 iteration: grid <= iters)
-__device__ __forceinline__ int ln_owner(int i, int iters, int grid) {
-  return (int)((((long long)i + 1) * grid - 1) / iters);
-}
 
 template <int NX, int KSUB>
 __global__ void __launch_bounds__(kLnThreads, 1)
@@ -197,6 +191,7 @@ __global__ void __launch_bounds__(kLnThreads, 1)
         float* w = p.ws + ((size_t)(c * 2 + slot) * NX) * kLnTile + nl;
 #pragma unroll
         for (int q = 0; q < NX; ++q) w[q * kLnTile] = acc[q];
+        if (p.defer) continue;  // the consumer sums the pieces (k7_get)
         // the group's barrier orders the 128 threads' partial stores before thread 0's
         // GPU-scope release (one fence per piece instead of one per thread); the last piece
         // acquires the others the same way before reading them
@@ -333,7 +328,7 @@ using namespace choreo;
 
 static int linear_impl(const void* x, int x_rows, int split, const void* w, int n, int k, void* y,
                        float* workspace, int* tile_counters, int grid_ctas, int silu_f,
-                       void* stream) {
+                       void* stream, ChoreoK7Pieces* pieces = nullptr) {
   if (!x || !w || !y || !workspace || !tile_counters || x_rows <= 0 || n <= 0 || k <= 0 ||
       (split && (x_rows & 1)))
     return CHOREO_EINVAL;
@@ -354,7 +349,12 @@ static int linear_impl(const void* x, int x_rows, int split, const void* w, int 
   int grid = grid_ctas > 0 ? grid_ctas : 148;
   if (grid > iters) grid = iters;
   LinearParams p{reinterpret_cast<float*>(y), workspace, tile_counters, n, KB, iters, grid,
-                 split ? x_rows / 2 : x_rows, split, silu_f};
+                 split ? x_rows / 2 : x_rows, split, silu_f, pieces ? 1 : 0};
+  if (pieces) {
+    if (silu_f) return CHOREO_EINVAL;
+    *pieces = ChoreoK7Pieces{reinterpret_cast<const float*>(y), workspace, n, KB, iters, grid, NX,
+                             split};
+  }
   auto s = as_stream(stream);
 #define LN_CASE(nx)                                                                       \
   return ksub == 1   ? launch_linear<nx, 1>(p, x, x_rows, w, n, k, s)                     \
@@ -380,4 +380,13 @@ extern "C" int choreo_linear_gate_up_silu(const void* x, int x_rows, int split, 
                                           int* tile_counters, void* stream) {
   if (f <= 0) return CHOREO_EINVAL;
   return linear_impl(x, x_rows, split, w_gu, f, d, act, workspace, tile_counters, 0, f, stream);
+}
+
+extern "C" int choreo_linear_skinny_pieces(const void* x, int x_rows, int split, const void* w,
+                                           int n, int k, float* y, float* workspace,
+                                           int* tile_counters, int grid_ctas,
+                                           ChoreoK7Pieces* pieces, void* stream) {
+  if (!pieces) return CHOREO_EINVAL;
+  return linear_impl(x, x_rows, split, w, n, k, y, workspace, tile_counters, grid_ctas, 0, stream,
+                     pieces);
 }

@@ -20,7 +20,8 @@ __global__ void rope_append_kernel(const TI* __restrict__ qkv, int ld, int n_row
                                    TP* __restrict__ kp, TP* __restrict__ vp, int layer, int n_kv,
                                    int n_pages, int page_size, int n_heads, int hd,
                                    const float* __restrict__ cos_t,
-                                   const float* __restrict__ sin_t, int max_delta) {
+                                   const float* __restrict__ sin_t, int max_delta,
+                                   ChoreoK7Pieces pv) {
   pdl_trigger();
   pdl_wait();
   const int half = hd >> 1;
@@ -33,8 +34,16 @@ __global__ void rope_append_kernel(const TI* __restrict__ qkv, int ld, int n_row
     const int head = rem / half;  // 0..n_heads+2*n_kv-1 in qkv column order
     const int i = rem % half;
     const TI* src = qkv + (int64_t)r * ld + head * hd + 2 * i;
-    float e = to_f32(src[0]);
-    float o = to_f32(src[1]);
+    float e, o;
+    if (pv.ws) {  // deferred K7 qkv (f32; pairs never straddle a 128-column tile)
+      float eo[2];
+      k7_get<2>(pv, r, head * hd + 2 * i, eo);
+      e = eo[0];
+      o = eo[1];
+    } else {
+      e = to_f32(src[0]);
+      o = to_f32(src[1]);
+    }
     if (split) {  // stacked hi/lo GEMM halves (rows r and n_rows + r)
       e += to_f32(src[(int64_t)n_rows * ld]);
       o += to_f32(src[(int64_t)n_rows * ld + 1]);
@@ -161,13 +170,40 @@ int choreo_rope_append(const void* qkv, int qkv_dtype, int ld_qkv, int n_rows, i
 #define K1(TI, TP)                                                                               \
   launch_k(rope_append_kernel<TI, TP>, blocks, 256, 0, s,                                              \
       (const TI*)qkv, ld_qkv, n_rows, qkv_split, pos, dst_page, dst_slot, q_out, (TP*)k_pool, (TP*)v_pool, \
-      layer, n_kv, n_pages, page_size, n_heads, head_dim, cos_t, sin_t, max_delta)
+      layer, n_kv, n_pages, page_size, n_heads, head_dim, cos_t, sin_t, max_delta, ChoreoK7Pieces{})
   if (qkv_dtype == CHOREO_F32 && pool_dtype == CHOREO_F32) K1(float, float);
   else if (qkv_dtype == CHOREO_F32 && pool_dtype == CHOREO_BF16) K1(float, __nv_bfloat16);
   else if (qkv_dtype == CHOREO_BF16 && pool_dtype == CHOREO_BF16) K1(__nv_bfloat16, __nv_bfloat16);
   else K1(__nv_bfloat16, float);
 #undef K1
   return launch_status("choreo_rope_append");
+}
+
+int choreo_rope_append_pieces(const ChoreoK7Pieces* qkv, int n_rows, const int32_t* pos,
+                              const int32_t* dst_page, const int32_t* dst_slot, float* q_out,
+                              void* k_pool, void* v_pool, int pool_dtype, int layer, int n_kv,
+                              int n_pages, int page_size, int n_heads, int head_dim,
+                              const float* cos_t, const float* sin_t, int max_delta,
+                              void* stream) {
+  if (!qkv || !qkv->y || !qkv->ws || !pos || !dst_page || !dst_slot || !q_out || !k_pool ||
+      !v_pool || !cos_t || !sin_t)
+    return CHOREO_EINVAL;
+  if (!dtype_ok(pool_dtype) || head_dim < 2 || (head_dim & 1) || n_kv <= 0 || n_heads % n_kv ||
+      qkv->n < (n_heads + 2 * n_kv) * head_dim)
+    return CHOREO_EINVAL;
+  if (n_rows == 0) return CHOREO_OK;
+  const int64_t total = (int64_t)n_rows * (n_heads + 2 * n_kv) * (head_dim / 2);
+  const int blocks = grid_for(total, 256);
+  auto s = as_stream(stream);
+  if (pool_dtype == CHOREO_BF16)
+    launch_k(rope_append_kernel<float, __nv_bfloat16>, blocks, 256, 0, s, qkv->y, qkv->n, n_rows, 0,
+             pos, dst_page, dst_slot, q_out, (__nv_bfloat16*)k_pool, (__nv_bfloat16*)v_pool, layer,
+             n_kv, n_pages, page_size, n_heads, head_dim, cos_t, sin_t, max_delta, *qkv);
+  else
+    launch_k(rope_append_kernel<float, float>, blocks, 256, 0, s, qkv->y, qkv->n, n_rows, 0, pos,
+             dst_page, dst_slot, q_out, (float*)k_pool, (float*)v_pool, layer, n_kv, n_pages,
+             page_size, n_heads, head_dim, cos_t, sin_t, max_delta, *qkv);
+  return launch_status("choreo_rope_append_pieces");
 }
 
 int choreo_rerotate(void* k_pool, int pool_dtype, int n_layers, int n_kv, int n_pages,

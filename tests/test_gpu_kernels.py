@@ -587,3 +587,76 @@ def test_linear_gate_up_silu_matches_separate(rows, split, f, d):
     if split:
         g, u = g[:rows] + g[rows:], u[:rows] + u[rows:]
     torch.testing.assert_close(a, torch.nn.functional.silu(g) * u, rtol=1e-2, atol=1e-2)
+
+
+@pytest.mark.parametrize("rows,split,grid", [(16, True, 0), (16, True, 37), (8, False, 0),
+                                             (40, False, 37), (5, True, 148)])
+def test_k7_pieces_consumers_bit_identical(rows, split, grid):
+    """Deferred K7 outputs (cut tiles left as per-CTA pieces, ChoreoK7Pieces) read through
+    RoPE/append and residual+RMSNorm give exactly the values of the reduced K7 path."""
+    import ctypes
+    H, Hk, hd, d = 8, 2, 128, 1024
+    n_qkv = (H + 2 * Hk) * hd
+    cfg = ModelConfig(n_layers=2, n_heads=H, n_kv_heads=Hk, head_dim=hd, ffn_dim=64,
+                      vocab_size=300, context_window=4096, rope_base=500000.0)
+    rot = RotationTableDevice(cfg, "cuda")
+    g = torch.Generator(device="cuda").manual_seed(rows + grid)
+    xm = torch.randn(2 * rows if split else rows, d, device="cuda", generator=g).to(torch.bfloat16)
+    ws = torch.empty(148 * 2 * 128 * 128, device="cuda")
+    st = _stream()
+    R = rows
+
+    def pieces(w):
+        y = torch.full((R, w.shape[0]), float("nan"), device="cuda")
+        cnt = torch.zeros((w.shape[0] + 127) // 128, dtype=torch.int32, device="cuda")
+        pv = nat.K7Pieces()
+        nat.linear_skinny_pieces(xm.data_ptr(), xm.shape[0], int(split), w.data_ptr(), w.shape[0],
+                                 w.shape[1], y.data_ptr(), ws.data_ptr(), cnt.data_ptr(), grid,
+                                 ctypes.addressof(pv), st)
+        assert int(cnt.abs().sum()) == 0
+        return y, pv
+
+    # qkv -> RoPE / page append
+    w = (torch.randn(n_qkv, d, device="cuda", generator=g) / d ** 0.5).to(torch.bfloat16)
+    pos = torch.randint(0, 4096, (R,), dtype=torch.int32, device="cuda")
+    flat = torch.randperm(5 * 64, device="cuda")[:R].to(torch.int32)
+    page, slot = flat // 64, flat % 64
+    outs = []
+    for mode in ("reduced", "pieces"):
+        kp = torch.zeros(2, Hk, 5, 64, hd, dtype=torch.bfloat16, device="cuda")
+        vp = torch.zeros_like(kp)
+        q = torch.empty(R, H, hd, device="cuda")
+        if mode == "reduced":
+            y = _linear(xm, split, w, grid)
+            nat.rope_append(y.data_ptr(), nat.F32, n_qkv, R, 0, pos.data_ptr(), page.data_ptr(),
+                            slot.data_ptr(), q.data_ptr(), kp.data_ptr(), vp.data_ptr(), nat.BF16, 1,
+                            Hk, 5, 64, H, hd, rot.cos.data_ptr(), rot.sin.data_ptr(), rot.max_delta, st)
+        else:
+            y, pv = pieces(w)
+            nat.rope_append_pieces(ctypes.addressof(pv), R, pos.data_ptr(), page.data_ptr(),
+                                   slot.data_ptr(), q.data_ptr(), kp.data_ptr(), vp.data_ptr(),
+                                   nat.BF16, 1, Hk, 5, 64, H, hd, rot.cos.data_ptr(),
+                                   rot.sin.data_ptr(), rot.max_delta, st)
+        torch.cuda.synchronize()
+        outs.append((q, kp, vp))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+    # o_proj / down_proj -> residual add + RMSNorm (hi/lo bf16 out)
+    w2 = (torch.randn(d, d, device="cuda", generator=g) / d ** 0.5).to(torch.bfloat16)
+    gamma = torch.rand(d, device="cuda", generator=g).to(torch.bfloat16)
+    x0 = torch.randn(R, d, device="cuda", generator=g)
+    res = []
+    for mode in ("reduced", "pieces"):
+        x = x0.clone()
+        h = torch.empty(2 * R, d, dtype=torch.bfloat16, device="cuda")
+        if mode == "reduced":
+            y = _linear(xm, split, w2, grid)
+            nat.residual_rmsnorm(x.data_ptr(), y.data_ptr(), nat.F32, 0, gamma.data_ptr(), nat.BF16,
+                                 R, d, 1e-5, h.data_ptr(), nat.BF16, 1, None, 0, st)
+        else:
+            y, pv = pieces(w2)
+            nat.residual_rmsnorm_pieces(x.data_ptr(), ctypes.addressof(pv), gamma.data_ptr(),
+                                        nat.BF16, R, d, 1e-5, h.data_ptr(), nat.BF16, 1, st)
+        torch.cuda.synchronize()
+        res.append((x, h))
+    assert torch.equal(res[0][0], res[1][0]) and torch.equal(res[0][1], res[1][1])
