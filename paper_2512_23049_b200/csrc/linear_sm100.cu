@@ -12,7 +12,9 @@
 //   * TMA producer warp with an 8-stage ring (16 KB of weights + the activation chunk per
 //     stage, ~150 KB in flight per SM), single-thread MMA issue, 4 epilogue warps;
 //   * a tile cut between CTAs is reduced deterministically: each piece is written to a
-//     per-CTA slot, the last piece to arrive sums all pieces in CTA order;
+//     per-CTA slot, the last piece to arrive sums all pieces in CTA order -- or, in the
+//     deferred mode (choreo_linear_skinny_pieces), the pieces stay in their slots and the
+//     consuming kernel sums them in the same order (k7_get, bit-identical);
 //   * with split activations (x rows r and R + r are the hi/lo halves of one row) the
 //     halves are loaded to B rows r and NX/2 + r and the epilogue adds them: y has R rows.
 // Replaces the dense projections of reference model.py:172-174, 185-189, 193 at decode
