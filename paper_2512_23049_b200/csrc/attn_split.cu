@@ -617,8 +617,9 @@ static int launch_decode(const DecodeParams& d, int grid, cudaStream_t s) {
 
 // ============================================================ combine
 // One CTA (4 warps) per (row, head): lanes own 4 head dims each (float4), warps take
-// every 4th partial slot of the row's CSR list with the loads of 4 slots in flight,
-// then the warps' numerators/denominators are merged in smem (LSE rule).
+// every 4th partial slot of the row's CSR list with the loads of 4 slots in flight and keep
+// an online (max, denominator, numerator) -- one pass over the partials, no separate max
+// pass -- then the warps' states are merged in smem (LSE rule).
 template <typename TO>
 __global__ void __launch_bounds__(128) attn_combine_kernel(
     const float* __restrict__ part_o, const float* __restrict__ part_lse,
@@ -632,66 +633,71 @@ __global__ void __launch_bounds__(128) attn_combine_kernel(
   __shared__ float s_mx[4];
   __shared__ float4 s_num[4][32];
   __shared__ float s_den[4];
-  float mx = -INFINITY;
-  for (int i = b + threadIdx.x; i < e; i += blockDim.x)
-    mx = fmaxf(mx, part_lse[(int64_t)row_part[i] * n_heads + h]);
-  mx = warp_max(mx);
-  if (lane == 0) s_mx[warp] = mx;
-  __syncthreads();
-  mx = fmaxf(fmaxf(s_mx[0], s_mx[1]), fmaxf(s_mx[2], s_mx[3]));
   const bool active = 4 * lane < hd;
   float4 num = make_float4(0.f, 0.f, 0.f, 0.f);
-  float den = 0.f;
-  if (mx != -INFINITY) {
-    int i = b + warp;
-    for (; i + 12 < e; i += 16) {  // 4 slots per warp iteration, loads batched
-      int pi[4];
-      float l[4];
-      float4 o[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        pi[k] = row_part[i + 4 * k];
-        l[k] = part_lse[(int64_t)pi[k] * n_heads + h];
-        o[k] = active ? *reinterpret_cast<const float4*>(part_o + ((int64_t)pi[k] * n_heads + h) * hd + 4 * lane)
-                      : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float wgt = l[k] == -INFINITY ? 0.f : __expf(l[k] - mx);
-        den += wgt;
-        num.x += wgt * o[k].x;
-        num.y += wgt * o[k].y;
-        num.z += wgt * o[k].z;
-        num.w += wgt * o[k].w;
-      }
+  float den = 0.f, mx = -INFINITY;
+  auto rescale = [&](float m_new) {
+    if (m_new > mx) {
+      const float f = mx == -INFINITY ? 0.f : __expf(mx - m_new);
+      num.x *= f;
+      num.y *= f;
+      num.z *= f;
+      num.w *= f;
+      den *= f;
+      mx = m_new;
     }
-    for (; i < e; i += 4) {
-      const int pi = row_part[i];
-      const float l = part_lse[(int64_t)pi * n_heads + h];
-      if (l == -INFINITY) continue;
-      const float wgt = __expf(l - mx);
-      den += wgt;
-      if (active) {
-        const float4 o = *reinterpret_cast<const float4*>(part_o + ((int64_t)pi * n_heads + h) * hd + 4 * lane);
-        num.x += wgt * o.x;
-        num.y += wgt * o.y;
-        num.z += wgt * o.z;
-        num.w += wgt * o.w;
-      }
+  };
+  auto add = [&](float l, const float4& o) {
+    if (l == -INFINITY) return;
+    const float wgt = __expf(l - mx);
+    den += wgt;
+    num.x += wgt * o.x;
+    num.y += wgt * o.y;
+    num.z += wgt * o.z;
+    num.w += wgt * o.w;
+  };
+  int i = b + warp;
+  for (; i + 12 < e; i += 16) {  // 4 slots per warp iteration, loads batched
+    int pi[4];
+    float l[4];
+    float4 o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      pi[k] = row_part[i + 4 * k];
+      l[k] = part_lse[(int64_t)pi[k] * n_heads + h];
+      o[k] = active ? *reinterpret_cast<const float4*>(part_o + ((int64_t)pi[k] * n_heads + h) * hd + 4 * lane)
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
     }
+    rescale(fmaxf(fmaxf(l[0], l[1]), fmaxf(l[2], l[3])));
+#pragma unroll
+    for (int k = 0; k < 4; ++k) add(l[k], o[k]);
+  }
+  for (; i < e; i += 4) {
+    const int pi = row_part[i];
+    const float l = part_lse[(int64_t)pi * n_heads + h];
+    const float4 o = active ? *reinterpret_cast<const float4*>(part_o + ((int64_t)pi * n_heads + h) * hd + 4 * lane)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+    rescale(l);
+    add(l, o);
   }
   s_num[warp][lane] = num;
-  if (lane == 0) s_den[warp] = den;
+  if (lane == 0) {
+    s_den[warp] = den;
+    s_mx[warp] = mx;
+  }
   __syncthreads();
   if (warp == 0 && active) {
-    float4 t = s_num[0][lane];
-    for (int k = 1; k < 4; ++k) {
-      t.x += s_num[k][lane].x;
-      t.y += s_num[k][lane].y;
-      t.z += s_num[k][lane].z;
-      t.w += s_num[k][lane].w;
+    const float M = fmaxf(fmaxf(s_mx[0], s_mx[1]), fmaxf(s_mx[2], s_mx[3]));
+    float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+    float dsum = 0.f;
+    for (int k = 0; k < 4; ++k) {
+      const float f = s_mx[k] == -INFINITY ? 0.f : __expf(s_mx[k] - M);
+      t.x += f * s_num[k][lane].x;
+      t.y += f * s_num[k][lane].y;
+      t.z += f * s_num[k][lane].z;
+      t.w += f * s_num[k][lane].w;
+      dsum += f * s_den[k];
     }
-    const float dsum = s_den[0] + s_den[1] + s_den[2] + s_den[3];
     const float inv = dsum > 0.f ? 1.f / dsum : 0.f;
     const float y[4] = {t.x * inv, t.y * inv, t.z * inv, t.w * inv};
     const int64_t oi = ((int64_t)r * n_heads + h) * hd + 4 * lane;
