@@ -112,7 +112,7 @@ __device__ __forceinline__ void st4_split(void* out, int dt, int64_t i_hi, int64
 }
 
 template <int CH>
-__global__ void residual_rmsnorm_vec(float* __restrict__ x, const float* __restrict__ delta,
+__global__ void __launch_bounds__(1024) residual_rmsnorm_vec(float* __restrict__ x, const float* __restrict__ delta,
                                      int delta_split, int n_rows, const void* __restrict__ w,
                                      int w_dt, int d, float eps, void* __restrict__ out, int out_dt,
                                      int out_split, const int32_t* __restrict__ row_map,
@@ -141,7 +141,7 @@ __global__ void residual_rmsnorm_vec(float* __restrict__ x, const float* __restr
       if (delta) {
         float4 a;
         if (pv.ws)
-          choreo::k7_get<4>(pv, r, 4 * i, &a.x);  // deferred K7 output
+          choreo::k7_get<4, 2>(pv, r, 4 * i, &a.x);  // deferred K7 output
         else
           a = ld4(delta + (int64_t)r * d + 4 * i);
         float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
