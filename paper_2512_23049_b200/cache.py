@@ -253,6 +253,24 @@ class DeviceKvCache:
         self._views = None
         return pages, slots
 
+    def release_prefix_pages(self, message_id: int, n_tokens: int) -> int:
+        """Return the pages holding only tokens [0, n_tokens) of a message to the pool (the
+        re-encoding comparator's dead prompt copies).  The message must never be read
+        below n_tokens again; its page-table entries for them become -1.  Returns the
+        number of pages released."""
+        e = self._entry(message_id)
+        P = self.page_size
+        n = len(e.pages) if n_tokens >= e.length else n_tokens // P
+        freed = 0
+        for i in range(n):
+            if e.pages[i] >= 0:
+                self._free.append(e.pages[i])
+                e.pages[i] = -1
+                self.page_table.set(e.pt + i, -1)
+                self.token_count -= min(P, e.length - i * P)
+                freed += 1
+        return freed
+
     def _relocate_chain(self, e: _Entry, cap: int) -> None:
         e.pt, e.pt_cap = self._pt_next, cap
         self._pt_next += cap

@@ -367,10 +367,23 @@ class Engine:
             active = [s for s in states if not s.done and pending[s.mid]]
             if not active:
                 return
+            # capacity for the whole step first: the reference runs the step's forward and
+            # then appends message by message, so the messages before the first one that
+            # does not fit get their K/V and the append of that one raises (cache.py:114-117,
+            # engine.py:430-433).  Same here: encode the prefix that fits, then raise.
+            room = self.cache.capacity - self.cache.token_count
+            n_fit = 0
+            for s in active:
+                if len(pending[s.mid]) > room:
+                    break
+                room -= len(pending[s.mid])
+                n_fit += 1
+            if n_fit < len(active):
+                self._encode_only(active[:n_fit], pending)
+                self._check_capacity(len(pending[active[n_fit].mid]))
             calls, logit_rows, owners, r = [], [], [], 0
             for s in active:
                 toks = pending[s.mid]
-                self._check_capacity(len(toks))
                 first = s.appended
                 pages, slots = self.cache.reserve_slots(s.mid, toks)
                 calls.append(CallRows(s.mid, s.parents, first, toks, pages, slots, s.new_off))
@@ -455,6 +468,19 @@ class Engine:
                 pending[s.mid] = [tok]
                 if len(s.generated) >= s.call.sampling.max_tokens:
                     s.finishing = True
+
+    def _encode_only(self, states: list, pending: dict) -> None:
+        """Encode (append) the pending tokens of `states` without selecting: the part of a
+        step that precedes a capacity failure."""
+        calls = []
+        for s in states:
+            toks = pending[s.mid]
+            pages, slots = self.cache.reserve_slots(s.mid, toks)
+            calls.append(CallRows(s.mid, s.parents, s.appended, toks, pages, slots, s.new_off))
+            s.appended += len(toks)
+            pending[s.mid] = []
+        if calls:
+            self._runner.forward(StepPlan(calls, np.zeros(0, np.int32)))
 
     def _may_accept(self, s: _Dec) -> bool:
         """engine.py:394-399."""

@@ -122,6 +122,40 @@ def plan_counts(calls: list, msg_len: np.ndarray, P: int, rpb: int, ppi: int,
     return Plan(n_vis, n_blk, n_items, n_parts, max_row, item_pages)
 
 
+K3_MAX_CALLS = 1024  # assemble.cu kMaxCalls
+K3_MAX_PAIRS = 4096  # assemble.cu kMaxPairs (page-centric mode)
+K3_MAX_PARENT_ID = (1 << 21) - 1  # parent ids are packed as (parent << 11 | call)
+
+
+def split_plan(plan: StepPlan) -> list:
+    """Cut a step into [(sub-plan, per-call mode)] pieces that fit K3's limits.
+
+    Greedy in call order (the logit rows stay in call order, so the pieces' logits
+    concatenate to the step's).  A piece takes the per-call mode when one of its calls
+    alone has more than K3_MAX_PAIRS parents or a parent id does not fit the sort key."""
+    calls = plan.calls
+    pairs = [len(c.parents) for c in calls]
+    big_id = any(p > K3_MAX_PARENT_ID for c in calls for p in c.parents)
+    if len(calls) <= K3_MAX_CALLS and sum(pairs) <= K3_MAX_PAIRS:
+        return [(plan, big_id)]
+    starts = np.cumsum([0] + [len(c.tokens) for c in calls])
+    logit_rows = np.asarray(plan.logit_rows, np.int64)
+    out, i = [], 0
+    while i < len(calls):
+        j, npair = i, 0
+        while (j < len(calls) and j - i < K3_MAX_CALLS
+               and (j == i or npair + pairs[j] <= K3_MAX_PAIRS)):
+            npair += pairs[j]
+            j += 1
+        lo, hi = starts[i], starts[j]
+        sel = logit_rows[(logit_rows >= lo) & (logit_rows < hi)] - lo
+        percall = npair > K3_MAX_PAIRS or any(
+            p > K3_MAX_PARENT_ID for c in calls[i:j] for p in c.parents)
+        out.append((StepPlan(calls[i:j], sel.astype(np.int32)), percall))
+        i = j
+    return out
+
+
 class Runner:
     """Executes StepPlans for one (weights, cache) pair on the current stream."""
 
@@ -172,6 +206,9 @@ class Runner:
         # GEMM its programmatic-launch overlap, so these times are conservative.
         self.time_linear = False
         self.linear_times: list = []
+        # synchronise after K3 and check its overflow flag (tests set CHOREO_CHECK_ASSEMBLY=1;
+        # the host sizes every buffer from plan_counts, so a flag here is a planner bug)
+        self.check_assembly = os.environ.get("CHOREO_CHECK_ASSEMBLY", "0") == "1"
 
     def _weight_ptrs(self):
         if self._wptrs is None:
@@ -318,7 +355,27 @@ class Runner:
         self._k7_cnt = torch.zeros(cdiv(n_max, 128) + 1, dtype=torch.int32, device=self.dev)
 
     def forward(self, plan: StepPlan) -> torch.Tensor | None:
-        """Run one step; returns f32 logits [n_logit_rows, V] or None."""
+        """Run one step; returns f32 logits [n_logit_rows, V] or None.
+
+        K3 (assemble.cu) plans a step in one CTA with fixed shared-memory tables: at most
+        K3_MAX_CALLS calls and, page-centric, K3_MAX_PAIRS (parent, call) pairs with parent
+        ids < 2^21.  A step beyond those limits is cut here, on the host and before any
+        launch, into sub-steps that each fit; the calls of one step never see each other
+        (batch peers are invisible, reference masking.py:77-79), so running them as
+        consecutive sub-steps gives the same K/V and logits.  A single call with more
+        than K3_MAX_PAIRS parents runs with per-call page lists (mode 1), which have no
+        pair limit."""
+        chunks = split_plan(plan)
+        if len(chunks) == 1:
+            return self._forward_one(plan, force_percall=chunks[0][1])
+        out = []
+        for sub, percall in chunks:
+            lg = self._forward_one(sub, force_percall=percall)
+            if lg is not None:
+                out.append(lg)
+        return torch.cat(out) if out else None
+
+    def _forward_one(self, plan: StepPlan, force_percall: bool = False) -> torch.Tensor | None:
         cfg, cache = self.cfg, self.cache
         stream = torch.cuda.current_stream(self.dev).cuda_stream
         R = plan.n_rows
@@ -346,7 +403,7 @@ class Runner:
         use_k4 = (self.pool_dtc == nat.BF16 and P == 64 and hd in (64, 128) and G <= 128
                   and max(len(c.tokens) for c in plan.calls) >= 64
                   and os.environ.get("CHOREO_PREFILL_K4", "1") != "0")
-        mode0 = max(len(c.tokens) for c in plan.calls) < 64
+        mode0 = max(len(c.tokens) for c in plan.calls) < 64 and not force_percall
         # decode-sized bf16 steps: K5 v2 (TMA page ring, <= 32 query vectors per item)
         v2 = (not use_k4 and mode0 and self.pool_dtc == nat.BF16 and P == 64
               and hd in (64, 128) and G <= 32 and os.environ.get("CHOREO_K5V2", "1") != "0")
@@ -354,7 +411,7 @@ class Runner:
         # pages per item: about two waves of (2 CTAs/SM x 148 SMs) per layer, and at
         # most 512 partials per row for the combine
         # prefill-sized steps: per-call page lists (a row block already fills an M tile)
-        mode = 1 if max(len(c.tokens) for c in plan.calls) >= 64 else 0
+        mode = 1 if max(len(c.tokens) for c in plan.calls) >= 64 or force_percall else 0
         # decode-sized bf16 steps: fused K5 (fat items, in-kernel combine)
         fused = (not use_k4 and not v2 and mode == 0 and self.pool_dtc == nat.BF16 and P == 64
                  and hd in (64, 128) and rpb <= 16
@@ -425,6 +482,11 @@ class Runner:
                      plan_.n_vis, plan_.n_blk_rows, n_items, n_parts, mode, nat.ptr(fat), stream)
         self.launches += 1
         self.last_assembly = (vis, blk_rows, items, row_part_off, row_part, counts, plan_, rowt_d)
+        if self.check_assembly:  # debug/test: K3 must never report an overflow
+            c = counts.cpu().tolist()
+            if c[3] != 0 or c[1] != n_items:
+                raise nat.NativeError(f"choreo_assemble overflow: counts {c}, planned items "
+                                      f"{n_items}")
 
         S = 2 if self.split else 1  # stacked hi/lo activation rows
         sp = int(self.split)

@@ -18,7 +18,11 @@ workflow (weights are read once per step instead of once per workflow).
 
 Semantics are unchanged: a message's tokens depend only on its own tokens and its
 parents (reference masking.py:36-40), and workflows never share messages unless the
-caller makes them, so each workflow gets exactly what it would get alone.  Calls are
+caller makes them, so each workflow's greedy and teacher-forced tokens and logits are
+exactly what it would get alone.  Message ids (and so the physical cache layout) are
+allocated across the merged calls, and temperature sampling draws its Philox counter from
+the message id (reference engine.py:388-392), so sampled tokens are a valid draw but not
+the solo run's draw.  Calls are
 validated by the engine before any mutation; if merging makes two workflows place a
 shared parent at different offsets (``OffsetConflictError``) the tick falls back to one
 engine call per workflow.

@@ -14,12 +14,18 @@ tests/golden/ and is small:
   ref_baseline_runs.json  the same scripts through the reference BaselineEngine
   ref_baseline_logits.npz (re-encoding comparator, f64 weights): traces with its
                           cost counters (flops, tokens encoded, trie hits) + logits
+  ref_sampling_runs.json  temperature / top-p runs of the scripts with free decodes,
+  ref_sampling_logits.npz f64 weights, three (temperature, top_p, seed) settings: the
+                          reference's sampled tokens and the logits each selection saw
+                          (engine.py:374-392 -- pins K6b and the oracle's nucleus())
+  ref_trace_branching.jsonl  a trace file written by the reference's Trace.to_jsonl
 
 variants: "f64"  = init_weights(DEFAULT_CONFIG) as the reference builds it;
           "bf16" = the same weights rounded to bfloat16 (RNE) and upcast, the
                    weight set both sides share for the bf16 GPU parity runs.
 
-Usage:  python tests/golden/make_golden.py
+Usage:  python tests/golden/make_golden.py [part ...]   (parts: core sampling trace;
+        default all)
 """
 
 from __future__ import annotations
@@ -131,7 +137,45 @@ def run_baseline() -> tuple[dict, dict]:
     return runs, logits
 
 
+SAMPLING_SCRIPTS = ["branching", "bsm", "conversation", "maditer", "tot"]
+SAMPLING_SETTINGS = [(0.7, 0.95, 1), (1.3, 0.5, 2), (0.9, 1.0, 3)]
+
+
+def run_sampling() -> tuple[dict, dict]:
+    """The scripts with free decodes, every decode sampled with temperature + top-p."""
+    weights = ref_weights("f64")
+    runs, logits = {}, {}
+    for t, top_p, seed in SAMPLING_SETTINGS:
+        for name in SAMPLING_SCRIPTS:
+            script = json.loads((REF / "fixtures" / "scripts" / f"{name}.json").read_text())
+            script["sampling"] = dict(script.get("sampling", {}), mode="temperature",
+                                      temperature=t, top_p=top_p, seed=seed)
+            key = f"{name}@T{t}_p{top_p}_s{seed}"
+            eng = Engine(weights, seed=0, record_logits=True)
+            trace = run_script(eng, script)
+            runs[key] = {"script": name, "sampling": script["sampling"],
+                         "steps": _trace_steps(trace, key, logits)}
+    return runs, logits
+
+
+def write_ref_trace() -> None:
+    """A trace file in the reference's own jsonl layout (read by tests/test_script_cpu)."""
+    script = json.loads((REF / "fixtures" / "scripts" / "branching.json").read_text())
+    eng = Engine(ref_weights("f64"), seed=0, record_logits=True)
+    run_script(eng, script).to_jsonl(HERE / "ref_trace_branching.jsonl")
+
+
 def main() -> None:
+    parts = set(sys.argv[1:]) or {"core", "sampling", "trace"}
+    if "sampling" in parts:
+        runs, logits = run_sampling()
+        (HERE / "ref_sampling_runs.json").write_text(json.dumps(runs, sort_keys=True) + "\n")
+        np.savez_compressed(HERE / "ref_sampling_logits.npz", **logits)
+        print("sampling selections:", sum(len(v) for v in logits.values()))
+    if "trace" in parts:
+        write_ref_trace()
+    if "core" not in parts:
+        return
     (HERE / "scripts").mkdir(exist_ok=True)
     for name in SCRIPTS:
         shutil.copyfile(REF / "fixtures" / "scripts" / f"{name}.json",

@@ -195,3 +195,22 @@ def test_tensor_core_paths_long_prompt_bf16():
     assert base.stats[2].cache_hit_tokens == len(frame_message(text)) + 2
     for g, c in zip(res["baseline"], res["choreo"]):
         assert float(np.abs(g - c).max()) <= 2e-2
+
+
+@pytest.mark.parametrize("prefix_cache", [True, False])
+def test_storage_is_bounded_by_distinct_tokens(prefix_cache):
+    """re-encoded prompts must not accumulate.  300 decodes that re-read the same
+    ~200-token prompt (≈ 70K re-encoded tokens, past the old 64K store limit) neither raise
+    CapacityError nor grow the pool: after the first, every decode's pages go back."""
+    eng = BaselineEngine(_weights(), prefix_cache=prefix_cache)
+    ids = [eng.prefill(P.PrefillCall(t * 20)) for t in ("abcd ", "efgh ")]
+    first = None
+    for i in range(300):
+        m = eng.decode(P.DecodeCall("Q:", parents=ids, sampling=P.SamplingParams(max_tokens=4)))
+        if first is None:
+            first = eng.generated_token_ids(m)
+            pages_after_first = eng.store.n_pages - len(eng.store._free)
+        assert eng.generated_token_ids(m) == first
+    assert eng.store.n_pages - len(eng.store._free) == (pages_after_first if prefix_cache else 0)
+    assert eng.stats[-1].cache_hit_tokens == (len(frame_message("abcd " * 20)) * 2
+                                              + len(frame_header("Q:")) - 1 if prefix_cache else 0)

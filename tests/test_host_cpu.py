@@ -222,3 +222,39 @@ def test_config_roundtrip_and_presets():
     assert P.ModelConfig.from_dict(cfg.to_dict()) == cfg
     with pytest.raises(ValueError):
         P.ModelConfig(n_heads=6, n_kv_heads=4)
+
+
+def _rows(msg, parents, n_tok):
+    return CallRows(msg, list(parents), 0, [1] * n_tok, np.zeros(n_tok, np.int32),
+                    np.zeros(n_tok, np.int32), 0)
+
+
+def test_split_plan_respects_k3_limits():
+    """Steps past K3's 1024 calls / 4096 page-centric pairs are cut in call order; the logit
+    rows are remapped per piece and concatenate back to the step's (model.split_plan)."""
+    from paper_2512_23049_b200.model import (K3_MAX_CALLS, K3_MAX_PAIRS, StepPlan,
+                                             split_plan)
+    rng = np.random.default_rng(0)
+    for n_calls, max_par in ((64, 70), (1030, 0), (3000, 5), (10, 4200), (5, 3)):
+        calls = [_rows(1_000_000 + i, rng.choice(9000, int(rng.integers(0, max_par + 1)),
+                                                 replace=False), int(rng.integers(1, 4)))
+                 for i in range(n_calls)]
+        n_rows = sum(len(c.tokens) for c in calls)
+        lr = np.sort(rng.choice(n_rows, min(n_rows, 200), replace=False)).astype(np.int32)
+        pieces = split_plan(StepPlan(calls, lr))
+        assert [c for p, _ in pieces for c in p.calls] == calls
+        base, got = 0, []
+        for p, percall in pieces:
+            pairs = sum(len(c.parents) for c in p.calls)
+            assert len(p.calls) <= K3_MAX_CALLS
+            assert percall == (pairs > K3_MAX_PAIRS)
+            if percall:
+                assert len(p.calls) == 1
+            got += (np.asarray(p.logit_rows) + base).tolist()
+            base += p.n_rows
+        assert got == lr.tolist()
+        if n_calls <= K3_MAX_CALLS and sum(len(c.parents) for c in calls) <= K3_MAX_PAIRS:
+            assert len(pieces) == 1
+    # parent ids past the 21-bit sort key take per-call lists
+    (p, percall), = split_plan(StepPlan([_rows(1, [1 << 21], 1)], np.zeros(1, np.int32)))
+    assert percall

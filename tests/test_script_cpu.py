@@ -87,3 +87,71 @@ def test_cli_diff_exit_codes(tmp_path, capsys):
     b.to_jsonl(pb)
     assert main(["diff", str(pa), str(pb)]) == 1
     assert "difference" in capsys.readouterr().out
+
+
+REF_TRACE = os.path.join(GOLD, "ref_trace_branching.jsonl")
+
+
+def test_reads_a_trace_written_by_the_reference(tmp_path):
+    """tests/golden/ref_trace_branching.jsonl was written by the reference's own
+    Trace.to_jsonl (make_golden.py `trace`): it loads, equals the recorded run, and our
+    writer reproduces its layout key for key (so the reference's `diff` reads ours)."""
+    tr = Trace.from_jsonl(REF_TRACE)
+    assert tr.script_name == "branching" and tr.meta == {}
+    assert diff_traces(tr, _trace()) == []
+    assert tr.steps[-1].logits  # recorded logits come back
+    p = tmp_path / "ours.jsonl"
+    tr.to_jsonl(p)
+    ref_lines = [json.loads(x) for x in open(REF_TRACE)]
+    our_lines = [json.loads(x) for x in open(p)]
+
+    def keys(d):
+        return {k: (keys(v) if isinstance(v, dict) and k != "logits" else
+                    [keys(m) for m in v] if k == "messages" else None) for k, v in d.items()}
+    assert [keys(d) for d in our_lines] == [keys(d) for d in ref_lines]
+    assert diff_traces(Trace.from_jsonl(p), tr, compare_logits=True, atol=0.0) == []
+
+
+@pytest.mark.parametrize("text", ["", "not json\n", '{"kind": "other"}\n',
+                                  '{"kind": "trace"}\n',
+                                  '{"kind": "trace", "script": "s", "engine": "e", "seed": 0}\n'
+                                  '{"index": 0}\n'])
+def test_malformed_trace_raises_script_error(tmp_path, text):
+    from paper_2512_23049_b200.errors import ScriptError
+    p = tmp_path / "bad.jsonl"
+    p.write_text(text)
+    with pytest.raises(ScriptError):
+        Trace.from_jsonl(p)
+
+
+@pytest.mark.parametrize("mutate", [
+    lambda s: s.update(name=""),
+    lambda s: s.update(steps=[]),
+    lambda s: s["steps"][0].update(name=""),
+    lambda s: s["steps"][0].update(op="encode"),
+    lambda s: s["steps"][0].update(content=5),
+    lambda s: s["steps"][1].update(parents=["nope"]),
+    lambda s: s["steps"][1].update(parents="u1"),
+    lambda s: s["steps"][1].update(offsets=[0, 1]),
+    lambda s: s["steps"][1].update(offsets=["0"]),
+    lambda s: s["steps"][1].update(new_offset=1.5),
+    lambda s: s["steps"][1].update(sampling={"temp": 1}),
+    lambda s: s["steps"][1].update(force=[1, "a"]),
+    lambda s: s.update(sampling=[]),
+    lambda s: s["steps"].append(dict(s["steps"][0])),
+    lambda s: s["steps"].append({"name": "par", "op": "decode_parallel", "calls": []}),
+    lambda s: s["steps"].append({"name": "par", "op": "decode_parallel",
+                                 "calls": [{"name": "x", "header": "h"},
+                                           {"name": "x", "header": "h"}]}),
+])
+def test_validate_script_rejects_malformed_scripts_up_front(mutate):
+    """The reference's script checks (script.py:39-123): every malformed script raises
+    ScriptError before any engine call."""
+    from paper_2512_23049_b200.errors import ScriptError
+    from paper_2512_23049_b200.script import validate_script
+    script = json.load(open(os.path.join(GOLD, "scripts", "branching.json")))
+    validate_script(copy.deepcopy(script))
+    assert script["steps"][1].get("parents")
+    mutate(script)
+    with pytest.raises(ScriptError):
+        validate_script(script)
