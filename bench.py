@@ -11,19 +11,23 @@ U(256, 512) (bench.py run_pair protocol, src/bench.py:94-109) so every run does
 identical work.  Weights: random-init Llama-3.1-8B shape, bf16, drawn on device.
 
 Reported (rank 0, one JSON line):
-  value    decode tokens/s over the timed workflows, device-busy time: the sum of
-           CUDA-event durations of every forward step (inputs staged in HBM; host
-           gaps between steps excluded).
-  e2e      the same tokens / CUDA-event time of the whole workflows through the
-           public Engine API (host strings and host token lists in, H2D of each
-           step's token/page metadata and D2H of results inside the timed region).
-  ttft_p50_ms  per-message TTFT (decode_parallel call start -> first token), p50.
-  roofline decode attention kernel (K5 split) vs measured HBM bandwidth.
-  cpu_baseline  the CPU oracle (NumPy restatement of the reference) on this host.
-  reencode_baseline  one instance of the same debate through the device
-           BaselineEngine (the paper's re-encoding comparator): TTFT and decode rate
-           beside ours on the same GPU and weights.
-  kernel_rooflines  K2 / K4 / K5 microbenchmarks (tools/kernel_bench.py).
+  value    teacher-forced arm: decode tokens/s over the timed workflows, device-busy
+           time (the sum of CUDA-event durations of every forward step).
+  e2e      free-running arm: the same debates with greedy replies (K6 argmax on the
+           device, each step's tokens read back to the host) through the public Engine
+           API, tokens / CUDA-event time of the whole workflows; H2D of each step's
+           metadata and D2H of its tokens inside the timed region (bytes declared).
+  e2e_forced  the teacher-forced arm's end-to-end rate (no per-step readback).
+  ttft_p50_ms  per-message TTFT (decode_parallel call start -> first token on the host),
+           p50, free-running arm.
+  roofline K7 (the step's dominant kernel) vs measured HBM bandwidth;
+  attention_roofline  K5 v2 the same way.
+  cpu_baseline  the reference's algorithm (CPU oracle, f64) on this host's cores, on a
+           bounded sample (CpuC3Sample; `--impl reference` is the full reference arm).
+  reencode_baseline  the same debate through the device BaselineEngine (the paper's
+           re-encoding comparator) as the reference's pair ratios.
+  kernel_rooflines  K2 / K4 / K5 / K7 microbenchmarks (tools/kernel_bench.py).
+  c1_tiny  config C1 (the reference's tiny model) on the GPU, f32.
 Multi-GPU (torchrun): each rank runs its own independent workflow instances
 (seed = rank), no collectives on the data path; value = all ranks' tokens / max
 rank time ("scaling": "weak").
@@ -70,8 +74,12 @@ def workflow_inputs(seed: int, n_agents: int, n_rounds: int):
     return sys_text, question, forced
 
 
-def run_debate(engine, P, inputs, n_agents: int, n_rounds: int) -> dict:
-    """madpar layout (workflows.py:294-327) through the public Engine API."""
+def run_debate(engine, P, inputs, n_agents: int, n_rounds: int, free: bool = False) -> dict:
+    """madpar layout (workflows.py:294-327) through the public Engine API.
+
+    free=False: replies teacher-forced to their seeded lengths (run_pair protocol);
+    free=True: replies decoded greedily (device argmax + token read back every step),
+    max_tokens = the same seeded lengths."""
     sys_text, question, forced = inputs
     sys_id = engine.prefill(P.PrefillCall(sys_text))
     q_id = engine.prefill(P.PrefillCall(question))
@@ -89,8 +97,9 @@ def run_debate(engine, P, inputs, n_agents: int, n_rounds: int) -> dict:
             calls.append(P.DecodeCall(
                 f"Agent {i + 1}:", parents=[sys_id, q_id] + others,
                 offsets=[0, engine.message_token_count(sys_id)] + [placed[m] for m in others],
-                new_offset=cursor, sampling=P.SamplingParams(max_tokens=512)))
-        prev = engine.decode_parallel(calls, force_tokens=forced[r])
+                new_offset=cursor,
+                sampling=P.SamplingParams(max_tokens=len(forced[r][i]) if free else 512)))
+        prev = engine.decode_parallel(calls, force_tokens=None if free else forced[r])
         st = engine.last_stats
         ttft += [st.ttft[m] for m in prev]
         generated += sum(len(engine.generated_token_ids(m)) for m in prev)
@@ -199,108 +208,195 @@ def measured_peaks() -> dict:
 # ---------------------------------------------------------------------------- CPU side
 
 
-def cpu_reference_sample(n_agents: int, gen_tokens: int, seed: int = 0) -> dict:
-    """Time the CPU oracle (NumPy restatement of the reference engine) on a bounded
-    sample of the workload: one round-2 decode_parallel of n_agents agents over a
-    synthetic round-1 cache (sys 64 + q 160 + n_agents replies of ~384 tokens) with
-    gen_tokens forced tokens each, at the full 8B width (GQA 32/8) and the full
-    128256-row head.  The sample runs twice, with 1 and 2 layers, so per-forward time
-    is t(L) = a + b L; results are extrapolated to L = 32 and labelled so."""
-    from oracle import choreo_oracle as O
-
-    cores = len(os.sched_getaffinity(0))
-    L_FULL = 32
-    rng = np.random.default_rng(seed)
-    base = dict(n_heads=32, n_kv_heads=8, head_dim=128, ffn_dim=14336, vocab_size=128256,
+C3_SHAPE = dict(n_heads=32, head_dim=128, ffn_dim=14336, vocab_size=128256,
                 context_window=32768, rope_base=500000.0)
-    d, dkv, f, v = 4096, 1024, 14336, 128256
-
-    def u(shp, fi, fo):
-        b = np.float32(np.sqrt(6.0 / (fi + fo)))
-        return (rng.random(shp, dtype=np.float32) * 2 - 1) * b
-
-    def layer():
-        return {"attn_norm": np.ones(d, np.float32), "wq": u((d, d), d, d),
-                "wk": u((d, dkv), d, dkv), "wv": u((d, dkv), d, dkv), "wo": u((d, d), d, d),
-                "ffn_norm": np.ones(d, np.float32), "w_gate": u((d, f), d, f),
-                "w_up": u((d, f), d, f), "w_down": u((f, d), f, d)}
-
-    shared = {"embed": u((v, d), v, d), "out_head": u((d, v), d, v),
-              "out_norm": np.ones(d, np.float32)}
-    layers = [layer(), layer()]
-    lens = [64, 160] + [int(rng.integers(256, 513)) + 10 for _ in range(n_agents)]
-    kvs = [rng.standard_normal((2, n, 8, 128), dtype=np.float32) for n in lens]
-
-    def run(n_layers: int):
-        shape = O.Shape(n_layers=n_layers, **base)
-        eng = O.Oracle(dict(shared, layers=layers[:n_layers]), shape, capacity=1 << 16)
-        st = eng.store
-        for m, n in enumerate(lens):
-            start = [0, 64][m] if m < 2 else 224
-            st.msgs[m] = O.Msg("prefilled", start, "", None)
-            st.append(m, [97] * n, np.arange(n) + start, kvs[m][:n_layers], kvs[m][:n_layers])
-        eng.next_id = len(lens)
-        prev = list(range(2, 2 + n_agents))
-        placed, cursor = {}, 224
-        for m in prev:
-            placed[m] = cursor
-            cursor += lens[m]
-        calls = []
-        for i in range(n_agents):
-            others = [m for j, m in enumerate(prev) if j != i]
-            calls.append({"header": f"Agent {i + 1}:", "parents": [0, 1] + others,
-                          "offsets": [0, 64] + [placed[m] for m in others], "new_offset": cursor,
-                          "sampling": O.Sampling(max_tokens=512)})
-        t0 = time.perf_counter()
-        eng.decode_batch(calls, [[97] * gen_tokens for _ in range(n_agents)])
-        t = time.perf_counter() - t0
-        st_ = eng.stats[-1]
-        return t, st_.tokens_encoded, sorted(st_.ttft.values())
-
-    t1, n_rows, ttft1 = run(1)
-    t2, _, ttft2 = run(2)
-    b_layer = max(t2 - t1, 0.0)
-    t_ext = t1 + (L_FULL - 1) * b_layer
-    ttft_ext = [x1 + (L_FULL - 1) * max(x2 - x1, 0.0) for x1, x2 in zip(ttft1, ttft2)]
-    # every encoded token of a parallel decode is one agent's decode step (header tokens are
-    # fed one per step by the reference), so encoded rows / time is its decode rate
-    return {"value": n_rows / t_ext, "unit": "tokens/s", "cores": cores, "kind": "port",
-            "extrapolated": True, "t_sample_s": t1 + t2,
-            "ttft_p50_ms": 1e3 * statistics.median(ttft_ext),
-            "sample": (f"oracle (NumPy f32, {cores} host threads): one round-2 decode_parallel of "
-                       f"{n_agents} agents x {gen_tokens} forced tokens (headers fed one token per "
-                       f"step, as the reference) over a synthetic {sum(lens)}-token cache, 8B width, "
-                       f"full 128256-row head, timed at 1 and 2 layers and extrapolated to 32")}
 
 
-def reference_arm(args) -> None:
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
+def _cpu_threads() -> int:
     cores = len(os.sched_getaffinity(0))
     try:  # torchrun exports OMP_NUM_THREADS=1 before numpy loads: lift it for the CPU arm
         from threadpoolctl import threadpool_limits
         threadpool_limits(limits=cores)
     except ImportError:
         pass
-    vals, ttfts, t_all = [], [], 0.0
-    for i in range(args.warmup + args.steps):
+    return cores
+
+
+class CpuC3Sample:
+    """The reference's algorithm (the CPU oracle, a NumPy restatement of reference
+    engine.py / model.py, f64 like the reference's default or f32) on a bounded sample of
+    C3: the reference has no GQA, so heads are MHA-expanded (32 KV
+    heads); full width and the full 128256-row head; one round-2 agent of the debate over
+    a synthetic round-1 cache (sys 64 + q 160 + 8 replies of U(256,512)+10 tokens), its
+    header encoded as one batch and then decode capped at the first token plus 8 steps.
+    Full depth is infeasible on the host (an 8B MHA model in f64 is ~70 GB), so the same
+    sample runs at 1 and 2 layers and t(L) = a + b L is extrapolated to L = 32
+    (labelled "extrapolated")."""
+
+    GEN = 9  # first token + 8 decode steps
+
+    def __init__(self, dtype, seed: int = 0) -> None:
+        from oracle import choreo_oracle as O
+
+        self.O, self.dtype = O, np.dtype(dtype)
+        rng = np.random.default_rng(seed)
+        d, f, v = 4096, 14336, 128256
+
+        block = (rng.random(1 << 24, dtype=np.float32) * 2 - 1).astype(self.dtype)
+
+        def u(shp, fi, fo):
+            # the scaled-uniform bounds of init_weights over a tiled random block: the values
+            # do not change the timing, and drawing ~1G fresh values would take ~30 s
+            return np.resize(block, shp) * np.sqrt(6.0 / (fi + fo))
+
+        def layer():
+            return {"attn_norm": np.ones(d, self.dtype), "wq": u((d, d), d, d),
+                    "wk": u((d, d), d, d), "wv": u((d, d), d, d), "wo": u((d, d), d, d),
+                    "ffn_norm": np.ones(d, self.dtype), "w_gate": u((d, f), d, f),
+                    "w_up": u((d, f), d, f), "w_down": u((f, d), f, d)}
+
+        self.w = {"embed": u((v, d), v, d), "out_head": u((d, v), d, v),
+                  "out_norm": np.ones(d, self.dtype), "layers": [layer(), layer()]}
+        self.lens = [64, 160] + [int(rng.integers(256, 513)) + 10 for _ in range(8)]
+        self.kv = [rng.standard_normal((2, n, 32, 128), dtype=np.float32).astype(self.dtype)
+                   for n in self.lens]
+
+    def _engine(self, n_layers: int):
+        O = self.O
+        shape = O.Shape(n_layers=n_layers, **C3_SHAPE)  # n_kv_heads None: MHA, as the reference
+        eng = O.Oracle(dict(self.w, layers=self.w["layers"][:n_layers]), shape, capacity=1 << 13)
+        st, cursor = eng.store, 224
+        for m, n in enumerate(self.lens):
+            start = [0, 64][m] if m < 2 else cursor
+            cursor += n if m >= 2 else 0
+            st.msgs[m] = O.Msg("prefilled", start, "", None)
+            kv = self.kv[m][:n_layers]
+            st.append(m, [97] * n, np.arange(n) + start, kv, kv)
+        eng.next_id = len(self.lens)
+        call = {"header": "Agent 1:", "parents": list(range(len(self.lens) - 1)),
+                "offsets": [st.msgs[m].offset for m in range(len(self.lens) - 1)],
+                "new_offset": cursor, "sampling": O.Sampling(max_tokens=self.GEN)}
+        return eng, call
+
+    def run(self, n_layers: int) -> tuple:
+        """(seconds, generated tokens, TTFT seconds) of the sample at n_layers."""
+        eng, call = self._engine(n_layers)
         t0 = time.perf_counter()
-        res = cpu_reference_sample(args.agents, args.ref_tokens, seed=i)
+        m = eng.decode(call, [97] * self.GEN)
+        t = time.perf_counter() - t0
+        return t, len(eng.generated(m)), eng.stats[-1].ttft[m]
+
+    @staticmethod
+    def extrapolate(t1: float, t2: float, L: int = 32) -> float:
+        return t1 + (L - 1) * max(t2 - t1, 0.0)
+
+    def describe(self, cores: int) -> str:
+        return (f"oracle (the reference algorithm in NumPy {self.dtype.name}, {cores} host "
+                f"threads), MHA-expanded 32 KV heads, 8B width, full 128256-row head: one "
+                f"round-2 debate agent over a {sum(self.lens)}-token synthetic cache, header "
+                f"as one batch then first token + 8 decode steps; timed at 1 and 2 layers and "
+                f"extrapolated to 32")
+
+
+def cpu_c1_full(dtype=np.float64) -> dict:
+    """Config C1 (the reference's own tiny model) at full size, no extrapolation: three
+    prefills, then the reordered / gapped / moved decode of 16 greedy tokens."""
+    from oracle import choreo_oracle as O
+
+    texts = ["System: answer the question using the notes.", "Note: the river is long.",
+             "Question: which river is long?"]
+    w = O.init_weights(O.TINY)
+    if np.dtype(dtype) != np.float64:
+        w = O.round_weights(w, "f32")
+    ttft, tps = [], []
+    for _ in range(5):
+        eng = O.Oracle(w, O.TINY)
+        for t in texts:
+            eng.prefill({"message": t})
+        t0 = time.perf_counter()
+        m = eng.decode({"header": "Answer:", "parents": [2, 0], "offsets": [0, 37],
+                        "sampling": O.Sampling(max_tokens=16)})
+        wall = time.perf_counter() - t0
+        ttft.append(eng.stats[-1].ttft[m])
+        tps.append(len(eng.generated(m)) / wall)
+    return {"ttft_p50_ms": round(1e3 * statistics.median(ttft), 3),
+            "decode_tokens_per_s": round(statistics.median(tps), 1),
+            "dtype": np.dtype(dtype).name, "extrapolated": False}
+
+
+def c1_tiny(P) -> dict:
+    """Config C1 on the GPU (f32 engine, the reference's tiny model): same protocol as
+    cpu_c1_full, so the two lines compare directly."""
+    import torch
+
+    w = P.DeviceWeights.from_host(P.init_weights(P.DEFAULT_CONFIG), dtype=torch.float32)
+    texts = ["System: answer the question using the notes.", "Note: the river is long.",
+             "Question: which river is long?"]
+    ttft, tps = [], []
+    for _ in range(6):
+        eng = P.Engine(w)
+        for t in texts:
+            eng.prefill(P.PrefillCall(t))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        m = eng.decode(P.DecodeCall("Answer:", parents=[2, 0], offsets=[0, 37],
+                                    sampling=P.SamplingParams(max_tokens=16)))
+        wall = time.perf_counter() - t0
+        ttft.append(eng.last_stats.ttft[m])
+        tps.append(len(eng.generated_token_ids(m)) / wall)
+    return {"ttft_p50_ms": round(1e3 * statistics.median(ttft[1:]), 3),
+            "decode_tokens_per_s": round(statistics.median(tps[1:]), 1), "dtype": "f32",
+            "tokens": eng.generated_token_ids(m)}
+
+
+def bench_config(args, world: int) -> dict:
+    """The workload both arms report (the driver compares the arms' config)."""
+    return {"workload": WORKLOAD, "model": args.model, "agents": args.agents,
+            "rounds": args.rounds, "reply_tokens": "U(256,512)",
+            "parallelism": f"replicas x{world} (independent workflows per GPU)"}
+
+
+def reference_arm(args) -> None:
+    """`--impl reference`: the reference's CPU algorithm (oracle port) on the host cores,
+    same metric / unit / config as our arm; rank 0 only."""
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    cores = _cpu_threads()
+    f64 = CpuC3Sample(np.float64)
+    rates, ttfts, t_steps = [], [], []
+    t1s, t2s = [], []
+    for i in range(args.warmup + args.steps):
+        # a step is one bounded sample; depths alternate so each step stays ~5 s
+        t0 = time.perf_counter()
+        t, gen, ttft = f64.run(1 + i % 2)
+        (t1s if i % 2 == 0 else t2s).append((t, gen, ttft))
         if i >= args.warmup:
-            vals.append(res["value"])
-            ttfts.append(res["ttft_p50_ms"])
-            t_all += time.perf_counter() - t0
-    value = statistics.median(vals)
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
+            t_steps.append(time.perf_counter() - t0)
+    t1 = statistics.median(x[0] for x in t1s)
+    t2 = statistics.median(x[0] for x in t2s) if t2s else t1
+    gen = t1s[0][1]
+    value = gen / CpuC3Sample.extrapolate(t1, t2)
+    ttft = CpuC3Sample.extrapolate(statistics.median(x[2] for x in t1s),
+                                   statistics.median(x[2] for x in t2s) if t2s else 0.0)
+    sample = f64.describe(cores)
+    del f64
+    f32 = CpuC3Sample(np.float32)
+    r1, r2 = f32.run(1), f32.run(2)
+    f32_value = r1[1] / CpuC3Sample.extrapolate(r1[0], r2[0])
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "tokens/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * t_all / max(1, args.steps), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "ttft_p50_ms": statistics.median(ttfts),
-            "config": {"workload": WORKLOAD, "sample": res["sample"]},
-            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
-                             "sample": res["sample"]},
-            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+            "ms_per_step": round(1e3 * statistics.mean(t_steps), 1), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "ttft_p50_ms": round(1e3 * ttft, 1),
+            "config": bench_config(args, args.gpus),
+            "extrapolated": True,
+            "cpu_baseline": {"value": round(value, 4), "unit": "tokens/s", "cores": cores,
+                             "kind": "port", "sample": sample},
+            "f32": {"value": round(f32_value, 4), "unit": "tokens/s",
+                    "ttft_p50_ms": round(1e3 * CpuC3Sample.extrapolate(r1[2], r2[2]), 1),
+                    "sample": f32.describe(cores)},
+            "c1_tiny_full": cpu_c1_full(),
+            "e2e": {"value": round(value, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -308,29 +404,44 @@ def reference_arm(args) -> None:
 # ---------------------------------------------------------------------------- GPU side
 
 
-def reencode_baseline(P, weights, inputs, args, choreo_ttft, choreo_tps) -> dict:
+def reencode_baseline(P, weights, inputs, args, choreo_eng) -> dict:
     """The paper's comparison on the same GPU and weights: one instance of the same
     debate through the re-encoding BaselineEngine (parents concatenated in list order
     and re-encoded per call behind an exact prefix trie, decode_parallel sequential,
-    reference baseline.py) — TTFT and decode rate beside the choreographed engine's."""
+    reference baseline.py) and through the choreography engine, reported as the
+    reference's pair ratios (baseline over choreography: mean TTFT, FLOPs, wall;
+    reference bench.py:138-149)."""
     import torch
 
-    eng = P.BaselineEngine(weights, capacity=1 << 17)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    res = run_debate(eng, P, inputs, args.agents, args.rounds)
-    torch.cuda.synchronize()
-    wall = time.perf_counter() - t0
+    def one(eng):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = run_debate(eng, P, inputs, args.agents, args.rounds)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        flops = {k: sum(getattr(s_, k) for s_ in eng.stats)
+                 for k in ("prefill_flops", "decode_flops")}
+        return res, wall, flops
+
+    choreo_eng.reset()
+    rc, wall_c, fc = one(choreo_eng)
+    eng = P.BaselineEngine(weights)
+    rb, wall_b, fb = one(eng)
     hits = sum(s.cache_hit_tokens for s in eng.stats)
     enc = sum(s.tokens_encoded for s in eng.stats)
-    p50 = statistics.median(res["ttft"])
     out = {"engine": "BaselineEngine (device, re-encoding + prefix trie)", "workflows": 1,
-           "ttft_p50_ms": round(1e3 * p50, 3),
-           "ttft_p90_ms": round(1e3 * sorted(res["ttft"])[int(0.9 * (len(res["ttft"]) - 1))], 3),
-           "decode_tokens_per_s": round(res["generated"] / wall, 2),
+           "ttft_p50_ms": round(1e3 * statistics.median(rb["ttft"]), 3),
+           "ttft_mean_ms": round(1e3 * statistics.mean(rb["ttft"]), 3),
+           "decode_tokens_per_s": round(rb["generated"] / wall_b, 2),
            "tokens_encoded": enc, "trie_hit_tokens": hits,
-           "ttft_p50_speedup": round(p50 / statistics.median(choreo_ttft), 2),
-           "decode_speedup_e2e": round(choreo_tps / (res["generated"] / wall), 2)}
+           "pair_ratios": {
+               "ttft": round(statistics.mean(rb["ttft"]) / statistics.mean(rc["ttft"]), 2),
+               "prefill_flops": round(fb["prefill_flops"] / max(fc["prefill_flops"], 1), 2),
+               "decode_flops": round(fb["decode_flops"] / max(fc["decode_flops"], 1), 2),
+               "total_flops": round(sum(fb.values()) / max(sum(fc.values()), 1), 2),
+               "wall": round(wall_b / wall_c, 2),
+               "definition": "baseline / choreography on the same teacher-forced debate, "
+                             "mean TTFT as the reference's pair_ratios"}}
     del eng
     torch.cuda.empty_cache()
     return out
@@ -474,7 +585,6 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--agents", type=int, default=8)
     ap.add_argument("--rounds", type=int, default=3)
-    ap.add_argument("--ref-tokens", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-kernels", action="store_true",
                     help="skip the K2/K4/K5 kernel microbenchmarks (tools/kernel_bench.py)")
@@ -528,25 +638,47 @@ def main() -> None:
     step_events, attn_events = [], []
     runner.step_events = step_events
     launches0, h2d0, d2h0 = runner.launches, runner.h2d_bytes, eng.d2h_bytes
-    ttft, generated = [], 0
+    ttft_forced, generated = [], 0
     sync_all()
     with ClockSampler(local) as clocks:
+        # arm 1, teacher-forced replies: `value` (device-busy rate) and e2e_forced
         ev_start = torch.cuda.Event(enable_timing=True)
         ev_end = torch.cuda.Event(enable_timing=True)
         ev_start.record()
         for i in range(args.steps):
             eng.reset()
             res = run_debate(eng, P, inputs[i], args.agents, args.rounds)
-            ttft += res["ttft"]
+            ttft_forced += res["ttft"]
             generated += res["generated"]
         ev_end.record()
         sync_all()
-    runner.step_events = None
-    elapsed = ev_start.elapsed_time(ev_end) / 1e3
-    busy = sum(a.elapsed_time(b) for a, b in step_events) / 1e3
-    launches = runner.launches - launches0
-    h2d = (runner.h2d_bytes - h2d0) / args.steps
-    d2h = (eng.d2h_bytes - d2h0) / args.steps
+        runner.step_events = None
+        elapsed = ev_start.elapsed_time(ev_end) / 1e3
+        busy = sum(a.elapsed_time(b) for a, b in step_events) / 1e3
+        launches = runner.launches - launches0
+        h2d_forced = (runner.h2d_bytes - h2d0) / args.steps
+        d2h_forced = (eng.d2h_bytes - d2h0) / args.steps
+        # arm 2, free-running greedy replies (K6 argmax + the tokens read back to the host
+        # every step): the headline e2e and TTFT
+        eng.reset()
+        run_debate(eng, P, inputs[0], args.agents, args.rounds, free=True)  # warm-up
+        sync_all()
+        l1, h1, d1 = runner.launches, runner.h2d_bytes, eng.d2h_bytes
+        ttft, gen_free = [], 0
+        ev_fs = torch.cuda.Event(enable_timing=True)
+        ev_fe = torch.cuda.Event(enable_timing=True)
+        ev_fs.record()
+        for i in range(args.steps):
+            eng.reset()
+            res = run_debate(eng, P, inputs[i], args.agents, args.rounds, free=True)
+            ttft += res["ttft"]
+            gen_free += res["generated"]
+        ev_fe.record()
+        sync_all()
+    elapsed_free = ev_fs.elapsed_time(ev_fe) / 1e3
+    launches += runner.launches - l1
+    h2d = (runner.h2d_bytes - h1) / args.steps
+    d2h = (eng.d2h_bytes - d1) / args.steps
     # per-kernel rooflines: one more instance of the same workflow right after the timed
     # region with CUDA events around every K5 and K7 launch (kept out of the timed region:
     # an event between two launches costs the second its programmatic-launch overlap)
@@ -556,14 +688,14 @@ def main() -> None:
     runner.attn_events, runner.time_linear = None, False
     torch.cuda.synchronize()
     if world > 1:
-        t = torch.tensor([elapsed, busy], device="cuda")
+        t = torch.tensor([elapsed, busy, elapsed_free], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed, busy = t.tolist()
-        g = torch.tensor([generated], device="cuda", dtype=torch.float64)
+        elapsed, busy, elapsed_free = t.tolist()
+        g = torch.tensor([generated, gen_free], device="cuda", dtype=torch.float64)
         dist.all_reduce(g)
-        generated_all = g.item()
+        generated_all, gen_free_all = g.tolist()
     else:
-        generated_all = generated
+        generated_all, gen_free_all = generated, gen_free
 
     # decode attention (K5) roofline, from the events of the last timed workflow
     peaks = measured_peaks()
@@ -634,7 +766,7 @@ def main() -> None:
         return
     reencode = None
     if world == 1 and not args.no_reencode:
-        reencode = reencode_baseline(P, weights, inputs[0], args, ttft, generated_all / elapsed)
+        reencode = reencode_baseline(P, weights, inputs[0], args, eng)
     kernels = None
     if world == 1 and not args.no_kernels:
         sys.path.insert(0, os.path.join(ROOT, "tools"))
@@ -647,10 +779,17 @@ def main() -> None:
     c2 = None
     if world == 1 and not args.no_c2:
         c2 = c2_agents(P, rank)
+    c1 = c1_tiny(P) if world == 1 else None
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_reference_sample(args.agents, args.ref_tokens)
-        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        cores = _cpu_threads()
+        smp = CpuC3Sample(np.float64)
+        r1, r2 = smp.run(1), smp.run(2)
+        cpu = {"value": round(r1[1] / CpuC3Sample.extrapolate(r1[0], r2[0]), 4),
+               "unit": "tokens/s", "cores": cores, "kind": "port", "extrapolated": True,
+               "ttft_p50_ms": round(1e3 * CpuC3Sample.extrapolate(r1[2], r2[2]), 1),
+               "sample": smp.describe(cores)}
+        del smp
     line = {
         "metric": METRIC, "value": round(generated_all / busy, 2), "unit": "tokens/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -658,15 +797,23 @@ def main() -> None:
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "ttft_p50_ms": round(1e3 * statistics.median(ttft), 3),
         "ttft_p90_ms": round(1e3 * sorted(ttft)[int(0.9 * (len(ttft) - 1))], 3),
-        "config": {"workload": WORKLOAD, "model": args.model, "agents": args.agents,
-                   "rounds": args.rounds, "reply_tokens": "U(256,512) teacher-forced",
-                   "weights": "random-init bf16 (device draw)", "kv_cache": "paged bf16, P=64",
-                   "activations": "split hi/lo bf16 GEMM inputs, f32 residual",
-                   "value_definition": "generated tokens / sum of per-step device time",
-                   "l2": "inputs larger than L2 (16 GB of weights streamed per step)",
-                   "parallelism": f"replicas x{world} (independent workflows per GPU)"},
-        "e2e": {"value": round(generated_all / elapsed, 2), "unit": "tokens/s",
-                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+        "config": bench_config(args, world),
+        "setup": {"weights": "random-init bf16 (device draw)", "kv_cache": "paged bf16, P=64",
+                  "activations": "split hi/lo bf16 GEMM inputs, f32 residual",
+                  "value_definition": "teacher-forced replies (U(256,512)): generated tokens / "
+                                      "sum of per-step device time",
+                  "e2e_definition": "free-running greedy replies (max_tokens = the same seeded "
+                                    "lengths): generated tokens / CUDA-event time of the whole "
+                                    "workflows through the public Engine API; every step "
+                                    "uploads its metadata (H2D) and reads its tokens back (D2H)",
+                  "l2": "inputs larger than L2 (16 GB of weights streamed per step)"},
+        "e2e": {"value": round(gen_free_all / elapsed_free, 2), "unit": "tokens/s",
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "generated_tokens": int(gen_free_all)},
+        "e2e_forced": {"value": round(generated_all / elapsed, 2), "unit": "tokens/s",
+                       "h2d_bytes_per_step": int(h2d_forced),
+                       "d2h_bytes_per_step": int(d2h_forced),
+                       "ttft_p50_ms": round(1e3 * statistics.median(ttft_forced), 3)},
         "gpu_launches": int(launches),
         "generated_tokens": int(generated_all),
         "roofline": roofline,
@@ -675,6 +822,7 @@ def main() -> None:
         "reencode_baseline": reencode,
         "c4_batched_workflows": c4,
         "c2_agents_1b": c2,
+        "c1_tiny": c1,
         "c5_tensor_parallel_70b": c5,
         "cpu_baseline": cpu,
         "clocks": clocks.summary(),

@@ -39,6 +39,7 @@ struct LinearParams {
   int silu_f;  // > 0: gate|up projection with SiLU(gate)*up fused (tile t = gate rows
                // [64t, 64t+64) over up rows [F + 64t, ...)); N counts act columns (= F)
   int defer;   // 1: cut tiles stay as pieces in ws for the consumer (ChoreoK7Pieces)
+  int stages;  // ring depth (<= LnCfg::kStages): sets the shared memory a CTA holds
 };
 
 template <int NX, int KSUB>
@@ -47,7 +48,7 @@ struct LnCfg {
   static constexpr int kXBytes = NX * 128;       // one k-block of the activations
   static constexpr int kStageBytes = KSUB * (kWBytes + kXBytes);
   static constexpr int kStages = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
-  static constexpr int kSmem = kStages * kStageBytes + 1024;
+  static constexpr int smem(int stages) { return stages * kStageBytes + 1024; }
   static constexpr int kTmemCols = 2 * NX < 32 ? 32 : 2 * NX;
 };
 
@@ -73,7 +74,7 @@ __global__ void __launch_bounds__(kLnThreads, 1)
   const int c = blockIdx.x;
   const int b = ln_begin(c, p.iters, p.grid), e = ln_begin(c + 1, p.iters, p.grid);
   if (tid == 0) {
-    for (int i = 0; i < C::kStages; ++i) {
+    for (int i = 0; i < p.stages; ++i) {
       mbar_init(&full_bar[i], 1);
       mbar_init(&empty_bar[i], 1);
     }
@@ -122,7 +123,8 @@ __global__ void __launch_bounds__(kLnThreads, 1)
       };
       // weights do not depend on the previous kernel: fill the ring with them before the
       // programmatic-dependency wait, then add the activations (written by the predecessor)
-      const int pre = min(e - b, C::kStages);
+      const int NS = p.stages;
+      const int pre = min(e - b, NS);
       for (int j = 0; j < pre; ++j) {
         mbar_arrive_expect_tx(&full_bar[j], C::kStageBytes);
         load_w(b + j, j);
@@ -130,8 +132,8 @@ __global__ void __launch_bounds__(kLnThreads, 1)
       pdl_wait();
       for (int j = 0; j < pre; ++j) load_x(b + j, j);
       for (int i = b + pre; i < e; ++i) {
-        const int j = i - b, st = j % C::kStages;
-        mbar_wait(&empty_bar[st], ((j / C::kStages) & 1) ^ 1);
+        const int j = i - b, st = j % NS;
+        mbar_wait(&empty_bar[st], ((j / NS) & 1) ^ 1);
         mbar_arrive_expect_tx(&full_bar[st], C::kStageBytes);
         load_w(i, st);
         load_x(i, st);
@@ -140,14 +142,15 @@ __global__ void __launch_bounds__(kLnThreads, 1)
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------------------------------------- MMA issuer
       constexpr uint32_t idesc = umma_idesc_bf16(kLnTile, NX, false);
+      const int NS = p.stages;
       int seg = 0;
       for (int i = b; i < e; ++i) {
-        const int j = i - b, st = j % C::kStages, kb = i % p.KB;
+        const int j = i - b, st = j % NS, kb = i % p.KB;
         const bool first = (i == b) || kb == 0;
         const bool last = (i == e - 1) || kb == p.KB - 1;
         const int buf = seg & 1;
         if (first && seg >= 2) mbar_wait(&acc_empty[buf], ((seg >> 1) - 1) & 1);
-        mbar_wait(&full_bar[st], (j / C::kStages) & 1);
+        mbar_wait(&full_bar[st], (j / NS) & 1);
         tc_fence_after();
         const uint32_t waddr = smem_addr(base + st * C::kStageBytes);
         const uint32_t xaddr = waddr + KSUB * C::kWBytes;
@@ -303,11 +306,12 @@ static int launch_linear(const LinearParams& p, const void* x, int x_rows, const
       !ln_map(&mx, x, (uint64_t)x_rows, (uint64_t)K, p.split ? NX / 2 : NX,
               CU_TENSOR_MAP_L2_PROMOTION_L2_128B))
     return CHOREO_ELAUNCH;
-  constexpr int smem = LnCfg<NX, KSUB>::kSmem;
+  using C = LnCfg<NX, KSUB>;
+  const int smem = C::smem(p.stages);
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(linear_skinny_sm100<NX, KSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         smem);
+                         C::smem(C::kStages));
     attr_set = true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -350,18 +354,30 @@ static int linear_impl(const void* x, int x_rows, int split, const void* w, int 
   const int iters = n_tiles * KB;
   int grid = grid_ctas > 0 ? grid_ctas : 148;
   if (grid > iters) grid = iters;
+  static int max_smem = -1;  // CHOREO_K7_SMEM_KB: cap the ring's shared memory (co-residency)
+  if (max_smem < 0) {
+    const char* e = getenv("CHOREO_K7_SMEM_KB");
+    max_smem = e ? atoi(e) * 1024 : 0;
+  }
   LinearParams p{reinterpret_cast<float*>(y), workspace, tile_counters, n, KB, iters, grid,
-                 split ? x_rows / 2 : x_rows, split, silu_f, pieces ? 1 : 0};
+                 split ? x_rows / 2 : x_rows, split, silu_f, pieces ? 1 : 0, 0};
   if (pieces) {
     if (silu_f) return CHOREO_EINVAL;
     *pieces = ChoreoK7Pieces{reinterpret_cast<const float*>(y), workspace, n, KB, iters, grid, NX,
                              split};
   }
   auto s = as_stream(stream);
+  auto stages_for = [&](int full, int stage_bytes) {
+    int st = full;
+    if (max_smem > 0) st = (max_smem - 1024) / stage_bytes;
+    return st < 2 ? 2 : st > full ? full : st;
+  };
+#define LN_STAGES(nx, ks) \
+  (p.stages = stages_for(LnCfg<nx, ks>::kStages, LnCfg<nx, ks>::kStageBytes), p)
 #define LN_CASE(nx)                                                                       \
-  return ksub == 1   ? launch_linear<nx, 1>(p, x, x_rows, w, n, k, s)                     \
-         : ksub == 2 ? launch_linear<nx, 2>(p, x, x_rows, w, n, k, s)                     \
-                     : launch_linear<nx, 4>(p, x, x_rows, w, n, k, s);
+  return ksub == 1   ? launch_linear<nx, 1>(LN_STAGES(nx, 1), x, x_rows, w, n, k, s)      \
+         : ksub == 2 ? launch_linear<nx, 2>(LN_STAGES(nx, 2), x, x_rows, w, n, k, s)      \
+                     : launch_linear<nx, 4>(LN_STAGES(nx, 4), x, x_rows, w, n, k, s);
   switch (NX) {
     case 16: LN_CASE(16)
     case 32: LN_CASE(32)
@@ -369,6 +385,7 @@ static int linear_impl(const void* x, int x_rows, int split, const void* w, int 
     default: LN_CASE(128)
   }
 #undef LN_CASE
+#undef LN_STAGES
 }
 
 extern "C" int choreo_linear_skinny(const void* x, int x_rows, int split, const void* w, int n,
