@@ -360,7 +360,8 @@ def run_all() -> list:
 
 if __name__ == "__main__":
     if "--k7" in sys.argv:
-        for r in k7_linear():
+        rows = int(os.environ.get("K7_ROWS", "8"))
+        for r in k7_linear(rows):
             print(json.dumps(r))
         sys.exit(0)
     if "--k5-sweep" in sys.argv:
