@@ -209,8 +209,6 @@ class Runner:
         # synchronise after K3 and check its overflow flag (tests set CHOREO_CHECK_ASSEMBLY=1;
         # the host sizes every buffer from plan_counts, so a flag here is a planner bug)
         self.check_assembly = os.environ.get("CHOREO_CHECK_ASSEMBLY", "0") == "1"
-        # wide decode-sized steps (the parallel header step) on K4's 128-vector tiles
-        self.header_k4 = os.environ.get("CHOREO_HEADER_K4", "0") == "1"
 
     def _weight_ptrs(self):
         if self._wptrs is None:
@@ -403,8 +401,7 @@ class Runner:
         # prefill-sized steps run K4 (tcgen05, 128-row M tiles); decode-sized steps K5
         G = H // Hk
         use_k4 = (self.pool_dtc == nat.BF16 and P == 64 and hd in (64, 128) and G <= 128
-                  and (max(len(c.tokens) for c in plan.calls) >= 64
-                       or (self.header_k4 and R >= 64))
+                  and max(len(c.tokens) for c in plan.calls) >= 64
                   and os.environ.get("CHOREO_PREFILL_K4", "1") != "0")
         mode0 = max(len(c.tokens) for c in plan.calls) < 64 and not force_percall
         # decode-sized bf16 steps: K5 v2 (TMA page ring, <= 32 query vectors per item)
