@@ -113,7 +113,7 @@ int choreo_rerotate(void* k_pool, int pool_dtype, int n_layers, int n_kv, int n_
  *       (group >= 0: parent group index; -1-c: own pages of call c)
  *   row_part_off[n_rows + 1], row_part[]: per-row CSR list of the partial slots to merge
  *   counts[0..3] = {n_vis_pages, n_items, n_partials, status (0 ok, <0 over capacity)}
- * fat (optional, int32 [n_items][64]): self-contained item records for choreo_decode_attn:
+ * fat (optional, int32 [n_items][64]): self-contained item records for choreo_decode_attn_v2:
  *   {n_rows, n_pages, partial base, 0, row ids[16], row_t[16], page[8], page_len[8],
  *    own_base[8], pad[4]}; requires rows_per_block <= 16 and pages_per_item <= 8.
  * mode 0 = page-centric groups (decode-sized steps); mode 1 = per-call lists (prefill-sized
@@ -135,17 +135,16 @@ int choreo_assemble(const int32_t* msg_len, const int32_t* msg_pt, int32_t* page
  * q: f32 [n_rows][n_heads][hd] (already rotated, K1).  For each item and KV head writes
  * per-(row, q-head) partials: part_o f32 [n_partials][n_heads][hd] (normalised) and
  * part_lse f32 [n_partials][n_heads] (natural-log sum-exp; -inf if nothing visible).
- * bf16 pools with page_size 64 and hd 64/128 run on tensor cores (mma.sync, cp.async
- * double-buffered page pipeline); f32 pools run the SIMT f32 path.  grid_ctas = persistent
- * CTAs (0 = auto).  flags (tensor-core path): bit 0 = Q as a hi/lo bf16 pair, bit 1 = P as
- * a hi/lo pair (each doubles that product's MMAs; 0 = plain bf16).  Replaces model.py:177-184 + tensor.py:65-75 (gather, concat, scores,
- * masked softmax, P.V). */
+ * The generic path: SIMT with f32 math over f32 or bf16 pages, any head_dim in
+ * {8,16,32,64,128}; the f32 parity variant and the shapes K4 / K5 v2 do not take run here.
+ * grid_ctas = persistent CTAs (0 = auto).  Replaces model.py:177-184 + tensor.py:65-75
+ * (gather, concat, scores, masked softmax, P.V). */
 int choreo_attn_split(const float* q, const void* k_pool, const void* v_pool, int pool_dtype,
                       int layer, int n_kv, int n_pages, int page_size, int n_heads, int head_dim,
                       const int32_t* row_t, const int32_t* vis_page, const int32_t* vis_len,
                       const int32_t* vis_own, const int32_t* blk_rows, const int32_t* items,
                       const int32_t* counts, int max_items, float* part_o, float* part_lse,
-                      int grid_ctas, int flags, void* stream);
+                      int grid_ctas, void* stream);
 
 /* K4 choreographed prefill attention on tcgen05 tensor cores (bf16 pools, page_size 64,
  * head_dim 64 or 128).  Same items / partials contract as choreo_attn_split, with items
@@ -164,20 +163,6 @@ int choreo_prefill_attn(const float* q, const void* k_pool, const void* v_pool, 
                         const int32_t* items, const int32_t* counts, int max_items, float* part_o,
                         float* part_lse, int grid_ctas, void* out, int out_split, int n_rows,
                         void* stream);
-
-/* Fused decode attention (bf16 pools, page_size 64, head_dim 64/128): K5's tensor-core
- * split-KV math over K3 fat items (one 256-byte record per item, no dependent lookups) with
- * the LSE combine fused in: each (row, kv head) has an arrival counter in row_counters
- * (int32 [n_rows * n_kv], all zero on entry, left zero on exit); the CTA that delivers a
- * row's last partial merges them and writes out[row] (bf16, hi/lo pair if out_split).
- * row_counters == NULL: partials only (run choreo_attn_combine afterwards).
- * flags as choreo_attn_split.  Replaces model.py:177-184 for decode-sized steps. */
-int choreo_decode_attn(const float* q, const void* k_pool, const void* v_pool, int layer, int n_kv,
-                       int n_pages, int page_size, int n_heads, int head_dim,
-                       const int32_t* fat_items, const int32_t* counts, int max_items,
-                       const int32_t* row_part_off, const int32_t* row_part, float* part_o,
-                       float* part_lse, int32_t* row_counters, void* out, int out_split,
-                       int n_rows, int flags, int grid_ctas, void* stream);
 
 /* Combine each row's partials (CSR row_part_off / row_part, <= 512 per row) into
  * out[r][h][:] (out_dtype; hi/lo pair if out_split) with the LSE merge. */
@@ -259,9 +244,9 @@ int choreo_linear_gate_up_silu(const void* x, int x_rows, int split, const void*
                                void* stream);
 
 /* Native decode-step executor: every layer of a decode-sized bf16 step (split hi/lo
- * activations or plain bf16; page_size 64; fused K5 items from choreo_assemble with a
- * fat buffer) issued in one call — per layer: residual_rmsnorm, K7 qkv, K1 rope_append,
- * K5 decode attention (v1 fused items or v2 TMA ring), combine, K7 o_proj, residual_rmsnorm, K7 gate|up, silu_mul,
+ * activations or plain bf16; page_size 64; K5 v2 items from choreo_assemble, page-centric
+ * mode) issued in one call — per layer: residual_rmsnorm, K7 qkv, K1 rope_append,
+ * K5 v2 decode attention, combine, K7 o_proj, residual_rmsnorm, K7 gate|up (+SwiGLU),
  * K7 down.  Replaces the per-layer loop of model.py:169-189.  Weight arrays are HOST
  * arrays of n_layers DEVICE pointers (bf16, (out, in) layout).  On return `delta` holds
  * the last layer's down_proj output (the caller adds it and runs the final norm / head).
@@ -281,7 +266,7 @@ typedef struct {
   const float* cos_t;
   const float* sin_t;
   int max_delta;
-  int n_rows, split, attn_flags, n_items;
+  int n_rows, split, n_items;
   const int32_t* pos;
   const int32_t* page;
   const int32_t* slot;
@@ -304,9 +289,7 @@ typedef struct {
   float* k7_ws;
   int* k7_cnt;
   void** attn_events;
-  /* attention kernel: 0 = choreo_decode_attn over `fat` items, 1 = choreo_decode_attn_v2
-   * over the K3 arrays below (row_t, vis_*, blk_rows, items) */
-  int attn_kernel;
+  /* K3 arrays K5 v2 reads (choreo_assemble outputs) */
   const int32_t* row_t;
   const int32_t* vis_page;
   const int32_t* vis_len;

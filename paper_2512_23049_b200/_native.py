@@ -31,10 +31,8 @@ SIGNATURES: dict[str, list] = {
     "choreo_rerotate": [_P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _I, _P, _P, _I, _P],
     "choreo_assemble": [_P, _P, _P, _P, _P, _I, _P, _I, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P,
                         _P, _P, _P, _I, _I, _I, _I, _I, _P, _P],
-    "choreo_decode_attn": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P, _I, _P, _P, _P, _P, _P, _P,
-                           _I, _I, _I, _I, _P],
     "choreo_attn_split": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P,
-                          _I, _P, _P, _I, _I, _P],
+                          _I, _P, _P, _I, _P],
     "choreo_prefill_attn": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P,
                             _P, _P, _I, _P, _P, _I, _P, _I, _I, _P],
     "choreo_attn_combine": [_P, _P, _P, _P, _I, _I, _I, _P, _I, _I, _P],
@@ -113,7 +111,6 @@ assemble = _Caller("choreo_assemble")
 attn_split = _Caller("choreo_attn_split")
 attn_combine = _Caller("choreo_attn_combine")
 prefill_attn = _Caller("choreo_prefill_attn")
-decode_attn = _Caller("choreo_decode_attn")
 select_greedy = _Caller("choreo_select_greedy")
 selftest_umma = _Caller("choreo_selftest_umma")
 linear_skinny = _Caller("choreo_linear_skinny")
@@ -133,11 +130,10 @@ class DecodeStep(ctypes.Structure):
         [(n, _P) for n in ("attn_norm", "w_qkv", "wo", "ffn_norm", "w_gu", "w_down")] + \
         [("eps", _F), ("k_pool", _P), ("v_pool", _P), ("n_pages", _I), ("page_size", _I),
          ("cos_t", _P), ("sin_t", _P), ("max_delta", _I), ("n_rows", _I), ("split", _I),
-         ("attn_flags", _I), ("n_items", _I)] + \
+         ("n_items", _I)] + \
         [(n, _P) for n in ("pos", "page", "slot", "fat", "counts", "row_part_off", "row_part",
                            "x", "delta_in", "h", "qkv", "q", "part_o", "part_lse", "attn", "ao",
                            "gu", "act", "delta", "k7_ws", "k7_cnt", "attn_events")] + \
-        [("attn_kernel", _I)] + \
         [(n, _P) for n in ("row_t", "vis_page", "vis_len", "vis_own", "blk_rows", "items",
                            "linear_events")] + \
         [(n, _I) for n in ("layer_begin", "layer_end", "part")]

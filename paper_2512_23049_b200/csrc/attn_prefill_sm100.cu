@@ -38,7 +38,6 @@ struct PrefillParams {
   float* part_o;
   float* part_lse;
   float scale_log2;
-  int* dbg;  // optional progress counters (mapped host memory) for pipeline debugging
   // When out != nullptr every row has exactly one item: the epilogue writes the final
   // normalised row out[row][head*hd + d] (bf16; hi/lo pair at rows r / n_rows + r when
   // out_split) and no partials / combine are needed.
@@ -46,13 +45,6 @@ struct PrefillParams {
   int out_split, n_rows;
 };
 
-#define PF_DBG(i, v)                                     \
-  do {                                                   \
-    if (p.dbg && blockIdx.x == 0) {                      \
-      *reinterpret_cast<volatile int*>(p.dbg + (i)) = (v); \
-      __threadfence_system();                            \
-    }                                                    \
-  } while (0)
 
 constexpr int kPfThreads = 352;     // 11 warps: TMA, MMA tile 0, 2 x 4 softmax, MMA tile 1
 constexpr int kPfMma1Warp = 10;
@@ -87,26 +79,15 @@ __device__ __forceinline__ float2 add2(float2 a, float2 b) {
   return *reinterpret_cast<float2*>(&z);
 }
 
-// 2^x on the FMA/ALU pipes only (FA4-style offload of the SFU): round x to the nearest
-// integer n with the 1.5*2^23 magic number, fit 2^f on f in [-0.5, 0.5] with a cubic
-// (max rel. error 1.4e-4 < bf16 ulp), add n to the exponent bits.
-__device__ __forceinline__ float ex2_poly(float x) {
-  x = fmaxf(x, -125.f);
-  const float t = x + 12582912.f;
-  const float f = x - (t - 12582912.f);
-  const float p = fmaf(fmaf(fmaf(0.05502927f, f, 0.24225698f), f, 0.69325305f), f, 0.99995134f);
-  return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
-}
-
 // Two query tiles per CTA (M = 2 x 128 query vectors of one KV head) share every K/V
 // page, and their MMAs ping-pong on the tensor core: while softmax warpgroup t works on
 // S_t, the tensor core runs the other tile's S / PV.  TMEM (512 columns) per tile t:
 // S double buffer at [256t, 256t+128), O at [256t+128, 256t+128+HD).  Per page g:
 //   MMA : one issuing thread per tile (warps 1 and 10), so a tile's S(g+1) goes out as
 //         soon as its PV(g-1) has, independent of the other tile's softmax progress;
-//   SMX_t: ld S_t(g), release it, exp2 (POLY of every 4 on the FMA pipe), wait PV_t(g-1),
+//   SMX_t: ld S_t(g), release it, exp2, wait PV_t(g-1),
 //          write P_t(g), lazily rescale O_t.
-template <int HD, int POLY>
+template <int HD>
 __global__ void __launch_bounds__(kPfThreads, 1)
     attn_prefill_sm100(PrefillParams p, const __grid_constant__ CUtensorMap tmK,
                        const __grid_constant__ CUtensorMap tmV) {
@@ -332,7 +313,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
 #pragma unroll
           for (int k = 0; k < kPfKeys; k += 2) {
             float2 x = add2(make_float2(s[k], s[k + 1]), nm);
-            x.x = ((k & 3) < POLY) ? ex2_poly(x.x) : ex2(x.x);
+            x.x = ex2(x.x);
             x.y = ex2(x.y);
             s[k] = x.x;
             s[k + 1] = x.y;
@@ -344,7 +325,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
 #pragma unroll
           for (int k = 0; k < kPfKeys; ++k) {
             const float x = s[k] - mrow;
-            const float e = ((k & 3) < POLY) ? ex2_poly(x) : ex2(x);
+            const float e = ex2(x);
             s[k] = k < lim ? e : 0.f;
             sm[k & 7] += s[k];
           }
@@ -449,7 +430,7 @@ static bool encode_pool_map(CUtensorMap* map, const void* pool, uint64_t rows, i
   return tmap_bf16_2d(map, pool, rows, (uint64_t)hd, 64, 64, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
 }
 
-template <int HD, int POLY>
+template <int HD>
 static int launch_prefill(const PrefillParams& p, const void* k_pool, const void* v_pool,
                           uint64_t rows, int grid, cudaStream_t s) {
   CUtensorMap mk, mv;
@@ -458,27 +439,17 @@ static int launch_prefill(const PrefillParams& p, const void* k_pool, const void
   const int smem = PfSmem<HD>::kTotal;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attn_prefill_sm100<HD, POLY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(attn_prefill_sm100<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          smem);
     attr = true;
   }
-  launch_k(attn_prefill_sm100<HD, POLY>, grid, kPfThreads, smem, s, p, mk, mv);
+  launch_k(attn_prefill_sm100<HD>, grid, kPfThreads, smem, s, p, mk, mv);
   return launch_status("choreo_prefill_attn");
 }
 
 }  // namespace choreo
 
 using namespace choreo;
-
-extern "C" int choreo_prefill_attn_dbg(const float* q, const void* k_pool, const void* v_pool,
-                                       int pool_dtype, int n_layers, int layer, int n_kv,
-                                       int n_pages, int page_size, int n_heads, int head_dim,
-                                       const int32_t* row_t, const int32_t* vis_page,
-                                       const int32_t* vis_len, const int32_t* vis_own,
-                                       const int32_t* blk_rows, const int32_t* items,
-                                       const int32_t* counts, int max_items, float* part_o,
-                                       float* part_lse, int grid_ctas, int* dbg, void* out,
-                                       int out_split, int n_rows, void* stream);
 
 extern "C" int choreo_prefill_attn(const float* q, const void* k_pool, const void* v_pool,
                                    int pool_dtype, int n_layers, int layer, int n_kv, int n_pages,
@@ -488,20 +459,6 @@ extern "C" int choreo_prefill_attn(const float* q, const void* k_pool, const voi
                                    const int32_t* items, const int32_t* counts, int max_items,
                                    float* part_o, float* part_lse, int grid_ctas, void* out,
                                    int out_split, int n_rows, void* stream) {
-  return choreo_prefill_attn_dbg(q, k_pool, v_pool, pool_dtype, n_layers, layer, n_kv, n_pages,
-                                 page_size, n_heads, head_dim, row_t, vis_page, vis_len, vis_own,
-                                 blk_rows, items, counts, max_items, part_o, part_lse, grid_ctas,
-                                 nullptr, out, out_split, n_rows, stream);
-}
-
-extern "C" int choreo_prefill_attn_dbg(const float* q, const void* k_pool, const void* v_pool,
-                                   int pool_dtype, int n_layers, int layer, int n_kv, int n_pages,
-                                   int page_size, int n_heads, int head_dim, const int32_t* row_t,
-                                   const int32_t* vis_page, const int32_t* vis_len,
-                                   const int32_t* vis_own, const int32_t* blk_rows,
-                                   const int32_t* items, const int32_t* counts, int max_items,
-                                   float* part_o, float* part_lse, int grid_ctas, int* dbg,
-                                   void* out, int out_split, int n_rows, void* stream) {
   if (!q || !k_pool || !v_pool || !row_t || !vis_page || !vis_len || !vis_own || !blk_rows ||
       !items || !counts || !part_o || !part_lse || n_kv <= 0 || n_heads % n_kv)
     return CHOREO_EINVAL;
@@ -511,24 +468,13 @@ extern "C" int choreo_prefill_attn_dbg(const float* q, const void* k_pool, const
   if (max_items <= 0) return CHOREO_OK;
   PrefillParams p{q, layer, n_kv, n_pages, page_size, n_heads, row_t, vis_page, vis_len, vis_own,
                   blk_rows, items, counts, part_o, part_lse,
-                  1.4426950408889634f / sqrtf((float)head_dim), dbg,
+                  1.4426950408889634f / sqrtf((float)head_dim),
                   reinterpret_cast<__nv_bfloat16*>(out), out_split, n_rows};
   int grid = grid_ctas > 0 ? grid_ctas : max_items * n_kv;
   if (grid > 148) grid = 148;
   const uint64_t rows = (uint64_t)n_layers * n_kv * n_pages * page_size;
   if (rows > 0x7fffffffull) return CHOREO_EUNSUPPORTED;
   auto s = as_stream(stream);
-  static int poly = -1;  // exp2 offload to the FMA pipe: elements with (k & 3) < poly
-  if (poly < 0) {
-    const char* e = getenv("CHOREO_K4_POLY");
-    poly = e ? atoi(e) : 0;
-  }
-  if (head_dim == 128) {
-    switch (poly) {
-      case 1: return launch_prefill<128, 1>(p, k_pool, v_pool, rows, grid, s);
-      case 3: return launch_prefill<128, 3>(p, k_pool, v_pool, rows, grid, s);
-      default: return launch_prefill<128, 0>(p, k_pool, v_pool, rows, grid, s);
-    }
-  }
-  return launch_prefill<64, 0>(p, k_pool, v_pool, rows, grid, s);
+  if (head_dim == 128) return launch_prefill<128>(p, k_pool, v_pool, rows, grid, s);
+  return launch_prefill<64>(p, k_pool, v_pool, rows, grid, s);
 }

@@ -7,7 +7,7 @@
 //   K7 qkv = h @ Wqkv^T                 (weights streamed; PDL prefetch under the norm;
 //                                        cut tiles left as pieces for RoPE, ChoreoK7Pieces)
 //   K1 rope_append (q rotated to f32, K/V written into the message pages)
-//   K5 decode attention over the K3 fat items (+ LSE combine)
+//   K5 v2 decode attention over the K3 page-centric items (+ LSE combine)
 //   K7 ao = attn @ Wo^T
 //   residual_rmsnorm (x += ao; h = norm(x))
 //   K7 act = silu(h @ Wg^T) * (h @ Wu^T) (SwiGLU in the epilogue) ; K7 delta = act @ Wdown^T
@@ -82,16 +82,10 @@ extern "C" int choreo_decode_layers(const ChoreoDecodeStep* s, void* stream) {
                              H, hd, s->cos_t, s->sin_t, s->max_delta, stream));
     }
     if (ev) cudaEventRecord(ev[2 * l], as_stream(stream));
-    if (s->attn_kernel == 1)
-      CHK(choreo_decode_attn_v2(s->q, s->k_pool, s->v_pool, s->n_layers, l, Hk, s->n_pages,
-                                s->page_size, H, hd, s->row_t, s->vis_page, s->vis_len, s->vis_own,
-                                s->blk_rows, s->items, s->counts, s->n_items, s->part_o,
-                                s->part_lse, s->fat, 0, stream));
-    else
-      CHK(choreo_decode_attn(s->q, s->k_pool, s->v_pool, l, Hk, s->n_pages, s->page_size, H, hd,
-                             s->fat, s->counts, s->n_items, s->row_part_off, s->row_part,
-                             s->part_o, s->part_lse, nullptr, s->attn, sp, R, s->attn_flags, 0,
-                             stream));
+    CHK(choreo_decode_attn_v2(s->q, s->k_pool, s->v_pool, s->n_layers, l, Hk, s->n_pages,
+                              s->page_size, H, hd, s->row_t, s->vis_page, s->vis_len, s->vis_own,
+                              s->blk_rows, s->items, s->counts, s->n_items, s->part_o,
+                              s->part_lse, s->fat, 0, stream));
     if (ev) cudaEventRecord(ev[2 * l + 1], as_stream(stream));
     CHK(choreo_attn_combine(s->part_o, s->part_lse, s->row_part_off, s->row_part, R, H, hd,
                             s->attn, CHOREO_BF16, sp, stream));

@@ -183,14 +183,8 @@ class Runner:
         # launching stream and (start, end, algorithmic_bytes) tuples are appended.
         self.attn_events = None
         self.step_events = None  # when a list: (start, end) events around each step's GPU work
-        self._counters = None  # fused decode arrival counters (zero between launches)
-        # in-kernel LSE combine (arrival counters) vs the separate combine kernel; the
-        # separate kernel is faster today (the in-kernel finaliser runs serially in the tail)
-        self.fused_combine = os.environ.get("CHOREO_FUSED_COMBINE", "0") == "1"
         # bf16 engines carry GEMM activations as hi/lo bf16 pairs (see choreo_b200.h)
         self.split = self.dt == torch.bfloat16 and split_activations
-        # K5 tensor-core precision: bit0 Q hi/lo, bit1 P hi/lo (env override for studies)
-        self.attn_flags = int(os.environ.get("CHOREO_ATTN_FLAGS", "3"))
         # K7 weight-streaming linear for decode-sized bf16 steps (cuBLAS above 128 GEMM rows)
         self.k7 = self.dt == torch.bfloat16 and os.environ.get("CHOREO_K7", "1") != "0"
         self._k7_ws = self._k7_cnt = None
@@ -257,7 +251,16 @@ class Runner:
     def _mm(self, a, w, out_f32: bool):
         if out_f32 and a.dtype != torch.float32:
             return torch.mm(a, w.t(), out_dtype=torch.float32)
-        return torch.mm(a, w.t())
+        # the f32 parity variant needs true-f32 GEMMs (1e-4 contract): TF32 is pinned off
+        # for this call whatever the caller set globally
+        mm = torch.backends.cuda.matmul
+        if not mm.allow_tf32:
+            return torch.mm(a, w.t())
+        mm.allow_tf32 = False
+        try:
+            return torch.mm(a, w.t())
+        finally:
+            mm.allow_tf32 = True
 
     def _attn_algorithmic_bytes(self, plan: StepPlan, msg_len, R: int, n_parts: int) -> int:
         """unique KV bytes the step's attention must read (each visible
@@ -308,7 +311,7 @@ class Runner:
             k_pool=cache.k_pool.data_ptr(), v_pool=cache.v_pool.data_ptr(), n_pages=cache.n_pages,
             page_size=cache.page_size, cos_t=self.rot.cos.data_ptr(), sin_t=self.rot.sin.data_ptr(),
             max_delta=self.rot.max_delta, n_rows=R, split=int(self.split),
-            attn_flags=self.attn_flags, n_items=n_items, pos=pos_d.data_ptr(),
+            n_items=n_items, pos=pos_d.data_ptr(),
             page=page_d.data_ptr(), slot=slot_d.data_ptr(), fat=nat.ptr(fat),
             counts=counts.data_ptr(), row_part_off=row_part_off.data_ptr(),
             row_part=row_part.data_ptr(), x=x.data_ptr(), delta_in=None, h=h.data_ptr(),
@@ -320,7 +323,6 @@ class Runner:
             linear_events=ctypes.cast(lev, ctypes.c_void_p) if lev is not None else None)
         if v2 is not None:
             _, rowt_d, vis, blk_rows, items = v2
-            st.attn_kernel = 1
             st.row_t, st.vis_page, st.vis_len, st.vis_own = (
                 rowt_d.data_ptr(), vis[0].data_ptr(), vis[1].data_ptr(), vis[2].data_ptr())
             st.blk_rows, st.items = blk_rows.data_ptr(), items.data_ptr()
@@ -412,10 +414,6 @@ class Runner:
         # most 512 partials per row for the combine
         # prefill-sized steps: per-call page lists (a row block already fills an M tile)
         mode = 1 if max(len(c.tokens) for c in plan.calls) >= 64 or force_percall else 0
-        # decode-sized bf16 steps: fused K5 (fat items, in-kernel combine)
-        fused = (not use_k4 and not v2 and mode == 0 and self.pool_dtc == nat.BF16 and P == 64
-                 and hd in (64, 128) and rpb <= 16
-                 and os.environ.get("CHOREO_FUSED_DECODE", "1") != "0")
         work = plan_counts(plan.calls, msg_len, P, rpb, 1, mode)
         ppi = max(1, cdiv(work.item_pages * Hk, (2 if use_k4 else 1 if v2 else 3) * 148))
         if v2:  # persistent CTAs: about one (item, kv head) unit per SM; unit record <= 32 pages
@@ -424,12 +422,6 @@ class Runner:
         if v2:  # grow items until the units fit one wave of CTAs (else a few CTAs run two)
             while plan_.n_items * Hk > 148 and ppi < 32:
                 ppi = min(32, ppi + max(1, ppi // 4))
-                plan_ = plan_counts(plan.calls, msg_len, P, rpb, ppi, mode)
-        if fused:
-            # one wave of resident CTAs (3 per SM): a second item on a few CTAs would
-            # double the kernel's length
-            while plan_.n_items * Hk > 3 * 148 and ppi < 8:
-                ppi += 1
                 plan_ = plan_counts(plan.calls, msg_len, P, rpb, ppi, mode)
         while plan_.max_row_parts > 512 and not (v2 and ppi >= 32):
             ppi *= 2
@@ -469,11 +461,8 @@ class Runner:
         row_part_off = torch.empty(R + 1, dtype=torch.int32, device=self.dev)
         row_part = torch.empty(max(n_parts, 1), dtype=torch.int32, device=self.dev)
         counts = torch.empty(4, dtype=torch.int32, device=self.dev)
-        v2_fat = v2 and rpb <= 16 and os.environ.get("CHOREO_K5V2_FAT", "1") != "0"
         fat = (torch.empty(max(n_items, 1), 64, dtype=torch.int32, device=self.dev)
-               if fused or v2_fat else None)
-        if fused and (self._counters is None or self._counters.numel() < R * Hk):
-            self._counters = torch.zeros(max(R * Hk, 1024), dtype=torch.int32, device=self.dev)
+               if v2 and rpb <= 16 else None)
         nat.assemble(cache.msg_len.dev.data_ptr(), cache.msg_pt.dev.data_ptr(),
                      cache.page_table.dev.data_ptr(), calls_d.data_ptr(), parents_d.data_ptr(),
                      n_calls, rowt_d.data_ptr(), R, None, 0, P, rpb, ppi, vis[0].data_ptr(),
@@ -505,13 +494,11 @@ class Runner:
         act = torch.empty(S * R, cfg.ffn_dim, dtype=self.dt, device=self.dev)
         delta = None
         launches = 2
-        native = ((fused or v2) and k7 and self.native_step and not self.fused_combine
-                  and self.dt == torch.bfloat16)
+        native = v2 and k7 and self.native_step and self.dt == torch.bfloat16
         if native:
             delta = self._native_layers(R, q, part_o, part_lse, attn, h, act, x, pos_d, page_d,
                                         slot_d, fat, counts, n_items, row_part_off, row_part,
-                                        attn_bytes, stream,
-                                        (v2, rowt_d, vis, blk_rows, items) if v2 else None)
+                                        attn_bytes, stream, (v2, rowt_d, vis, blk_rows, items))
             # per layer: norm, K7 qkv, rope, K5, combine, K7 o, norm, K7 gate|up(+SwiGLU), K7 down
             launches += (9 if cfg.ffn_dim % 64 == 0 else 10) * len(self.w.layers)
         for layer, lw in enumerate([] if native else self.w.layers):
@@ -535,13 +522,6 @@ class Runner:
                                    vis[2].data_ptr(), blk_rows.data_ptr(), items.data_ptr(),
                                    counts.data_ptr(), n_items, part_o.data_ptr(),
                                    part_lse.data_ptr(), nat.ptr(fat), 0, stream)
-            elif fused:
-                nat.decode_attn(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(), layer,
-                                Hk, cache.n_pages, P, H, hd, fat.data_ptr(), counts.data_ptr(),
-                                n_items, row_part_off.data_ptr(), row_part.data_ptr(),
-                                part_o.data_ptr(), part_lse.data_ptr(),
-                                self._counters.data_ptr() if self.fused_combine else None,
-                                attn.data_ptr(), sp, R, self.attn_flags, 0, stream)
             elif use_k4:
                 nat.prefill_attn(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(),
                                  self.pool_dtc, cfg.n_layers, layer, Hk, cache.n_pages, P, H, hd,
@@ -556,11 +536,11 @@ class Runner:
                                rowt_d.data_ptr(), vis[0].data_ptr(), vis[1].data_ptr(),
                                vis[2].data_ptr(), blk_rows.data_ptr(), items.data_ptr(),
                                counts.data_ptr(), n_items, part_o.data_ptr(), part_lse.data_ptr(),
-                               0, self.attn_flags, stream)
+                               0, stream)
             if self.attn_events is not None:
                 ev1.record()
                 self.attn_events.append((ev0, ev1, attn_bytes))
-            if not direct and not (fused and self.fused_combine):
+            if not direct:
                 nat.attn_combine(part_o.data_ptr(), part_lse.data_ptr(), row_part_off.data_ptr(),
                                  row_part.data_ptr(), R, H, hd, attn.data_ptr(), self.dtc, sp,
                                  stream)

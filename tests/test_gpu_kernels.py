@@ -264,7 +264,7 @@ def test_attention_matches_dense_reference(dt, hd, H, Hk, mode):
                    nat.dtype_code(DT[dt]), L, Hk, cache.n_pages, cache.page_size, H, hd,
                    rt_d.data_ptr(), vis[0].data_ptr(), vis[1].data_ptr(), vis[2].data_ptr(),
                    blk.data_ptr(), items.data_ptr(), counts.data_ptr(), out["plan"].n_items,
-                   part_o.data_ptr(), part_lse.data_ptr(), 0, 3, _stream())
+                   part_o.data_ptr(), part_lse.data_ptr(), 0, _stream())
     nat.attn_combine(part_o.data_ptr(), part_lse.data_ptr(), rpo.data_ptr(), rp.data_ptr(), R, H,
                      hd, o.data_ptr(), nat.F32, 0, _stream())
     torch.cuda.synchronize()
@@ -362,77 +362,6 @@ def test_prefill_tcgen05_matches_dense_reference(hd, H, Hk, ppi):
             p /= p.sum()
             worst = max(worst, float(np.abs(got[r, h] - p @ vv).max()))
     assert worst < 2e-2, worst
-
-
-@pytest.mark.parametrize("hd,H,Hk", [(128, 32, 8), (64, 16, 2)])
-def test_fused_decode_matches_dense_reference(hd, H, Hk):
-    """choreo_decode_attn: fat items + in-kernel LSE combine over page-centric groups
-    (agents sharing reordered parents, causal own pages); counters left at zero."""
-    rng = np.random.default_rng(11)
-    cfg = ModelConfig(n_layers=2, n_heads=H, n_kv_heads=Hk, head_dim=hd)
-    cache, lens = _random_cache(cfg, rng, 8, dtype=torch.bfloat16)
-    calls = []
-    for a in range(6):
-        own = 8 + a
-        n = int(rng.integers(1, 150))
-        cache.register_message(own, "decoded", 0)
-        cache.reserve_slots(own, [1] * n)
-        cache.log_append(own, 0, n)
-        parents = [int(p) for p in rng.permutation(8)[:int(rng.integers(0, 7))]]
-        calls.append((own, parents, [n - 1]))
-    cache.k_pool.copy_(torch.randn_like(cache.k_pool))
-    cache.v_pool.copy_(torch.randn_like(cache.v_pool))
-    G = H // Hk
-    rpb = max(1, min(16, 64 // G))
-    out, (rt_d, vis, blk, items, rpo, rp, counts) = _assemble(cache, calls, rpb, 2, 0)
-    R = len(out["row_t"])
-    n_items = out["plan"].n_items
-    fat = torch.empty(n_items, 64, dtype=torch.int32, device="cuda")
-    # rebuild with fat records
-    from paper_2512_23049_b200.model import CallRows, plan_counts  # noqa: F401
-    tab, par, off = [], [], 0
-    for own, parents, ts in calls:
-        tab += [own, len(par), len(parents), off, len(ts)]
-        par += parents
-        off += len(ts)
-    dev = lambda a: torch.tensor(a, dtype=torch.int32, device="cuda")  # noqa: E731
-    pl_ = out["plan"]
-    tab_d, par_d = dev(tab), dev(par + [0])  # keep alive until the kernel ran
-    nat.assemble(cache.msg_len.dev.data_ptr(), cache.msg_pt.dev.data_ptr(),
-                 cache.page_table.dev.data_ptr(), tab_d.data_ptr(), par_d.data_ptr(),
-                 len(calls), rt_d.data_ptr(), R, None, 0, 64, rpb, 2, vis[0].data_ptr(),
-                 vis[1].data_ptr(), vis[2].data_ptr(), blk.data_ptr(), items.data_ptr(),
-                 rpo.data_ptr(), rp.data_ptr(), counts.data_ptr(), pl_.n_vis, pl_.n_blk_rows,
-                 n_items, pl_.n_parts, 0, fat.data_ptr(), _stream())
-    q = torch.randn(R, H, hd, device="cuda")
-    part_o = torch.empty(pl_.n_parts, H, hd, device="cuda")
-    part_lse = torch.empty(pl_.n_parts, H, device="cuda")
-    counters = torch.zeros(R * Hk, dtype=torch.int32, device="cuda")
-    o2 = torch.zeros(2 * R, H * hd, dtype=torch.bfloat16, device="cuda")
-    L = 1
-    for _ in range(2):  # twice: counters must come back to zero
-        nat.decode_attn(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(), L, Hk,
-                        cache.n_pages, 64, H, hd, fat.data_ptr(), counts.data_ptr(), n_items,
-                        rpo.data_ptr(), rp.data_ptr(), part_o.data_ptr(), part_lse.data_ptr(),
-                        counters.data_ptr(), o2.data_ptr(), 1, R, 3, 0, _stream())
-    torch.cuda.synchronize()
-    assert int(counters.abs().sum()) == 0
-    got = (o2[:R].float() + o2[R:].float()).cpu().numpy().reshape(R, H, hd)
-    sets = _expand_rows(cache, out, R)
-    K = cache.k_pool[L].float().cpu().numpy().astype(np.float64)
-    V = cache.v_pool[L].float().cpu().numpy().astype(np.float64)
-    qn = q.cpu().numpy().astype(np.float64)
-    P_ = cache.page_size
-    for r in range(R):
-        toks = sets[r]
-        pg = np.array([cache._messages[m].pages[i // P_] for m, i in toks])
-        sl = np.array([i % P_ for m, i in toks])
-        for h in range(H):
-            kk, vv = K[h // G, pg, sl], V[h // G, pg, sl]
-            s = kk @ qn[r, h] / np.sqrt(hd)
-            p = np.exp(s - s.max())
-            p /= p.sum()
-            np.testing.assert_allclose(got[r, h], p @ vv, rtol=1e-3, atol=1e-3)
 
 
 @pytest.mark.parametrize("ppi", [1, 2, 5])

@@ -19,8 +19,58 @@ import torch.multiprocessing as mp
 from oracle import choreo_oracle as O
 
 import paper_2512_23049_b200 as P
-from paper_2512_23049_b200.parallel import (TPLayout, replica_assignment, shard_weights,
-                                            tp_forward_numpy)
+from paper_2512_23049_b200.parallel import TPLayout, replica_assignment, shard_weights
+
+
+def tp_forward_numpy(shard, layout: TPLayout, x: np.ndarray, k_ctx, v_ctx, pos,
+                     rot_cos, rot_sin, allreduce) -> tuple:
+    """Reference TP forward of one group in NumPy (CPU tests): same decomposition as the
+    GPU runner — local heads, partial o_proj / down_proj outputs, ``allreduce(sum)``.
+
+    x: (T, d) embeddings; k_ctx/v_ctx: (L, n_ctx, kv_local, hd) this rank's cached slice.
+    Returns (final hidden (T, d), new local K, new local V).
+    """
+    cfg = layout.config
+    T, hd = x.shape[0], cfg.head_dim
+    H, Hk = layout.n_heads, layout.kv_heads
+    G = H // Hk
+
+    def rms(a, w):
+        return a / np.sqrt(np.mean(a * a, axis=-1, keepdims=True) + 1e-6) * w
+
+    def rope(a):
+        c = rot_cos[pos][:, None, :]
+        s = rot_sin[pos][:, None, :]
+        e, o = a[..., 0::2], a[..., 1::2]
+        y = np.empty_like(a)
+        y[..., 0::2] = e * c - o * s
+        y[..., 1::2] = e * s + o * c
+        return y
+
+    ks = np.empty((cfg.n_layers, T, Hk, hd))
+    vs = np.empty_like(ks)
+    n_ctx = k_ctx.shape[1]
+    mask = np.concatenate([np.ones((T, n_ctx), bool), np.tril(np.ones((T, T), bool))], axis=1)
+    for layer, lw in enumerate(shard.layers):
+        h = rms(x, lw.attn_norm)
+        q = rope((h @ lw.wq).reshape(T, H, hd))
+        k = rope((h @ lw.wk).reshape(T, Hk, hd))
+        v = (h @ lw.wv).reshape(T, Hk, hd)
+        ks[layer], vs[layer] = k, v
+        K = np.concatenate([k_ctx[layer], k])
+        V = np.concatenate([v_ctx[layer], v])
+        att = np.empty((T, H, hd))
+        for hq in range(H):
+            s = (q[:, hq] @ K[:, hq // G].T) / np.sqrt(hd)
+            s = np.where(mask, s, -np.inf)
+            p = np.exp(s - s.max(axis=1, keepdims=True))
+            p /= p.sum(axis=1, keepdims=True)
+            att[:, hq] = p @ V[:, hq // G]
+        x = x + allreduce(att.reshape(T, H * hd) @ lw.wo)
+        g = rms(x, lw.ffn_norm)
+        a = g @ lw.w_gate
+        x = x + allreduce((a / (1 + np.exp(-a)) * (g @ lw.w_up)) @ lw.w_down)
+    return x, ks, vs
 
 
 def _free_port() -> int:

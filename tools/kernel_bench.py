@@ -193,8 +193,7 @@ def k4_prefill(n_msgs: int = 8, rows: int = 1024, n_par: int = 24, n_layers: int
             "items": plan.n_items}
 
 
-def k5_decode(n_workflows: int = 1, agents: int = 8, tc: bool = False, fused: bool = True,
-              v2: bool = False) -> dict:
+def k5_decode(n_workflows: int = 1, agents: int = 8, tc: bool = False, v2: bool = True) -> dict:
     """One decode step of C3 round 2 (agents see sys, q and the other agents' replies)."""
     cfg = LLAMA_3_1_8B
     H, Hk, hd = cfg.n_heads, cfg.kv_heads, cfg.head_dim
@@ -225,11 +224,6 @@ def k5_decode(n_workflows: int = 1, agents: int = 8, tc: bool = False, fused: bo
                           cache.msg_len.host, 64, rpb, ppi).n_items * Hk > 148 and ppi < 32:
             ppi = min(32, ppi + max(1, ppi // 4))
     ppi = int(os.environ.get("K5_PPI", ppi))
-    fused = fused and not tc and not v2
-    if fused and "K5_PPI" not in os.environ:  # same one-wave fit as the runner
-        while plan_counts([CallRows(c[0], c[1], c[2], [0], None, None, 0) for c in calls],
-                          cache.msg_len.host, 64, rpb, ppi).n_items * Hk > 3 * 148 and ppi < 8:
-            ppi += 1
     plan, b, R = _assemble(cache, calls, rpb, ppi)
     q = torch.randn(R, H, hd, device="cuda")
     po = torch.empty(plan.n_parts, H, hd, device="cuda")
@@ -238,8 +232,6 @@ def k5_decode(n_workflows: int = 1, agents: int = 8, tc: bool = False, fused: bo
     v = b["vis"]
     stream = torch.cuda.current_stream().cuda_stream
 
-    counters = torch.zeros(R * Hk + 1024, dtype=torch.int32, device="cuda")
-    in_kernel_combine = os.environ.get("K5_FUSED_COMBINE", "1") == "1"
 
     def run():
         if v2:
@@ -249,14 +241,6 @@ def k5_decode(n_workflows: int = 1, agents: int = 8, tc: bool = False, fused: bo
                                b["blk"].data_ptr(), b["items"].data_ptr(), b["counts"].data_ptr(),
                                plan.n_items, po.data_ptr(), pl.data_ptr(),
                                b["fat"].data_ptr(), 0, stream)
-            return
-        if fused:
-            nat.decode_attn(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(), 0, Hk,
-                            cache.n_pages, 64, H, hd, b["fat"].data_ptr(), b["counts"].data_ptr(),
-                            plan.n_items, b["rpo"].data_ptr(), b["rp"].data_ptr(), po.data_ptr(),
-                            pl.data_ptr(), counters.data_ptr() if in_kernel_combine else None,
-                            out.data_ptr(), 1, R,
-                            int(os.environ.get("CHOREO_ATTN_FLAGS", "3")), 0, stream)
             return
         if tc:
             nat.prefill_attn(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(),
@@ -268,14 +252,13 @@ def k5_decode(n_workflows: int = 1, agents: int = 8, tc: bool = False, fused: bo
         nat.attn_split(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(), nat.BF16, 0,
                        Hk, cache.n_pages, 64, H, hd, b["rt"].data_ptr(), v[0].data_ptr(),
                        v[1].data_ptr(), v[2].data_ptr(), b["blk"].data_ptr(), b["items"].data_ptr(),
-                       b["counts"].data_ptr(), plan.n_items, po.data_ptr(), pl.data_ptr(), 0,
-                       int(os.environ.get("CHOREO_ATTN_FLAGS", "3")), stream)
+                       b["counts"].data_ptr(), plan.n_items, po.data_ptr(), pl.data_ptr(), 0, stream)
 
     def run_comb():
         nat.attn_combine(po.data_ptr(), pl.data_ptr(), b["rpo"].data_ptr(), b["rp"].data_ptr(), R,
                          H, hd, out.data_ptr(), nat.BF16, 1, stream)
     t = _time(run)
-    tcomb = 0.0 if (fused and in_kernel_combine) else _time(run_comb)
+    tcomb = _time(run_comb)
     uniq = sum(cache.message_length(m) for m in set(p for c in calls for p in c[1]))
     uniq += sum(c[2] + 1 for c in calls)
     nbytes = 2 * uniq * Hk * hd * 2 + R * H * hd * 4 + plan.n_parts * H * (hd + 1) * 4
@@ -284,11 +267,10 @@ def k5_decode(n_workflows: int = 1, agents: int = 8, tc: bool = False, fused: bo
     ach = nbytes / t / 1e9
     return {"kernel": ("choreo_decode_attn_v2 (K5 v2: TMA page ring, page-centric)" if v2 else
                        "choreo_prefill_attn on decode items (tcgen05)" if tc else
-                       "choreo_decode_attn (K5 fused, page-centric)" if fused
-                       else "choreo_attn_split (K5, page-centric decode)"), "bound": "hbm",
+                       "choreo_attn_split (K5 generic SIMT, page-centric decode)"), "bound": "hbm",
             "work": f"{n_workflows} workflow(s) x {agents} agents, 1 layer",
             "algorithmic_bytes": nbytes, "logical_kv_bytes": logical, "us": round(t * 1e6, 2),
-            "combine_us": round(tcomb * 1e6, 2), "fused_combine": fused, "achieved": round(ach, 1),
+            "combine_us": round(tcomb * 1e6, 2), "achieved": round(ach, 1),
             "unit": "GB/s",
             "peak": pk["hbm_gbs"], "frac": round(ach / pk["hbm_gbs"], 4), "items": plan.n_items,
             "pages_per_item": ppi}
@@ -352,8 +334,8 @@ def k5_sweep() -> list:
 
 
 def run_all() -> list:
-    out = [k2_rerotate(), k4_prefill(), k5_decode(1), k5_decode(8), k5_decode(1, fused=False),
-           k5_decode(8, fused=False)]
+    out = [k2_rerotate(), k4_prefill(), k5_decode(1), k5_decode(8), k5_decode(1, v2=False),
+           k5_decode(8, v2=False)]
     torch.cuda.empty_cache()
     return out
 
