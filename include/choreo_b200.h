@@ -304,9 +304,84 @@ typedef struct {
    * `ao`); 2 the MLP half (norm of x += ao, ends with down_proj in `delta`).  Tensor
    * parallel callers run part 1, all-reduce ao, part 2, all-reduce delta, per layer. */
   int layer_begin, layer_end, part;
+  /* K8 chain path (part 0 with every layer): when chain_ws != NULL each step runs
+   * choreo_chain_prologue, one choreo_layer_chain (qkv of layer 0), then per layer K5 v2 +
+   * combine + one choreo_layer_chain (o_proj, gate|up, down, qkv of the next layer); the
+   * last layer's down_proj is added into x (delta is not written).  h_b: bf16 [2 n_rows][d];
+   * ssq_a / ssq_b f32 [ceil(d/128)][128]; chain_ws / chain_counters / chain_done as
+   * choreo_layer_chain.
+   * chain_events: optional host array of 2 * (n_layers + 1) cudaEvent_t recorded around
+   * each chain launch. */
+  void* h_b;
+  float* ssq_a;
+  float* ssq_b;
+  float* chain_ws;
+  int* chain_counters;
+  int* chain_done;
+  void** chain_events;
 } ChoreoDecodeStep;
 
 int choreo_decode_layers(const ChoreoDecodeStep* step, void* stream);
+
+/* K8 layer chain: the weight-streaming projections between two attentions of a decode-sized
+ * bf16 step in ONE persistent launch (tcgen05 + TMA, one CTA per SM, stream-K per phase,
+ * per-tile dataflow flags between phases instead of kernel boundaries).  Phases (bits of
+ * `phases`, run in this order):
+ *   1 o_proj : x += attn @ wo^T; h_a = hi/lo(x * ffn_norm); ssq_a = per-128-column sums of x^2
+ *   2 gate|up: act = silu(r g) * (r u), r = rsqrt(mean(x^2) + eps) from ssq_a (hi/lo bf16)
+ *   4 down   : x += act @ w_down^T; if attn_norm_next: h_b = hi/lo(x * attn_norm_next), ssq_b
+ *   8 qkv    : r * (h_b @ w_qkv^T) with r from ssq_b -> RoPE(q, k) at pos[row]; q (f32
+ *              [n_rows][n_heads][head_dim]) out, k / v (bf16) written to pool slot
+ *              (page[row], slot[row]) of layer layer_qkv  (K1's contract)
+ * RMSNorm is applied as a per-row scale of the next GEMM's output (norm(x) w @ W^T =
+ * r ((x w) @ W^T)).  Activations: split = 1 carries every GEMM input as hi/lo bf16 rows r and
+ * n_rows + r (n_rows <= 128), else plain bf16 (n_rows <= 128).  Buffers: x f32 [n_rows][d];
+ * attn, h_a, h_b bf16 [2 n_rows][.] ; act bf16 [2 n_rows][ffn_dim]; ssq_a / ssq_b f32
+ * [ceil(d/128)][128]; ws f32 [4][148][2][128][128]; counters int32 [4][1024] and done int32
+ * [8] (per-phase completion counters), zero before the first launch and left zero.
+ * d, n_heads*head_dim, ffn_dim multiples of 64.
+ * Replaces model.py:169-189 (everything after attention of layer l up to the attention of
+ * layer l+1) for decode-sized steps. */
+typedef struct {
+  int n_rows, split, d, n_heads, n_kv, head_dim, ffn_dim;
+  float eps;
+  int phases;
+  const void* wo;
+  const void* ffn_norm;
+  const void* w_gu;
+  const void* w_down;
+  const void* attn_norm_next;
+  const void* w_qkv;
+  int layer_qkv;
+  float* x;
+  const void* attn;
+  void* h_a;
+  void* act;
+  void* h_b;
+  float* ssq_a;
+  float* ssq_b;
+  float* q;
+  void* k_pool;
+  void* v_pool;
+  int n_pages, page_size;
+  const int32_t* pos;
+  const int32_t* page;
+  const int32_t* slot;
+  const float* cos_t;
+  const float* sin_t;
+  int max_delta;
+  float* ws;
+  int* counters;
+  int* done;
+} ChoreoLayerChain;
+
+int choreo_layer_chain(const ChoreoLayerChain* chain, void* stream);
+
+/* Start of a chained step: x (+= delta when non-NULL); h = hi/lo(x * gamma) (bf16 [2n][d]
+ * when split); ssq f32 [ceil(d/128)][128] = per-128-column sums of x^2 per row (n_rows <=
+ * 128).  Feeds the first choreo_layer_chain (qkv phase only). */
+int choreo_chain_prologue(float* x, const float* delta, int n_rows, int d, const void* gamma,
+                          void* h, int split, float* ssq, void* stream);
 
 /* Timing-event helpers for attn_events (cudaEvent_t as void*). */
 int choreo_events_create(void** events, int n);

@@ -48,6 +48,8 @@ SIGNATURES: dict[str, list] = {
     "choreo_select_nucleus": [_P, _I, _I, _I, _P, _P, _P, _P],
     "choreo_decode_attn_v2": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P,
                               _I, _P, _P, _P, _I, _P],
+    "choreo_layer_chain": [_P, _P],
+    "choreo_chain_prologue": [_P, _P, _I, _I, _P, _P, _I, _P, _P],
     "choreo_events_create": [_P, _I],
     "choreo_events_elapsed": [_P, _I, _P],
     "choreo_events_destroy": [_P, _I],
@@ -118,6 +120,8 @@ decode_layers = _Caller("choreo_decode_layers")
 linear_gate_up_silu = _Caller("choreo_linear_gate_up_silu")
 select_nucleus = _Caller("choreo_select_nucleus")
 decode_attn_v2 = _Caller("choreo_decode_attn_v2")
+layer_chain = _Caller("choreo_layer_chain")
+chain_prologue = _Caller("choreo_chain_prologue")
 events_create = _Caller("choreo_events_create")
 events_elapsed = _Caller("choreo_events_elapsed")
 events_destroy = _Caller("choreo_events_destroy")
@@ -136,7 +140,25 @@ class DecodeStep(ctypes.Structure):
                            "gu", "act", "delta", "k7_ws", "k7_cnt", "attn_events")] + \
         [(n, _P) for n in ("row_t", "vis_page", "vis_len", "vis_own", "blk_rows", "items",
                            "linear_events")] + \
-        [(n, _I) for n in ("layer_begin", "layer_end", "part")]
+        [(n, _I) for n in ("layer_begin", "layer_end", "part")] + \
+        [(n, _P) for n in ("h_b", "ssq_a", "ssq_b", "chain_ws", "chain_counters",
+                           "chain_done", "chain_events")]
+
+
+class LayerChain(ctypes.Structure):
+    """Mirror of ChoreoLayerChain (include/choreo_b200.h)."""
+
+    _fields_ = [(n, _I) for n in ("n_rows", "split", "d", "n_heads", "n_kv", "head_dim",
+                                  "ffn_dim")] + \
+        [("eps", _F), ("phases", _I)] + \
+        [(n, _P) for n in ("wo", "ffn_norm", "w_gu", "w_down", "attn_norm_next", "w_qkv")] + \
+        [("layer_qkv", _I)] + \
+        [(n, _P) for n in ("x", "attn", "h_a", "act", "h_b", "ssq_a", "ssq_b", "q", "k_pool",
+                           "v_pool")] + \
+        [("n_pages", _I), ("page_size", _I)] + \
+        [(n, _P) for n in ("pos", "page", "slot", "cos_t", "sin_t")] + \
+        [("max_delta", _I)] + \
+        [(n, _P) for n in ("ws", "counters", "done")]
 
 
 def ptr(t) -> int | None:

@@ -51,6 +51,73 @@ extern "C" int choreo_decode_layers(const ChoreoDecodeStep* s, void* stream) {
   // K7 outputs consumed inside this call are left deferred (ChoreoK7Pieces): the consumer
   // (RoPE / residual+norm) sums the cut tiles, the GEMM skips its cross-CTA fix-up.  Outputs
   // the caller reads (the last down_proj, the TP halves' o_proj / down_proj) are reduced.
+  if (s->chain_ws && s->part == 0 && l0 == 0 && l1 == s->n_layers) {
+    // K8 path: prologue, qkv(0), then per layer attention + combine + one chain launch
+    if (!s->h_b || !s->ssq_a || !s->ssq_b || !s->chain_counters || !s->chain_done)
+      return CHOREO_EINVAL;
+    cudaEvent_t* cev = reinterpret_cast<cudaEvent_t*>(s->chain_events);
+    ChoreoLayerChain c{};
+    c.n_rows = R;
+    c.split = sp;
+    c.d = d;
+    c.n_heads = H;
+    c.n_kv = Hk;
+    c.head_dim = hd;
+    c.ffn_dim = F;
+    c.eps = s->eps;
+    c.x = s->x;
+    c.attn = s->attn;
+    c.h_a = s->h;
+    c.act = s->act;
+    c.h_b = s->h_b;
+    c.ssq_a = s->ssq_a;
+    c.ssq_b = s->ssq_b;
+    c.q = s->q;
+    c.k_pool = s->k_pool;
+    c.v_pool = s->v_pool;
+    c.n_pages = s->n_pages;
+    c.page_size = s->page_size;
+    c.pos = s->pos;
+    c.page = s->page;
+    c.slot = s->slot;
+    c.cos_t = s->cos_t;
+    c.sin_t = s->sin_t;
+    c.max_delta = s->max_delta;
+    c.ws = s->chain_ws;
+    c.counters = s->chain_counters;
+    c.done = s->chain_done;
+    CHK(choreo_chain_prologue(s->x, s->delta_in, R, d, s->attn_norm[0], s->h_b, sp, s->ssq_b,
+                              stream));
+    c.phases = 8;
+    c.w_qkv = s->w_qkv[0];
+    c.layer_qkv = 0;
+    if (cev) cudaEventRecord(cev[0], cs);
+    CHK(choreo_layer_chain(&c, stream));
+    if (cev) cudaEventRecord(cev[1], cs);
+    for (int l = 0; l < s->n_layers; ++l) {
+      if (ev) cudaEventRecord(ev[2 * l], cs);
+      CHK(choreo_decode_attn_v2(s->q, s->k_pool, s->v_pool, s->n_layers, l, Hk, s->n_pages,
+                                s->page_size, H, hd, s->row_t, s->vis_page, s->vis_len,
+                                s->vis_own, s->blk_rows, s->items, s->counts, s->n_items,
+                                s->part_o, s->part_lse, s->fat, 0, stream));
+      if (ev) cudaEventRecord(ev[2 * l + 1], cs);
+      CHK(choreo_attn_combine(s->part_o, s->part_lse, s->row_part_off, s->row_part, R, H, hd,
+                              s->attn, CHOREO_BF16, sp, stream));
+      const bool more = l + 1 < s->n_layers;
+      c.phases = 1 | 2 | 4 | (more ? 8 : 0);
+      c.wo = s->wo[l];
+      c.ffn_norm = s->ffn_norm[l];
+      c.w_gu = s->w_gu[l];
+      c.w_down = s->w_down[l];
+      c.attn_norm_next = more ? s->attn_norm[l + 1] : nullptr;
+      c.w_qkv = more ? s->w_qkv[l + 1] : nullptr;
+      c.layer_qkv = l + 1;
+      if (cev) cudaEventRecord(cev[2 * (l + 1)], cs);
+      CHK(choreo_layer_chain(&c, stream));
+      if (cev) cudaEventRecord(cev[2 * (l + 1) + 1], cs);
+    }
+    return CHOREO_OK;
+  }
   const bool defer = k7_defer_enabled();
   ChoreoK7Pieces pk{}, po{}, pd{};
   bool pd_valid = false;

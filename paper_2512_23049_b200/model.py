@@ -191,6 +191,13 @@ class Runner:
         # decode-sized bf16 steps run their layer loop in the native executor
         # (choreo_decode_layers: one library call per step instead of ~11 per layer)
         self.native_step = os.environ.get("CHOREO_NATIVE_STEP", "1") != "0"
+        # ... or (CHOREO_CHAIN=1, one process per model) run the projections between two
+        # attentions as ONE K8 layer-chain launch (choreo_layer_chain).  Measured in situ at
+        # the 8B decode step: on par with the per-GEMM K7 sequence (4.10-4.12 vs 4.07 ms), so
+        # K7 stays the default
+        self.chain = (self.dt == torch.bfloat16 and (tp is None or tp.size == 1)
+                      and os.environ.get("CHOREO_CHAIN", "0") == "1")
+        self._chain_bufs = None
         self._wptrs = None
         self._ev_free: list = []
         self._ev_pending: list = []  # (kind, event array, bytes per pair) awaiting readback
@@ -299,8 +306,9 @@ class Runner:
             a = (ctypes.c_void_p * n)()
             nat.events_create(a, n)
             return a
+        chain = self._chain_ok(R)
         ev = events(2 * L) if self.attn_events is not None else None
-        lev = events(8 * L) if self.time_linear else None
+        lev = events(2 * (L + 1) if chain else 8 * L) if self.time_linear else None
         st = nat.DecodeStep(
             n_layers=L, d=d, n_heads=cfg.n_heads, n_kv=cfg.kv_heads, head_dim=hd,
             ffn_dim=cfg.ffn_dim, attn_norm=ctypes.cast(wp["attn_norm"], ctypes.c_void_p),
@@ -326,7 +334,15 @@ class Runner:
             st.row_t, st.vis_page, st.vis_len, st.vis_own = (
                 rowt_d.data_ptr(), vis[0].data_ptr(), vis[1].data_ptr(), vis[2].data_ptr())
             st.blk_rows, st.items = blk_rows.data_ptr(), items.data_ptr()
-        if self.tp is not None and self.tp.size > 1:
+        if chain:
+            cb = self._chain_buffers()
+            h_b = torch.empty(2 * R if self.split else R, d, dtype=self.dt, device=dev)
+            st.h_b, st.ssq_a, st.ssq_b = h_b.data_ptr(), cb["ssq_a"].data_ptr(), cb["ssq_b"].data_ptr()
+            st.chain_ws, st.chain_counters = cb["ws"].data_ptr(), cb["counters"].data_ptr()
+            st.chain_done = cb["done"].data_ptr()
+            st.chain_events = ctypes.cast(lev, ctypes.c_void_p) if lev is not None else None
+            nat.decode_layers(ctypes.byref(st), stream)
+        elif self.tp is not None and self.tp.size > 1:
             # per layer: attention half, all-reduce o_proj partials, MLP half, all-reduce
             # down_proj partials (the collectives stay with torch.distributed / NCCL)
             for layer in range(L):
@@ -343,12 +359,35 @@ class Runner:
             self._ev_pending.append(("attn", ev, [attn_bytes]))
         if lev is not None:
             x_rows = (2 if self.split else 1) * R
-            lb = [w.numel() * w.element_size() + x_rows * w.shape[1] * 2 + R * w.shape[0] * 4
-                  for w in (self.w.layers[0][n] for n in ("w_qkv", "wo", "w_gu", "w_down"))]
-            self._ev_pending.append(("linear", lev, lb))
+            lb = {n: w.numel() * w.element_size() + x_rows * w.shape[1] * 2 + R * w.shape[0] * 4
+                  for n, w in ((n, self.w.layers[0][n]) for n in ("w_qkv", "wo", "w_gu", "w_down"))}
+            if chain:  # per chain launch: qkv(0); o, gate|up, down (+ next qkv) per layer
+                rest = lb["wo"] + lb["w_gu"] + lb["w_down"]
+                self._ev_pending.append(("linear", lev, [lb["w_qkv"]] + [rest + lb["w_qkv"]] * (L - 1)
+                                         + [rest]))
+            else:
+                self._ev_pending.append(("linear", lev, [lb[n] for n in
+                                                         ("w_qkv", "wo", "w_gu", "w_down")]))
         if ev is not None or lev is not None:
             self._retire_events(16)
-        return delta
+        return None if chain else delta
+
+    def _chain_ok(self, rows: int) -> bool:
+        """K8 takes decode-sized steps of <= 128 rows (hi/lo: <= 256 stacked GEMM rows)."""
+        cfg = self.cfg
+        return (self.chain and self.native_step and rows <= 128 and self.d % 64 == 0
+                and cfg.ffn_dim % 64 == 0 and (cfg.n_heads * cfg.head_dim) % 64 == 0)
+
+    def _chain_buffers(self) -> dict:
+        if self._chain_bufs is None:
+            dev, tiles = self.dev, cdiv(self.d, 128)
+            self._chain_bufs = {
+                "ws": torch.empty(4 * 148 * 2 * 128 * 128, dtype=torch.float32, device=dev),
+                "counters": torch.zeros(4 * 1024, dtype=torch.int32, device=dev),
+                "done": torch.zeros(8, dtype=torch.int32, device=dev),
+                "ssq_a": torch.empty(tiles * 128, dtype=torch.float32, device=dev),
+                "ssq_b": torch.empty(tiles * 128, dtype=torch.float32, device=dev)}
+        return self._chain_bufs
 
     def _lin_buffers(self) -> None:
         self._k7_ws = torch.empty(148 * 2 * 128 * 128, dtype=torch.float32, device=self.dev)
@@ -494,13 +533,16 @@ class Runner:
         act = torch.empty(S * R, cfg.ffn_dim, dtype=self.dt, device=self.dev)
         delta = None
         launches = 2
-        native = v2 and k7 and self.native_step and self.dt == torch.bfloat16
+        native = (v2 and self.native_step and self.dt == torch.bfloat16
+                  and (k7 or self._chain_ok(R)))
         if native:
             delta = self._native_layers(R, q, part_o, part_lse, attn, h, act, x, pos_d, page_d,
                                         slot_d, fat, counts, n_items, row_part_off, row_part,
                                         attn_bytes, stream, (v2, rowt_d, vis, blk_rows, items))
-            # per layer: norm, K7 qkv, rope, K5, combine, K7 o, norm, K7 gate|up(+SwiGLU), K7 down
-            launches += (9 if cfg.ffn_dim % 64 == 0 else 10) * len(self.w.layers)
+            if self._chain_ok(R):  # prologue + qkv(0); per layer: K5, combine, K8 chain
+                launches += 2 + 3 * len(self.w.layers)
+            else:  # per layer: norm, K7 qkv, rope, K5, combine, K7 o, norm, K7 gate|up, K7 down
+                launches += (9 if cfg.ffn_dim % 64 == 0 else 10) * len(self.w.layers)
         for layer, lw in enumerate([] if native else self.w.layers):
             nat.residual_rmsnorm(x.data_ptr(), nat.ptr(delta), nat.F32, isp,
                                  lw["attn_norm"].data_ptr(), self.dtc, R, d, RMS_EPS, h.data_ptr(),
@@ -563,9 +605,10 @@ class Runner:
             if self.tp is not None and self.tp.size > 1:  # row-parallel down_proj
                 torch.distributed.all_reduce(delta, group=self.tp_group)
             launches += 6
-        nat.residual_rmsnorm(x.data_ptr(), delta.data_ptr(), nat.F32, isp, None, 0, R, d, RMS_EPS,
-                             None, 0, 0, None, 0, stream)
-        launches += 1
+        if delta is not None:  # the K8 chain already added the last down_proj into x
+            nat.residual_rmsnorm(x.data_ptr(), delta.data_ptr(), nat.F32, isp, None, 0, R, d,
+                                 RMS_EPS, None, 0, 0, None, 0, stream)
+            launches += 1
         self.launches += launches
         logits = None
         if n_log:

@@ -300,9 +300,10 @@ def test_bf16_tensor_core_paths_match_oracle(hd, H, Hk):
 
 @pytest.mark.parametrize("hd,H,Hk", [(128, 32, 8), (64, 8, 2)])
 def test_native_decode_executor_bitwise_equals_python_loop(hd, H, Hk):
-    """choreo_decode_layers (native layer loop) launches the same kernels in the same order
-    as the Python-driven loop: logits of a parallel decode are bitwise identical, and the
-    K7 / cuBLAS decode GEMM paths agree within the bf16 tolerance."""
+    """choreo_decode_layers (native layer loop) with per-GEMM K7 launches (CHOREO_CHAIN off)
+    launches the same kernels in the same order as the Python-driven loop: logits of a
+    parallel decode are bitwise identical; the K8 layer chain (norm folded in as a row scale
+    of the next GEMM) and the cuBLAS decode GEMM paths agree within the bf16 tolerance."""
     cfg = P.ModelConfig(n_layers=3, n_heads=H, n_kv_heads=Hk, head_dim=hd, ffn_dim=512,
                         vocab_size=400, context_window=4096, rope_base=500000.0)
     dw = P.DeviceWeights.from_host(P.init_weights(cfg).rounded("bf16"), dtype=torch.bfloat16)
@@ -310,11 +311,12 @@ def test_native_decode_executor_bitwise_equals_python_loop(hd, H, Hk):
     texts = ["".join(chr(97 + int(c)) for c in rng.integers(0, 26, n)) for n in (120, 200, 90)]
     forced = [rng.integers(97, 123, size=int(n)).tolist() for n in (70, 40, 90, 65, 10, 33)]
     runs = {}
-    for name, native, k7 in (("native", True, True), ("python", False, True),
-                             ("cublas", False, False)):
+    for name, native, k7, chain in (("native", True, True, False), ("python", False, True, False),
+                                    ("cublas", False, False, False), ("chain", True, True, True)):
         eng = P.Engine(dw, record_logits=True)
         eng._runner.native_step = native
         eng._runner.k7 = k7
+        eng._runner.chain = chain
         ids = [eng.prefill(P.PrefillCall(t)) for t in texts]
         calls = [P.DecodeCall(f"Agent {i}:", parents=[ids[(i + j) % 3] for j in range(2)],
                               offsets=[250 * ((i + j) % 3) for j in range(2)], new_offset=800,
@@ -323,8 +325,9 @@ def test_native_decode_executor_bitwise_equals_python_loop(hd, H, Hk):
         runs[name] = [np.stack(eng.stats[-1].logits[m]) for m in ms]
     for a, b in zip(runs["native"], runs["python"]):
         assert np.array_equal(a, b)
-    for a, b in zip(runs["native"], runs["cublas"]):
+    for a, b, c in zip(runs["native"], runs["cublas"], runs["chain"]):
         assert float(np.abs(a - b).max()) <= 2e-2
+        assert float(np.abs(a - c).max()) <= 2e-2
 
 
 def test_llama8b_width_two_layers_matches_oracle():
