@@ -207,8 +207,8 @@ typedef struct {
  *   y[r][n] = sum_k x[r][k] * w[n][k]      x: bf16 [x_rows][k], w: bf16 [n][k] (out, in),
  *                                          y: f32 [x_rows / (1 + split)][n].
  * split = 1: x rows r and x_rows/2 + r are the hi/lo halves of one activation row and
- * y row r is their sum.  x_rows <= 128 (<= 64 output rows when split), k % 8 == 0.
- * workspace: f32 [148 * 2 * 128 * 128] partial tiles; tile_counters: int32 [ceil(n/128)],
+ * y row r is their sum.  x_rows <= 256 when split (<= 128 output rows), else <= 128; k % 8 == 0.
+ * workspace: f32 [148 * 2 * NX * 128] partial tiles (NX = x_rows rounded up to 16/32/64/128/256); tile_counters: int32 [ceil(n/128)],
  * zero on entry, left zero on exit.  grid_ctas <= 0: one CTA per SM (148).
  * Replaces the x @ W projections of model.py:172-174, 185-189 and the head at 193 for
  * decode-sized steps (the reference runs them as NumPy matmuls). */

@@ -115,8 +115,8 @@ __host__ __device__ __forceinline__ int ln_owner(int i, int iters, int grid) {
 }
 
 // element (r, n..n+W-1) of a deferred K7 output (ChoreoK7Pieces): y for tiles one CTA owns,
-// else the per-CTA partials of the tile summed in CTA order from 0 (the reducer's order; for
-// split activations hi and lo rows are summed separately, then added) -- bit-identical
+// else the per-CTA partials of the tile (hi + lo halves already summed per piece) added in
+// CTA order from 0 -- the reducer's order, so the values are bit-identical
 template <int W, int B = 4>
 __device__ __forceinline__ void k7_get(const ChoreoK7Pieces& v, int r, int n, float* out) {
   const int t = n >> 7, nl = n & 127;
@@ -127,39 +127,34 @@ __device__ __forceinline__ void k7_get(const ChoreoK7Pieces& v, int r, int n, fl
     for (int e = 0; e < W; ++e) out[e] = v.y[(size_t)r * v.n + n + e];
     return;
   }
-  float a[W], b[W];
+  const int rows = v.split ? v.nx / 2 : v.nx;  // rows of one piece
+  float a[W];
 #pragma unroll
-  for (int e = 0; e < W; ++e) a[e] = b[e] = 0.f;
+  for (int e = 0; e < W; ++e) a[e] = 0.f;
   // pieces are fetched B at a time (all loads in flight together), then added in CTA
   // order: a tile spans ~3-7 CTAs, one dependent round trip per piece would dominate
   for (int c0 = c_lo; c0 <= c_hi; c0 += B) {
-    float pa[B][W], pb[B][W];
+    float pa[B][W];
 #pragma unroll
     for (int j = 0; j < B; ++j) {
       const int cc = c0 + j;
       if (cc <= c_hi) {
         const int sl = ln_begin(cc, v.iters, v.grid) >= lo ? 0 : 1;
-        const float* pc = v.ws + ((size_t)(cc * 2 + sl) * v.nx) * 128 + nl;
+        const float* pc = v.ws + ((size_t)(cc * 2 + sl) * rows) * 128 + nl;
 #pragma unroll
-        for (int e = 0; e < W; ++e) {
-          pa[j][e] = pc[r * 128 + e];
-          pb[j][e] = v.split ? pc[(v.nx / 2 + r) * 128 + e] : 0.f;
-        }
+        for (int e = 0; e < W; ++e) pa[j][e] = pc[r * 128 + e];
       }
     }
 #pragma unroll
     for (int j = 0; j < B; ++j) {
       if (c0 + j <= c_hi) {
 #pragma unroll
-        for (int e = 0; e < W; ++e) {
-          a[e] += pa[j][e];
-          b[e] += pb[j][e];
-        }
+        for (int e = 0; e < W; ++e) a[e] += pa[j][e];
       }
     }
   }
 #pragma unroll
-  for (int e = 0; e < W; ++e) out[e] = v.split ? a[e] + b[e] : a[e];
+  for (int e = 0; e < W; ++e) out[e] = a[e];
 }
 
 }  // namespace choreo

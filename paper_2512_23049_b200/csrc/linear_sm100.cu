@@ -53,9 +53,6 @@ struct LnCfg {
   static constexpr int kTmemCols = 2 * NX < 32 ? 32 : 2 * NX;
 };
 
-template <int NX>
-__host__ __device__ constexpr int p_split_rows() { return NX; }
-
 
 template <int NX, int KSUB>
 __global__ void __launch_bounds__(kLnThreads, 1)
@@ -178,25 +175,53 @@ __global__ void __launch_bounds__(kLnThreads, 1)
     const int et = tid - 64;          // 0..127
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     int seg = 0;
+    // output rows are handled in chunks of RC: split activations pair TMEM column r (hi half)
+    // with NX/2 + r (lo half); at NX 16 both halves come from one 16-column load
+    constexpr int RC = NX == 16 ? 8 : 16;
+    const int rows_half = p.split ? NX / 2 : NX;  // output rows the accumulator holds
     for (int t = b / p.KB; t * p.KB < e; ++t, ++seg) {
       const int buf = seg & 1;
       const int lo = t * p.KB, hi = lo + p.KB;
       const int c_lo = ln_owner(lo, p.iters, p.grid), c_hi = ln_owner(hi - 1, p.iters, p.grid);
       mbar_wait(&acc_full[buf], (seg >> 1) & 1);
       tc_fence_after();
-      float acc[NX];
+      const uint32_t tb = tmem_base + lane_off + buf * NX;
+      // raw accumulator columns of chunk r0: a = rows r0.. (hi half), bb = NX/2 + r0.. (lo)
+      auto ld_chunk = [&](int r0, float* a, float* bb) {
+        if (NX == 16) {
+          float t16[16];
+          tmem_ld16(tb, t16);
+          tmem_wait_ld();
 #pragma unroll
-      for (int q = 0; q < NX / 16; ++q) tmem_ld16(tmem_base + lane_off + buf * NX + q * 16, acc + q * 16);
-      tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(&acc_empty[buf]);
+          for (int i = 0; i < RC; ++i) {
+            a[i] = p.split ? t16[i] : t16[r0 + i];
+            bb[i] = p.split ? t16[8 + i] : 0.f;
+          }
+        } else {
+          tmem_ld16(tb + r0, a);
+          if (p.split) tmem_ld16(tb + NX / 2 + r0, bb);
+          tmem_wait_ld();
+          if (!p.split) {
+#pragma unroll
+            for (int i = 0; i < RC; ++i) bb[i] = 0.f;
+          }
+        }
+      };
       const int n = t * kLnTile + nl;
-      if (c_lo != c_hi) {
-        // piece of a tile cut between CTAs: park it, the last piece reduces in CTA order
+      const bool cut = c_lo != c_hi;
+      if (cut) {
+        // piece of a tile cut between CTAs: park it (hi + lo halves summed: rows_half rows x
+        // 128, the layout k7_get reads); the last piece reduces in CTA order
         const int slot = (b >= lo) ? 0 : 1;
-        float* w = p.ws + ((size_t)(c * 2 + slot) * NX) * kLnTile + nl;
+        float* w = p.ws + ((size_t)(c * 2 + slot) * rows_half) * kLnTile + nl;
+        for (int r0 = 0; r0 < rows_half; r0 += RC) {
+          float a[16], bb[16];
+          ld_chunk(r0, a, bb);
 #pragma unroll
-        for (int q = 0; q < NX; ++q) w[q * kLnTile] = acc[q];
+          for (int i = 0; i < RC; ++i) w[(r0 + i) * kLnTile] = p.split ? a[i] + bb[i] : a[i];
+        }
+        tc_fence_before();
+        mbar_arrive(&acc_empty[buf]);
         if (p.defer) continue;  // the consumer sums the pieces (k7_get)
         // the group's barrier orders the 128 threads' partial stores before thread 0's
         // GPU-scope release (one fence per piece instead of one per thread); the last piece
@@ -210,58 +235,85 @@ __global__ void __launch_bounds__(kLnThreads, 1)
         }
         asm volatile("bar.sync 1, 128;\n" ::: "memory");
         if (!s_last) continue;
-#pragma unroll
-        for (int q = 0; q < NX; ++q) acc[q] = 0.f;
-        for (int cc = c_lo; cc <= c_hi; ++cc) {
-          const int sl = (ln_begin(cc, p.iters, p.grid) >= lo) ? 0 : 1;
-          const volatile float* r = p.ws + ((size_t)(cc * 2 + sl) * NX) * kLnTile + nl;
-#pragma unroll
-          for (int q = 0; q < NX; ++q) acc[q] += r[q * kLnTile];
-        }
         if (et == 0) p.counters[t] = 0;
       }
+      // final rows of chunk r0 -> v: the pieces summed in CTA order (the order k7_get uses,
+      // so deferred and reduced outputs are bit-identical), 4 pieces' loads in flight
+      auto final_chunk = [&](int r0, float* v) {
+        if (!cut) {
+          float a[16], bb[16];
+          ld_chunk(r0, a, bb);
+#pragma unroll
+          for (int i = 0; i < RC; ++i) v[i] = p.split ? a[i] + bb[i] : a[i];
+          return;
+        }
+#pragma unroll
+        for (int i = 0; i < RC; ++i) v[i] = 0.f;
+        for (int c0 = c_lo; c0 <= c_hi; c0 += 4) {
+          float pv[4][RC];
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            const int cc = c0 + jj;
+            if (cc <= c_hi) {
+              const int sl = (ln_begin(cc, p.iters, p.grid) >= lo) ? 0 : 1;
+              const float* r = p.ws + ((size_t)(cc * 2 + sl) * rows_half + r0) * kLnTile + nl;
+#pragma unroll
+              for (int i = 0; i < RC; ++i) pv[jj][i] = __ldcg(r + i * kLnTile);
+            }
+          }
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj)
+            if (c0 + jj <= c_hi) {
+#pragma unroll
+              for (int i = 0; i < RC; ++i) v[i] += pv[jj][i];
+            }
+        }
+      };
       if (p.silu_f) {
         // lanes 0-63 hold gate, 64-127 up of the same 64 ffn columns: exchange through smem
-        // in 16-row chunks, then act = silu(g) * u (the formula of choreo_silu_mul) as bf16
+        // in chunks, then act = silu(g) * u (the formula of choreo_silu_mul) as bf16
         // (hi/lo rows r and out_rows + r when split)
         const int j = t * 64 + (nl & 63);
         __nv_bfloat16* act = reinterpret_cast<__nv_bfloat16*>(p.y);
         const int64_t lo_off = (int64_t)p.out_rows * p.silu_f;
-#pragma unroll
-        for (int r0 = 0; r0 < (p_split_rows<NX>()); r0 += 16) {
+        for (int r0 = 0; r0 < rows_half; r0 += RC) {
+          float v[16];
+          final_chunk(r0, v);
           asm volatile("bar.sync 1, 128;\n" ::: "memory");  // s_xch free
           if (nl >= 64) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const int r = r0 + i;
-              if (r < NX) s_xch[i * 64 + (nl - 64)] = p.split ? (r < NX / 2 ? acc[r] + acc[NX / 2 + r] : 0.f) : acc[r];
-            }
+            for (int i = 0; i < RC; ++i) s_xch[i * 64 + (nl - 64)] = v[i];
           }
           asm volatile("bar.sync 1, 128;\n" ::: "memory");
           if (nl < 64) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
+            for (int i = 0; i < RC; ++i) {
               const int r = r0 + i;
-              if (r < p.out_rows && r < NX) {
-                const float g = p.split ? (r < NX / 2 ? acc[r] + acc[NX / 2 + r] : 0.f) : acc[r];
-                const float v = g / (1.0f + expf(-g)) * s_xch[i * 64 + nl];
-                const __nv_bfloat16 hi = __float2bfloat16_rn(v);
-                act[(int64_t)r * p.silu_f + j] = hi;
-                if (p.split) act[lo_off + (int64_t)r * p.silu_f + j] = __float2bfloat16_rn(v - __bfloat162float(hi));
+              if (r < p.out_rows) {
+                const float g = v[i];
+                const float vv = g / (1.0f + expf(-g)) * s_xch[i * 64 + nl];
+                const __nv_bfloat16 h = __float2bfloat16_rn(vv);
+                act[(int64_t)r * p.silu_f + j] = h;
+                if (p.split) act[lo_off + (int64_t)r * p.silu_f + j] = __float2bfloat16_rn(vv - __bfloat162float(h));
               }
             }
           }
         }
-      } else if (n < p.N) {
-        if (p.split) {
+      } else {
+        // every lane runs final_chunk: tcgen05.ld is warp-collective (columns past N too)
+        for (int r0 = 0; r0 < rows_half && r0 < p.out_rows; r0 += RC) {
+          float v[16];
+          final_chunk(r0, v);
+          if (n < p.N) {
 #pragma unroll
-          for (int r = 0; r < NX / 2; ++r)
-            if (r < p.out_rows) p.y[(size_t)r * p.N + n] = acc[r] + acc[NX / 2 + r];
-        } else {
-#pragma unroll
-          for (int r = 0; r < NX; ++r)
-            if (r < p.out_rows) p.y[(size_t)r * p.N + n] = acc[r];
+            for (int i = 0; i < RC; ++i)
+              if (r0 + i < p.out_rows) p.y[(size_t)(r0 + i) * p.N + n] = v[i];
+          }
         }
+      }
+      if (!cut) {
+        tc_fence_before();
+        mbar_arrive(&acc_empty[buf]);
       }
     }
   }
@@ -318,11 +370,11 @@ static int linear_impl(const void* x, int x_rows, int split, const void* w, int 
   if (!x || !w || !y || !workspace || !tile_counters || x_rows <= 0 || n <= 0 || k <= 0 ||
       (split && (x_rows & 1)))
     return CHOREO_EINVAL;
-  if (x_rows > 128 || k % 8) return CHOREO_EUNSUPPORTED;  // TMA: 16-byte row pitch
+  if (x_rows > 256 || (!split && x_rows > 128) || k % 8) return CHOREO_EUNSUPPORTED;
   if (silu_f && silu_f % 64) return CHOREO_EUNSUPPORTED;
   const int R = split ? x_rows / 2 : x_rows;  // output rows
   const int xr = split ? 2 * R : R;
-  const int NX = xr <= 16 ? 16 : xr <= 32 ? 32 : xr <= 64 ? 64 : 128;
+  const int NX = xr <= 16 ? 16 : xr <= 32 ? 32 : xr <= 64 ? 64 : xr <= 128 ? 128 : 256;
   static int ksub = -1;
   if (ksub < 0) {
     const char* e = getenv("CHOREO_K7_KSUB");
@@ -330,7 +382,8 @@ static int linear_impl(const void* x, int x_rows, int split, const void* w, int 
     if (ksub != 1 && ksub != 2 && ksub != 4) ksub = 2;
   }
   const int n_tiles = silu_f ? silu_f / 64 : (n + kLnTile - 1) / kLnTile;
-  const int KB = (k + kLnKB * ksub - 1) / (kLnKB * ksub);  // iteration = ksub k-blocks
+  const int ks = NX == 256 ? 1 : ksub;  // 256 activation rows: one k-block per stage
+  const int KB = (k + kLnKB * ks - 1) / (kLnKB * ks);  // iteration = ks k-blocks
   const int iters = n_tiles * KB;
   int grid = grid_ctas > 0 ? grid_ctas : 148;
   if (grid > iters) grid = iters;
@@ -362,7 +415,9 @@ static int linear_impl(const void* x, int x_rows, int split, const void* w, int 
     case 16: LN_CASE(16)
     case 32: LN_CASE(32)
     case 64: LN_CASE(64)
-    default: LN_CASE(128)
+    case 128: LN_CASE(128)
+    default:  // 256 activation rows: one k-block per stage (48 KB)
+      return launch_linear<256, 1>(LN_STAGES(256, 1), x, x_rows, w, n, k, s);
   }
 #undef LN_CASE
 #undef LN_STAGES

@@ -239,7 +239,10 @@ class Runner:
         return out
 
     def _k7_ok(self, rows: int) -> bool:
-        """K7 takes the step when its stacked GEMM input has <= 128 rows."""
+        """K7 takes the step when its stacked GEMM input has <= 128 rows.  (K7 runs up to 256
+        stacked rows, NX 256, but measured at the C3 header step -- 72 rows = 144 stacked --
+        it is slower than cuBLAS there: every weight tile re-reads a 32 KB activation block
+        per k-block and only 64 KB of weights fit in flight per SM.)"""
         return self.k7 and (2 * rows if self.split else rows) <= 128
 
     def _lin(self, a, w, rows: int):
@@ -390,7 +393,7 @@ class Runner:
         return self._chain_bufs
 
     def _lin_buffers(self) -> None:
-        self._k7_ws = torch.empty(148 * 2 * 128 * 128, dtype=torch.float32, device=self.dev)
+        self._k7_ws = torch.empty(148 * 2 * 256 * 128, dtype=torch.float32, device=self.dev)
         n_max = max(self.w.out_head.shape[0], self.w.layers[0]["w_gu"].shape[0],
                     self.w.layers[0]["w_qkv"].shape[0], self.d)
         self._k7_cnt = torch.zeros(cdiv(n_max, 128) + 1, dtype=torch.int32, device=self.dev)

@@ -31,7 +31,7 @@ SHAPES_8B = {"qkv": (6144, D), "o_proj": (D, D), "down": (D, F), "head": (V, D)}
 def _k7(x, split, w):
     rows = x.shape[0] // (2 if split else 1)
     y = torch.full((rows, w.shape[0]), float("nan"), device="cuda")
-    ws = torch.empty(148 * 2 * 128 * 128, device="cuda")
+    ws = torch.empty(148 * 2 * 256 * 128, device="cuda")
     cnt = torch.zeros((w.shape[0] + 127) // 128, dtype=torch.int32, device="cuda")
     nat.linear_skinny(x.data_ptr(), x.shape[0], int(split), w.data_ptr(), w.shape[0], w.shape[1],
                       y.data_ptr(), ws.data_ptr(), cnt.data_ptr(), 0, _stream())
@@ -40,11 +40,13 @@ def _k7(x, split, w):
     return y
 
 
-@pytest.mark.parametrize("rows", [8, 64])
+@pytest.mark.parametrize("rows", [8, 64, 72, 128])
 @pytest.mark.parametrize("name", sorted(SHAPES_8B))
 def test_k7_values_at_8b_decode_shapes(name, rows):
-    """K7 at the bench's decode GEMMs (8 agents = 16 stacked hi/lo rows, NX 16) and at its
-    64-row limit (NX 128), including the 128256 x 4096 head (1002 tiles, 1 GB of weights):
+    """K7 at the bench's decode GEMMs (8 agents = 16 stacked hi/lo rows, NX 16), at 64 rows
+    (NX 128), at the C3 parallel header step (8 agents x 9 header tokens = 72 rows = 144
+    stacked, NX 256) and at its 128-row limit, including the 128256 x 4096 head (1002
+    tiles, 1 GB of weights):
     within 1e-4 relative of the f32 matmul of the same bf16 operands, bitwise
     deterministic run to run."""
     torch.backends.cuda.matmul.allow_tf32 = False
@@ -67,7 +69,7 @@ def test_k7_values_at_8b_decode_shapes(name, rows):
     assert float((y - exact).abs().max()) <= 1e-3 * float(exact.abs().max())
 
 
-@pytest.mark.parametrize("rows", [8, 64])
+@pytest.mark.parametrize("rows", [8, 64, 72])
 def test_k7_gate_up_silu_at_8b(rows):
     """The fused gate|up + SiLU epilogue at the 8B FFN (28672 x 4096 weights)."""
     g = torch.Generator(device="cuda").manual_seed(rows)
@@ -78,7 +80,7 @@ def test_k7_gate_up_silu_at_8b(rows):
     w = ((torch.rand(2 * F, D, device="cuda", generator=g) * 2 - 1) * (6 / (D + F)) ** 0.5
          ).to(torch.bfloat16)
     act = torch.empty(2 * rows, F, dtype=torch.bfloat16, device="cuda")
-    ws = torch.empty(148 * 2 * 128 * 128, device="cuda")
+    ws = torch.empty(148 * 2 * 256 * 128, device="cuda")
     cnt = torch.zeros(F // 64 + 1, dtype=torch.int32, device="cuda")
     nat.linear_gate_up_silu(xm.data_ptr(), 2 * rows, 1, w.data_ptr(), F, D, act.data_ptr(),
                             ws.data_ptr(), cnt.data_ptr(), _stream())

@@ -425,7 +425,7 @@ def test_decode_v2_matches_dense_reference(hd, H, Hk, ppi):
 def _linear(x, split, w, grid=0):
     rows = x.shape[0] // (2 if split else 1)
     y = torch.full((rows, w.shape[0]), float("nan"), device="cuda")
-    ws = torch.empty(148 * 2 * 128 * 128, device="cuda")
+    ws = torch.empty(148 * 2 * 256 * 128, device="cuda")
     cnt = torch.zeros((w.shape[0] + 127) // 128, dtype=torch.int32, device="cuda")
     nat.linear_skinny(x.data_ptr(), x.shape[0], int(split), w.data_ptr(), w.shape[0], w.shape[1],
                       y.data_ptr(), ws.data_ptr(), cnt.data_ptr(), grid, _stream())
@@ -436,13 +436,14 @@ def _linear(x, split, w, grid=0):
 
 @pytest.mark.parametrize("rows,split", [(1, False), (8, True), (16, False), (16, True), (5, True),
                                         (32, True), (40, False), (64, False), (64, True),
-                                        (100, False), (37, True)])
+                                        (100, False), (37, True), (72, True), (128, True),
+                                        (65, True), (128, False)])
 @pytest.mark.parametrize("n,k", [(4096, 4096), (6144, 4096), (4096, 14336), (300, 64), (1000, 200)])
 def test_linear_skinny_matches_f32_reference(rows, split, n, k):
     """K7 (tcgen05 stream-K weight streaming) = x @ w^T in f32 over bf16 inputs; with split
     activations the hi/lo halves are summed; deterministic run to run."""
-    if split and 2 * rows > 128:
-        pytest.skip("split supports <= 64 output rows")
+    if split and 2 * rows > 256:
+        pytest.skip("split supports <= 128 output rows")
     g = torch.Generator(device="cuda").manual_seed(rows * 7 + n)
     xm = torch.randn(2 * rows if split else rows, k, device="cuda", generator=g).to(torch.bfloat16)
     w = (torch.randn(n, k, device="cuda", generator=g) / k ** 0.5).to(torch.bfloat16)
@@ -486,7 +487,7 @@ def test_select_nucleus_matches_host_sampler(vocab):
     assert out.cpu().tolist() == want
 
 
-@pytest.mark.parametrize("rows,split", [(8, True), (3, True), (20, False), (64, True)])
+@pytest.mark.parametrize("rows,split", [(8, True), (3, True), (20, False), (64, True), (72, True)])
 @pytest.mark.parametrize("f,d", [(14336, 4096), (256, 192)])
 def test_linear_gate_up_silu_matches_separate(rows, split, f, d):
     """K7 with SwiGLU fused (tiles pair 64 gate rows with their 64 up rows) == K7 on
@@ -498,7 +499,7 @@ def test_linear_gate_up_silu_matches_separate(rows, split, f, d):
     S = 2 if split else 1
     fused = torch.zeros(S * rows, f, dtype=torch.bfloat16, device="cuda")
     sep = torch.zeros(S * rows, f, dtype=torch.bfloat16, device="cuda")
-    ws = torch.empty(148 * 2 * 128 * 128, device="cuda")
+    ws = torch.empty(148 * 2 * 256 * 128, device="cuda")
     cnt = torch.zeros(2 * f // 128 + 2, dtype=torch.int32, device="cuda")
     nat.linear_gate_up_silu(xm.data_ptr(), xm.shape[0], int(split), w.data_ptr(), f, d,
                             fused.data_ptr(), ws.data_ptr(), cnt.data_ptr(), _stream())
@@ -519,7 +520,7 @@ def test_linear_gate_up_silu_matches_separate(rows, split, f, d):
 
 
 @pytest.mark.parametrize("rows,split,grid", [(16, True, 0), (16, True, 37), (8, False, 0),
-                                             (40, False, 37), (5, True, 148)])
+                                             (40, False, 37), (5, True, 148), (72, True, 0)])
 def test_k7_pieces_consumers_bit_identical(rows, split, grid):
     """Deferred K7 outputs (cut tiles left as per-CTA pieces, ChoreoK7Pieces) read through
     RoPE/append and residual+RMSNorm give exactly the values of the reduced K7 path."""
@@ -531,7 +532,7 @@ def test_k7_pieces_consumers_bit_identical(rows, split, grid):
     rot = RotationTableDevice(cfg, "cuda")
     g = torch.Generator(device="cuda").manual_seed(rows + grid)
     xm = torch.randn(2 * rows if split else rows, d, device="cuda", generator=g).to(torch.bfloat16)
-    ws = torch.empty(148 * 2 * 128 * 128, device="cuda")
+    ws = torch.empty(148 * 2 * 256 * 128, device="cuda")
     st = _stream()
     R = rows
 
