@@ -5,7 +5,11 @@
 // values come from the f64-derived table cos/sin[(delta + W) * (hd/2) + i] stored as
 // f32 (tensor.py:103-107), so index math is exact and values match the reference's
 // table cast to f32.
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
+#include "sm100.cuh"
+#include "tmap.cuh"
 
 namespace choreo {
 
@@ -141,6 +145,68 @@ __global__ void __launch_bounds__(256) rerotate_kernel(
   }
 }
 
+// bf16 pools, head_dim 64 / 128 (the 8B geometry): the page tile comes in by TMA (the
+// pool's 2D view [layers*kv*pages*64][hd], SW128 boxes of 64 keys x 64 dims -- the map K4 /
+// K5 v2 use), one bulk copy per (layer, kv head, listed page) CTA with no per-thread
+// address math on the read side; the valid rows are rotated out of shared memory and
+// written back with 16-byte stores (slots past page_len are never written).
+template <int HD>
+__global__ void __launch_bounds__(128) rerotate_tma_kernel(
+    __nv_bfloat16* __restrict__ kp, const __grid_constant__ CUtensorMap tm, int n_kv,
+    int n_pages, const int32_t* __restrict__ pages, const int32_t* __restrict__ page_len,
+    const int32_t* __restrict__ delta, int n_list, const float* __restrict__ cos_t,
+    const float* __restrict__ sin_t, int max_delta) {
+  using namespace sm100;
+  constexpr int kR = HD / 64, kHalf = 64 * 128;
+  __shared__ __align__(1024) uint8_t tile[kR * kHalf];
+  __shared__ float cs[HD];  // [hd/2] cos then [hd/2] sin
+  __shared__ uint64_t bar;
+  pdl_trigger();
+  const int i = blockIdx.x % n_list;
+  const int lh = blockIdx.x / n_list;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  pdl_wait();
+  const int dl = delta[i];
+  if (dl == 0) return;
+  const int len = page_len[i], half = HD >> 1;
+  const int layer = lh / n_kv, h = lh % n_kv;
+  const int64_t row0 = (((int64_t)layer * n_kv + h) * n_pages + pages[i]) * 64;
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(&bar, kR * kHalf);
+#pragma unroll
+    for (int r = 0; r < kR; ++r) tma_load_2d(tile + r * kHalf, &tm, &bar, r * 64, (int)row0);
+  }
+  const int64_t trow = (int64_t)(dl + max_delta) * half;
+  for (int j = threadIdx.x; j < half; j += blockDim.x) {
+    cs[j] = cos_t[trow + j];
+    cs[half + j] = sin_t[trow + j];
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  __nv_bfloat16* base = kp + row0 * HD;
+  constexpr int vpr = HD / 8;  // 16-byte vectors per key row
+  const int nvec = len * vpr;
+  for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
+    const int key = v / vpr, cch = v % vpr;
+    uint4 raw = *reinterpret_cast<const uint4*>(tile + (cch >> 3) * kHalf + key * 128 +
+                                                (((cch & 7) ^ (key & 7)) << 4));
+    __nv_bfloat16* x = reinterpret_cast<__nv_bfloat16*>(&raw);
+    const int p0 = cch * 4;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float c = cs[p0 + j], sn = cs[half + p0 + j];
+      const float e = __bfloat162float(x[2 * j]), o = __bfloat162float(x[2 * j + 1]);
+      x[2 * j] = __float2bfloat16_rn(e * c - o * sn);
+      x[2 * j + 1] = __float2bfloat16_rn(e * sn + o * c);
+    }
+    *reinterpret_cast<uint4*>(base + (int64_t)v * 8) = raw;
+  }
+}
+
 static int grid_for(int64_t total, int threads) {
   int64_t b = (total + threads - 1) / threads;
   const int64_t cap = 148 * 16;
@@ -219,6 +285,21 @@ int choreo_rerotate(void* k_pool, int pool_dtype, int n_layers, int n_kv, int n_
   if (blocks > 0x7fffffff) return CHOREO_EUNSUPPORTED;
   auto s = as_stream(stream);
   const size_t smem = sizeof(float) * head_dim;
+  const uint64_t pool_rows = (uint64_t)n_layers * n_kv * n_pages * page_size;
+  if (pool_dtype == CHOREO_BF16 && page_size == 64 && (head_dim == 64 || head_dim == 128) &&
+      pool_rows <= 0x7fffffffull) {
+    CUtensorMap tm;
+    if (!tmap_bf16_2d(&tm, k_pool, pool_rows, (uint64_t)head_dim, 64, 64,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B))
+      return CHOREO_ELAUNCH;
+    if (head_dim == 128)
+      launch_k(rerotate_tma_kernel<128>, (int)blocks, 128, 0, s, (__nv_bfloat16*)k_pool, tm, n_kv,
+               n_pages, pages, page_len, delta, n_list, cos_t, sin_t, max_delta);
+    else
+      launch_k(rerotate_tma_kernel<64>, (int)blocks, 128, 0, s, (__nv_bfloat16*)k_pool, tm, n_kv,
+               n_pages, pages, page_len, delta, n_list, cos_t, sin_t, max_delta);
+    return launch_status("choreo_rerotate");
+  }
   if (pool_dtype == CHOREO_BF16)
     launch_k(rerotate_kernel<__nv_bfloat16, 4>, (int)blocks, 256, smem, s, 
         (__nv_bfloat16*)k_pool, n_kv, n_pages, page_size, head_dim, pages, page_len, delta, n_list,

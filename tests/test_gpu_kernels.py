@@ -64,8 +64,9 @@ def test_rope_append(dt, hd, H, Hk):
 
 
 @pytest.mark.parametrize("dt", ["f32", "bf16"])
-@pytest.mark.parametrize("hd", [8, 16, 128])
+@pytest.mark.parametrize("hd", [8, 16, 64, 128])
 def test_rerotate(dt, hd):
+    """K2 (bf16 pools at hd 64 / 128: TMA-fed page tiles) against the oracle's rotor."""
     W = 2048
     cfg = ModelConfig(n_layers=3, n_heads=2, head_dim=hd, context_window=W)
     rot = RotationTableDevice(cfg, "cuda")
