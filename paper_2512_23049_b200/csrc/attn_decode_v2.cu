@@ -139,10 +139,12 @@ __global__ void __launch_bounds__(kDvThreads, 1)
     }
     for (int i = 0; i < kDvUnits; ++i) {
       mbar_init(&unit_full[i], 32);
-      mbar_init(&unit_empty[i], kDvConsumers);
+      mbar_init(&unit_empty[i], kDvConsumers * 32);  // every consumer lane (own reads)
     }
-    mbar_init(&merge_full, kDvConsumers);
-    mbar_init(&merge_empty, 2);
+    // merge scratch hand-offs are arrived on by every lane that wrote / read it (each
+    // lane's own accesses are then ordered by its own arrive -- no reliance on __syncwarp)
+    mbar_init(&merge_full, kDvConsumers * 32);
+    mbar_init(&merge_empty, 2 * 32);
     fence_barrier_init();
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
@@ -231,8 +233,7 @@ __global__ void __launch_bounds__(kDvThreads, 1)
     for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++u) {
       mbar_wait(&merge_full, u & 1);
       dv_merge_unit<HD>(p, merge, mt, lane, G);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&merge_empty);
+      mbar_arrive(&merge_empty);
     }
     return;
   }
@@ -406,8 +407,7 @@ __global__ void __launch_bounds__(kDvThreads, 1)
       if (lane == 0) mbar_arrive(&empty_bar[st]);
     }
 
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&unit_empty[sl]);
+    mbar_arrive(&unit_empty[sl]);
     // ---- hand the key-slice state to the merge warps ----
     lA += __shfl_xor_sync(0xffffffffu, lA, 1);
     lA += __shfl_xor_sync(0xffffffffu, lA, 2);
@@ -437,8 +437,7 @@ __global__ void __launch_bounds__(kDvThreads, 1)
       hdr[1] = pbase;
       hdr[2] = kvh;
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&merge_full);
+    mbar_arrive(&merge_full);
   }
 }
 
