@@ -165,7 +165,8 @@ __global__ void __launch_bounds__(kChThreads, 1)
   __shared__ float s_xch[16 * 64];  // gate|up: up values of 16 rows x 64 columns
   __shared__ float s_red[4][16];    // per-quadrant partial sums of squares
   __shared__ float s_r[128];        // per-row RMSNorm scale of the current phase
-  __shared__ int s_pos[128], s_pg[128], s_sl[128];  // qkv: position, page, slot per row
+  __shared__ int s_pos[128];         // qkv: position per row
+  __shared__ long long s_koff[128];  // qkv: pool offset of (layer, kv head 0, page, slot, 0)
 
   pdl_trigger();
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -347,8 +348,8 @@ __global__ void __launch_bounds__(kChThreads, 1)
           s_r[et] = 1.0f / sqrtf(acc / (float)d + p.eps);
           if (ph == kPhQKV) {
             s_pos[et] = __ldg(p.pos + et);
-            s_pg[et] = __ldg(p.page + et);
-            s_sl[et] = __ldg(p.slot + et);
+            s_koff[et] = pool_off(p.layer, 0, __ldg(p.page + et), __ldg(p.slot + et), p.n_kv,
+                                  p.n_pages, p.page_size, p.hd);
           }
         }
         epi_bar();
@@ -471,6 +472,14 @@ __global__ void __launch_bounds__(kChThreads, 1)
           } else {
             tmem_rows(r0, v);
           }
+#ifdef CHOREO_TRACE
+          if (et == 0 && last_seg && r0 == 0 && (ph == kPhD || ph == kPhQKV)) {
+            float sacc = 0.f;
+            for (int i = 0; i < RC; ++i) sacc += v[i];  // consume the loads before the stamp
+            if (sacc == 12345.678f) s_last = 7;
+            TR(ph == kPhD ? 42 : 45);
+          }
+#endif
           if (ph == kPhO || ph == kPhD) {
             // x += y ; h = hi/lo(x * gamma) ; partial sums of squares per row.  Every load of
             // the chunk is issued before any store (stores could alias the loads for the
@@ -500,6 +509,7 @@ __global__ void __launch_bounds__(kChThreads, 1)
                 }
               }
             }
+            if (et == 0 && last_seg && r0 == 0 && ph == kPhD) TR(43);
             if (P.gamma) {
 #pragma unroll
               for (int i = 0; i < RC; ++i) {
@@ -563,23 +573,22 @@ __global__ void __launch_bounds__(kChThreads, 1)
               val[i] = r0 + i < R ? s_r[r0 + i] * v[i] : 0.f;
               other[i] = __shfl_xor_sync(0xffffffffu, val[i], 1);
             }
+            // destination of this lane's column: q (f32) or the K / V pool slot of the row
+            const int64_t hs = (int64_t)p.n_pages * p.page_size * hd;  // pool stride per kv head
+            const int kind = head < H ? 0 : head < H + Hk ? 1 : 2;
+            const int64_t coff = kind == 0 ? (int64_t)head * hd + kk
+                                 : (int64_t)(kind == 1 ? head - H : head - H - Hk) * hs + kk;
+            __nv_bfloat16* const pool = kind == 1 ? p.k_pool : p.v_pool;
 #pragma unroll
             for (int i = 0; i < RC; ++i) {
               const int row = r0 + i;
               if (row < R && n < P.N) {
-                const int pg = s_pg[row], sl = s_sl[row];
-                if (head >= H + Hk) {
-                  p.v_pool[pool_off(p.layer, head - H - Hk, pg, sl, Hk, p.n_pages, p.page_size, hd) + kk] =
-                      __float2bfloat16_rn(val[i]);
-                } else {
-                  const float ev = odd ? other[i] : val[i], ov = odd ? val[i] : other[i];
-                  const float res = odd ? (ev * sn[i] + ov * cs[i]) : (ev * cs[i] - ov * sn[i]);
-                  if (head < H)
-                    p.q[((size_t)row * H + head) * hd + kk] = res;
-                  else
-                    p.k_pool[pool_off(p.layer, head - H, pg, sl, Hk, p.n_pages, p.page_size, hd) + kk] =
-                        __float2bfloat16_rn(res);
-                }
+                const float ev = odd ? other[i] : val[i], ov = odd ? val[i] : other[i];
+                const float res = odd ? (ev * sn[i] + ov * cs[i]) : (ev * cs[i] - ov * sn[i]);
+                if (kind == 0)
+                  p.q[(int64_t)row * H * hd + coff] = res;
+                else
+                  pool[s_koff[row] + coff] = __float2bfloat16_rn(kind == 1 ? res : val[i]);
               }
             }
           }

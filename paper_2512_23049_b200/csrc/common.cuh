@@ -107,11 +107,14 @@ __device__ __forceinline__ float warp_max(float v) {
 
 // stream-K split of `iters` iterations over `grid` CTAs (K7): first iteration of CTA c, and
 // the CTA owning iteration i (every CTA owns >= 1 iteration: grid <= iters)
+// (32-bit unsigned arithmetic: c * iters and (i + 1) * grid stay below 2^32 for every
+// shape here -- grid <= 148, iters <= 2^24 -- and a 64-bit division is a ~100-instruction
+// software routine that these kernels inline in many places)
 __host__ __device__ __forceinline__ int ln_begin(int c, int iters, int grid) {
-  return (int)(((long long)c * iters) / grid);
+  return (int)(((unsigned)c * (unsigned)iters) / (unsigned)grid);
 }
 __host__ __device__ __forceinline__ int ln_owner(int i, int iters, int grid) {
-  return (int)((((long long)i + 1) * grid - 1) / iters);
+  return (int)((((unsigned)i + 1u) * (unsigned)grid - 1u) / (unsigned)iters);
 }
 
 // element (r, n..n+W-1) of a deferred K7 output (ChoreoK7Pieces): y for tiles one CTA owns,

@@ -63,6 +63,10 @@ for ph, pn in enumerate(["o", "gu", "down", "qkv"]):
     print(pn.ljust(5) + "  ".join(f"{n}: {np.nanmin(cols[:, i]):7.2f}/{np.nanmedian(cols[:, i]):7.2f}/"
                                   f"{np.nanmax(cols[:, i]):7.2f}" for i, n in enumerate(names)))
     ep = rel[:, 26 + ph * 4: 30 + ph * 4]
+    if ph == 2:
+        print("      down final: v ready %.2f  after x/h stores %.2f" % (np.nanmedian(rel[:, 42]), np.nanmedian(rel[:, 43])))
+    if ph == 3:
+        print("      qkv final: v ready %.2f" % np.nanmedian(rel[:, 45]))
     print("      last segment: " + "  ".join(
         f"{n}: {np.nanmin(ep[:, i]):7.2f}/{np.nanmedian(ep[:, i]):7.2f}/{np.nanmax(ep[:, i]):7.2f}"
         for i, n in enumerate(["acc_full", "pieces_in", "final", "published"])))
