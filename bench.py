@@ -189,9 +189,9 @@ class ClockSampler:
 
 def ncu_traffic() -> dict:
     """Per-launch DRAM traffic of K7 / K5 v2 from the committed ncu capture of the same
-    decode step (profiles/r1_traffic.json, dram__bytes_read.sum + dram__bytes_write.sum)."""
+    decode step (profiles/r2_traffic.json, dram__bytes_read.sum + dram__bytes_write.sum)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "r2_traffic.json")) as fh:
             return json.load(fh)
     except OSError:
         return {}
@@ -775,7 +775,7 @@ def main() -> None:
         del eng, weights
         torch.cuda.empty_cache()
         kernels = ([kb.k2_rerotate(), kb.k4_prefill(), kb.k5_decode(1, v2=True),
-                    kb.k5_decode(8, v2=True)] + kb.k7_linear())
+                    kb.k5_decode(8, v2=True)] + kb.k7_linear() + [kb.k8_chain()])
     c2 = None
     if world == 1 and not args.no_c2:
         c2 = c2_agents(P, rank)

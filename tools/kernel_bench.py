@@ -285,7 +285,7 @@ def k7_linear(x_rows: int = 8, split: bool = True) -> list:
     shapes = {"qkv": ((cfg.n_heads + 2 * cfg.kv_heads) * cfg.head_dim, d), "o_proj": (d, d),
               "gate_up": (2 * f, d), "down": (d, f), "head": (cfg.vocab_size, d)}
     rows = 2 * x_rows if split else x_rows
-    ws = torch.empty(148 * 2 * 128 * 128, device="cuda")
+    ws = torch.empty(148 * 2 * 256 * 128, device="cuda")
     pk = peaks()
     out = []
     stream = torch.cuda.current_stream().cuda_stream
@@ -331,6 +331,50 @@ def k5_sweep() -> list:
             out.append((tc, ppi, r["us"], r["combine_us"], r["items"]))
     os.environ.pop("K5_PPI")
     return out
+
+
+def k8_chain(rows: int = 8) -> dict:
+    """K8 layer chain (o_proj, gate|up, down, next qkv in one persistent launch, norms /
+    SwiGLU / RoPE in the epilogues) at the 8B layer shape, back-to-back launches (438 MB of
+    weights each, > L2), beside the sum of the four K7 launches at the same shapes."""
+    import ctypes
+
+    sys.path.insert(0, ROOT)
+    from tests.test_gpu_chain import _Bufs, _Layer, _rope_tables
+
+    cfg = LLAMA_3_1_8B
+    d, H, Hk, hd, F = cfg.model_dim, cfg.n_heads, cfg.kv_heads, cfg.head_dim, cfg.ffn_dim
+    lw = _Layer(d, H, Hk, hd, F, seed=1)
+    b = _Bufs(rows, d, H, Hk, hd, F, True, n_pages=16)
+    W = 8192
+    cos_t, sin_t = _rope_tables(hd, W)
+    pos = torch.arange(rows, dtype=torch.int32, device="cuda") + 100
+    page = torch.zeros(rows, dtype=torch.int32, device="cuda")
+    slot = torch.arange(rows, dtype=torch.int32, device="cuda")
+    for t in (b.x, b.attn, b.h_a, b.h_b, b.act):
+        t.normal_()
+    b.ssq_a.fill_(float(d))
+    b.ssq_b.fill_(float(d))
+    stream = torch.cuda.current_stream().cuda_stream
+    st = nat.LayerChain(
+        n_rows=rows, split=1, d=d, n_heads=H, n_kv=Hk, head_dim=hd, ffn_dim=F, eps=1e-6, phases=15,
+        wo=lw.wo.data_ptr(), ffn_norm=lw.g_ffn.data_ptr(), w_gu=lw.w_gu.data_ptr(),
+        w_down=lw.w_down.data_ptr(), attn_norm_next=lw.g_attn.data_ptr(),
+        w_qkv=lw.w_qkv.data_ptr(), layer_qkv=0, x=b.x.data_ptr(), attn=b.attn.data_ptr(),
+        h_a=b.h_a.data_ptr(), act=b.act.data_ptr(), h_b=b.h_b.data_ptr(),
+        ssq_a=b.ssq_a.data_ptr(), ssq_b=b.ssq_b.data_ptr(), q=b.q.data_ptr(),
+        k_pool=b.k_pool.data_ptr(), v_pool=b.v_pool.data_ptr(), n_pages=b.k_pool.shape[2],
+        page_size=64, pos=pos.data_ptr(), page=page.data_ptr(), slot=slot.data_ptr(),
+        cos_t=cos_t.data_ptr(), sin_t=sin_t.data_ptr(), max_delta=W, ws=b.ws.data_ptr(),
+        counters=b.counters.data_ptr(), done=b.done.data_ptr())
+    t = _time(lambda: nat.layer_chain(ctypes.byref(st), stream))
+    nbytes = sum(w.numel() * 2 for w in (lw.wo, lw.w_gu, lw.w_down, lw.w_qkv))
+    pk = peaks()
+    ach = nbytes / t / 1e9
+    return {"kernel": "choreo_layer_chain (K8: o_proj + gate|up + down + next qkv, one launch)",
+            "bound": "hbm", "shape": f"{rows} rows (x2 hi/lo), 8B layer", "algorithmic_bytes": nbytes,
+            "us": round(t * 1e6, 2), "achieved": round(ach, 1), "unit": "GB/s",
+            "peak": pk["hbm_gbs"], "frac": round(ach / pk["hbm_gbs"], 4)}
 
 
 def run_all() -> list:
