@@ -47,6 +47,14 @@ const char* choreo_last_error(void);
 int choreo_embed(const void* embed, int embed_dtype, int d, const int32_t* ids, int n_rows,
                  float* x, void* stream);
 
+/* choreo_embed where row r takes sel_src[sel[r]] instead of ids[r] when sel[r] >= 0: the
+ * token a device selection (choreo_select_greedy / _nucleus output) of the previous step
+ * left in device memory, so a pipelined decode step needs no host round trip for its
+ * input ids. */
+int choreo_embed_select(const void* embed, int embed_dtype, int d, const int32_t* ids,
+                        const int32_t* sel, const int32_t* sel_src, int n_rows, float* x,
+                        void* stream);
+
 /* Split activations ("*_split" flags): a bf16 activation row y is emitted as the pair
  * hi = bf16(y) at row r and lo = bf16(y - hi) at row n + r of a stacked [2n][.] buffer;
  * a bf16 GEMM over the 2n rows then a sum of the two output halves sees y with ~16

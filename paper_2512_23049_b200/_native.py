@@ -24,6 +24,7 @@ _F = ctypes.c_float
 # name -> argtypes (all functions return int status)
 SIGNATURES: dict[str, list] = {
     "choreo_embed": [_P, _I, _I, _P, _I, _P, _P],
+    "choreo_embed_select": [_P, _I, _I, _P, _P, _P, _I, _P, _P],
     "choreo_residual_rmsnorm": [_P, _P, _I, _I, _P, _I, _I, _I, _F, _P, _I, _I, _P, _I, _P],
     "choreo_silu_mul": [_P, _I, _I, _I, _I, _P, _I, _I, _P],
     "choreo_rope_append": [_P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I,
@@ -95,6 +96,7 @@ class _Caller:
 
 
 embed = _Caller("choreo_embed")
+embed_select = _Caller("choreo_embed_select")
 residual_rmsnorm = _Caller("choreo_residual_rmsnorm")
 linear_skinny_pieces = _Caller("choreo_linear_skinny_pieces")
 rope_append_pieces = _Caller("choreo_rope_append_pieces")

@@ -253,6 +253,23 @@ class DeviceKvCache:
         self._views = None
         return pages, slots
 
+    def set_token(self, message_id: int, index: int, token: int) -> None:
+        """Record the id of a token reserved before its value was known on the host (a
+        pipelined decode step encodes the device-selected token of the previous step)."""
+        self._entry(message_id).tokens[index] = int(token)
+        self._views = None
+
+    def unreserve_last(self, message_id: int) -> None:
+        """Undo the last reserve_slots of one token: a pipelined decode step encoded the
+        device-selected token of a message the host then saw stop (EOS, window, limit).
+        The slot lies past the message's length again, so nothing can see it; its page
+        stays with the message."""
+        e = self._entry(message_id)
+        e.tokens.pop()
+        self.msg_len.set(message_id, e.length)
+        self.token_count -= 1
+        self._views = None
+
     def release_prefix_pages(self, message_id: int, n_tokens: int) -> int:
         """Return the pages holding only tokens [0, n_tokens) of a message to the pool (the
         re-encoding comparator's dead prompt copies).  The message must never be read

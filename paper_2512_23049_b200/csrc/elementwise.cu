@@ -14,12 +14,17 @@ void set_last_error(const char* where, cudaError_t err) {
   snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(err));
 }
 
+// sel (optional): row r embeds sel_src[sel[r]] instead of ids[r] when sel[r] >= 0 -- the
+// token a device selection (K6 / K6b) of the previous step wrote, so a pipelined decode
+// step needs no host round trip for its input ids.
 __global__ void embed_kernel(const void* __restrict__ embed, int dt, int d,
-                             const int32_t* __restrict__ ids, float* __restrict__ x) {
+                             const int32_t* __restrict__ ids, const int32_t* __restrict__ sel,
+                             const int32_t* __restrict__ sel_src, float* __restrict__ x) {
   pdl_trigger();
   pdl_wait();
   const int r = blockIdx.x;
-  const int64_t src = (int64_t)ids[r] * d;
+  const int si = sel ? sel[r] : -1;
+  const int64_t src = (int64_t)(si >= 0 ? sel_src[si] : ids[r]) * d;
   for (int i = threadIdx.x; i < d; i += blockDim.x) x[(int64_t)r * d + i] = load_any(embed, dt, src + i);
 }
 
@@ -237,8 +242,20 @@ int choreo_embed(const void* embed, int embed_dtype, int d, const int32_t* ids, 
                  float* x, void* stream) {
   if (!embed || !ids || !x || d <= 0 || n_rows < 0 || !dtype_ok(embed_dtype)) return CHOREO_EINVAL;
   if (n_rows == 0) return CHOREO_OK;
-  launch_k(embed_kernel, n_rows, 256, 0, as_stream(stream), embed, embed_dtype, d, ids, x);
+  launch_k(embed_kernel, n_rows, 256, 0, as_stream(stream), embed, embed_dtype, d, ids,
+           (const int32_t*)nullptr, (const int32_t*)nullptr, x);
   return launch_status("choreo_embed");
+}
+
+int choreo_embed_select(const void* embed, int embed_dtype, int d, const int32_t* ids,
+                        const int32_t* sel, const int32_t* sel_src, int n_rows, float* x,
+                        void* stream) {
+  if (!embed || !ids || !sel || !sel_src || !x || d <= 0 || n_rows < 0 || !dtype_ok(embed_dtype))
+    return CHOREO_EINVAL;
+  if (n_rows == 0) return CHOREO_OK;
+  launch_k(embed_kernel, n_rows, 256, 0, as_stream(stream), embed, embed_dtype, d, ids, sel,
+           sel_src, x);
+  return launch_status("choreo_embed_select");
 }
 
 int choreo_residual_rmsnorm(float* x, const void* delta, int delta_dtype, int delta_split,

@@ -182,6 +182,9 @@ class Engine:
         self.tp, self.tp_group = tp, tp_group
         self.seed = int(seed)
         self.record_logits = record_logits
+        # free-running decode steps are enqueued before the previous step's tokens are read
+        # back (the selected ids flow to the next step on the device; _decode_loop)
+        self.pipeline = True
         self.device = device
         cache_cfg = tp.local_config() if tp is not None else self.config
         self.cache = DeviceKvCache(cache_cfg, capacity=capacity, dtype=weights.torch_dtype,
@@ -361,17 +364,46 @@ class Engine:
 
         Event order per message is the reference's: encode header, select,
         [encode token, select]*, with the stop rules of engine.py:394-413/448-463.
+
+        Pipelined (``self.pipeline``; free-running messages selected on the device, no host
+        logits): the step that encodes a message's selected token is enqueued BEFORE the
+        host reads that token back -- its embedding row takes the id straight from the
+        selection kernel's output (choreo_embed_select) -- and the host resolves the
+        previous step's tokens while the GPU runs the next one, so the per-step token
+        read-back no longer leaves the GPU idle.  A message the host then sees stop (EOS)
+        had one token encoded speculatively: its slot is unreserved (past the message's
+        length, so no later step can see it), and that row's accounting and selection are
+        dropped -- tokens, logits, cache and statistics equal the non-pipelined run.
         """
         pending = {s.mid: list(s.hdr) for s in states}
+        pipeline = self.pipeline and not self.record_logits and self.device_sampling
+        prev = None  # unresolved device selection of the previous step
         while True:
-            active = [s for s in states if not s.done and pending[s.mid]]
+            # ---- rows of this step: known tokens, and (pipelined) one device-selected token
+            # for each message of the unresolved selection that may still accept it
+            spec = {}
+            if prev is not None:
+                for s, k, i in prev["free"]:
+                    if not s.done and self._may_accept(s):
+                        spec[s.mid] = i
+            active = [s for s in states if not s.done and (pending[s.mid] or s.mid in spec)]
+            room = self.cache.capacity - self.cache.token_count
+            if prev is not None and sum(len(pending[s.mid]) or 1 for s in active) > room:
+                # not every row fits: settle the previous selection first, then run the
+                # reference's capacity order on known tokens
+                self._resolve(prev, stats, t0, pending, None)
+                prev, spec = None, {}
+                active = [s for s in states if not s.done and pending[s.mid]]
             if not active:
-                return
+                if prev is None:
+                    return
+                self._resolve(prev, stats, t0, pending, None)
+                prev = None
+                continue
             # capacity for the whole step first: the reference runs the step's forward and
             # then appends message by message, so the messages before the first one that
             # does not fit get their K/V and the append of that one raises (cache.py:114-117,
             # engine.py:430-433).  Same here: encode the prefix that fits, then raise.
-            room = self.cache.capacity - self.cache.token_count
             n_fit = 0
             for s in active:
                 if len(pending[s.mid]) > room:
@@ -382,92 +414,189 @@ class Engine:
                 self._encode_only(active[:n_fit], pending)
                 self._check_capacity(len(pending[active[n_fit].mid]))
             calls, logit_rows, owners, r = [], [], [], 0
+            sel = np.full(0, -1, np.int32)
+            sel_rows = []
+            spec_rows = {}  # mid -> (token index in the message, flops added)
             for s in active:
-                toks = pending[s.mid]
+                is_spec = s.mid in spec
+                toks = [0] if is_spec else pending[s.mid]
                 first = s.appended
                 pages, slots = self.cache.reserve_slots(s.mid, toks)
                 calls.append(CallRows(s.mid, s.parents, first, toks, pages, slots, s.new_off))
+                if is_spec:
+                    sel_rows.append((r, spec[s.mid]))
                 r += len(toks)
                 # FLOP accounting as the reference would have executed it
+                fl = 0
                 if lone or len(states) == 1:
                     if first == 0:
-                        stats.decode_flops += encode_flops(self.config, len(toks), s.n_par, "last")
+                        fl = encode_flops(self.config, len(toks), s.n_par, "last")
                     else:
-                        stats.decode_flops += encode_flops(self.config, 1, s.n_par + first, "all")
+                        fl = encode_flops(self.config, 1, s.n_par + first, "all")
                 else:
                     for j in range(len(toks)):
-                        stats.decode_flops += encode_flops(self.config, 1, s.n_par + first + j, "all")
+                        fl += encode_flops(self.config, 1, s.n_par + first + j, "all")
+                stats.decode_flops += fl
                 stats.tokens_encoded += len(toks)
                 s.appended += len(toks)
+                if is_spec:
+                    spec_rows[s.mid] = (first, fl)
+                    # the token, if accepted, may be the message's last (max_tokens)
+                    if len(s.generated) + 1 >= s.call.sampling.max_tokens:
+                        s.finishing = True
                 if not s.finishing:
                     logit_rows.append(r - 1)
                     owners.append(s)
-            logits = self._runner.forward(StepPlan(calls, np.asarray(logit_rows, np.int32)))
+            plan = StepPlan(calls, np.asarray(logit_rows, np.int32))
+            if sel_rows:
+                plan.sel = np.full(r, -1, np.int32)
+                for row, i in sel_rows:
+                    plan.sel[row] = i
+                plan.sel_src = prev["out"]
+            logits = self._runner.forward(plan)
             for s in active:
                 pending[s.mid] = []
                 if s.finishing:
                     s.done = True
-            if not owners:
+            cur = None
+            if owners:
+                cur = self._select(owners, logits, stats, t0, pending, pipeline)
+            if prev is not None:
+                # the GPU runs this step while the host settles the previous one
+                void = self._resolve(prev, stats, t0, pending, spec_rows)
+                if void and cur is not None:  # their selections in this step are moot
+                    cur["free"] = [e for e in cur["free"] if e[0].mid not in void]
+            prev = cur if cur is not None and cur["free"] else None
+
+    def _select(self, owners: list, logits, stats: CallStats, t0: float, pending: dict,
+                pipeline: bool):
+        """Select one token per owner row: forced tokens directly, free ones on the device
+        (K6 greedy / K6b nucleus).  Pipelined, the free tokens stay on the device and are
+        returned unresolved (copied to pinned host memory behind an event); otherwise they
+        are read back and applied now.  Selection indices are assigned at launch."""
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        n_own = len(owners)
+        ks = []
+        for s in owners:
+            ks.append(s.sel)
+            s.sel += 1
+        free = [s for s in owners if s.forced is None]
+        want_g = any(s.call.sampling.mode == "greedy" for s in free)
+        want_n = any(s.call.sampling.mode != "greedy" for s in free) and self.device_sampling
+        out = None
+        if want_g or want_n:
+            out = torch.empty(2, n_own, dtype=torch.int32, device=self.device)
+            if want_g:  # K6 greedy over every owner row (non-greedy rows ignored)
+                nat.select_greedy(logits.data_ptr(), n_own, logits.shape[1], logits.shape[1],
+                                  0, out[0].data_ptr(), stream)
+                self._runner.launches += 1
+            if want_n:  # K6b nucleus: the reference's f64 algorithm + Philox stream
+                params = np.array([[s.call.sampling.temperature, s.call.sampling.top_p]
+                                   for s in owners], np.float64)
+                m64 = 0xFFFFFFFFFFFFFFFF
+                keys = np.array([[self.seed & m64, s.call.sampling.seed & m64, s.mid, k]
+                                 for s, k in zip(owners, ks)], np.uint64).view(np.int64)
+                pd, kd = h2d(params, self.device), h2d(keys, self.device)
+                nat.select_nucleus(logits.data_ptr(), n_own, logits.shape[1],
+                                   logits.shape[1], pd.data_ptr(), kd.data_ptr(),
+                                   out[1].data_ptr(), stream)
+                self._runner.launches += 1
+        # flat index of each free owner's token in `out` (greedy row 0, nucleus row 1)
+        free_idx = [(s, k, (0 if s.call.sampling.mode == "greedy" else 1) * n_own + i)
+                    for i, (s, k) in enumerate(zip(owners, ks)) if s.forced is None]
+        if pipeline and out is not None and len(free_idx) == len([s for s in free]):
+            # a ring of pinned read-back buffers (a buffer is reused two steps later, after
+            # its tokens were read)
+            self._pin_i = (getattr(self, "_pin_i", 0) + 1) % 3
+            ring = getattr(self, "_pin", None)
+            if ring is None or ring[0].numel() < 2 * n_own:
+                ring = self._pin = [torch.empty(max(64, 2 * n_own), dtype=torch.int32,
+                                                pin_memory=True) for _ in range(3)]
+            host = ring[self._pin_i][:2 * n_own]
+            flat = out.view(-1)
+            host.copy_(flat, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            self.d2h_bytes += out.nbytes
+            cur = {"free": free_idx, "out": flat, "host": host, "event": ev}
+        else:
+            cur = None
+        host_logits = None
+        toks = None
+        if out is not None and cur is None:
+            toks = out.view(-1).cpu().numpy()
+            self.d2h_bytes += out.nbytes
+        if self.record_logits or (not self.device_sampling and any(
+                s.forced is None and s.call.sampling.mode != "greedy" for s in owners)):
+            hl = logits.double().cpu().numpy()
+            self.d2h_bytes += logits.nbytes
+            host_logits = hl
+        elif out is None and any(k == 0 for k in ks):
+            # all forced: the host already knows the tokens; synchronise only at a
+            # message's first selection so its TTFT is the time its logits exist
+            torch.cuda.current_stream(self.device).synchronize()
+        for i, (s, k) in enumerate(zip(owners, ks)):
+            if stats.logits is not None:
+                stats.logits[s.mid].append(host_logits[i].copy())
+            if s.forced is not None:
+                tok = s.forced[k] if k < len(s.forced) else None
+            elif cur is not None:
+                continue  # resolved with the next step in flight (_resolve)
+            elif s.call.sampling.mode == "greedy":
+                tok = int(toks[i])
+            elif self.device_sampling:
+                tok = int(toks[n_own + i])
+            else:
+                tok = _sample_nucleus(host_logits[i], self._generatable, s.call.sampling,
+                                      self.seed, s.mid, k)
+            self._accept(s, k, tok, stats, t0, pending)
+        return cur
+
+    def _accept(self, s: _Dec, k: int, tok, stats: CallStats, t0: float, pending: dict,
+                spec_index=None) -> bool:
+        """Apply selection k of message s (engine.py:394-413).  spec_index: the message's
+        token index already encoded with this token (pipelined step), patched or undone."""
+        if k == 0:
+            stats.ttft[s.mid] = time.perf_counter() - t0
+        if tok is None or tok == EOS_MSG or not self._may_accept(s):
+            s.done = True
+            return False
+        s.generated.append(tok)
+        if spec_index is not None:
+            self.cache.set_token(s.mid, spec_index, tok)
+        else:
+            pending[s.mid] = [tok]
+        if len(s.generated) >= s.call.sampling.max_tokens:
+            s.finishing = True
+        return True
+
+    def _resolve(self, prev: dict, stats: CallStats, t0: float, pending: dict,
+                 spec_rows) -> set:
+        """Read back a pipelined selection and apply it.  Messages whose token the current
+        step already encoded (spec_rows: mid -> (token index, flops)) keep it if accepted;
+        if the token stops the message, the encoding is undone (slot unreserved, accounting
+        subtracted).  Returns the mids whose current-step rows were undone."""
+        prev["event"].synchronize()
+        toks = prev["host"].numpy()
+        void = set()
+        for s, k, i in prev["free"]:
+            sp = spec_rows.get(s.mid) if spec_rows else None
+            if sp is not None:
+                s.appended -= 1  # _may_accept sees the count at selection time
+            ok = self._accept(s, k, int(toks[i]), stats, t0, pending,
+                              spec_index=None if sp is None else sp[0])
+            if sp is None:
                 continue
-            greedy_tok = nucleus_tok = None
-            n_own = len(owners)
-            stream = torch.cuda.current_stream(self.device).cuda_stream
-            free = [s for s in owners if s.forced is None]
-            want_g = any(s.call.sampling.mode == "greedy" for s in free)
-            want_n = any(s.call.sampling.mode != "greedy" for s in free) and self.device_sampling
-            if want_g or want_n:
-                out = torch.empty(2, n_own, dtype=torch.int32, device=self.device)
-                if want_g:  # K6 greedy over every owner row (non-greedy rows ignored)
-                    nat.select_greedy(logits.data_ptr(), n_own, logits.shape[1], logits.shape[1],
-                                      0, out[0].data_ptr(), stream)
-                    self._runner.launches += 1
-                if want_n:  # K6b nucleus: the reference's f64 algorithm + Philox stream
-                    params = np.array([[s.call.sampling.temperature, s.call.sampling.top_p]
-                                       for s in owners], np.float64)
-                    m64 = 0xFFFFFFFFFFFFFFFF
-                    keys = np.array([[self.seed & m64, s.call.sampling.seed & m64, s.mid, s.sel]
-                                     for s in owners], np.uint64).view(np.int64)
-                    pd, kd = h2d(params, self.device), h2d(keys, self.device)
-                    nat.select_nucleus(logits.data_ptr(), n_own, logits.shape[1],
-                                       logits.shape[1], pd.data_ptr(), kd.data_ptr(),
-                                       out[1].data_ptr(), stream)
-                    self._runner.launches += 1
-                toks = out.cpu().numpy()
-                self.d2h_bytes += out.nbytes
-                greedy_tok, nucleus_tok = toks[0], (toks[1] if want_n else None)
-            host_logits = None
-            if self.record_logits or (not self.device_sampling and any(
-                    s.forced is None and s.call.sampling.mode != "greedy" for s in owners)):
-                hl = logits.double().cpu().numpy()
-                self.d2h_bytes += logits.nbytes
-                host_logits = hl
-            elif not (want_g or want_n) and any(s.sel == 0 for s in owners):
-                # all forced: the host already knows the tokens; synchronise only at a
-                # message's first selection so its TTFT is the time its logits exist
-                torch.cuda.current_stream(self.device).synchronize()
-            for i, s in enumerate(owners):
-                if stats.logits is not None:
-                    stats.logits[s.mid].append(host_logits[i].copy())
-                if s.sel == 0:
-                    stats.ttft[s.mid] = time.perf_counter() - t0
-                k = s.sel
-                s.sel += 1
-                if s.forced is not None:
-                    tok = s.forced[k] if k < len(s.forced) else None
-                elif s.call.sampling.mode == "greedy":
-                    tok = int(greedy_tok[i])
-                elif nucleus_tok is not None:
-                    tok = int(nucleus_tok[i])
-                else:
-                    tok = _sample_nucleus(host_logits[i], self._generatable, s.call.sampling,
-                                          self.seed, s.mid, k)
-                if tok is None or tok == EOS_MSG or not self._may_accept(s):
-                    s.done = True
-                    continue
-                s.generated.append(tok)
-                pending[s.mid] = [tok]
-                if len(s.generated) >= s.call.sampling.max_tokens:
-                    s.finishing = True
+            if ok:
+                s.appended += 1
+            else:
+                self.cache.unreserve_last(s.mid)
+                stats.decode_flops -= sp[1]
+                stats.tokens_encoded -= 1
+                s.finishing = False
+                s.done = True
+                void.add(s.mid)
+        return void
 
     def _encode_only(self, states: list, pending: dict) -> None:
         """Encode (append) the pending tokens of `states` without selecting: the part of a

@@ -49,6 +49,10 @@ class CallRows:
 class StepPlan:
     calls: list
     logit_rows: np.ndarray  # row indices needing logits
+    # pipelined decode: row r embeds sel_src[sel[r]] (a device-selected token of the previous
+    # step, still unknown to the host) when sel[r] >= 0
+    sel: np.ndarray | None = None
+    sel_src: torch.Tensor | None = None
 
     @property
     def n_rows(self) -> int:
@@ -151,7 +155,8 @@ def split_plan(plan: StepPlan) -> list:
         sel = logit_rows[(logit_rows >= lo) & (logit_rows < hi)] - lo
         percall = npair > K3_MAX_PAIRS or any(
             p > K3_MAX_PARENT_ID for c in calls[i:j] for p in c.parents)
-        out.append((StepPlan(calls[i:j], sel.astype(np.int32)), percall))
+        sub_sel = None if plan.sel is None else np.asarray(plan.sel[lo:hi], np.int32)
+        out.append((StepPlan(calls[i:j], sel.astype(np.int32), sub_sel, plan.sel_src), percall))
         i = j
     return out
 
@@ -473,9 +478,11 @@ class Runner:
         direct = use_k4 and plan_.max_row_parts == 1 and self.dt == torch.bfloat16
         n_log = len(plan.logit_rows)
 
+        sel = plan.sel if plan.sel is not None and (plan.sel >= 0).any() else None
         ints = np.concatenate([ids, row_t, pos, pages, slots, np.asarray(call_tab, np.int32),
                                np.asarray(parents + [0], np.int32),
-                               np.asarray(plan.logit_rows, np.int32)])
+                               np.asarray(plan.logit_rows, np.int32)]
+                              + ([np.asarray(sel, np.int32)] if sel is not None else []))
         dints = h2d(ints, self.dev)
         self.h2d_bytes += ints.nbytes
         if self.step_events is not None:
@@ -496,6 +503,7 @@ class Runner:
         calls_d = take(5 * n_calls)
         parents_d = take(len(parents) + 1)
         logit_d = take(n_log)
+        sel_d = take(R) if sel is not None else None
 
         vis = torch.empty(3, max(plan_.n_vis, 1), dtype=torch.int32, device=self.dev)
         blk_rows = torch.empty(max(plan_.n_blk_rows, 1), dtype=torch.int32, device=self.dev)
@@ -527,7 +535,12 @@ class Runner:
         isp = 0 if k7 else sp
         mm = (lambda a, w: self._lin(a, w, R)) if k7 else (lambda a, w: self._mm(a, w, True))
         x = torch.empty(R, d, dtype=torch.float32, device=self.dev)
-        nat.embed(self.w.embed.data_ptr(), self.dtc, d, ids_d.data_ptr(), R, x.data_ptr(), stream)
+        if sel_d is not None:  # pipelined decode: ids of the previous step's device selection
+            nat.embed_select(self.w.embed.data_ptr(), self.dtc, d, ids_d.data_ptr(),
+                             sel_d.data_ptr(), plan.sel_src.data_ptr(), R, x.data_ptr(), stream)
+        else:
+            nat.embed(self.w.embed.data_ptr(), self.dtc, d, ids_d.data_ptr(), R, x.data_ptr(),
+                      stream)
         q = torch.empty(R, H, hd, dtype=torch.float32, device=self.dev)
         part_o = torch.empty(max(n_parts, 1), H, hd, dtype=torch.float32, device=self.dev)
         part_lse = torch.empty(max(n_parts, 1), H, dtype=torch.float32, device=self.dev)
