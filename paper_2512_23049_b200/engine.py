@@ -239,6 +239,7 @@ class Engine:
                                self.tp, self.tp_group)
         other._generatable = self._generatable
         other.device_sampling = self.device_sampling
+        other.pipeline = self.pipeline
         other._next_id = self._next_id
         other.stats = []
         other.d2h_bytes = 0
@@ -373,7 +374,8 @@ class Engine:
         read-back no longer leaves the GPU idle.  A message the host then sees stop (EOS)
         had one token encoded speculatively: its slot is unreserved (past the message's
         length, so no later step can see it), and that row's accounting and selection are
-        dropped -- tokens, logits, cache and statistics equal the non-pipelined run.
+        dropped: tokens, cache layout and statistics equal the synchronous run's, values up
+        to summation order (the undone row was part of that step's batch).
         """
         pending = {s.mid: list(s.hdr) for s in states}
         pipeline = self.pipeline and not self.record_logits and self.device_sampling

@@ -420,3 +420,54 @@ def test_wide_header_step_matches_oracle():
         assert got.shape == want.shape
         worst = max(worst, float(np.abs(got - want).max()))
     assert worst <= 2e-2, worst
+
+
+@pytest.mark.parametrize("mode", ["f32", "bf16"])
+def test_pipelined_decode_equals_synchronous(mode):
+    """Pipelined free-running decode (the step encoding a selected token is enqueued before
+    the host reads the token; a stop undoes that row) == the synchronous loop: generated
+    tokens, stop reasons (EOS at different steps, max_tokens, the context-window edge), the
+    cache (ids, positions, token ids; K/V up to summation order), the physical interleaving
+    and the call statistics.  The EOS texts are messages on which the tiny model's greedy decode emits
+    EOS (found with the CPU oracle); a follow-up decode reads everything back."""
+    texts = [("ywnyzzclphjquperwfoixbm", "lduzzyjtzoypemphskyfrcdnmmm", "Q4:"),
+             ("cvgpfwtnlofb", "yzxsnlxwsduyztzce", "Ans:")]
+    runs = {}
+    for pipe in (False, True):
+        eng = _engine(mode)
+        eng.pipeline = pipe
+        W = eng.config.context_window
+        ids = []
+        for a, b, _ in texts:
+            ids += [eng.prefill(P.PrefillCall(a)), eng.prefill(P.PrefillCall(b))]
+        calls = [P.DecodeCall(texts[0][2], parents=[ids[0], ids[1]],
+                              sampling=P.SamplingParams(max_tokens=40)),
+                 P.DecodeCall(texts[1][2], parents=[ids[2], ids[3]],
+                              sampling=P.SamplingParams(max_tokens=40)),
+                 P.DecodeCall("Short:", parents=[ids[2], ids[3]],
+                              sampling=P.SamplingParams(max_tokens=3)),
+                 P.DecodeCall("Edge:", parents=[ids[0]], new_offset=W - 12,
+                              sampling=P.SamplingParams(max_tokens=40))]
+        ms = eng.decode_parallel(calls)
+        st = eng.last_stats
+        lone = eng.decode(P.DecodeCall("Then:", parents=list(ms[:2]),
+                                       sampling=P.SamplingParams(max_tokens=12)))
+        c = eng.cache
+        n = c.token_count
+        runs[pipe] = dict(
+            gen=[eng.generated_token_ids(m) for m in ms + [lone]],
+            ids=c.msg_ids[:n].tolist(), pos=c.positions[:n].tolist(),
+            tok=c.token_ids[:n].tolist(), keys=np.asarray(c.keys[:n]).copy(),
+            values=np.asarray(c.values[:n]).copy(),
+            stats=(st.decode_flops, st.tokens_encoded, st.prefill_flops, sorted(st.ttft)))
+    a, b = runs[False], runs[True]
+    assert a["gen"] == b["gen"]
+    assert len(a["gen"][0]) < 40 or len(a["gen"][1]) < 40, "no EOS stop exercised"
+    assert len(a["gen"][2]) == 3 and len(a["gen"][3]) < 40
+    for k in ("ids", "pos", "tok", "stats"):
+        assert a[k] == b[k], k
+    # a row encoded speculatively and undone changed that step's batch (split-KV items,
+    # GEMM rows), so the other rows' K/V agree up to summation order, not bitwise
+    tol = 1e-5 if mode == "f32" else 1e-2
+    np.testing.assert_allclose(a["keys"], b["keys"], rtol=tol, atol=tol)
+    np.testing.assert_allclose(a["values"], b["values"], rtol=tol, atol=tol)
