@@ -243,6 +243,7 @@ __global__ void __launch_bounds__(kDvThreads, 1)
     // (a per-page dependent load would cap the ring at one page per L2 round trip); lane 0
     // issues the TMA copies
     uint32_t gp = 0;
+    const uint64_t pol = l2_policy_evict_first();  // K/V pages: read once per step and layer
     for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
       const int32_t* it = p.items + 6 * (w / p.n_kv);
       const int iv = lane < 4 ? it[lane] : 0;
@@ -261,8 +262,9 @@ __global__ void __launch_bounds__(kDvThreads, 1)
             mbar_arrive_expect_tx(&full_bar[st], C::kSlot);
 #pragma unroll
             for (int r = 0; r < C::kR; ++r) {
-              tma_load_2d(dst + r * C::kHalf, &tmK, &full_bar[st], r * 64, row0);
-              tma_load_2d(dst + (C::kR + r) * C::kHalf, &tmV, &full_bar[st], r * 64, row0);
+              tma_load_2d_hint(dst + r * C::kHalf, &tmK, &full_bar[st], r * 64, row0, pol);
+              tma_load_2d_hint(dst + (C::kR + r) * C::kHalf, &tmV, &full_bar[st], r * 64, row0,
+                               pol);
             }
           }
           __syncwarp();

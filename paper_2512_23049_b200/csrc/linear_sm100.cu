@@ -91,6 +91,9 @@ __global__ void __launch_bounds__(kLnThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------------------------------------- TMA producer
+      // weights are read once per step: evict-first keeps the step's activations, pieces
+      // and code resident in L2 under the 16 GB stream
+      const uint64_t pol = l2_policy_evict_first();
       auto load_w = [&](int i, int st) {
         uint8_t* dst = base + st * C::kStageBytes;
         const int t = i / p.KB, kb = (i % p.KB) * KSUB;
@@ -98,11 +101,13 @@ __global__ void __launch_bounds__(kLnThreads, 1)
 #pragma unroll
         for (int u = 0; u < KSUB; ++u)
           if (p.silu_f) {  // 64 gate rows over the matching 64 up rows
-            tma_load_2d(dst + u * C::kWBytes, &tmW, &full_bar[st], (kb + u) * kLnKB, t * 64);
-            tma_load_2d(dst + u * C::kWBytes + 64 * 128, &tmW, &full_bar[st], (kb + u) * kLnKB,
-                        p.silu_f + t * 64);
+            tma_load_2d_hint(dst + u * C::kWBytes, &tmW, &full_bar[st], (kb + u) * kLnKB, t * 64,
+                             pol);
+            tma_load_2d_hint(dst + u * C::kWBytes + 64 * 128, &tmW, &full_bar[st],
+                             (kb + u) * kLnKB, p.silu_f + t * 64, pol);
           } else {
-            tma_load_2d(dst + u * C::kWBytes, &tmW, &full_bar[st], (kb + u) * kLnKB, t * kLnTile);
+            tma_load_2d_hint(dst + u * C::kWBytes, &tmW, &full_bar[st], (kb + u) * kLnKB,
+                             t * kLnTile, pol);
           }
       };
       auto load_x = [&](int i, int st) {
