@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(1024) residual_rmsnorm_vec(float* __restrict__
       if (delta) {
         float4 a;
         if (pv.ws)
-          choreo::k7_get<4, 2>(pv, r, 4 * i, &a.x);  // deferred K7 output
+          choreo::k7_get<4, 4>(pv, r, 4 * i, &a.x);  // deferred K7 output
         else
           a = ld4(delta + (int64_t)r * d + 4 * i);
         float4 b = make_float4(0.f, 0.f, 0.f, 0.f);

@@ -131,6 +131,35 @@ def test_pages_belong_to_one_message_and_views():
         c.reserve_slots(1, [0] * 5000)
 
 
+def test_speculative_token_set_and_unreserve():
+    """Pipelined decode bookkeeping (engine._decode_loop): a slot reserved for a token the
+    host does not know yet gets its id later (set_token), or is undone (unreserve_last):
+    length, token count, the device length table and the views return to the state before
+    the reservation, the page stays with the message."""
+    c = _cache_cpu()
+    c.register_message(0, "decoded", 0)
+    c.reserve_slots(0, [5, 6, 7])
+    pages_before = list(c._messages[0].pages)
+    p, s = c.reserve_slots(0, [0])  # speculative: id unknown
+    assert s.tolist() == [3] and c.message_length(0) == 4 and c.token_count == 4
+    c.set_token(0, 3, 42)
+    assert c._messages[0].tokens == [5, 6, 7, 42]
+    c.reserve_slots(0, [0])
+    c.unreserve_last(0)
+    assert c.message_length(0) == 4 and c.token_count == 4
+    assert int(c.msg_len.host[0]) == 4
+    assert c._messages[0].pages == pages_before
+    c.log_append(0, 0, 4)
+    assert c.token_ids.tolist() == [5, 6, 7, 42]
+    # a stop right at a page boundary: the new page stays allocated but unused
+    c.register_message(1, "decoded", 0)
+    c.reserve_slots(1, list(range(64)))
+    c.reserve_slots(1, [0])
+    assert len(c._messages[1].pages) == 2
+    c.unreserve_last(1)
+    assert c.message_length(1) == 64 and c.token_count == 68
+
+
 def test_page_chain_relocates_when_reservation_is_exceeded():
     c = _cache_cpu()
     c.register_message(0, "decoded", 0, max_tokens=10)  # reserves one page-table entry
