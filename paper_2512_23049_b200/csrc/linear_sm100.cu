@@ -9,8 +9,9 @@
 //   * stream-K: the (tile, k-block) iteration space is cut into one equal contiguous range
 //     per CTA (one CTA per SM), so every SM streams the same number of weight bytes
 //     whatever the tile count (qkv: 48 tiles, o_proj/down: 32, gate|up: 224, head: 1002);
-//   * TMA producer warp with an 8-stage ring (16 KB of weights + the activation chunk per
-//     stage, ~150 KB in flight per SM), single-thread MMA issue, 4 epilogue warps;
+//   * TMA producer warp with a 4-stage ring (2 k-blocks = 32 KB of weights + the activation
+//     chunk per stage, ~144 KB in flight per SM; weights loaded evict-first), single-thread
+//     MMA issue, 4 epilogue warps;
 //   * a tile cut between CTAs is reduced deterministically: each piece is written to a
 //     per-CTA slot, the last piece to arrive sums all pieces in CTA order -- or, in the
 //     deferred mode (choreo_linear_skinny_pieces), the pieces stay in their slots and the
@@ -48,7 +49,9 @@ struct LnCfg {
   static constexpr int kWBytes = kLnTile * 128;  // one k-block of the weight tile
   static constexpr int kXBytes = NX * 128;       // one k-block of the activations
   static constexpr int kStageBytes = KSUB * (kWBytes + kXBytes);
-  static constexpr int kStages = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
+  // at most 4 stages: measured on the 8B decode step (tools/k7_ab.sh), a 4-stage ring (148 KB
+  // at NX 16) beats 5 stages by ~1 % and 2 stages lose 8 %
+  static constexpr int kStages = (200 * 1024) / kStageBytes > 4 ? 4 : (200 * 1024) / kStageBytes;
   static constexpr int smem(int stages) { return stages * kStageBytes + 1024; }
   static constexpr int kTmemCols = 2 * NX < 32 ? 32 : 2 * NX;
 };
