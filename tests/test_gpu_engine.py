@@ -471,3 +471,33 @@ def test_pipelined_decode_equals_synchronous(mode):
     tol = 1e-5 if mode == "f32" else 1e-2
     np.testing.assert_allclose(a["keys"], b["keys"], rtol=tol, atol=tol)
     np.testing.assert_allclose(a["values"], b["values"], rtol=tol, atol=tol)
+
+
+def test_pipelined_decode_sampling_and_capacity():
+    """Pipelined decode with device nucleus sampling (selection indices assigned at launch)
+    and with a capacity failure mid-decode: same tokens, same error, same cache state as the
+    synchronous loop (the reference's capacity order: the step's prefix that fits is encoded,
+    then CapacityError)."""
+    runs = {}
+    for pipe in (False, True):
+        eng = _engine("f32", capacity=160)
+        eng.pipeline = pipe
+        a = eng.prefill(P.PrefillCall("cvgpfwtnlofb"))
+        b = eng.prefill(P.PrefillCall("yzxsnlxwsduyztzce"))
+        sp = P.SamplingParams(mode="temperature", temperature=1.3, top_p=0.9, seed=7,
+                              max_tokens=30)
+        ms = eng.decode_parallel([P.DecodeCall("T1:", parents=[a, b], sampling=sp),
+                                  P.DecodeCall("T2:", parents=[a], sampling=sp)])
+        gen = [eng.generated_token_ids(m) for m in ms]
+        err = None
+        try:
+            eng.decode_parallel([P.DecodeCall("Long:", parents=[a],
+                                              sampling=P.SamplingParams(max_tokens=200)),
+                                 P.DecodeCall("Also:", parents=[b],
+                                              sampling=P.SamplingParams(max_tokens=200))])
+        except P.CapacityError as e:
+            err = type(e).__name__
+        n = eng.cache.token_count
+        runs[pipe] = (gen, err, n, eng.cache.msg_ids[:n].tolist(), eng.cache.token_ids[:n].tolist())
+    assert runs[False] == runs[True]
+    assert runs[True][1] == "CapacityError"
