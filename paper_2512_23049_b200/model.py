@@ -203,6 +203,7 @@ class Runner:
         self.chain = (self.dt == torch.bfloat16 and (tp is None or tp.size == 1)
                       and os.environ.get("CHOREO_CHAIN", "0") == "1")
         self._chain_bufs = None
+        self.wide_k4 = os.environ.get("CHOREO_WIDE_K4", "1") != "0"
         self._wptrs = None
         self._ev_free: list = []
         self._ev_pending: list = []  # (kind, event array, bytes per pair) awaiting readback
@@ -449,8 +450,13 @@ class Runner:
         msg_len = cache.msg_len.host
         # prefill-sized steps run K4 (tcgen05, 128-row M tiles); decode-sized steps K5
         G = H // Hk
+        # wide decode-sized steps (>= 64 rows, e.g. the parallel header step of 8 agents)
+        # also run K4: its 256-vector items read each shared parent page once per 64 rows,
+        # where K5 v2's 32-vector units re-read it once per 8 rows (measured: C3 header step
+        # 6.5 -> 5.8 ms, tools/hdr_ab.sh)
+        wide = R >= 64 and self.wide_k4
         use_k4 = (self.pool_dtc == nat.BF16 and P == 64 and hd in (64, 128) and G <= 128
-                  and max(len(c.tokens) for c in plan.calls) >= 64
+                  and (max(len(c.tokens) for c in plan.calls) >= 64 or wide)
                   and os.environ.get("CHOREO_PREFILL_K4", "1") != "0")
         mode0 = max(len(c.tokens) for c in plan.calls) < 64 and not force_percall
         # decode-sized bf16 steps: K5 v2 (TMA page ring, <= 32 query vectors per item)
@@ -465,6 +471,8 @@ class Runner:
         ppi = max(1, cdiv(work.item_pages * Hk, (2 if use_k4 else 1 if v2 else 3) * 148))
         if v2:  # persistent CTAs: about one (item, kv head) unit per SM; unit record <= 32 pages
             ppi = min(max(ppi, 4), 32)
+        if use_k4 and mode == 0:  # page-centric K4 items: long page runs keep its pipeline full
+            ppi = max(ppi, 16)
         plan_ = plan_counts(plan.calls, msg_len, P, rpb, ppi, mode)
         if v2:  # grow items until the units fit one wave of CTAs (else a few CTAs run two)
             while plan_.n_items * Hk > 148 and ppi < 32:
