@@ -389,16 +389,19 @@ def test_device_nucleus_sampling_matches_host_sampler(mode):
     assert any(len(t) > 0 for t in runs[0])
 
 
-def test_wide_header_step_matches_oracle():
+@pytest.mark.parametrize("wide_k4", [True, False])
+def test_wide_header_step_matches_oracle(wide_k4):
     """A parallel decode whose header step has >= 64 rows (8 agents x 14-token headers:
-    cuBLAS projections, page-centric K5 v2 over row blocks); logits within 2e-2 of the
-    oracle (bf16-rounded weights), teacher-forced on its tokens."""
+    cuBLAS projections; attention on page-centric K4 items -- the engine's choice for wide
+    steps -- or on K5 v2 row blocks); logits within 2e-2 of the oracle (bf16-rounded
+    weights), teacher-forced on its tokens."""
     shape = O.Shape(n_layers=2, n_heads=8, n_kv_heads=2, head_dim=128, ffn_dim=256,
                     vocab_size=300, context_window=2048, rope_base=500000.0)
     cfg = P.ModelConfig(**{k: getattr(shape, k) for k in shape.__dataclass_fields__})
     ref = O.Oracle(O.round_weights(O.init_weights(shape), "bf16"), shape, record_logits=True)
     eng = P.Engine(P.DeviceWeights.from_host(P.init_weights(cfg).rounded("bf16"),
                                              dtype=torch.bfloat16), record_logits=True)
+    eng._runner.wide_k4 = wide_k4
     rng = np.random.default_rng(5)
     texts = ["".join(chr(97 + int(c)) for c in rng.integers(0, 26, n)) for n in (150, 90, 200)]
     for t in texts:
