@@ -202,6 +202,41 @@ __global__ void silu_mul_kernel(const void* __restrict__ gu, int dt, int in_spli
   }
 }
 
+// f32 gate|up (stacked hi/lo halves when in_split) -> bf16 act (hi/lo when out_split), four
+// columns per thread with 16-byte loads (the wide header step's prefill-sized GEMMs go
+// through cuBLAS, so this runs over [2R][2F] f32 there).
+__global__ void silu_mul_vec4_kernel(const float* __restrict__ gu, int in_split, int n_rows,
+                                     int f, __nv_bfloat16* __restrict__ out, int out_split) {
+  pdl_trigger();
+  pdl_wait();
+  const int f4 = f >> 2;
+  const int n4 = n_rows * f4;
+  const int64_t lo_in = (int64_t)n_rows * 2 * f, lo_out = (int64_t)n_rows * f;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x) {
+    const int r = i / f4, c = (i - r * f4) * 4;
+    const float* gp = gu + (int64_t)r * 2 * f + c;
+    float4 g = *reinterpret_cast<const float4*>(gp);
+    float4 u = *reinterpret_cast<const float4*>(gp + f);
+    if (in_split) {
+      const float4 gl = *reinterpret_cast<const float4*>(gp + lo_in);
+      const float4 ul = *reinterpret_cast<const float4*>(gp + lo_in + f);
+      g.x += gl.x; g.y += gl.y; g.z += gl.z; g.w += gl.w;
+      u.x += ul.x; u.y += ul.y; u.z += ul.z; u.w += ul.w;
+    }
+    const float y[4] = {g.x / (1.0f + expf(-g.x)) * u.x, g.y / (1.0f + expf(-g.y)) * u.y,
+                        g.z / (1.0f + expf(-g.z)) * u.z, g.w / (1.0f + expf(-g.w)) * u.w};
+    __nv_bfloat16 h[4], l[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      h[k] = __float2bfloat16_rn(y[k]);
+      l[k] = __float2bfloat16_rn(y[k] - __bfloat162float(h[k]));
+    }
+    const int64_t o = (int64_t)r * f + c;
+    *reinterpret_cast<uint2*>(out + o) = *reinterpret_cast<const uint2*>(h);
+    if (out_split) *reinterpret_cast<uint2*>(out + lo_out + o) = *reinterpret_cast<const uint2*>(l);
+  }
+}
+
 // K6: one warp per row; generatable ids are 0..255 and 257 (EOS).  Ties keep the
 // lowest id, as np.argmax does (engine.py:371).
 __global__ void select_greedy_kernel(const float* __restrict__ logits, int n_rows, int64_t ld,
@@ -322,6 +357,15 @@ int choreo_silu_mul(const void* gu, int gu_dtype, int in_split, int n_rows, int 
   if (out_split && out_dtype != CHOREO_BF16) return CHOREO_EINVAL;
   const int64_t n = (int64_t)n_rows * f;
   if (n == 0) return CHOREO_OK;
+  if (gu_dtype == CHOREO_F32 && out_dtype == CHOREO_BF16 && f % 4 == 0 &&
+      (int64_t)n_rows * 2 * f * (in_split ? 2 : 1) < (1ll << 31)) {
+    int64_t blocks = (n / 4 + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    launch_k(silu_mul_vec4_kernel, (int)blocks, 256, 0, as_stream(stream),
+             reinterpret_cast<const float*>(gu), in_split, n_rows, f,
+             reinterpret_cast<__nv_bfloat16*>(out), out_split);
+    return launch_status("choreo_silu_mul");
+  }
   int64_t blocks = (n + 255) / 256;
   if (blocks > 148 * 64) blocks = 148 * 64;
   launch_k(silu_mul_kernel, (int)blocks, 256, 0, as_stream(stream), gu, gu_dtype, in_split, n_rows, f,
