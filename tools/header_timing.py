@@ -3,6 +3,8 @@ import os, sys, time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import torch
+if os.environ.get("BLAS"):
+    torch.backends.cuda.preferred_blas_library(os.environ["BLAS"])
 import paper_2512_23049_b200 as P
 from bench import workflow_inputs, run_debate
 
