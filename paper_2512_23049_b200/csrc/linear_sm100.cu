@@ -383,14 +383,9 @@ static int linear_impl(const void* x, int x_rows, int split, const void* w, int 
   const int R = split ? x_rows / 2 : x_rows;  // output rows
   const int xr = split ? 2 * R : R;
   const int NX = xr <= 16 ? 16 : xr <= 32 ? 32 : xr <= 64 ? 64 : xr <= 128 ? 128 : 256;
-  static int ksub = -1;
-  if (ksub < 0) {
-    const char* e = getenv("CHOREO_K7_KSUB");
-    ksub = e ? atoi(e) : 2;
-    if (ksub != 1 && ksub != 2 && ksub != 4) ksub = 2;
-  }
   const int n_tiles = silu_f ? silu_f / 64 : (n + kLnTile - 1) / kLnTile;
-  const int ks = NX == 256 ? 1 : ksub;  // 256 activation rows: one k-block per stage
+  // k-blocks per ring stage: 2 (1 at 256 activation rows, whose X block alone is 32 KB)
+  const int ks = NX == 256 ? 1 : 2;
   const int KB = (k + kLnKB * ks - 1) / (kLnKB * ks);  // iteration = ks k-blocks
   const int iters = n_tiles * KB;
   int grid = grid_ctas > 0 ? grid_ctas : 148;
@@ -415,10 +410,7 @@ static int linear_impl(const void* x, int x_rows, int split, const void* w, int 
   };
 #define LN_STAGES(nx, ks) \
   (p.stages = stages_for(LnCfg<nx, ks>::kStages, LnCfg<nx, ks>::kStageBytes), p)
-#define LN_CASE(nx)                                                                       \
-  return ksub == 1   ? launch_linear<nx, 1>(LN_STAGES(nx, 1), x, x_rows, w, n, k, s)      \
-         : ksub == 2 ? launch_linear<nx, 2>(LN_STAGES(nx, 2), x, x_rows, w, n, k, s)      \
-                     : launch_linear<nx, 4>(LN_STAGES(nx, 4), x, x_rows, w, n, k, s);
+#define LN_CASE(nx) return launch_linear<nx, 2>(LN_STAGES(nx, 2), x, x_rows, w, n, k, s);
   switch (NX) {
     case 16: LN_CASE(16)
     case 32: LN_CASE(32)
