@@ -172,6 +172,17 @@ int choreo_prefill_attn(const float* q, const void* k_pool, const void* v_pool, 
                         float* part_lse, int grid_ctas, void* out, int out_split, int n_rows,
                         void* stream);
 
+/* choreo_decode_attn_v2 reading Q from q_k5 (choreo_rope_append_pieces_ex's output) with
+ * one 1-D bulk copy per vector half instead of per-lane loads and conversion (NULL: q). */
+int choreo_decode_attn_v2_ex(const float* q, const void* k_pool, const void* v_pool,
+                             int n_layers, int layer, int n_kv, int n_pages, int page_size,
+                             int n_heads, int head_dim, const int32_t* row_t,
+                             const int32_t* vis_page, const int32_t* vis_len,
+                             const int32_t* vis_own, const int32_t* blk_rows,
+                             const int32_t* items, const int32_t* counts, int max_items,
+                             float* part_o, float* part_lse, const int32_t* fat_items,
+                             int grid_ctas, const void* q_k5, void* stream);
+
 /* Combine each row's partials (CSR row_part_off / row_part, <= 512 per row) into
  * out[r][h][:] (out_dtype; hi/lo pair if out_split) with the LSE merge. */
 int choreo_attn_combine(const float* part_o, const float* part_lse, const int32_t* row_part_off,
@@ -236,6 +247,16 @@ int choreo_rope_append_pieces(const ChoreoK7Pieces* qkv, int n_rows, const int32
                               void* k_pool, void* v_pool, int pool_dtype, int layer, int n_kv,
                               int n_pages, int page_size, int n_heads, int head_dim,
                               const float* cos_t, const float* sin_t, int max_delta, void* stream);
+
+/* choreo_rope_append_pieces that also writes q_k5 (bf16 [n_rows][n_heads][2][head_dim]): each
+ * rotated query vector times q_scale as a hi/lo bf16 pair -- the record format K5 v2 stages
+ * with bulk copies (choreo_decode_attn_v2_ex, q_scale = log2(e) / sqrt(head_dim)). */
+int choreo_rope_append_pieces_ex(const ChoreoK7Pieces* qkv, int n_rows, const int32_t* pos,
+                                 const int32_t* dst_page, const int32_t* dst_slot, float* q_out,
+                                 void* k_pool, void* v_pool, int pool_dtype, int layer, int n_kv,
+                                 int n_pages, int page_size, int n_heads, int head_dim,
+                                 const float* cos_t, const float* sin_t, int max_delta,
+                                 void* q_k5, float q_scale, void* stream);
 
 /* choreo_residual_rmsnorm with delta = a deferred K7 projection (x += delta; out = norm(x)). */
 int choreo_residual_rmsnorm_pieces(float* x, const ChoreoK7Pieces* delta, const void* w,
@@ -327,6 +348,9 @@ typedef struct {
   int* chain_counters;
   int* chain_done;
   void** chain_events;
+  /* optional bf16 [n_rows][n_heads][2][head_dim]: RoPE writes K5 v2's Q record format there and
+   * K5 v2 stages it with bulk copies (choreo_rope_append_pieces_ex / _decode_attn_v2_ex) */
+  void* q_k5;
 } ChoreoDecodeStep;
 
 int choreo_decode_layers(const ChoreoDecodeStep* step, void* stream);

@@ -51,6 +51,10 @@ SIGNATURES: dict[str, list] = {
                               _I, _P, _P, _P, _I, _P],
     "choreo_layer_chain": [_P, _P],
     "choreo_chain_prologue": [_P, _P, _I, _I, _P, _P, _I, _P, _P],
+    "choreo_rope_append_pieces_ex": [_P, _I, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I,
+                                     _P, _P, _I, _P, _F, _P],
+    "choreo_decode_attn_v2_ex": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P,
+                                 _P, _P, _I, _P, _P, _P, _I, _P, _P],
     "choreo_events_create": [_P, _I],
     "choreo_events_elapsed": [_P, _I, _P],
     "choreo_events_destroy": [_P, _I],
@@ -122,6 +126,8 @@ decode_layers = _Caller("choreo_decode_layers")
 linear_gate_up_silu = _Caller("choreo_linear_gate_up_silu")
 select_nucleus = _Caller("choreo_select_nucleus")
 decode_attn_v2 = _Caller("choreo_decode_attn_v2")
+decode_attn_v2_ex = _Caller("choreo_decode_attn_v2_ex")
+rope_append_pieces_ex = _Caller("choreo_rope_append_pieces_ex")
 layer_chain = _Caller("choreo_layer_chain")
 chain_prologue = _Caller("choreo_chain_prologue")
 events_create = _Caller("choreo_events_create")
@@ -144,7 +150,7 @@ class DecodeStep(ctypes.Structure):
                            "linear_events")] + \
         [(n, _I) for n in ("layer_begin", "layer_end", "part")] + \
         [(n, _P) for n in ("h_b", "ssq_a", "ssq_b", "chain_ws", "chain_counters",
-                           "chain_done", "chain_events")]
+                           "chain_done", "chain_events", "q_k5")]
 
 
 class LayerChain(ctypes.Structure):

@@ -54,7 +54,28 @@ struct DvParams {
   float* part_lse;
   float scale_log2;
   const int32_t* fat;  // optional K3 item records (rows <= 16): faster unit staging
+  int trace_slot;      // diagnostics builds (-DCHOREO_TRACE) only
+  // optional: Q already in the unit record's format (log2-domain scale, hi/lo bf16,
+  // [row][head][2][HD], written by RoPE) -- staged by 1-D bulk copies instead of loads
+  const __nv_bfloat16* q_k5;
 };
+
+#ifdef CHOREO_TRACE
+__device__ long long* g_dv_trace = nullptr;
+__device__ __forceinline__ void dv_trace(int slot, int i) {
+  if (g_dv_trace) {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_dv_trace[((size_t)(slot & 63) * 148 + blockIdx.x) * 16 + i] = t;
+  }
+}
+static int g_dv_launches = 0;
+#define DTR(i) dv_trace(p.trace_slot, i)
+#else
+#define DTR(i) \
+  do {         \
+  } while (0)
+#endif
 
 template <int HD>
 struct DvCfg {
@@ -150,7 +171,9 @@ __global__ void __launch_bounds__(kDvThreads, 1)
     tma_prefetch_desc(&tmV);
   }
   __syncthreads();
+  if (tid == 0) DTR(0);
   pdl_wait();
+  if (tid == 0) DTR(1);
   // step data (K3's counts and items) only after the programmatic-dependency wait: with
   // every kernel triggering its dependents at its start, a chain of launches can be
   // resident long before this step's K3 finished
@@ -164,6 +187,7 @@ __global__ void __launch_bounds__(kDvThreads, 1)
     for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++u) {
       const int sl = u % kDvUnits;
       mbar_wait(&unit_empty[sl], ((u / kDvUnits) & 1) ^ 1);
+      if (lane == 0 && u == 0) DTR(14);
       int* ui = reinterpret_cast<int*>(units + sl * C::kUnit);
       __nv_bfloat16* qs = reinterpret_cast<__nv_bfloat16*>(units + sl * C::kUnit + C::kUnitInts * 4);
       const int kvh = w % p.n_kv;
@@ -182,6 +206,7 @@ __global__ void __launch_bounds__(kDvThreads, 1)
         rt = rr < 12 ? t0 : t1;
       }
       const int rb = __shfl_sync(0xffffffffu, iv, 0), nr = __shfl_sync(0xffffffffu, iv, 1);
+      if (lane == 0 && u == 0) DTR(12);
       const int vb = __shfl_sync(0xffffffffu, iv, 2), nv = __shfl_sync(0xffffffffu, iv, 3);
       const int pbase = __shfl_sync(0xffffffffu, iv, 4);
       if (!p.fat) {
@@ -199,6 +224,25 @@ __global__ void __launch_bounds__(kDvThreads, 1)
       ui[8 + lane] = lane < M ? rt : -1;
       ui[40 + lane] = lane < nv ? p.vis_len[vb + lane] : 0;
       ui[72 + lane] = lane < nv ? p.vis_own[vb + lane] : -1;
+      if (p.q_k5) {
+        // lane m < M: two 256-byte bulk copies (hi, lo) of its vector; lanes >= M zero theirs
+        if (lane == 0) mbar_arrive_expect_tx(&unit_full[sl], (uint32_t)M * 2 * HD * 2);
+        __syncwarp();
+        if (lane < M) {
+          const __nv_bfloat16* src = p.q_k5 + ((int64_t)rid * p.n_heads + kvh * G + lane % G) * 2 * HD;
+          bulk_g2s(qs + lane * C::kQLd, src, HD * 2, &unit_full[sl]);
+          bulk_g2s(qs + (32 + lane) * C::kQLd, src + HD, HD * 2, &unit_full[sl]);
+        } else {
+#pragma unroll
+          for (int d = 0; d < HD; d += 8) {
+            *reinterpret_cast<uint4*>(qs + lane * C::kQLd + d) = make_uint4(0, 0, 0, 0);
+            *reinterpret_cast<uint4*>(qs + (32 + lane) * C::kQLd + d) = make_uint4(0, 0, 0, 0);
+          }
+        }
+        if (lane != 0) mbar_arrive(&unit_full[sl]);  // lane 0 arrived with the byte count
+        if (lane == 0 && u == 0) DTR(3);
+        continue;
+      }
       // Q: lane = 4 dims of every vector; all loads in flight at once (one round trip),
       // then scaled to the log2 domain and stored as bf16 (rows past M are zero)
       const float sc = p.scale_log2;
@@ -210,6 +254,16 @@ __global__ void __launch_bounds__(kDvThreads, 1)
         if (m < M && 4 * lane < HD)
           v[m] = *reinterpret_cast<const float4*>(p.q + ((int64_t)r * p.n_heads + kvh * G + m % G) * HD + 4 * lane);
       }
+#ifdef CHOREO_TRACE
+      if (u == 0) {  // consume the loads before the stamp
+        float sacc = 0.f;
+        for (int m = 0; m < 32; ++m) sacc += v[m].x;
+        if (lane == 0) {
+          if (sacc == 1234.5f) ui[0] = 0;
+          DTR(13);
+        }
+      }
+#endif
       if (4 * lane < HD) {
 #pragma unroll
         for (int m = 0; m < 32; ++m) {
@@ -223,6 +277,7 @@ __global__ void __launch_bounds__(kDvThreads, 1)
         }
       }
       mbar_arrive(&unit_full[sl]);
+      if (lane == 0 && u == 0) DTR(3);
     }
     return;
   }
@@ -234,7 +289,9 @@ __global__ void __launch_bounds__(kDvThreads, 1)
       mbar_wait(&merge_full, u & 1);
       dv_merge_unit<HD>(p, merge, mt, lane, G);
       mbar_arrive(&merge_empty);
+      if (mt == 0 && lane == 0 && u == 0) DTR(8);
     }
+    if (mt == 0 && lane == 0) DTR(9);
     return;
   }
   if (warp == kDvProducer) {
@@ -257,6 +314,7 @@ __global__ void __launch_bounds__(kDvThreads, 1)
           if (lane == 0) {
             const int st = gp % kDvSlots;
             mbar_wait(&empty_bar[st], ((gp / kDvSlots) & 1) ^ 1);
+            if (gp == 0) DTR(2);
             const int row0 = ((p.layer * p.n_kv + kvh) * p.n_pages + page) * 64;
             uint8_t* dst = base + st * C::kSlot;
             mbar_arrive_expect_tx(&full_bar[st], C::kSlot);
@@ -283,6 +341,7 @@ __global__ void __launch_bounds__(kDvThreads, 1)
   for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++u) {
     const int sl = u % kDvUnits;
     mbar_wait(&unit_full[sl], (u / kDvUnits) & 1);
+    if (warp == 0 && lane == 0 && u == 0) DTR(4);
     const int* ui = reinterpret_cast<const int*>(units + sl * C::kUnit);
     const __nv_bfloat16* qs = reinterpret_cast<const __nv_bfloat16*>(units + sl * C::kUnit + C::kUnitInts * 4);
     const int M = ui[0], nv = ui[2], pbase = ui[3], kvh = ui[4];
@@ -314,6 +373,7 @@ __global__ void __launch_bounds__(kDvThreads, 1)
     for (int j = 0; j < nv; ++j, ++gp) {
       const int st = gp % kDvSlots;
       mbar_wait(&full_bar[st], (gp / kDvSlots) & 1);
+      if (warp == 0 && lane == 0 && u == 0 && j == 0) DTR(5);
       if (active) {
         const uint32_t kb = smem_addr(base + st * C::kSlot);
         const uint32_t vbase = kb + C::kR * C::kHalf;
@@ -410,6 +470,7 @@ __global__ void __launch_bounds__(kDvThreads, 1)
     }
 
     mbar_arrive(&unit_empty[sl]);
+    if (warp == 0 && lane == 0 && u == 0) DTR(6);
     // ---- hand the key-slice state to the merge warps ----
     lA += __shfl_xor_sync(0xffffffffu, lA, 1);
     lA += __shfl_xor_sync(0xffffffffu, lA, 2);
@@ -440,7 +501,9 @@ __global__ void __launch_bounds__(kDvThreads, 1)
       hdr[2] = kvh;
     }
     mbar_arrive(&merge_full);
+    if (warp == 0 && lane == 0 && u == 0) DTR(7);
   }
+  if (warp == 0 && lane == 0) DTR(11);
 }
 
 // Merge warp of m-tile mt: lane = (row, 64-dim half); combines the four key slices' (O, m,
@@ -522,6 +585,23 @@ static int launch_dv(const DvParams& p, const void* k_pool, const void* v_pool, 
 
 using namespace choreo;
 
+#ifdef CHOREO_TRACE
+extern "C" int choreo_dv_set_trace(long long* buf) {
+  g_dv_launches = 0;
+  return cudaMemcpyToSymbol(g_dv_trace, &buf, sizeof(buf)) == cudaSuccess ? 0 : -2;
+}
+#endif
+
+extern "C" int choreo_decode_attn_v2_ex(const float* q, const void* k_pool, const void* v_pool,
+                                        int n_layers, int layer, int n_kv, int n_pages,
+                                        int page_size, int n_heads, int head_dim,
+                                        const int32_t* row_t, const int32_t* vis_page,
+                                        const int32_t* vis_len, const int32_t* vis_own,
+                                        const int32_t* blk_rows, const int32_t* items,
+                                        const int32_t* counts, int max_items, float* part_o,
+                                        float* part_lse, const int32_t* fat_items, int grid_ctas,
+                                        const void* q_k5, void* stream);
+
 extern "C" int choreo_decode_attn_v2(const float* q, const void* k_pool, const void* v_pool,
                                      int n_layers, int layer, int n_kv, int n_pages, int page_size,
                                      int n_heads, int head_dim, const int32_t* row_t,
@@ -530,6 +610,21 @@ extern "C" int choreo_decode_attn_v2(const float* q, const void* k_pool, const v
                                      const int32_t* items, const int32_t* counts, int max_items,
                                      float* part_o, float* part_lse, const int32_t* fat_items,
                                      int grid_ctas, void* stream) {
+  return choreo_decode_attn_v2_ex(q, k_pool, v_pool, n_layers, layer, n_kv, n_pages, page_size,
+                                  n_heads, head_dim, row_t, vis_page, vis_len, vis_own, blk_rows,
+                                  items, counts, max_items, part_o, part_lse, fat_items,
+                                  grid_ctas, nullptr, stream);
+}
+
+extern "C" int choreo_decode_attn_v2_ex(const float* q, const void* k_pool, const void* v_pool,
+                                        int n_layers, int layer, int n_kv, int n_pages,
+                                        int page_size, int n_heads, int head_dim,
+                                        const int32_t* row_t, const int32_t* vis_page,
+                                        const int32_t* vis_len, const int32_t* vis_own,
+                                        const int32_t* blk_rows, const int32_t* items,
+                                        const int32_t* counts, int max_items, float* part_o,
+                                        float* part_lse, const int32_t* fat_items, int grid_ctas,
+                                        const void* q_k5, void* stream) {
   if (!q || !k_pool || !v_pool || !row_t || !vis_page || !vis_len || !vis_own || !blk_rows ||
       !items || !counts || !part_o || !part_lse || n_kv <= 0 || n_heads % n_kv)
     return CHOREO_EINVAL;
@@ -541,7 +636,10 @@ extern "C" int choreo_decode_attn_v2(const float* q, const void* k_pool, const v
   const int G = n_heads / n_kv;
   DvParams p{q, layer, n_kv, n_pages, n_heads, row_t, vis_page, vis_len, vis_own, blk_rows, items,
              counts, part_o, part_lse, 1.4426950408889634f / sqrtf((float)head_dim),
-             32 / G <= 16 ? fat_items : nullptr};
+             32 / G <= 16 ? fat_items : nullptr, 0, reinterpret_cast<const __nv_bfloat16*>(q_k5)};
+#ifdef CHOREO_TRACE
+  p.trace_slot = g_dv_launches++;
+#endif
   int grid = grid_ctas > 0 ? grid_ctas : max_items * n_kv;
   if (grid > 148) grid = 148;
   auto s = as_stream(stream);

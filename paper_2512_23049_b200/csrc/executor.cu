@@ -14,6 +14,8 @@
 // The final residual add, norm and head stay with the caller (they depend on which rows
 // need logits).  Every kernel is one of the library's C-ABI entry points, so results are
 // bit-identical to the Python-driven sequence.
+#include <math.h>
+
 #include "common.cuh"
 
 using namespace choreo;
@@ -137,9 +139,10 @@ extern "C" int choreo_decode_layers(const ChoreoDecodeStep* s, void* stream) {
       CHK(choreo_linear_skinny_pieces(s->h, x_rows, sp, s->w_qkv[l], n_qkv, d, s->qkv, s->k7_ws,
                                       s->k7_cnt, 0, &pk, stream));
       LIN_EV(1);
-      CHK(choreo_rope_append_pieces(&pk, R, s->pos, s->page, s->slot, s->q, s->k_pool, s->v_pool,
-                                    CHOREO_BF16, l, Hk, s->n_pages, s->page_size, H, hd, s->cos_t,
-                                    s->sin_t, s->max_delta, stream));
+      CHK(choreo_rope_append_pieces_ex(&pk, R, s->pos, s->page, s->slot, s->q, s->k_pool,
+                                       s->v_pool, CHOREO_BF16, l, Hk, s->n_pages, s->page_size, H,
+                                       hd, s->cos_t, s->sin_t, s->max_delta, s->q_k5,
+                                       1.4426950408889634f / sqrtf((float)hd), stream));
     } else {
       CHK(choreo_linear_skinny(s->h, x_rows, sp, s->w_qkv[l], n_qkv, d, s->qkv, s->k7_ws,
                                s->k7_cnt, 0, stream));
@@ -149,10 +152,11 @@ extern "C" int choreo_decode_layers(const ChoreoDecodeStep* s, void* stream) {
                              H, hd, s->cos_t, s->sin_t, s->max_delta, stream));
     }
     if (ev) cudaEventRecord(ev[2 * l], as_stream(stream));
-    CHK(choreo_decode_attn_v2(s->q, s->k_pool, s->v_pool, s->n_layers, l, Hk, s->n_pages,
-                              s->page_size, H, hd, s->row_t, s->vis_page, s->vis_len, s->vis_own,
-                              s->blk_rows, s->items, s->counts, s->n_items, s->part_o,
-                              s->part_lse, s->fat, 0, stream));
+    CHK(choreo_decode_attn_v2_ex(s->q, s->k_pool, s->v_pool, s->n_layers, l, Hk, s->n_pages,
+                                 s->page_size, H, hd, s->row_t, s->vis_page, s->vis_len,
+                                 s->vis_own, s->blk_rows, s->items, s->counts, s->n_items,
+                                 s->part_o, s->part_lse, s->fat, 0,
+                                 defer ? s->q_k5 : nullptr, stream));
     if (ev) cudaEventRecord(ev[2 * l + 1], as_stream(stream));
     CHK(choreo_attn_combine(s->part_o, s->part_lse, s->row_part_off, s->row_part, R, H, hd,
                             s->attn, CHOREO_BF16, sp, stream));

@@ -25,7 +25,8 @@ __global__ void rope_append_kernel(const TI* __restrict__ qkv, int ld, int n_row
                                    int n_pages, int page_size, int n_heads, int hd,
                                    const float* __restrict__ cos_t,
                                    const float* __restrict__ sin_t, int max_delta,
-                                   ChoreoK7Pieces pv) {
+                                   ChoreoK7Pieces pv, __nv_bfloat16* __restrict__ q_k5,
+                                   float q_scale) {
   pdl_trigger();
   pdl_wait();
   const int half = hd >> 1;
@@ -67,6 +68,14 @@ __global__ void rope_append_kernel(const TI* __restrict__ qkv, int ld, int n_row
       float* dst = q_out + ((int64_t)r * n_heads + head) * hd + 2 * i;
       dst[0] = re;
       dst[1] = ro;
+      if (q_k5) {  // K5 v2's Q record: log2-domain scale, hi/lo bf16 halves [hi hd][lo hd]
+        const float a0 = re * q_scale, a1 = ro * q_scale;
+        const __nv_bfloat162 h = __floats2bfloat162_rn(a0, a1);
+        const float2 hf = __bfloat1622float2(h);
+        __nv_bfloat16* k5 = q_k5 + ((int64_t)r * n_heads + head) * 2 * hd + 2 * i;
+        *reinterpret_cast<__nv_bfloat162*>(k5) = h;
+        *reinterpret_cast<__nv_bfloat162*>(k5 + hd) = __floats2bfloat162_rn(a0 - hf.x, a1 - hf.y);
+      }
     } else {
       const int h = head - n_heads;
       TP* dst = kp + pool_off(layer, h, dst_page[r], dst_slot[r], n_kv, n_pages, page_size, hd) + 2 * i;
@@ -236,7 +245,8 @@ int choreo_rope_append(const void* qkv, int qkv_dtype, int ld_qkv, int n_rows, i
 #define K1(TI, TP)                                                                               \
   launch_k(rope_append_kernel<TI, TP>, blocks, 256, 0, s,                                              \
       (const TI*)qkv, ld_qkv, n_rows, qkv_split, pos, dst_page, dst_slot, q_out, (TP*)k_pool, (TP*)v_pool, \
-      layer, n_kv, n_pages, page_size, n_heads, head_dim, cos_t, sin_t, max_delta, ChoreoK7Pieces{})
+      layer, n_kv, n_pages, page_size, n_heads, head_dim, cos_t, sin_t, max_delta, ChoreoK7Pieces{}, \
+      (__nv_bfloat16*)nullptr, 0.f)
   if (qkv_dtype == CHOREO_F32 && pool_dtype == CHOREO_F32) K1(float, float);
   else if (qkv_dtype == CHOREO_F32 && pool_dtype == CHOREO_BF16) K1(float, __nv_bfloat16);
   else if (qkv_dtype == CHOREO_BF16 && pool_dtype == CHOREO_BF16) K1(__nv_bfloat16, __nv_bfloat16);
@@ -245,12 +255,30 @@ int choreo_rope_append(const void* qkv, int qkv_dtype, int ld_qkv, int n_rows, i
   return launch_status("choreo_rope_append");
 }
 
+int choreo_rope_append_pieces_ex(const ChoreoK7Pieces* qkv, int n_rows, const int32_t* pos,
+                                 const int32_t* dst_page, const int32_t* dst_slot, float* q_out,
+                                 void* k_pool, void* v_pool, int pool_dtype, int layer, int n_kv,
+                                 int n_pages, int page_size, int n_heads, int head_dim,
+                                 const float* cos_t, const float* sin_t, int max_delta,
+                                 void* q_k5, float q_scale, void* stream);
+
 int choreo_rope_append_pieces(const ChoreoK7Pieces* qkv, int n_rows, const int32_t* pos,
                               const int32_t* dst_page, const int32_t* dst_slot, float* q_out,
                               void* k_pool, void* v_pool, int pool_dtype, int layer, int n_kv,
                               int n_pages, int page_size, int n_heads, int head_dim,
                               const float* cos_t, const float* sin_t, int max_delta,
                               void* stream) {
+  return choreo_rope_append_pieces_ex(qkv, n_rows, pos, dst_page, dst_slot, q_out, k_pool, v_pool,
+                                      pool_dtype, layer, n_kv, n_pages, page_size, n_heads,
+                                      head_dim, cos_t, sin_t, max_delta, nullptr, 0.f, stream);
+}
+
+int choreo_rope_append_pieces_ex(const ChoreoK7Pieces* qkv, int n_rows, const int32_t* pos,
+                                 const int32_t* dst_page, const int32_t* dst_slot, float* q_out,
+                                 void* k_pool, void* v_pool, int pool_dtype, int layer, int n_kv,
+                                 int n_pages, int page_size, int n_heads, int head_dim,
+                                 const float* cos_t, const float* sin_t, int max_delta,
+                                 void* q_k5, float q_scale, void* stream) {
   if (!qkv || !qkv->y || !qkv->ws || !pos || !dst_page || !dst_slot || !q_out || !k_pool ||
       !v_pool || !cos_t || !sin_t)
     return CHOREO_EINVAL;
@@ -264,11 +292,13 @@ int choreo_rope_append_pieces(const ChoreoK7Pieces* qkv, int n_rows, const int32
   if (pool_dtype == CHOREO_BF16)
     launch_k(rope_append_kernel<float, __nv_bfloat16>, blocks, 256, 0, s, qkv->y, qkv->n, n_rows, 0,
              pos, dst_page, dst_slot, q_out, (__nv_bfloat16*)k_pool, (__nv_bfloat16*)v_pool, layer,
-             n_kv, n_pages, page_size, n_heads, head_dim, cos_t, sin_t, max_delta, *qkv);
+             n_kv, n_pages, page_size, n_heads, head_dim, cos_t, sin_t, max_delta, *qkv,
+             reinterpret_cast<__nv_bfloat16*>(q_k5), q_scale);
   else
     launch_k(rope_append_kernel<float, float>, blocks, 256, 0, s, qkv->y, qkv->n, n_rows, 0, pos,
              dst_page, dst_slot, q_out, (float*)k_pool, (float*)v_pool, layer, n_kv, n_pages,
-             page_size, n_heads, head_dim, cos_t, sin_t, max_delta, *qkv);
+             page_size, n_heads, head_dim, cos_t, sin_t, max_delta, *qkv, (__nv_bfloat16*)nullptr,
+             0.f);
   return launch_status("choreo_rope_append_pieces");
 }
 

@@ -64,6 +64,16 @@ __device__ __forceinline__ void tma_load_2d_hint(void* smem_dst, const void* des
       "l"(desc), "r"(smem_addr(bar)), "r"(c0), "r"(c1), "l"(policy)
       : "memory");
 }
+// 1D bulk copy global -> shared (16-byte aligned, size a multiple of 16), completes on bar.
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+          "r"(smem_addr(smem_dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
 // Prefetch one tensor-map box into L2 (no shared memory, no completion tracking).
 __device__ __forceinline__ void tma_prefetch_l2_2d(const void* desc, int c0, int c1) {
   asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n" ::"l"(desc),

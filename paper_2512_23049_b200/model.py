@@ -203,6 +203,7 @@ class Runner:
         self.chain = (self.dt == torch.bfloat16 and (tp is None or tp.size == 1)
                       and os.environ.get("CHOREO_CHAIN", "0") == "1")
         self._chain_bufs = None
+        self.q_bulk = os.environ.get("CHOREO_Q_BULK", "1") != "0"
         self.wide_k4 = os.environ.get("CHOREO_WIDE_K4", "1") != "0"
         self._wptrs = None
         self._ev_free: list = []
@@ -338,6 +339,9 @@ class Runner:
             k7_cnt=self._k7_cnt.data_ptr(),
             attn_events=ctypes.cast(ev, ctypes.c_void_p) if ev is not None else None,
             linear_events=ctypes.cast(lev, ctypes.c_void_p) if lev is not None else None)
+        if self.q_bulk:  # RoPE writes K5 v2's Q record, K5 v2 bulk-copies it
+            q_k5 = torch.empty(R, cfg.n_heads, 2, hd, dtype=torch.bfloat16, device=dev)
+            st.q_k5 = q_k5.data_ptr()
         if v2 is not None:
             _, rowt_d, vis, blk_rows, items = v2
             st.row_t, st.vis_page, st.vis_len, st.vis_own = (

@@ -421,6 +421,28 @@ def test_decode_v2_matches_dense_reference(hd, H, Hk, ppi):
                 p /= p.sum()
                 worst = max(worst, float(np.abs(got[r, h] - p @ vv).max()))
         assert worst < 2e-2, (grid, worst)
+    # Q staged by bulk copies from the RoPE-written record (hi/lo of q * log2(e)/sqrt(hd)):
+    # the same bf16 operands as the per-lane conversion, so the partials are bit-identical
+    a = q * float(np.float32(1.4426950408889634) / np.sqrt(np.float32(hd)))
+    hi = a.bfloat16()
+    q_k5 = torch.cat([hi, (a - hi.float()).bfloat16()], dim=-1).contiguous()
+    part_o.zero_()
+    part_lse.zero_()
+    nat.decode_attn_v2(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(), 2, L, Hk,
+                       cache.n_pages, 64, H, hd, rt_d.data_ptr(), vis[0].data_ptr(),
+                       vis[1].data_ptr(), vis[2].data_ptr(), blk.data_ptr(), items.data_ptr(),
+                       counts.data_ptr(), pl_.n_items, part_o.data_ptr(), part_lse.data_ptr(),
+                       None, 5, _stream())
+    ref_o, ref_lse = part_o.clone(), part_lse.clone()
+    part_o.zero_()
+    part_lse.zero_()
+    nat.decode_attn_v2_ex(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(), 2, L, Hk,
+                          cache.n_pages, 64, H, hd, rt_d.data_ptr(), vis[0].data_ptr(),
+                          vis[1].data_ptr(), vis[2].data_ptr(), blk.data_ptr(), items.data_ptr(),
+                          counts.data_ptr(), pl_.n_items, part_o.data_ptr(), part_lse.data_ptr(),
+                          None, 5, q_k5.data_ptr(), _stream())
+    torch.cuda.synchronize()
+    assert torch.equal(part_o, ref_o) and torch.equal(part_lse, ref_lse)
 
 
 def _linear(x, split, w, grid=0):
