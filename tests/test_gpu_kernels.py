@@ -460,7 +460,8 @@ def _linear(x, split, w, grid=0):
 @pytest.mark.parametrize("rows,split", [(1, False), (8, True), (16, False), (16, True), (5, True),
                                         (32, True), (40, False), (64, False), (64, True),
                                         (100, False), (37, True), (72, True), (128, True),
-                                        (65, True), (128, False)])
+                                        (65, True), (128, False), (80, True), (96, True),
+                                        (120, True)])
 @pytest.mark.parametrize("n,k", [(4096, 4096), (6144, 4096), (4096, 14336), (300, 64), (1000, 200)])
 def test_linear_skinny_matches_f32_reference(rows, split, n, k):
     """K7 (tcgen05 stream-K weight streaming) = x @ w^T in f32 over bf16 inputs; with split
