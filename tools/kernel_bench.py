@@ -233,14 +233,20 @@ def k5_decode(n_workflows: int = 1, agents: int = 8, tc: bool = False, v2: bool 
     stream = torch.cuda.current_stream().cuda_stream
 
 
+    # the runner's Q record (RoPE writes it; K5 v2 stages it with bulk copies), K5_QBULK=0: off
+    qa = q * float(np.float32(1.4426950408889634) / np.sqrt(np.float32(hd)))
+    qh = qa.bfloat16()
+    q_k5 = (torch.cat([qh, (qa - qh.float()).bfloat16()], -1).contiguous()
+            if os.environ.get("K5_QBULK", "1") != "0" else None)
+
     def run():
         if v2:
-            nat.decode_attn_v2(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(),
-                               cfg.n_layers, 0, Hk, cache.n_pages, 64, H, hd, b["rt"].data_ptr(),
-                               v[0].data_ptr(), v[1].data_ptr(), v[2].data_ptr(),
-                               b["blk"].data_ptr(), b["items"].data_ptr(), b["counts"].data_ptr(),
-                               plan.n_items, po.data_ptr(), pl.data_ptr(),
-                               b["fat"].data_ptr(), 0, stream)
+            nat.decode_attn_v2_ex(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(),
+                                  cfg.n_layers, 0, Hk, cache.n_pages, 64, H, hd,
+                                  b["rt"].data_ptr(), v[0].data_ptr(), v[1].data_ptr(),
+                                  v[2].data_ptr(), b["blk"].data_ptr(), b["items"].data_ptr(),
+                                  b["counts"].data_ptr(), plan.n_items, po.data_ptr(),
+                                  pl.data_ptr(), b["fat"].data_ptr(), 0, nat.ptr(q_k5), stream)
             return
         if tc:
             nat.prefill_attn(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(),
