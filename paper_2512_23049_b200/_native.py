@@ -54,7 +54,9 @@ SIGNATURES: dict[str, list] = {
     "choreo_rope_append_pieces_ex": [_P, _I, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I,
                                      _P, _P, _I, _P, _F, _P],
     "choreo_decode_attn_v2_ex": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P,
-                                 _P, _P, _I, _P, _P, _P, _I, _P, _P],
+                                 _P, _P, _I, _P, _P, _P, _I, _P, _P, _P],
+    "choreo_assemble_ex": [_P, _P, _P, _P, _P, _I, _P, _I, _P, _I, _I, _I, _I, _P, _P, _P, _P,
+                           _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P],
     "choreo_events_create": [_P, _I],
     "choreo_events_elapsed": [_P, _I, _P],
     "choreo_events_destroy": [_P, _I],
@@ -116,6 +118,7 @@ silu_mul = _Caller("choreo_silu_mul")
 rope_append = _Caller("choreo_rope_append")
 rerotate = _Caller("choreo_rerotate")
 assemble = _Caller("choreo_assemble")
+assemble_ex = _Caller("choreo_assemble_ex")
 attn_split = _Caller("choreo_attn_split")
 attn_combine = _Caller("choreo_attn_combine")
 prefill_attn = _Caller("choreo_prefill_attn")
@@ -150,7 +153,7 @@ class DecodeStep(ctypes.Structure):
                            "linear_events")] + \
         [(n, _I) for n in ("layer_begin", "layer_end", "part")] + \
         [(n, _P) for n in ("h_b", "ssq_a", "ssq_b", "chain_ws", "chain_counters",
-                           "chain_done", "chain_events", "q_k5")]
+                           "chain_done", "chain_events", "q_k5", "item_order")]
 
 
 class LayerChain(ctypes.Structure):

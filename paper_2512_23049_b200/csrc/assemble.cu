@@ -50,6 +50,7 @@ struct K3Params {
   int32_t* counts;
   int cap_vis, cap_blk_rows, cap_items, cap_parts;
   int32_t* fat;  // optional self-contained item records (kFatInts each), see write_fat
+  int32_t* order;  // optional: item indices by page count, descending (stable), see order_items
 };
 
 // Self-contained item record for the latency-bound decode kernel: one 256-byte load gives
@@ -79,6 +80,53 @@ __device__ void write_fat(const K3Params& p, int n_items) {
       f[44 + k] = ok ? p.vis_len[it[2] + k] : 0;
       f[52 + k] = ok ? p.vis_own[it[2] + k] : -1;
     }
+  }
+}
+
+// Item indices sorted by page count, descending, ties in item order (a stable counting sort
+// over the 32 possible counts).  K5 v2 deals the (item, kv head) units of a multi-wave step
+// to its persistent CTAs in this order, snaking across the grid (longest-first), so no CTA
+// is left with several long units while others idle.  Only the schedule changes: every
+// unit writes the same partial slots, so the results are bitwise independent of the order.
+__device__ void order_items(const int32_t* items, int n, int32_t* order) {
+  __shared__ int start[32];
+  __shared__ int wcnt[kThreads3 / 32][32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  auto key = [&](int i) { return 32 - min(max(items[6 * i + 3], 1), 32); };  // 0: longest
+  if (tid < 32) start[tid] = 0;
+  __syncthreads();
+  for (int i = tid; i < n; i += blockDim.x) atomicAdd(&start[key(i)], 1);
+  __syncthreads();
+  if (tid == 0) {
+    int run = 0;
+    for (int k = 0; k < 32; ++k) {
+      const int c = start[k];
+      start[k] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  for (int c0 = 0; c0 < n; c0 += blockDim.x) {
+    const int i = c0 + tid;
+    const int k = i < n ? key(i) : -1;
+    wcnt[warp][lane] = 0;
+    __syncwarp();
+    const unsigned peers = __match_any_sync(0xffffffffu, k);
+    const int rank = __popc(peers & ((1u << lane) - 1u));
+    if (k >= 0 && rank == 0) wcnt[warp][k] = __popc(peers);
+    __syncthreads();
+    if (k >= 0) {
+      int o = start[k] + rank;
+      for (int w = 0; w < warp; ++w) o += wcnt[w][k];
+      order[o] = i;
+    }
+    __syncthreads();
+    if (tid < 32) {
+      int t = 0;
+      for (int w = 0; w < nw; ++w) t += wcnt[w][tid];
+      start[tid] += t;
+    }
+    __syncthreads();
   }
 }
 
@@ -319,6 +367,10 @@ __global__ void __launch_bounds__(kThreads3) assemble_kernel(K3Params p) {
     __syncthreads();
     write_fat(p, S.tot_items);
   }
+  if (p.order) {
+    __syncthreads();
+    order_items(p.items, S.tot_items, p.order);
+  }
 }
 
 // Per-call mode (prefill-sized steps): each call's visible list is its parents' pages
@@ -424,20 +476,24 @@ __global__ void __launch_bounds__(kThreads3) assemble_percall_kernel(K3Params p)
     __syncthreads();
     write_fat(p, p.counts[1]);
   }
+  if (p.order) {
+    __syncthreads();
+    order_items(p.items, p.counts[1], p.order);
+  }
 }
 
 }  // namespace choreo
 
 using namespace choreo;
 
-extern "C" int choreo_assemble(const int32_t* msg_len, const int32_t* msg_pt, int32_t* page_table,
+extern "C" int choreo_assemble_ex(const int32_t* msg_len, const int32_t* msg_pt, int32_t* page_table,
                                const int32_t* calls, const int32_t* call_parents, int n_calls,
                                const int32_t* row_t, int n_rows, const int32_t* patch,
                                int n_patch, int page_size, int rows_per_block, int pages_per_item,
                                int32_t* vis_page, int32_t* vis_len, int32_t* vis_own,
                                int32_t* blk_rows, int32_t* items, int32_t* row_part_off,
                                int32_t* row_part, int32_t* counts, int cap_vis, int cap_blk_rows,
-                               int cap_items, int cap_parts, int mode, int32_t* fat,
+                               int cap_items, int cap_parts, int mode, int32_t* fat, int32_t* item_order,
                                void* stream) {
   if (!msg_len || !msg_pt || !page_table || !calls || !row_t || !vis_page || !vis_len ||
       !vis_own || !blk_rows || !items || !row_part_off || !row_part || !counts)
@@ -448,7 +504,7 @@ extern "C" int choreo_assemble(const int32_t* msg_len, const int32_t* msg_pt, in
   K3Params p{msg_len, msg_pt, page_table, calls, call_parents, n_calls, row_t, n_rows, patch,
              n_patch, page_size, rows_per_block, pages_per_item, vis_page, vis_len, vis_own,
              blk_rows, items, row_part_off, row_part, counts, cap_vis, cap_blk_rows, cap_items,
-             cap_parts, fat};
+             cap_parts, fat, item_order};
   if (mode == 1) {
     launch_k(assemble_percall_kernel, 1, kThreads3, 0, as_stream(stream), p);
     return launch_status("choreo_assemble");
@@ -461,4 +517,20 @@ extern "C" int choreo_assemble(const int32_t* msg_len, const int32_t* msg_pt, in
   }
   launch_k(assemble_kernel, 1, kThreads3, sizeof(Shared), as_stream(stream), p);
   return launch_status("choreo_assemble");
+}
+
+extern "C" int choreo_assemble(const int32_t* msg_len, const int32_t* msg_pt, int32_t* page_table,
+                               const int32_t* calls, const int32_t* call_parents, int n_calls,
+                               const int32_t* row_t, int n_rows, const int32_t* patch,
+                               int n_patch, int page_size, int rows_per_block, int pages_per_item,
+                               int32_t* vis_page, int32_t* vis_len, int32_t* vis_own,
+                               int32_t* blk_rows, int32_t* items, int32_t* row_part_off,
+                               int32_t* row_part, int32_t* counts, int cap_vis, int cap_blk_rows,
+                               int cap_items, int cap_parts, int mode, int32_t* fat,
+                               void* stream) {
+  return choreo_assemble_ex(msg_len, msg_pt, page_table, calls, call_parents, n_calls, row_t,
+                            n_rows, patch, n_patch, page_size, rows_per_block, pages_per_item,
+                            vis_page, vis_len, vis_own, blk_rows, items, row_part_off, row_part,
+                            counts, cap_vis, cap_blk_rows, cap_items, cap_parts, mode, fat,
+                            nullptr, stream);
 }

@@ -58,7 +58,26 @@ struct DvParams {
   // optional: Q already in the unit record's format (log2-domain scale, hi/lo bf16,
   // [row][head][2][HD], written by RoPE) -- staged by 1-D bulk copies instead of loads
   const __nv_bfloat16* q_k5;
+  // optional: K3's item order (page count descending).  A step with more units than CTAs
+  // deals them longest-first, snaking across the grid; else unit w = blockIdx.x + k * grid
+  const int32_t* order;
 };
+
+// k-th unit of this CTA (-1: none left).  Round k covers units [k G, k G + G) (G = grid);
+// with `snake` odd rounds run backwards, so the CTA that took round k's longest unit takes
+// round k+1's shortest.
+__device__ __forceinline__ int dv_unit(int k, int n_work, bool snake) {
+  const int g = gridDim.x;
+  const int s = k * g + ((snake && (k & 1)) ? g - 1 - (int)blockIdx.x : (int)blockIdx.x);
+  return s < n_work ? s : -1;
+}
+// item of each of the 32 units k0 + lane (one round trip for 32 units; -1 past the end)
+__device__ __forceinline__ int dv_items32(const DvParams& p, int k0, int lane, int n_work,
+                                          bool snake) {
+  const int s = dv_unit(k0 + lane, n_work, snake);
+  if (s < 0) return -1;
+  return snake ? p.order[s / p.n_kv] : s / p.n_kv;
+}
 
 #ifdef CHOREO_TRACE
 __device__ long long* g_dv_trace = nullptr;
@@ -178,26 +197,31 @@ __global__ void __launch_bounds__(kDvThreads, 1)
   // every kernel triggering its dependents at its start, a chain of launches can be
   // resident long before this step's K3 finished
   const int n_work = p.counts[1] * p.n_kv;
+  const bool snake = p.order != nullptr && n_work > (int)gridDim.x;
 
   if (warp == kDvLoader) {
     // ------------------------------------------------------------------ unit loader
     // stages each unit's metadata and its Q vectors (bf16, pre-scaled to the log2 domain)
     // one unit ahead of the consumers, so a unit boundary costs no dependent global loads
-    int u = 0;
-    for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++u) {
+    int ord = 0;
+    for (int u = 0;; ++u) {
+      const int w = dv_unit(u, n_work, snake);
+      if (w < 0) break;
+      if ((u & 31) == 0) ord = dv_items32(p, u, lane, n_work, snake);
+      const int item = __shfl_sync(0xffffffffu, ord, u & 31);
       const int sl = u % kDvUnits;
       mbar_wait(&unit_empty[sl], ((u / kDvUnits) & 1) ^ 1);
       if (lane == 0 && u == 0) DTR(14);
       int* ui = reinterpret_cast<int*>(units + sl * C::kUnit);
       __nv_bfloat16* qs = reinterpret_cast<__nv_bfloat16*>(units + sl * C::kUnit + C::kUnitInts * 4);
       const int kvh = w % p.n_kv;
-      const int32_t* it = p.items + 6 * (w / p.n_kv);
+      const int32_t* it = p.items + 6 * item;
       const int iv = lane < 5 ? it[lane] : 0;
       int rid, rt;
       if (p.fat) {
         // K3's self-contained item record supplies the rows and their row_t in the same
         // round trip as the item ([4..20) rid, [20..36) row_t)
-        const int32_t* fr = p.fat + (int64_t)(w / p.n_kv) * 64;
+        const int32_t* fr = p.fat + (int64_t)item * 64;
         const int f0 = fr[lane], f1 = fr[32 + lane];
         const int rr = min(lane / G, 15);
         rid = __shfl_sync(0xffffffffu, f0, 4 + rr);
@@ -284,8 +308,7 @@ __global__ void __launch_bounds__(kDvThreads, 1)
   if (warp >= kDvMerge) {
     // ------------------------------------------------------------------ merge warps
     const int mt = warp - kDvMerge;
-    int u = 0;
-    for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++u) {
+    for (int u = 0; dv_unit(u, n_work, snake) >= 0; ++u) {
       mbar_wait(&merge_full, u & 1);
       dv_merge_unit<HD>(p, merge, mt, lane, G);
       mbar_arrive(&merge_empty);
@@ -301,8 +324,12 @@ __global__ void __launch_bounds__(kDvThreads, 1)
     // issues the TMA copies
     uint32_t gp = 0;
     const uint64_t pol = l2_policy_evict_first();  // K/V pages: read once per step and layer
-    for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
-      const int32_t* it = p.items + 6 * (w / p.n_kv);
+    int ord = 0;
+    for (int u = 0;; ++u) {
+      const int w = dv_unit(u, n_work, snake);
+      if (w < 0) break;
+      if ((u & 31) == 0) ord = dv_items32(p, u, lane, n_work, snake);
+      const int32_t* it = p.items + 6 * __shfl_sync(0xffffffffu, ord, u & 31);
       const int iv = lane < 4 ? it[lane] : 0;
       const int vb = __shfl_sync(0xffffffffu, iv, 2), nv = __shfl_sync(0xffffffffu, iv, 3);
       const int kvh = w % p.n_kv;
@@ -337,8 +364,7 @@ __global__ void __launch_bounds__(kDvThreads, 1)
   const int g = lane >> 2, t = lane & 3;
   const int k0 = 16 * q4;                   // first key of this warp's slice
   uint32_t gp = 0;
-  int u = 0;
-  for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++u) {
+  for (int u = 0; dv_unit(u, n_work, snake) >= 0; ++u) {
     const int sl = u % kDvUnits;
     mbar_wait(&unit_full[sl], (u / kDvUnits) & 1);
     if (warp == 0 && lane == 0 && u == 0) DTR(4);
@@ -600,7 +626,8 @@ extern "C" int choreo_decode_attn_v2_ex(const float* q, const void* k_pool, cons
                                         const int32_t* blk_rows, const int32_t* items,
                                         const int32_t* counts, int max_items, float* part_o,
                                         float* part_lse, const int32_t* fat_items, int grid_ctas,
-                                        const void* q_k5, void* stream);
+                                        const void* q_k5, const int32_t* item_order,
+                                        void* stream);
 
 extern "C" int choreo_decode_attn_v2(const float* q, const void* k_pool, const void* v_pool,
                                      int n_layers, int layer, int n_kv, int n_pages, int page_size,
@@ -613,7 +640,7 @@ extern "C" int choreo_decode_attn_v2(const float* q, const void* k_pool, const v
   return choreo_decode_attn_v2_ex(q, k_pool, v_pool, n_layers, layer, n_kv, n_pages, page_size,
                                   n_heads, head_dim, row_t, vis_page, vis_len, vis_own, blk_rows,
                                   items, counts, max_items, part_o, part_lse, fat_items,
-                                  grid_ctas, nullptr, stream);
+                                  grid_ctas, nullptr, nullptr, stream);
 }
 
 extern "C" int choreo_decode_attn_v2_ex(const float* q, const void* k_pool, const void* v_pool,
@@ -624,7 +651,8 @@ extern "C" int choreo_decode_attn_v2_ex(const float* q, const void* k_pool, cons
                                         const int32_t* blk_rows, const int32_t* items,
                                         const int32_t* counts, int max_items, float* part_o,
                                         float* part_lse, const int32_t* fat_items, int grid_ctas,
-                                        const void* q_k5, void* stream) {
+                                        const void* q_k5, const int32_t* item_order,
+                                        void* stream) {
   if (!q || !k_pool || !v_pool || !row_t || !vis_page || !vis_len || !vis_own || !blk_rows ||
       !items || !counts || !part_o || !part_lse || n_kv <= 0 || n_heads % n_kv)
     return CHOREO_EINVAL;
@@ -636,7 +664,8 @@ extern "C" int choreo_decode_attn_v2_ex(const float* q, const void* k_pool, cons
   const int G = n_heads / n_kv;
   DvParams p{q, layer, n_kv, n_pages, n_heads, row_t, vis_page, vis_len, vis_own, blk_rows, items,
              counts, part_o, part_lse, 1.4426950408889634f / sqrtf((float)head_dim),
-             32 / G <= 16 ? fat_items : nullptr, 0, reinterpret_cast<const __nv_bfloat16*>(q_k5)};
+             32 / G <= 16 ? fat_items : nullptr, 0, reinterpret_cast<const __nv_bfloat16*>(q_k5),
+             item_order};
 #ifdef CHOREO_TRACE
   p.trace_slot = g_dv_launches++;
 #endif

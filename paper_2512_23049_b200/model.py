@@ -205,6 +205,9 @@ class Runner:
         self._chain_bufs = None
         self.q_bulk = os.environ.get("CHOREO_Q_BULK", "1") != "0"
         self.wide_k4 = os.environ.get("CHOREO_WIDE_K4", "1") != "0"
+        # K5 v2 unit schedule of multi-wave steps (no effect on results): longest-first snake
+        # deal (default) or unit w to CTA w mod grid (CHOREO_V2_LPT=0, for A/B timing)
+        self.v2_lpt = os.environ.get("CHOREO_V2_LPT", "1") != "0"
         self._wptrs = None
         self._ev_free: list = []
         self._ev_pending: list = []  # (kind, event array, bytes per pair) awaiting readback
@@ -343,10 +346,11 @@ class Runner:
             q_k5 = torch.empty(R, cfg.n_heads, 2, hd, dtype=torch.bfloat16, device=dev)
             st.q_k5 = q_k5.data_ptr()
         if v2 is not None:
-            _, rowt_d, vis, blk_rows, items = v2
+            _, rowt_d, vis, blk_rows, items, order = v2
             st.row_t, st.vis_page, st.vis_len, st.vis_own = (
                 rowt_d.data_ptr(), vis[0].data_ptr(), vis[1].data_ptr(), vis[2].data_ptr())
             st.blk_rows, st.items = blk_rows.data_ptr(), items.data_ptr()
+            st.item_order = nat.ptr(order)
         if chain:
             cb = self._chain_buffers()
             h_b = torch.empty(2 * R if self.split else R, d, dtype=self.dt, device=dev)
@@ -478,7 +482,9 @@ class Runner:
         if use_k4 and mode == 0:  # page-centric K4 items: long page runs keep its pipeline full
             ppi = max(ppi, 16)
         plan_ = plan_counts(plan.calls, msg_len, P, rpb, ppi, mode)
-        if v2:  # grow items until the units fit one wave of CTAs (else a few CTAs run two)
+        if v2:  # grow items until the units fit one wave of CTAs; steps that still need more
+            # waves (many workflows batched) deal them longest-first (K3 item_order; measured:
+            # one wave of longer items beats a longest-first deal of shorter ones in situ)
             while plan_.n_items * Hk > 148 and ppi < 32:
                 ppi = min(32, ppi + max(1, ppi // 4))
                 plan_ = plan_counts(plan.calls, msg_len, P, rpb, ppi, mode)
@@ -525,12 +531,15 @@ class Runner:
         counts = torch.empty(4, dtype=torch.int32, device=self.dev)
         fat = (torch.empty(max(n_items, 1), 64, dtype=torch.int32, device=self.dev)
                if v2 and rpb <= 16 else None)
-        nat.assemble(cache.msg_len.dev.data_ptr(), cache.msg_pt.dev.data_ptr(),
-                     cache.page_table.dev.data_ptr(), calls_d.data_ptr(), parents_d.data_ptr(),
-                     n_calls, rowt_d.data_ptr(), R, None, 0, P, rpb, ppi, vis[0].data_ptr(),
-                     vis[1].data_ptr(), vis[2].data_ptr(), blk_rows.data_ptr(), items.data_ptr(),
-                     row_part_off.data_ptr(), row_part.data_ptr(), counts.data_ptr(),
-                     plan_.n_vis, plan_.n_blk_rows, n_items, n_parts, mode, nat.ptr(fat), stream)
+        order = (torch.empty(max(n_items, 1), dtype=torch.int32, device=self.dev)
+                 if v2 and self.v2_lpt else None)
+        nat.assemble_ex(cache.msg_len.dev.data_ptr(), cache.msg_pt.dev.data_ptr(),
+                        cache.page_table.dev.data_ptr(), calls_d.data_ptr(), parents_d.data_ptr(),
+                        n_calls, rowt_d.data_ptr(), R, None, 0, P, rpb, ppi, vis[0].data_ptr(),
+                        vis[1].data_ptr(), vis[2].data_ptr(), blk_rows.data_ptr(),
+                        items.data_ptr(), row_part_off.data_ptr(), row_part.data_ptr(),
+                        counts.data_ptr(), plan_.n_vis, plan_.n_blk_rows, n_items, n_parts, mode,
+                        nat.ptr(fat), nat.ptr(order), stream)
         self.launches += 1
         self.last_assembly = (vis, blk_rows, items, row_part_off, row_part, counts, plan_, rowt_d)
         if self.check_assembly:  # debug/test: K3 must never report an overflow
@@ -566,7 +575,8 @@ class Runner:
         if native:
             delta = self._native_layers(R, q, part_o, part_lse, attn, h, act, x, pos_d, page_d,
                                         slot_d, fat, counts, n_items, row_part_off, row_part,
-                                        attn_bytes, stream, (v2, rowt_d, vis, blk_rows, items))
+                                        attn_bytes, stream,
+                                        (v2, rowt_d, vis, blk_rows, items, order))
             if self._chain_ok(R):  # prologue + qkv(0); per layer: K5, combine, K8 chain
                 launches += 2 + 3 * len(self.w.layers)
             else:  # per layer: norm, K7 qkv, rope, K5, combine, K7 o, norm, K7 gate|up, K7 down
@@ -586,12 +596,13 @@ class Runner:
                 ev1 = torch.cuda.Event(enable_timing=True)
                 ev0.record()
             if v2:
-                nat.decode_attn_v2(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(),
-                                   cfg.n_layers, layer, Hk, cache.n_pages, P, H, hd,
-                                   rowt_d.data_ptr(), vis[0].data_ptr(), vis[1].data_ptr(),
-                                   vis[2].data_ptr(), blk_rows.data_ptr(), items.data_ptr(),
-                                   counts.data_ptr(), n_items, part_o.data_ptr(),
-                                   part_lse.data_ptr(), nat.ptr(fat), 0, stream)
+                nat.decode_attn_v2_ex(q.data_ptr(), cache.k_pool.data_ptr(),
+                                      cache.v_pool.data_ptr(), cfg.n_layers, layer, Hk,
+                                      cache.n_pages, P, H, hd, rowt_d.data_ptr(),
+                                      vis[0].data_ptr(), vis[1].data_ptr(), vis[2].data_ptr(),
+                                      blk_rows.data_ptr(), items.data_ptr(), counts.data_ptr(),
+                                      n_items, part_o.data_ptr(), part_lse.data_ptr(),
+                                      nat.ptr(fat), 0, None, nat.ptr(order), stream)
             elif use_k4:
                 nat.prefill_attn(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(),
                                  self.pool_dtc, cfg.n_layers, layer, Hk, cache.n_pages, P, H, hd,

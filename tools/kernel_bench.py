@@ -100,15 +100,17 @@ def _assemble(cache, calls, rpb, ppi, mode=0):
                 rpo=torch.empty(R + 1, dtype=torch.int32, device="cuda"),
                 rp=torch.empty(plan.n_parts, dtype=torch.int32, device="cuda"),
                 counts=torch.empty(4, dtype=torch.int32, device="cuda"), rt=rt_d,
-                fat=torch.empty(max(plan.n_items, 1), 64, dtype=torch.int32, device="cuda"))
+                fat=torch.empty(max(plan.n_items, 1), 64, dtype=torch.int32, device="cuda"),
+                order=torch.empty(max(plan.n_items, 1), dtype=torch.int32, device="cuda"))
     v = bufs["vis"]
-    nat.assemble(cache.msg_len.dev.data_ptr(), cache.msg_pt.dev.data_ptr(),
+    nat.assemble_ex(cache.msg_len.dev.data_ptr(), cache.msg_pt.dev.data_ptr(),
                  cache.page_table.dev.data_ptr(), tab_d.data_ptr(), par_d.data_ptr(), len(calls),
                  rt_d.data_ptr(), R, None, 0, 64, rpb, ppi, v[0].data_ptr(), v[1].data_ptr(),
                  v[2].data_ptr(), bufs["blk"].data_ptr(), bufs["items"].data_ptr(),
                  bufs["rpo"].data_ptr(), bufs["rp"].data_ptr(), bufs["counts"].data_ptr(),
                  plan.n_vis, plan.n_blk_rows, plan.n_items, plan.n_parts, mode,
-                 bufs["fat"].data_ptr(), torch.cuda.current_stream().cuda_stream)
+                 bufs["fat"].data_ptr(), bufs["order"].data_ptr(),
+                 torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     assert int(bufs["counts"][3]) == 0
     return plan, bufs, R
@@ -225,6 +227,7 @@ def k5_decode(n_workflows: int = 1, agents: int = 8, tc: bool = False, v2: bool 
             ppi = min(32, ppi + max(1, ppi // 4))
     ppi = int(os.environ.get("K5_PPI", ppi))
     plan, b, R = _assemble(cache, calls, rpb, ppi)
+    order = None if os.environ.get("K5_ORDER", "1") == "0" else b["order"]  # K5_ORDER=0: w mod grid
     q = torch.randn(R, H, hd, device="cuda")
     po = torch.empty(plan.n_parts, H, hd, device="cuda")
     pl = torch.empty(plan.n_parts, H, device="cuda")
@@ -246,7 +249,8 @@ def k5_decode(n_workflows: int = 1, agents: int = 8, tc: bool = False, v2: bool 
                                   b["rt"].data_ptr(), v[0].data_ptr(), v[1].data_ptr(),
                                   v[2].data_ptr(), b["blk"].data_ptr(), b["items"].data_ptr(),
                                   b["counts"].data_ptr(), plan.n_items, po.data_ptr(),
-                                  pl.data_ptr(), b["fat"].data_ptr(), 0, nat.ptr(q_k5), stream)
+                                  pl.data_ptr(), b["fat"].data_ptr(), 0, nat.ptr(q_k5),
+                                  nat.ptr(order), stream)
             return
         if tc:
             nat.prefill_attn(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(),
