@@ -245,12 +245,13 @@ __global__ void __launch_bounds__(kDvThreads, 1)
         ui[3] = pbase;
         ui[4] = kvh;
       }
-      ui[8 + lane] = lane < M ? rt : -1;
-      ui[40 + lane] = lane < nv ? p.vis_len[vb + lane] : 0;
-      ui[72 + lane] = lane < nv ? p.vis_own[vb + lane] : -1;
+      // page lengths / own bases: loads issued here, stored after the Q copies are in flight
+      const int vl = lane < nv ? p.vis_len[vb + lane] : 0;
+      const int vo = lane < nv ? p.vis_own[vb + lane] : -1;
       if (p.q_k5) {
-        // lane m < M: two 256-byte bulk copies (hi, lo) of its vector; lanes >= M zero theirs
-        if (lane == 0) mbar_arrive_expect_tx(&unit_full[sl], (uint32_t)M * 2 * HD * 2);
+        // lane m < M: two 256-byte bulk copies (hi, lo) of its vector; lanes >= M zero theirs.
+        // The byte count is posted without an arrival: every lane arrives after its stores.
+        if (lane == 0) mbar_expect_tx(&unit_full[sl], (uint32_t)M * 2 * HD * 2);
         __syncwarp();
         if (lane < M) {
           const __nv_bfloat16* src = p.q_k5 + ((int64_t)rid * p.n_heads + kvh * G + lane % G) * 2 * HD;
@@ -263,10 +264,16 @@ __global__ void __launch_bounds__(kDvThreads, 1)
             *reinterpret_cast<uint4*>(qs + (32 + lane) * C::kQLd + d) = make_uint4(0, 0, 0, 0);
           }
         }
-        if (lane != 0) mbar_arrive(&unit_full[sl]);  // lane 0 arrived with the byte count
+        ui[8 + lane] = lane < M ? rt : -1;
+        ui[40 + lane] = vl;
+        ui[72 + lane] = vo;
+        mbar_arrive(&unit_full[sl]);
         if (lane == 0 && u == 0) DTR(3);
         continue;
       }
+      ui[8 + lane] = lane < M ? rt : -1;
+      ui[40 + lane] = vl;
+      ui[72 + lane] = vo;
       // Q: lane = 4 dims of every vector; all loads in flight at once (one round trip),
       // then scaled to the log2 domain and stored as bf16 (rows past M are zero)
       const float sc = p.scale_log2;

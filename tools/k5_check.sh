@@ -8,3 +8,4 @@ for wf in (1, 8, 1, 8):
     r = kb.k5_decode(wf); print('K5', wf, r['us'], r['frac'], r['items'], r['pages_per_item'])
 "
 for i in 1 2; do timeout 300 python tools/step_timing.py --steps 200 2>&1 | tail -1; done
+timeout 300 python tools/dv_trace_step.py 2>&1 | tail -18
