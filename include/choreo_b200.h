@@ -142,7 +142,10 @@ int choreo_assemble(const int32_t* msg_len, const int32_t* msg_pt, int32_t* page
 /* choreo_assemble plus item_order (optional, int32 [n_items]): the item indices sorted by
  * page count, descending, ties in item order.  choreo_decode_attn_v2_ex deals a multi-wave
  * step's units to its persistent CTAs longest-first in this order (schedule only: results
- * are bitwise the same with or without it). */
+ * are bitwise the same with or without it).  step_tag != 0 (mode 0; counts must then hold 6
+ * ints, 8-byte aligned): counts[4..5] = {step_tag, n_items} (one 64-bit release store, device
+ * scope) once every output is written, so a later kernel of the step may read them before
+ * its programmatic-dependency wait. */
 int choreo_assemble_ex(const int32_t* msg_len, const int32_t* msg_pt, int32_t* page_table,
                        const int32_t* calls, const int32_t* call_parents, int n_calls,
                        const int32_t* row_t, int n_rows, const int32_t* patch, int n_patch,
@@ -150,7 +153,7 @@ int choreo_assemble_ex(const int32_t* msg_len, const int32_t* msg_pt, int32_t* p
                        int32_t* vis_len, int32_t* vis_own, int32_t* blk_rows, int32_t* items,
                        int32_t* row_part_off, int32_t* row_part, int32_t* counts, int cap_vis,
                        int cap_blk_rows, int cap_items, int cap_parts, int mode, int32_t* fat,
-                       int32_t* item_order, void* stream);
+                       int32_t* item_order, int step_tag, void* stream);
 
 /* K5 split-KV attention over assembled work items (prefill and decode rows alike).
  * q: f32 [n_rows][n_heads][hd] (already rotated, K1).  For each item and KV head writes
@@ -188,7 +191,9 @@ int choreo_prefill_attn(const float* q, const void* k_pool, const void* v_pool, 
 /* choreo_decode_attn_v2 reading Q from q_k5 (choreo_rope_append_pieces_ex's output) with
  * one 1-D bulk copy per vector half instead of per-lane loads and conversion (NULL: q), and
  * (item_order, optional: choreo_assemble_ex's output) dealing the units of a step with more
- * units than CTAs longest-first, snaking across the grid (NULL: unit w to CTA w mod grid). */
+ * units than CTAs longest-first, snaking across the grid (NULL: unit w to CTA w mod grid).
+ * k3_tag != 0: the step_tag given to choreo_assemble_ex; once counts[4] holds it the loader
+ * and producer warps read the step's K3 outputs before the programmatic-dependency wait. */
 int choreo_decode_attn_v2_ex(const float* q, const void* k_pool, const void* v_pool,
                              int n_layers, int layer, int n_kv, int n_pages, int page_size,
                              int n_heads, int head_dim, const int32_t* row_t,
@@ -197,7 +202,7 @@ int choreo_decode_attn_v2_ex(const float* q, const void* k_pool, const void* v_p
                              const int32_t* items, const int32_t* counts, int max_items,
                              float* part_o, float* part_lse, const int32_t* fat_items,
                              int grid_ctas, const void* q_k5, const int32_t* item_order,
-                             void* stream);
+                             int k3_tag, void* stream);
 
 /* Combine each row's partials (CSR row_part_off / row_part, <= 512 per row) into
  * out[r][h][:] (out_dtype; hi/lo pair if out_split) with the LSE merge. */
@@ -369,6 +374,8 @@ typedef struct {
   void* q_k5;
   /* optional int32 [n_items]: choreo_assemble_ex's item_order (K5 v2 unit schedule) */
   const int32_t* item_order;
+  /* the step_tag given to choreo_assemble_ex (0: none), see choreo_decode_attn_v2_ex */
+  int k3_tag;
 } ChoreoDecodeStep;
 
 int choreo_decode_layers(const ChoreoDecodeStep* step, void* stream);

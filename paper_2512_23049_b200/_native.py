@@ -54,9 +54,9 @@ SIGNATURES: dict[str, list] = {
     "choreo_rope_append_pieces_ex": [_P, _I, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I,
                                      _P, _P, _I, _P, _F, _P],
     "choreo_decode_attn_v2_ex": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P,
-                                 _P, _P, _I, _P, _P, _P, _I, _P, _P, _P],
+                                 _P, _P, _I, _P, _P, _P, _I, _P, _P, _I, _P],
     "choreo_assemble_ex": [_P, _P, _P, _P, _P, _I, _P, _I, _P, _I, _I, _I, _I, _P, _P, _P, _P,
-                           _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P],
+                           _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _I, _P],
     "choreo_events_create": [_P, _I],
     "choreo_events_elapsed": [_P, _I, _P],
     "choreo_events_destroy": [_P, _I],
@@ -153,7 +153,8 @@ class DecodeStep(ctypes.Structure):
                            "linear_events")] + \
         [(n, _I) for n in ("layer_begin", "layer_end", "part")] + \
         [(n, _P) for n in ("h_b", "ssq_a", "ssq_b", "chain_ws", "chain_counters",
-                           "chain_done", "chain_events", "q_k5", "item_order")]
+                           "chain_done", "chain_events", "q_k5", "item_order")] + \
+        [("k3_tag", _I)]
 
 
 class LayerChain(ctypes.Structure):

@@ -51,7 +51,22 @@ struct K3Params {
   int cap_vis, cap_blk_rows, cap_items, cap_parts;
   int32_t* fat;  // optional self-contained item records (kFatInts each), see write_fat
   int32_t* order;  // optional: item indices by page count, descending (stable), see order_items
+  int tag;         // != 0: counts[4] = tag once every output is written (mode 0), see stamp
 };
+
+// counts[4..5] = {tag, n_items} (one 64-bit release store) after every output of the step
+// is written and visible device-wide: a later kernel that finds its step's tag there may
+// read the (step-static) K3 outputs before its programmatic-dependency wait (K5 v2 does, to
+// overlap its first lookups), the item count coming with the tag in one round trip.
+__device__ void stamp(const K3Params& p) {
+  if (!p.tag) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint64_t v = ((uint64_t)(uint32_t)p.counts[1] << 32) | (uint32_t)p.tag;
+    asm volatile("st.release.gpu.global.b64 [%0], %1;\n" ::"l"(p.counts + 4), "l"(v) : "memory");
+  }
+}
 
 // Self-contained item record for the latency-bound decode kernel: one 256-byte load gives
 // a CTA everything it needs (no dependent lookups of rows, row_t or page descriptors).
@@ -371,6 +386,7 @@ __global__ void __launch_bounds__(kThreads3) assemble_kernel(K3Params p) {
     __syncthreads();
     order_items(p.items, S.tot_items, p.order);
   }
+  stamp(p);
 }
 
 // Per-call mode (prefill-sized steps): each call's visible list is its parents' pages
@@ -494,7 +510,7 @@ extern "C" int choreo_assemble_ex(const int32_t* msg_len, const int32_t* msg_pt,
                                int32_t* blk_rows, int32_t* items, int32_t* row_part_off,
                                int32_t* row_part, int32_t* counts, int cap_vis, int cap_blk_rows,
                                int cap_items, int cap_parts, int mode, int32_t* fat, int32_t* item_order,
-                               void* stream) {
+                               int step_tag, void* stream) {
   if (!msg_len || !msg_pt || !page_table || !calls || !row_t || !vis_page || !vis_len ||
       !vis_own || !blk_rows || !items || !row_part_off || !row_part || !counts)
     return CHOREO_EINVAL;
@@ -504,7 +520,7 @@ extern "C" int choreo_assemble_ex(const int32_t* msg_len, const int32_t* msg_pt,
   K3Params p{msg_len, msg_pt, page_table, calls, call_parents, n_calls, row_t, n_rows, patch,
              n_patch, page_size, rows_per_block, pages_per_item, vis_page, vis_len, vis_own,
              blk_rows, items, row_part_off, row_part, counts, cap_vis, cap_blk_rows, cap_items,
-             cap_parts, fat, item_order};
+             cap_parts, fat, item_order, mode == 0 ? step_tag : 0};
   if (mode == 1) {
     launch_k(assemble_percall_kernel, 1, kThreads3, 0, as_stream(stream), p);
     return launch_status("choreo_assemble");
@@ -532,5 +548,5 @@ extern "C" int choreo_assemble(const int32_t* msg_len, const int32_t* msg_pt, in
                             n_rows, patch, n_patch, page_size, rows_per_block, pages_per_item,
                             vis_page, vis_len, vis_own, blk_rows, items, row_part_off, row_part,
                             counts, cap_vis, cap_blk_rows, cap_items, cap_parts, mode, fat,
-                            nullptr, stream);
+                            nullptr, 0, stream);
 }

@@ -61,6 +61,9 @@ struct DvParams {
   // optional: K3's item order (page count descending).  A step with more units than CTAs
   // deals them longest-first, snaking across the grid; else unit w = blockIdx.x + k * grid
   const int32_t* order;
+  // != 0: the step's K3 stamps counts[4] with this tag once its outputs are complete; the
+  // loader and producer then do their first lookups before the dependency wait
+  int k3_tag;
 };
 
 // k-th unit of this CTA (-1: none left).  Round k covers units [k G, k G + G) (G = grid);
@@ -191,12 +194,27 @@ __global__ void __launch_bounds__(kDvThreads, 1)
   }
   __syncthreads();
   if (tid == 0) DTR(0);
-  pdl_wait();
-  if (tid == 0) DTR(1);
-  // step data (K3's counts and items) only after the programmatic-dependency wait: with
+  // step data (K3's counts and items) only after the programmatic-dependency wait (with
   // every kernel triggering its dependents at its start, a chain of launches can be
-  // resident long before this step's K3 finished
-  const int n_work = p.counts[1] * p.n_kv;
+  // resident long before this step's K3 finished) -- unless K3 has stamped this step's tag:
+  // its outputs are then complete, and the loader / producer look up their first unit while
+  // the predecessor (RoPE) still runs, waiting only before they touch its outputs (Q, the
+  // appended K/V)
+  bool early = false;
+  int n_items = 0;
+  if (p.k3_tag != 0 && (warp == kDvLoader || warp == kDvProducer)) {
+    uint64_t v = 0;  // {tag, n_items}, K3's 64-bit release store
+    if (lane == 0)
+      asm volatile("ld.acquire.gpu.global.b64 %0, [%1];\n" : "=l"(v) : "l"(p.counts + 4) : "memory");
+    early = __shfl_sync(0xffffffffu, (int)(uint32_t)v, 0) == p.k3_tag;
+    n_items = __shfl_sync(0xffffffffu, (int)(v >> 32), 0);
+  }
+  if (!early) {
+    pdl_wait();
+    n_items = p.counts[1];
+  }
+  if (tid == 0) DTR(1);
+  const int n_work = n_items * p.n_kv;
   const bool snake = p.order != nullptr && n_work > (int)gridDim.x;
 
   if (warp == kDvLoader) {
@@ -248,6 +266,7 @@ __global__ void __launch_bounds__(kDvThreads, 1)
       // page lengths / own bases: loads issued here, stored after the Q copies are in flight
       const int vl = lane < nv ? p.vis_len[vb + lane] : 0;
       const int vo = lane < nv ? p.vis_own[vb + lane] : -1;
+      if (early && u == 0) pdl_wait();  // Q is the predecessor's output
       if (p.q_k5) {
         // lane m < M: two 256-byte bulk copies (hi, lo) of its vector; lanes >= M zero theirs.
         // The byte count is posted without an arrival: every lane arrives after its stores.
@@ -340,6 +359,7 @@ __global__ void __launch_bounds__(kDvThreads, 1)
       const int iv = lane < 4 ? it[lane] : 0;
       const int vb = __shfl_sync(0xffffffffu, iv, 2), nv = __shfl_sync(0xffffffffu, iv, 3);
       const int kvh = w % p.n_kv;
+      if (early && u == 0) pdl_wait();  // the pages hold the predecessor's K/V appends
       for (int j0 = 0; j0 < nv; j0 += 32) {
         const int pid = j0 + lane < nv ? p.vis_page[vb + j0 + lane] : 0;
         const int nj = min(32, nv - j0);
@@ -634,7 +654,7 @@ extern "C" int choreo_decode_attn_v2_ex(const float* q, const void* k_pool, cons
                                         const int32_t* counts, int max_items, float* part_o,
                                         float* part_lse, const int32_t* fat_items, int grid_ctas,
                                         const void* q_k5, const int32_t* item_order,
-                                        void* stream);
+                                        int k3_tag, void* stream);
 
 extern "C" int choreo_decode_attn_v2(const float* q, const void* k_pool, const void* v_pool,
                                      int n_layers, int layer, int n_kv, int n_pages, int page_size,
@@ -647,7 +667,7 @@ extern "C" int choreo_decode_attn_v2(const float* q, const void* k_pool, const v
   return choreo_decode_attn_v2_ex(q, k_pool, v_pool, n_layers, layer, n_kv, n_pages, page_size,
                                   n_heads, head_dim, row_t, vis_page, vis_len, vis_own, blk_rows,
                                   items, counts, max_items, part_o, part_lse, fat_items,
-                                  grid_ctas, nullptr, nullptr, stream);
+                                  grid_ctas, nullptr, nullptr, 0, stream);
 }
 
 extern "C" int choreo_decode_attn_v2_ex(const float* q, const void* k_pool, const void* v_pool,
@@ -659,7 +679,7 @@ extern "C" int choreo_decode_attn_v2_ex(const float* q, const void* k_pool, cons
                                         const int32_t* counts, int max_items, float* part_o,
                                         float* part_lse, const int32_t* fat_items, int grid_ctas,
                                         const void* q_k5, const int32_t* item_order,
-                                        void* stream) {
+                                        int k3_tag, void* stream) {
   if (!q || !k_pool || !v_pool || !row_t || !vis_page || !vis_len || !vis_own || !blk_rows ||
       !items || !counts || !part_o || !part_lse || n_kv <= 0 || n_heads % n_kv)
     return CHOREO_EINVAL;
@@ -672,7 +692,7 @@ extern "C" int choreo_decode_attn_v2_ex(const float* q, const void* k_pool, cons
   DvParams p{q, layer, n_kv, n_pages, n_heads, row_t, vis_page, vis_len, vis_own, blk_rows, items,
              counts, part_o, part_lse, 1.4426950408889634f / sqrtf((float)head_dim),
              32 / G <= 16 ? fat_items : nullptr, 0, reinterpret_cast<const __nv_bfloat16*>(q_k5),
-             item_order};
+             item_order, k3_tag};
 #ifdef CHOREO_TRACE
   p.trace_slot = g_dv_launches++;
 #endif

@@ -156,7 +156,7 @@ extern "C" int choreo_decode_layers(const ChoreoDecodeStep* s, void* stream) {
                                  s->page_size, H, hd, s->row_t, s->vis_page, s->vis_len,
                                  s->vis_own, s->blk_rows, s->items, s->counts, s->n_items,
                                  s->part_o, s->part_lse, s->fat, 0,
-                                 defer ? s->q_k5 : nullptr, s->item_order, stream));
+                                 defer ? s->q_k5 : nullptr, s->item_order, s->k3_tag, stream));
     if (ev) cudaEventRecord(ev[2 * l + 1], as_stream(stream));
     CHK(choreo_attn_combine(s->part_o, s->part_lse, s->row_part_off, s->row_part, R, H, hd,
                             s->attn, CHOREO_BF16, sp, stream));

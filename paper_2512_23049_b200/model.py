@@ -19,6 +19,7 @@ cuBLAS GEMMs via torch (bf16 in, f32 accumulate); the residual stream is f32.
 from __future__ import annotations
 
 import ctypes
+import itertools
 import os
 from dataclasses import dataclass
 
@@ -126,6 +127,7 @@ def plan_counts(calls: list, msg_len: np.ndarray, P: int, rpb: int, ppi: int,
     return Plan(n_vis, n_blk, n_items, n_parts, max_row, item_pages)
 
 
+_STEP_TAGS = itertools.count(1)  # K3 step tags (process-unique; int32 range is plenty)
 K3_MAX_CALLS = 1024  # assemble.cu kMaxCalls
 K3_MAX_PAIRS = 4096  # assemble.cu kMaxPairs (page-centric mode)
 K3_MAX_PARENT_ID = (1 << 21) - 1  # parent ids are packed as (parent << 11 | call)
@@ -346,11 +348,12 @@ class Runner:
             q_k5 = torch.empty(R, cfg.n_heads, 2, hd, dtype=torch.bfloat16, device=dev)
             st.q_k5 = q_k5.data_ptr()
         if v2 is not None:
-            _, rowt_d, vis, blk_rows, items, order = v2
+            _, rowt_d, vis, blk_rows, items, order, tag = v2
             st.row_t, st.vis_page, st.vis_len, st.vis_own = (
                 rowt_d.data_ptr(), vis[0].data_ptr(), vis[1].data_ptr(), vis[2].data_ptr())
             st.blk_rows, st.items = blk_rows.data_ptr(), items.data_ptr()
             st.item_order = nat.ptr(order)
+            st.k3_tag = tag
         if chain:
             cb = self._chain_buffers()
             h_b = torch.empty(2 * R if self.split else R, d, dtype=self.dt, device=dev)
@@ -528,7 +531,10 @@ class Runner:
         items = torch.empty(max(n_items, 1), 6, dtype=torch.int32, device=self.dev)
         row_part_off = torch.empty(R + 1, dtype=torch.int32, device=self.dev)
         row_part = torch.empty(max(n_parts, 1), dtype=torch.int32, device=self.dev)
-        counts = torch.empty(4, dtype=torch.int32, device=self.dev)
+        counts = torch.empty(6, dtype=torch.int32, device=self.dev)  # [4..5]: K3's step stamp
+        # a process-unique tag per step: K3 stamps counts[4] with it once its outputs are
+        # complete, and K5 v2 then reads them before its programmatic-dependency wait
+        tag = next(_STEP_TAGS) if v2 else 0
         fat = (torch.empty(max(n_items, 1), 64, dtype=torch.int32, device=self.dev)
                if v2 and rpb <= 16 else None)
         order = (torch.empty(max(n_items, 1), dtype=torch.int32, device=self.dev)
@@ -539,7 +545,7 @@ class Runner:
                         vis[1].data_ptr(), vis[2].data_ptr(), blk_rows.data_ptr(),
                         items.data_ptr(), row_part_off.data_ptr(), row_part.data_ptr(),
                         counts.data_ptr(), plan_.n_vis, plan_.n_blk_rows, n_items, n_parts, mode,
-                        nat.ptr(fat), nat.ptr(order), stream)
+                        nat.ptr(fat), nat.ptr(order), tag, stream)
         self.launches += 1
         self.last_assembly = (vis, blk_rows, items, row_part_off, row_part, counts, plan_, rowt_d)
         if self.check_assembly:  # debug/test: K3 must never report an overflow
@@ -576,7 +582,7 @@ class Runner:
             delta = self._native_layers(R, q, part_o, part_lse, attn, h, act, x, pos_d, page_d,
                                         slot_d, fat, counts, n_items, row_part_off, row_part,
                                         attn_bytes, stream,
-                                        (v2, rowt_d, vis, blk_rows, items, order))
+                                        (v2, rowt_d, vis, blk_rows, items, order, tag))
             if self._chain_ok(R):  # prologue + qkv(0); per layer: K5, combine, K8 chain
                 launches += 2 + 3 * len(self.w.layers)
             else:  # per layer: norm, K7 qkv, rope, K5, combine, K7 o, norm, K7 gate|up, K7 down
@@ -602,7 +608,7 @@ class Runner:
                                       vis[0].data_ptr(), vis[1].data_ptr(), vis[2].data_ptr(),
                                       blk_rows.data_ptr(), items.data_ptr(), counts.data_ptr(),
                                       n_items, part_o.data_ptr(), part_lse.data_ptr(),
-                                      nat.ptr(fat), 0, None, nat.ptr(order), stream)
+                                      nat.ptr(fat), 0, None, nat.ptr(order), tag, stream)
             elif use_k4:
                 nat.prefill_attn(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(),
                                  self.pool_dtc, cfg.n_layers, layer, Hk, cache.n_pages, P, H, hd,

@@ -125,7 +125,7 @@ def _random_cache(cfg, rng, n_msgs, P=64, dtype=torch.float32):
     return cache, lens
 
 
-def _assemble(cache, calls, rpb, ppi, mode=0, order=None):
+def _assemble(cache, calls, rpb, ppi, mode=0, order=None, tag=0):
     """calls: list of (own msg, parents, row_t list).  Returns host copies of K3 outputs
     (order: an int32 device tensor receiving choreo_assemble_ex's item_order)."""
     from paper_2512_23049_b200.model import plan_counts, CallRows
@@ -146,7 +146,7 @@ def _assemble(cache, calls, rpb, ppi, mode=0, order=None):
     items = torch.full((max(plan.n_items, 1), 6), -7, dtype=torch.int32, device="cuda")
     rpo = torch.full((R + 1,), -7, dtype=torch.int32, device="cuda")
     rp = torch.full((max(plan.n_parts, 1),), -7, dtype=torch.int32, device="cuda")
-    counts = torch.empty(4, dtype=torch.int32, device="cuda")
+    counts = torch.zeros(6, dtype=torch.int32, device="cuda")
     args = (cache.msg_len.dev.data_ptr(), cache.msg_pt.dev.data_ptr(),
             cache.page_table.dev.data_ptr(), tab_d.data_ptr(), par_d.data_ptr(), len(calls),
             rt_d.data_ptr(), R, None, 0, cache.page_size, rpb, ppi,
@@ -156,7 +156,7 @@ def _assemble(cache, calls, rpb, ppi, mode=0, order=None):
     if order is None:
         nat.assemble(*args, _stream())
     else:
-        nat.assemble_ex(*args, order.data_ptr(), _stream())
+        nat.assemble_ex(*args, order.data_ptr(), tag, _stream())
     out = dict(vis=vis.cpu().numpy(), blk=blk.cpu().numpy(), items=items.cpu().numpy(),
                rpo=rpo.cpu().numpy(), rp=rp.cpu().numpy(), counts=counts.cpu().numpy(),
                row_t=np.asarray(row_t), plan=plan)
@@ -445,13 +445,16 @@ def test_decode_v2_matches_dense_reference(hd, H, Hk, ppi):
                           cache.n_pages, 64, H, hd, rt_d.data_ptr(), vis[0].data_ptr(),
                           vis[1].data_ptr(), vis[2].data_ptr(), blk.data_ptr(), items.data_ptr(),
                           counts.data_ptr(), pl_.n_items, part_o.data_ptr(), part_lse.data_ptr(),
-                          None, 5, q_k5.data_ptr(), None, _stream())
+                          None, 5, q_k5.data_ptr(), None, 0, _stream())
     torch.cuda.synchronize()
     assert torch.equal(part_o, ref_o) and torch.equal(part_lse, ref_lse)
     # longest-first unit deal (K3 item_order, snaking over 5 CTAs): the schedule changes,
     # every unit still writes its own partial slots -> bitwise the same partials
     order = torch.full((max(pl_.n_items, 1),), -7, dtype=torch.int32, device="cuda")
-    out2, (rt2, vis2, blk2, items2, _, _, counts2) = _assemble(cache, calls, rpb, ppi, 0, order)
+    # (with K3's step tag: the loader / producer read K3's outputs before the dependency wait)
+    out2, (rt2, vis2, blk2, items2, _, _, counts2) = _assemble(cache, calls, rpb, ppi, 0, order,
+                                                               tag=77)
+    assert counts2[4:6].tolist() == [77, pl_.n_items], "K3 stamps {tag, n_items} after its outputs"
     nv = out2["items"][:pl_.n_items, 3]
     want = sorted(range(pl_.n_items), key=lambda i: (-min(max(int(nv[i]), 1), 32), i))
     assert order.cpu().tolist()[:pl_.n_items] == want, "item_order: stable, page count descending"
@@ -463,7 +466,7 @@ def test_decode_v2_matches_dense_reference(hd, H, Hk, ppi):
                               vis2[1].data_ptr(), vis2[2].data_ptr(), blk2.data_ptr(),
                               items2.data_ptr(), counts2.data_ptr(), pl_.n_items,
                               part_o.data_ptr(), part_lse.data_ptr(), None, grid,
-                              q_k5.data_ptr(), order.data_ptr(), _stream())
+                              q_k5.data_ptr(), order.data_ptr(), 77, _stream())
         torch.cuda.synchronize()
         assert torch.equal(part_o, ref_o) and torch.equal(part_lse, ref_lse), grid
 

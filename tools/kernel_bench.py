@@ -30,6 +30,8 @@ from paper_2512_23049_b200.cache import DeviceKvCache, RotationTableDevice, cdiv
 from paper_2512_23049_b200.config import LLAMA_3_1_8B  # noqa: E402
 from paper_2512_23049_b200.model import CallRows, plan_counts  # noqa: E402
 
+K3_TAG = 4242  # the runner's K3 step tag (K5 v2 reads K3's outputs before its dependency wait)
+
 
 def peaks() -> dict:
     try:
@@ -99,7 +101,7 @@ def _assemble(cache, calls, rpb, ppi, mode=0):
                 items=torch.empty(plan.n_items, 6, dtype=torch.int32, device="cuda"),
                 rpo=torch.empty(R + 1, dtype=torch.int32, device="cuda"),
                 rp=torch.empty(plan.n_parts, dtype=torch.int32, device="cuda"),
-                counts=torch.empty(4, dtype=torch.int32, device="cuda"), rt=rt_d,
+                counts=torch.zeros(6, dtype=torch.int32, device="cuda"), rt=rt_d,
                 fat=torch.empty(max(plan.n_items, 1), 64, dtype=torch.int32, device="cuda"),
                 order=torch.empty(max(plan.n_items, 1), dtype=torch.int32, device="cuda"))
     v = bufs["vis"]
@@ -109,7 +111,7 @@ def _assemble(cache, calls, rpb, ppi, mode=0):
                  v[2].data_ptr(), bufs["blk"].data_ptr(), bufs["items"].data_ptr(),
                  bufs["rpo"].data_ptr(), bufs["rp"].data_ptr(), bufs["counts"].data_ptr(),
                  plan.n_vis, plan.n_blk_rows, plan.n_items, plan.n_parts, mode,
-                 bufs["fat"].data_ptr(), bufs["order"].data_ptr(),
+                 bufs["fat"].data_ptr(), bufs["order"].data_ptr(), mode == 0 and K3_TAG,
                  torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     assert int(bufs["counts"][3]) == 0
@@ -250,7 +252,7 @@ def k5_decode(n_workflows: int = 1, agents: int = 8, tc: bool = False, v2: bool 
                                   v[2].data_ptr(), b["blk"].data_ptr(), b["items"].data_ptr(),
                                   b["counts"].data_ptr(), plan.n_items, po.data_ptr(),
                                   pl.data_ptr(), b["fat"].data_ptr(), 0, nat.ptr(q_k5),
-                                  nat.ptr(order), stream)
+                                  nat.ptr(order), K3_TAG, stream)
             return
         if tc:
             nat.prefill_attn(q.data_ptr(), cache.k_pool.data_ptr(), cache.v_pool.data_ptr(),
