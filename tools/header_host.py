@@ -20,7 +20,7 @@ cfg = P.PRESETS["llama-3.1-8b"]
 w = P.DeviceWeights.random(cfg, dtype=torch.bfloat16)
 eng = P.Engine(w, capacity=65536)
 orig = eng._runner.forward
-orig_asm = nat.assemble
+orig_asm = nat.assemble_ex
 rec, marks, state = [], {}, {"n": 0}
 
 
@@ -32,7 +32,7 @@ def asm(*a):
     return orig_asm(*a)
 
 
-nat.assemble = asm
+nat.assemble_ex = asm
 
 
 def fwd(plan):
