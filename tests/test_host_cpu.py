@@ -287,3 +287,50 @@ def test_split_plan_respects_k3_limits():
     # parent ids past the 21-bit sort key take per-call lists
     (p, percall), = split_plan(StepPlan([_rows(1, [1 << 21], 1)], np.zeros(1, np.int32)))
     assert percall
+
+
+def test_ctypes_struct_mirrors_match_the_c_header(tmp_path):
+    """The ctypes mirrors of the ABI structs (ChoreoK7Pieces, ChoreoDecodeStep,
+    ChoreoLayerChain) have the header's field names, order, offsets and size: a C program
+    compiled against include/choreo_b200.h prints offsetof / sizeof for every field."""
+    import ctypes
+    import shutil
+    import subprocess
+
+    from paper_2512_23049_b200 import _native as nat
+
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    hdr = os.path.join(ROOT, "include", "choreo_b200.h")
+    text = open(hdr).read()
+    mirrors = {"ChoreoK7Pieces": nat.K7Pieces, "ChoreoDecodeStep": nat.DecodeStep,
+               "ChoreoLayerChain": nat.LayerChain}
+    prog = ["#include <stddef.h>", "#include <stdio.h>", '#include "choreo_b200.h"',
+            "int main(void) {"]
+    for cname, py in mirrors.items():
+        body = re.search(r"typedef struct \{([^{}]*)\}\s*" + cname + ";", text).group(1)
+        body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+        names = []
+        for decl in body.split(";"):
+            decl = decl.strip()
+            if not decl:
+                continue
+            for part in decl.split(","):
+                m = re.search(r"(\w+)\s*(\[[^\]]*\])?\s*$", part.strip())
+                names.append(m.group(1))
+        assert [f[0] for f in py._fields_] == names, cname
+        for n in names:
+            prog.append(f'  printf("{cname} {n} %zu\\n", offsetof({cname}, {n}));')
+        prog.append(f'  printf("{cname} sizeof %zu\\n", sizeof({cname}));')
+    prog.append("  return 0;\n}")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(prog))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)],
+                   check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n")
+    for line in filter(None, out):
+        cname, field, val = line.split()
+        py = mirrors[cname]
+        got = ctypes.sizeof(py) if field == "sizeof" else getattr(py, field).offset
+        assert got == int(val), (cname, field, got, val)
