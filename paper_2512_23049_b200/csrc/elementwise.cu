@@ -184,6 +184,70 @@ __global__ void __launch_bounds__(1024) residual_rmsnorm_vec(float* __restrict__
   }
 }
 
+// The same (x += deferred K7 output; h = hi/lo(rmsnorm(x) * w)) with each row split over a
+// cluster of kNc CTAs of 128 threads (one float4 per thread): the CTAs are small enough to
+// become resident next to the running K7 CTAs (programmatic dependent launch), and the
+// row's sum of squares is combined through distributed shared memory in the same order as
+// residual_rmsnorm_vec (bit-identical outputs).
+constexpr int kNc = 8;
+__global__ void __launch_bounds__(128) residual_rmsnorm_cluster(float* __restrict__ x,
+                                                               const void* __restrict__ w,
+                                                               int w_dt, int d, float eps,
+                                                               __nv_bfloat16* __restrict__ out,
+                                                               int out_split, int n_rows,
+                                                               ChoreoK7Pieces pv) {
+  pdl_trigger();
+  const int r = blockIdx.x / kNc, part = blockIdx.x % kNc;
+  const int i = part * (d / kNc) + 4 * threadIdx.x;  // this thread's 4 columns
+  const bool on = 4 * threadIdx.x < d / kNc;
+  const float4 wv = on ? ld4_any(w, w_dt, i) : make_float4(0.f, 0.f, 0.f, 0.f);
+  pdl_wait();
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (on) {
+    float* xr = x + (int64_t)r * d + i;
+    v = ld4(xr);
+    float4 a;
+    choreo::k7_get<4, 4>(pv, r, i, &a.x);
+    v.x += a.x;
+    v.y += a.y;
+    v.z += a.z;
+    v.w += a.w;
+    *reinterpret_cast<float4*>(xr) = v;
+  }
+  // the row's sum of squares in the 1024-thread kernel's exact order (bitwise the same
+  // result): per-warp butterfly sums of 128-column blocks, then one butterfly over the
+  // blocks' sums (lane i = block i), gathered here from the cluster's CTAs over DSMEM
+  __shared__ float red[4];
+  __shared__ float tot_s;
+  float ss = 0.f;
+  ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;  // as residual_rmsnorm_vec
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  // cluster barrier: every CTA's block sums are written before any is read
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x, nb = d / 128, wpc = d / kNc / 128;  // blocks, per CTA
+    float t = 0.f;
+    if (lane < nb) {
+      const uint32_t local = static_cast<uint32_t>(__cvta_generic_to_shared(&red[lane % wpc]));
+      uint32_t remote;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(lane / wpc));
+      asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(t) : "r"(remote) : "memory");
+    }
+    t = warp_sum(t);
+    if (lane == 0) tot_s = t;
+  }
+  __syncthreads();
+  const float tot = tot_s;
+  // keep this CTA's shared memory alive until every CTA of the cluster has read it
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  if (!on) return;
+  const float inv = 1.0f / sqrtf(tot / (float)d + eps);
+  const float4 y = make_float4(v.x * inv * wv.x, v.y * inv * wv.y, v.z * inv * wv.z, v.w * inv * wv.w);
+  st4_split(out, CHOREO_BF16, (int64_t)r * d + i, (int64_t)(n_rows + r) * d + i, y, out_split);
+}
+
 __global__ void silu_mul_kernel(const void* __restrict__ gu, int dt, int in_split, int n_rows,
                                 int f, void* __restrict__ out, int out_dt, int out_split) {
   pdl_trigger();
@@ -327,6 +391,12 @@ int choreo_residual_rmsnorm(float* x, const void* delta, int delta_dtype, int de
   return launch_status("choreo_residual_rmsnorm");
 }
 
+static bool norm_cluster() {  // measurement switch: CHOREO_NORM_CLUSTER=0 -> 1024-thread CTAs
+  static int v = -1;
+  if (v < 0) v = getenv("CHOREO_NORM_CLUSTER") ? atoi(getenv("CHOREO_NORM_CLUSTER")) : 1;
+  return v != 0;
+}
+
 int choreo_residual_rmsnorm_pieces(float* x, const ChoreoK7Pieces* delta, const void* w,
                                    int w_dtype, int n_rows, int d, float eps, void* out,
                                    int out_dtype, int out_split, void* stream) {
@@ -336,6 +406,25 @@ int choreo_residual_rmsnorm_pieces(float* x, const ChoreoK7Pieces* delta, const 
   if (out_split && out_dtype != CHOREO_BF16) return CHOREO_EINVAL;
   if (d % 4 || d > 4 * 4 * 1024) return CHOREO_EUNSUPPORTED;
   if (n_rows == 0) return CHOREO_OK;
+  // (128-column blocks must not straddle CTAs: d a multiple of 128 kNc, at most 4 per CTA)
+  if (out_dtype == CHOREO_BF16 && d % (128 * kNc) == 0 && d / kNc <= 4 * 128 && norm_cluster()) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(n_rows * kNc);
+    cfg.blockDim = dim3(128);
+    cfg.stream = as_stream(stream);
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kNc;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    cudaLaunchKernelEx(&cfg, residual_rmsnorm_cluster, x, w, w_dtype, d, eps,
+                       reinterpret_cast<__nv_bfloat16*>(out), out_split, n_rows, *delta);
+    return launch_status("choreo_residual_rmsnorm_pieces");
+  }
   const int nvec = d / 4;
   int threads = nvec < 1024 ? ((nvec + 31) / 32) * 32 : 1024;
   const int ch = (nvec + threads - 1) / threads;
