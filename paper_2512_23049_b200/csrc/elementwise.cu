@@ -197,9 +197,13 @@ __global__ void __launch_bounds__(128) residual_rmsnorm_cluster(float* __restric
                                                                int out_split, int n_rows,
                                                                ChoreoK7Pieces pv) {
   pdl_trigger();
+  // CTA `part` of the row's cluster takes the 128-column blocks part, part + 8, part + 16,
+  // part + 24 (one per warp): the first two levels of the 32-block butterfly below are then
+  // CTA-local and only 8 values cross the cluster
   const int r = blockIdx.x / kNc, part = blockIdx.x % kNc;
-  const int i = part * (d / kNc) + 4 * threadIdx.x;  // this thread's 4 columns
-  const bool on = 4 * threadIdx.x < d / kNc;
+  const int blk = part + kNc * (threadIdx.x >> 5);
+  const int i = blk * 128 + 4 * (threadIdx.x & 31);  // this thread's 4 columns
+  const bool on = blk < d / 128;
   const float4 wv = on ? ld4_any(w, w_dt, i) : make_float4(0.f, 0.f, 0.f, 0.f);
   pdl_wait();
   float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -215,27 +219,31 @@ __global__ void __launch_bounds__(128) residual_rmsnorm_cluster(float* __restric
     *reinterpret_cast<float4*>(xr) = v;
   }
   // the row's sum of squares in the 1024-thread kernel's exact order (bitwise the same
-  // result): per-warp butterfly sums of 128-column blocks, then one butterfly over the
-  // blocks' sums (lane i = block i), gathered here from the cluster's CTAs over DSMEM
+  // result): per-warp butterfly sums of 128-column blocks, then the butterfly over the 32
+  // block sums (xor 16, 8, 4, 2, 1; absent blocks are +0, which adds exactly) -- its xor-16
+  // and xor-8 levels inside this CTA, its xor-4, 2, 1 levels over the cluster's 8 partials
   __shared__ float red[4];
-  __shared__ float tot_s;
+  __shared__ float part_s, tot_s;
   float ss = 0.f;
   ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;  // as residual_rmsnorm_vec
   ss = warp_sum(ss);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
   __syncthreads();
-  // cluster barrier: every CTA's block sums are written before any is read
+  if (threadIdx.x == 0) part_s = (red[0] + red[2]) + (red[1] + red[3]);
+  // cluster barrier: every CTA's partial is written before any is read
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
   if (threadIdx.x < 32) {
-    const int lane = threadIdx.x, nb = d / 128, wpc = d / kNc / 128;  // blocks, per CTA
+    const int lane = threadIdx.x;
     float t = 0.f;
-    if (lane < nb) {
-      const uint32_t local = static_cast<uint32_t>(__cvta_generic_to_shared(&red[lane % wpc]));
+    if (lane < kNc) {
+      const uint32_t local = static_cast<uint32_t>(__cvta_generic_to_shared(&part_s));
       uint32_t remote;
-      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(lane / wpc));
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(lane));
       asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(t) : "r"(remote) : "memory");
     }
-    t = warp_sum(t);
+    t += __shfl_xor_sync(0xffffffffu, t, 4);
+    t += __shfl_xor_sync(0xffffffffu, t, 2);
+    t += __shfl_xor_sync(0xffffffffu, t, 1);
     if (lane == 0) tot_s = t;
   }
   __syncthreads();
