@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(128) residual_rmsnorm_cluster(float* __restric
     float* xr = x + (int64_t)r * d + i;
     v = ld4(xr);
     float4 a;
-    choreo::k7_get<4, 4>(pv, r, i, &a.x);
+    choreo::k7_get<4, 8>(pv, r, i, &a.x);  // all of a tile's pieces in one round trip
     v.x += a.x;
     v.y += a.y;
     v.z += a.z;
