@@ -227,13 +227,31 @@ __global__ void __launch_bounds__(128) attn_combine_kernel(
 #pragma unroll
     for (int k = 0; k < 4; ++k) add(l[k], o[k]);
   }
-  for (; i < e; i += 4) {
-    const int pi = row_part[i];
-    const float l = part_lse[(int64_t)pi * n_heads + h];
-    const float4 o = active ? *reinterpret_cast<const float4*>(part_o + ((int64_t)pi * n_heads + h) * hd + 4 * lane)
-                            : make_float4(0.f, 0.f, 0.f, 0.f);
-    rescale(l);
-    add(l, o);
+  // the rest (< 16 slots per warp): the same per-slot rescale / add sequence as one slot at a
+  // time, with the loads of up to 4 slots issued together (bitwise the same result)
+  for (; i < e; i += 16) {
+    int pi[4];
+    float l[4];
+    float4 o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) pi[k] = i + 4 * k < e ? row_part[i + 4 * k] : 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      l[k] = -INFINITY;
+      o[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (i + 4 * k < e) {
+        l[k] = part_lse[(int64_t)pi[k] * n_heads + h];
+        if (active)
+          o[k] = *reinterpret_cast<const float4*>(part_o + ((int64_t)pi[k] * n_heads + h) * hd + 4 * lane);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (i + 4 * k < e) {
+        rescale(l[k]);
+        add(l[k], o[k]);
+      }
+    }
   }
   s_num[warp][lane] = num;
   if (lane == 0) {
