@@ -279,7 +279,10 @@ int choreo_rope_append_pieces_ex(const ChoreoK7Pieces* qkv, int n_rows, const in
                                  const float* cos_t, const float* sin_t, int max_delta,
                                  void* q_k5, float q_scale, void* stream);
 
-/* choreo_residual_rmsnorm with delta = a deferred K7 projection (x += delta; out = norm(x)). */
+/* choreo_residual_rmsnorm with delta = a deferred K7 projection (x += delta; out = norm(x)).
+ * bf16 outputs with d a multiple of 1024 (<= 4096) run one 8-CTA cluster of 128 threads per
+ * row (DSMEM reduction in the single-CTA kernel's order: bit-identical results);
+ * CHOREO_NORM_CLUSTER=0 selects the single-CTA kernel (A/B timing). */
 int choreo_residual_rmsnorm_pieces(float* x, const ChoreoK7Pieces* delta, const void* w,
                                    int w_dtype, int n_rows, int d, float eps, void* out,
                                    int out_dtype, int out_split, void* stream);
